@@ -1,0 +1,140 @@
+/* bb200.h — C-ABI of the B200-native BlockBatch batched denoising step.
+ *
+ * Plain C types only (pointers, sizes, ints, floats): no torch types.  Every
+ * call returns int (0 = OK, negative = error code below) and takes the CUDA
+ * stream to enqueue on as `void*` (a cudaStream_t).  Device buffers passed in
+ * are caller-owned; handles are not thread-safe (one stream per session).
+ *
+ * The reference has no native code; its seams are Python functions.  Each
+ * entry point below names the reference interface it replaces
+ * (/root/reference/pkg/src/blockbatch/<file>:<line>).
+ */
+#ifndef BB200_H
+#define BB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BB_API __attribute__((visibility("default")))
+
+/* ---- error codes (mapped by the Python wrapper onto errors.py:4-17) ---- */
+#define BB_OK 0
+#define BB_ERR_CONFIG (-1)     /* ConfigError   (errors.py:4)  */
+#define BB_ERR_CONTRACT (-2)   /* ContractError (errors.py:8)  */
+#define BB_ERR_STATE (-3)      /* StateError    (errors.py:12) */
+#define BB_ERR_RUNAWAY (-4)    /* RunawayError  (errors.py:16) */
+#define BB_ERR_CUDA (-10)      /* CUDA launch / runtime failure */
+#define BB_ERR_NOMEM (-11)     /* workspace too small           */
+
+/* ---- model ------------------------------------------------------------- */
+#define BB_ARCH_REF 0    /* reference synthetic denoiser (model.py:278-319): learned positions,
+                            single head with head_dim = d_model, no norm, no MLP */
+#define BB_ARCH_LLADA 1  /* LLaDA-8B / Dream-7B shape: RMSNorm, RoPE, MHA/GQA, SwiGLU, final norm */
+#define BB_DTYPE_F32 0   /* fp32 verification mode (SIMT kernels)            */
+#define BB_DTYPE_BF16 1  /* bf16 weights/activations/KV, fp32 accumulate (tcgen05) */
+
+/* ModelParams (model.py:115-133) + ModelDims (model.py:66-70) + the LLaDA/Dream shape. */
+typedef struct {
+  int arch, vocab_size, layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, max_len, qkv_bias, dtype;
+  float rope_theta, norm_eps, gamma;
+  int radius;
+  float head_scale, spike_cut, spike_gain;
+} bb_model_desc;
+
+/* Device pointers (caller-owned).  Matrices are (out, in) row-major in the
+ * model dtype; norms/bias fp32.  wgu interleaves gate/up rows in blocks of 64
+ * (rows [128t,128t+64) = gate features [64t,64t+64), next 64 = up). */
+typedef struct {
+  const void* emb;   /* [vocab+2][d]                  */
+  const void* pos;   /* [max_len][d]      (arch REF)   */
+  const void* wqkv;  /* [layers][(nh+2nkv)*hd][d]      */
+  const float* bqkv; /* [layers][(nh+2nkv)*hd] or NULL */
+  const void* wo;    /* [layers][d][nh*hd]             */
+  const void* wgu;   /* [layers][2*d_ff][d]            */
+  const void* wd;    /* [layers][d][d_ff]              */
+  const float* ln1;  /* [layers][d]                    */
+  const float* ln2;  /* [layers][d]                    */
+  const float* lnf;  /* [d]                            */
+  const void* head;  /* [vocab+1][d]                   */
+} bb_weights;
+
+/* Replaces build_model's product (model.py:210-241) as the forward's parameter set. */
+BB_API int bb_model_create(const bb_model_desc* desc, const bb_weights* w, void** model);
+BB_API int bb_model_destroy(void* model);
+
+/* ---- session: R requests x B block-size branches ------------------------ */
+/* SchedulerConfig (scheduler.py:32-63) + device layout knobs. */
+typedef struct {
+  int n_requests, n_branches;
+  int block_sizes[8];
+  int prompt_len, gen_len;
+  float tau_conf, tau_merge, tau_sync;
+  int refresh_interval, merge_enabled, sync_enabled;
+  int page_size;       /* KV page positions (<= 32, default 16)          */
+  int pages_per_item;  /* attention split (pages per work item, def. 4)  */
+  int trace;           /* record trace events (TraceEvent, decoding.py:61-75) */
+  int event_capacity;  /* events per request                              */
+} bb_session_desc;
+
+#define BB_VIEW_TOKENS 0   /* int32 [R][B][L]      branch rows              */
+#define BB_VIEW_TARGET 1   /* int32 [R][G]         planted targets (input)  */
+#define BB_VIEW_PROMPT 2   /* int32 [R][P]         prompts (input)          */
+#define BB_VIEW_CTRL 3     /* int32 [R][32]        status, NFE, counters    */
+#define BB_VIEW_BRANCH 4   /* int32 [R][B][8]      window, done, progress   */
+#define BB_VIEW_EVENTS 5   /* int32 [R][cap][20]   trace records            */
+#define BB_VIEW_COVERED 6  /* uint8 [R][B][L]      prob_covered             */
+#define BB_VIEW_PM_M 7     /* fp32  [R][B][L]      prob-map max logit       */
+#define BB_VIEW_PM_S 8     /* fp32  [R][B][L]      prob-map sum-exp         */
+#define BB_VIEW_PAGES 9    /* int32 [R][B][n_lp]   KV page tables           */
+#define BB_VIEW_REFC 10    /* int32 [R][pool]      page refcounts           */
+#define BB_VIEW_COUNT 11
+
+BB_API int bb_session_workspace_bytes(const void* model, const bb_session_desc* d, size_t* bytes);
+BB_API int bb_session_create(void* model, const bb_session_desc* d, void* workspace, size_t bytes, void** sess);
+BB_API int bb_session_destroy(void* sess);
+BB_API int bb_session_view(const void* sess, int which, long long* offset, long long* bytes);
+BB_API int bb_session_info(const void* sess, int* out, int n);
+BB_API int bb_session_ctrl(void* sess, int* host_out, void* stream);
+
+/* ---- the step ------------------------------------------------------------ */
+/* init_full_forward + per-branch commit + advance + merge_sync (scheduler.py:80-89, 283-307) */
+BB_API int bb_prefill(void* sess, void* stream);
+/* one loop iteration without refresh: active set, pack, fused forward over all
+ * active windows (1 NFE), Eq. 1 commit, EOS, advance, merge/sync
+ * (scheduler.py:92-131, 322-372; decoding.py:108-191) */
+BB_API int bb_block_step(void* sess, void* stream);
+/* periodic refresh (scheduler.py:373-391) */
+BB_API int bb_refresh(void* sess, void* stream);
+/* block step (+ refresh), optionally replayed from a captured CUDA graph */
+BB_API int bb_iteration(void* sess, int with_refresh, int use_graph, void* stream);
+/* run_blockbatch (scheduler.py:225-394) for all requests of the session */
+BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out);
+BB_API int bb_version(void);
+
+/* ---- debug / unit-test entry points (kernel-level) --------------------- */
+BB_API int bb_debug_gemm_tc(const void* W, const void* X, void* out, int n_out, int K, int rows, int BN, int mode,
+                            int max_grid, float* work, long long* work_floats, const int* tgt, const float* boost,
+                            float head_scale, float spike_cut, float spike_gain, void* stream);
+BB_API int bb_debug_gemm_simt(const float* W, const float* X, float* out, int n_out, int K, int rows,
+                              void* stream);
+
+/* step-operator seams on caller-supplied state (bit-exact given identical
+ * confidences; the same device code the fused step runs) */
+BB_API int bb_commit_probs(const float* probs, int n, int n_out, const int* pos, int* row, float tau, int* out,
+                           int* count, void* stream);
+BB_API int bb_merge_sync_maps(int n_branches, int L, int prompt_len, int vocab_size, int* rows, int* branch,
+                              unsigned char* covered, const float* probmaps, int n_out, float tau_merge,
+                              float tau_sync, int merge_enabled, int sync_enabled, int* events, int ev_cap,
+                              int* ctrl, float* ptab, unsigned char* ptab_ok, void* stream);
+/* device random-init (oracle/bb_oracle.py:hash_uniform); mode 1 = gate/up interleave */
+BB_API int bb_fill_hash_uniform(void* dst, int dtype, long long n, unsigned long long seed, int tensor_id, float c,
+                                long long start, int mode, int d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BB200_H */

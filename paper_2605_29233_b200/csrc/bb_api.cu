@@ -1,0 +1,694 @@
+// C-ABI implementation: model + session objects, workspace carving, the
+// per-iteration kernel sequence (captured once into CUDA graphs) and the
+// run_blockbatch loop with asynchronous status polling.
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <cmath>
+#include <vector>
+
+#include "bb200.h"
+#include "bb_common.cuh"
+#include "bb_gemm.cuh"
+#include "bb_layers.cuh"
+
+namespace bb {
+
+struct Model {
+  bb_model_desc desc;
+  Dims D;
+  Weights W;
+  float* rope = nullptr;  // owned (cudaMalloc), arch 1
+};
+
+struct LayerGemms {
+  TcGemm qkv, o, gu, dn;
+  SimtGemm sqkv, so, sgu, sdn;
+};
+
+struct PassGemms {
+  std::vector<LayerGemms> layers;
+  int BN = 64;
+};
+
+struct Session {
+  Model* M;
+  bb_session_desc desc;
+  Dims D;
+  Sess S;
+  DevState st;
+  Pass blk, full;
+  Head H;
+  PassGemms gb, gf;
+  TcGemm head_tc;
+  SimtGemm head_simt;
+  float* part = nullptr;
+  int* full_rows = nullptr;  // device scalar: rows of the full pass
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaGraphExec_t g_iter = nullptr, g_iter_ref = nullptr;
+  int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
+  cudaEvent_t ev[4] = {};
+  long long layout[BB_VIEW_COUNT][2];
+};
+
+// ------------------------------------------------------------------ helpers
+static int fail(int code, const char* msg) {
+  if (getenv("BB_DEBUG")) fprintf(stderr, "[bb200] %s\n", msg);
+  return code;
+}
+#define CK(x)                                              \
+  do {                                                     \
+    cudaError_t e_ = (x);                                  \
+    if (e_ != cudaSuccess) {                               \
+      if (getenv("BB_DEBUG"))                              \
+        fprintf(stderr, "[bb200] %s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      return BB_ERR_CUDA;                                  \
+    }                                                      \
+  } while (0)
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  bool dry;
+  template <typename T>
+  T* take(size_t count, size_t align = 256) {
+    off = (off + align - 1) / align * align;
+    T* p = dry ? nullptr : reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+static int validate_model(const bb_model_desc* m) {
+  if (m->vocab_size < 2 || m->layers < 1 || m->d_model < 1 || m->max_len < 1) return BB_ERR_CONFIG;
+  if (m->n_heads < 1 || m->n_kv_heads < 1 || m->n_heads % m->n_kv_heads) return BB_ERR_CONFIG;
+  if (m->head_dim != 32 && m->head_dim != 64 && m->head_dim != 128 && m->head_dim != 256) return BB_ERR_CONFIG;
+  if (m->dtype != BB_DTYPE_F32 && m->dtype != BB_DTYPE_BF16) return BB_ERR_CONFIG;
+  if (m->arch != BB_ARCH_REF && m->arch != BB_ARCH_LLADA) return BB_ERR_CONFIG;
+  if (m->arch == BB_ARCH_REF && (m->n_heads != 1 || m->head_dim != m->d_model || m->d_ff != 0)) return BB_ERR_CONFIG;
+  if (m->dtype == BB_DTYPE_BF16 && (m->d_model % 64 || (m->d_ff % 64) || (m->n_heads * m->head_dim) % 64))
+    return BB_ERR_CONFIG;
+  return BB_OK;
+}
+
+static Dims make_dims(const bb_model_desc* m) {
+  Dims D;
+  memset(&D, 0, sizeof(D));
+  D.arch = m->arch;
+  D.V = m->vocab_size;
+  D.n_out = m->vocab_size + 1;
+  D.n_ext = m->vocab_size + 2;
+  D.layers = m->layers;
+  D.d = m->d_model;
+  D.nh = m->n_heads;
+  D.nkv = m->n_kv_heads;
+  D.hd = m->head_dim;
+  D.dff = m->d_ff;
+  D.max_len = m->max_len;
+  D.qkv_bias = m->qkv_bias;
+  D.dtype = m->dtype;
+  D.qkv_out = (m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
+  D.attn_dim = m->n_heads * m->head_dim;
+  D.kv_dim = m->n_kv_heads * m->head_dim;
+  D.n_vtiles = (D.n_out + 127) / 128;
+  D.eps = m->norm_eps;
+  D.gamma = m->gamma;
+  D.head_scale = m->head_scale;
+  D.spike_cut = m->spike_cut;
+  D.spike_gain = m->spike_gain;
+  D.attn_scale = (float)(1.0 / std::sqrt((double)m->head_dim));
+  D.radius = m->radius;
+  return D;
+}
+
+static size_t esz(const Dims& D) { return D.dtype == BB_DTYPE_BF16 ? 2 : 4; }
+
+// Workspace plan.  dry = size query.
+static void plan(Session* s, char* base, bool dry) {
+  const Dims& D = s->D;
+  Sess& S = s->S;
+  Carver c{base, 0, dry};
+  const size_t e = esz(D);
+  const long long R = S.R, B = S.B, L = S.L;
+  DevState& st = s->st;
+  auto view = [&](int id, const void* p, size_t bytes) {
+    s->layout[id][0] = dry ? 0 : (long long)((const char*)p - base);
+    s->layout[id][1] = (long long)bytes;
+  };
+  st.tokens = c.take<int>(R * B * L);
+  view(BB_VIEW_TOKENS, st.tokens, R * B * L * 4);
+  st.target = c.take<int>(R * S.G);
+  view(BB_VIEW_TARGET, st.target, R * S.G * 4);
+  st.prompt = c.take<int>(R * S.P);
+  view(BB_VIEW_PROMPT, st.prompt, R * S.P * 4);
+  st.ctrl = c.take<int>(R * C_WORDS);
+  view(BB_VIEW_CTRL, st.ctrl, R * C_WORDS * 4);
+  st.br = c.take<int>(R * B * B_WORDS);
+  view(BB_VIEW_BRANCH, st.br, R * B * B_WORDS * 4);
+  st.covered = c.take<uint8_t>(R * B * L);
+  view(BB_VIEW_COVERED, st.covered, R * B * L);
+  st.pm_h = c.take<char>(R * B * L * D.d * e);
+  st.pm_m = c.take<float>(R * B * L);
+  view(BB_VIEW_PM_M, st.pm_m, R * B * L * 4);
+  st.pm_s = c.take<float>(R * B * L);
+  view(BB_VIEW_PM_S, st.pm_s, R * B * L * 4);
+  st.pm_boost = c.take<float>(R * B * L);
+  st.pt = c.take<int>(R * B * S.n_lp);
+  view(BB_VIEW_PAGES, st.pt, R * B * S.n_lp * 4);
+  st.refc = c.take<int>(R * S.pool);
+  view(BB_VIEW_REFC, st.refc, R * S.pool * 4);
+  st.freel = c.take<int>(R * S.pool);
+  st.free_top = c.take<int>(R);
+  st.copies = c.take<int>(R * S.max_copies * 2);
+  st.pm_copies = c.take<int>(R * MAXB * 2);
+  st.events = c.take<int>(R * (long long)S.ev_cap * EVW);
+  view(BB_VIEW_EVENTS, st.events, R * (long long)S.ev_cap * EVW * 4);
+  st.ptab = c.take<float>(R * B * L * B);
+  st.ptab_ok = c.take<uint8_t>(R * B * L);
+  const long long kv_el = (long long)D.layers * R * S.pool * D.nkv * S.ps * D.hd;
+  st.kv_k = c.take<char>(kv_el * e, 1024);
+  st.kv_v = c.take<char>(kv_el * e, 1024);
+
+  auto pass = [&](Pass& P, int rows_alloc, int max_items, int item_rows, int full) {
+    P.rows_alloc = rows_alloc;
+    P.full = full;
+    P.item_rows = item_rows;
+    P.slot_pos = c.take<int>(rows_alloc);
+    P.slot_req = c.take<int>(rows_alloc);
+    P.slot_br = c.take<int>(rows_alloc);
+    P.slot_tok = c.take<int>(rows_alloc);
+    P.rng_off = c.take<int>(R * MAXB);
+    P.rng_cnt = c.take<int>(R * MAXB);
+    P.items = c.take<int>(R * max_items * ITW);
+    P.n_items = c.take<int>(R);
+    P.skip = c.take<int>(1);
+    P.x = c.take<float>((long long)rows_alloc * D.d);
+    P.xn = c.take<char>((long long)rows_alloc * D.d * e, 1024);
+    P.q = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
+    P.attn = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
+    P.act = c.take<char>((long long)rows_alloc * (D.dff > 0 ? D.dff : 1) * e, 1024);
+    P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
+  };
+  pass(s->blk, round_up(S.NR, s->gb.BN), S.max_items, S.NRq, 0);
+  pass(s->full, round_up(S.NF, s->gf.BN), 1, S.L, 1);
+  Head& H = s->H;
+  const int rb = s->blk.rows_alloc;
+  H.masked = c.take<int>(rb);
+  H.boost = c.take<float>(rb);
+  H.tgt = c.take<int>(rb);
+  H.hpart = c.take<float4>((long long)rb * D.n_vtiles);
+  H.logits = D.dtype == BB_DTYPE_F32 ? c.take<float>((long long)rb * D.n_out) : nullptr;
+  H.res_conf = c.take<float>(rb);
+  H.res_arg = c.take<int>(rb);
+  H.res_m = c.take<float>(rb);
+  H.res_s = c.take<float>(rb);
+  H.skip = c.take<int>(1);
+  s->full_rows = c.take<int>(1);
+  // GEMM partial planes: max over all stream-K GEMMs of (slots x rows x n_out)
+  long long part = 1;
+  if (D.dtype == BB_DTYPE_BF16) {
+    const int outs[4] = {D.qkv_out, D.d, 2 * D.dff, D.d};
+    const int ks[4] = {D.d, D.attn_dim, D.d, D.dff};
+    for (int which = 0; which < 2; ++which) {
+      const int rows = which == 0 ? s->blk.rows_alloc : s->full.rows_alloc;
+      const int BN = which == 0 ? s->gb.BN : s->gf.BN;
+      for (int g = 0; g < 4; ++g) {
+        if (outs[g] == 0) continue;
+        const int ntiles = (outs[g] + 127) / 128, nch = rows / BN, KB = (ks[g] + 63) / 64;
+        const long long T = (long long)ntiles * nch * KB;
+        const int G = (int)(T < kNumSMs ? T : kNumSMs);
+        int ms = 1;
+        for (long long t = 0; t < (long long)ntiles * nch; ++t) {
+          const int ns = sk_owner(t * KB + KB - 1, T, G) - sk_owner(t * KB, T, G) + 1;
+          ms = ns > ms ? ns : ms;
+        }
+        const long long need = (long long)ms * rows * outs[g];
+        part = need > part ? need : part;
+      }
+    }
+  } else {
+    const int outs[4] = {D.qkv_out, D.d, 2 * D.dff, D.d};
+    for (int g = 0; g < 4; ++g) {
+      const long long need = (long long)s->full.rows_alloc * outs[g];
+      part = need > part ? need : part;
+    }
+  }
+  s->part = c.take<float>(part);
+  s->ws_bytes = c.off + 1024;
+}
+
+static int setup_gemms(Session* s) {
+  const Dims& D = s->D;
+  const Weights& W = s->M->W;
+  const size_t e = esz(D);
+  for (int which = 0; which < 2; ++which) {
+    Pass& P = which == 0 ? s->blk : s->full;
+    PassGemms& G = which == 0 ? s->gb : s->gf;
+    G.layers.resize(D.layers);
+    for (int l = 0; l < D.layers; ++l) {
+      LayerGemms& lg = G.layers[l];
+      const char* wqkv = (const char*)W.wqkv + (size_t)l * D.qkv_out * D.d * e;
+      const char* wo = (const char*)W.wo + (size_t)l * D.d * D.attn_dim * e;
+      const char* wgu = D.dff ? (const char*)W.wgu + (size_t)l * 2 * D.dff * D.d * e : nullptr;
+      const char* wd = D.dff ? (const char*)W.wd + (size_t)l * D.d * D.dff * e : nullptr;
+      if (D.dtype == BB_DTYPE_BF16) {
+        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
+        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
+        if (D.dff) {
+          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
+        }
+        TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
+        for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
+          all[g]->p.part = s->part;
+          all[g]->p.skip = P.skip;
+          all[g]->p.rows_valid = which == 1 ? s->full_rows : nullptr;
+        }
+      } else {
+        lg.sqkv = SimtGemm{(const float*)wqkv, (const float*)P.xn, D.qkv_out, D.d, P.rows_alloc,
+                           which == 1 ? s->full_rows : nullptr, P.skip, s->part, D.qkv_out};
+        lg.so = SimtGemm{(const float*)wo, (const float*)P.attn, D.d, D.attn_dim, P.rows_alloc,
+                         which == 1 ? s->full_rows : nullptr, P.skip, s->part, D.d};
+        if (D.dff) {
+          lg.sgu = SimtGemm{(const float*)wgu, (const float*)P.xn, 2 * D.dff, D.d, P.rows_alloc,
+                            which == 1 ? s->full_rows : nullptr, P.skip, s->part, 2 * D.dff};
+          lg.sdn = SimtGemm{(const float*)wd, (const float*)P.act, D.d, D.dff, P.rows_alloc,
+                            which == 1 ? s->full_rows : nullptr, P.skip, s->part, D.d};
+        }
+      }
+    }
+  }
+  if (D.dtype == BB_DTYPE_BF16) {
+    if (!tc_gemm_setup(s->head_tc, W.head, D.n_out, D.d, s->blk.xn, s->blk.rows_alloc, s->gb.BN, 1, 0))
+      return BB_ERR_CONFIG;
+    GemmTcParams& p = s->head_tc.p;
+    p.head_part = s->H.hpart;
+    p.boost = s->H.boost;
+    p.tgt = s->H.tgt;
+    p.head_scale = D.head_scale;
+    p.spike_cut = D.spike_cut;
+    p.spike_gain = D.spike_gain;
+    p.skip = s->H.skip;
+  } else {
+    s->head_simt = SimtGemm{(const float*)W.head, (const float*)s->blk.xn, D.n_out, D.d, s->blk.rows_alloc,
+                            nullptr, s->H.skip, s->H.logits, D.n_out};
+  }
+  return BB_OK;
+}
+
+static PartRef pref_tc(const TcGemm& g, const float* part) {
+  return PartRef{part, g.p.plane, g.p.ldp, g.sk};
+}
+static PartRef pref_simt(const SimtGemm& g) {
+  SplitK sk{};
+  return PartRef{g.out, 0, g.ldo, sk};
+}
+
+// ------------------------------------------------------------------ forward pass
+static cudaError_t run_gemm(Session* s, const TcGemm& tg, const SimtGemm& sg, PartRef* pr, cudaStream_t st) {
+  if (s->D.dtype == BB_DTYPE_BF16) {
+    *pr = pref_tc(tg, s->part);
+    return tc_gemm_launch(tg, st);
+  }
+  *pr = pref_simt(sg);
+  return simt_gemm_launch(sg, st);
+}
+
+static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
+  const Dims& D = s->D;
+  const Weights& W = s->M->W;
+  cudaError_t e;
+  if ((e = launch_embed(D, s->S, P, W, st)) != cudaSuccess) return e;
+  for (int l = 0; l < D.layers; ++l) {
+    LayerGemms& lg = G.layers[l];
+    PartRef pr;
+    if ((e = run_gemm(s, lg.qkv, lg.sqkv, &pr, st)) != cudaSuccess) return e;
+    if ((e = launch_post_qkv(D, s->S, P, s->st, W, l, pr, st)) != cudaSuccess) return e;
+    if ((e = launch_attn(D, s->S, P, s->st, l, st)) != cudaSuccess) return e;
+    if ((e = run_gemm(s, lg.o, lg.so, &pr, st)) != cudaSuccess) return e;
+    const float* next_ln = l + 1 < D.layers ? (D.arch == BB_ARCH_LLADA ? W.ln1 + (size_t)(l + 1) * D.d : nullptr)
+                                            : (D.arch == BB_ARCH_LLADA ? W.lnf : nullptr);
+    if (D.dff) {
+      if ((e = launch_post_residual(D, P, pr, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
+      if ((e = run_gemm(s, lg.gu, lg.sgu, &pr, st)) != cudaSuccess) return e;
+      if ((e = launch_post_gu(D, P, pr, st)) != cudaSuccess) return e;
+      if ((e = run_gemm(s, lg.dn, lg.sdn, &pr, st)) != cudaSuccess) return e;
+      if ((e = launch_post_residual(D, P, pr, next_ln, st)) != cudaSuccess) return e;
+    } else {
+      if ((e = launch_post_residual(D, P, pr, next_ln, st)) != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+static cudaError_t head(Session* s, cudaStream_t st) {
+  const Dims& D = s->D;
+  cudaError_t e;
+  if (D.dtype == BB_DTYPE_BF16) {
+    if ((e = tc_gemm_launch(s->head_tc, st)) != cudaSuccess) return e;
+  } else {
+    if ((e = simt_gemm_launch(s->head_simt, st)) != cudaSuccess) return e;
+    if ((e = launch_head_tiles_f32(D, s->blk, s->H, st)) != cudaSuccess) return e;
+  }
+  return launch_head_reduce(D, s->S, s->blk, s->H, s->st, st);
+}
+
+static int enqueue_prefill(Session* s, cudaStream_t st) {
+  const Dims& D = s->D;
+  const Sess& S = s->S;
+  CK(cudaMemsetAsync(s->full_rows, 0, sizeof(int), st));
+  const int nf = S.NF;
+  CK(cudaMemcpyAsync(s->full_rows, &nf, sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(launch_prefill_init(D, S, s->st, s->full, s->blk, s->H, st));
+  CK(forward(s, s->full, s->gf, st));
+  CK(launch_gather_head(D, S, s->full, s->blk, s->H, -1, st));
+  CK(head(s, st));
+  CK(launch_prefill_post(D, S, s->st, s->blk, s->H, st));
+  CK(launch_merge_prep(D, S, s->st, s->M->W, st));
+  CK(launch_merge_sync(D, S, s->st, 1, st));
+  CK(launch_copy_pages(D, S, s->st, 1, st));
+  return BB_OK;
+}
+
+static int enqueue_block_step(Session* s, cudaStream_t st) {
+  const Dims& D = s->D;
+  const Sess& S = s->S;
+  CK(cudaMemsetAsync(s->blk.skip, 1, sizeof(int), st));
+  CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
+  CK(launch_block_pack(D, S, s->st, s->blk, s->H, st));
+  CK(launch_copy_pages(D, S, s->st, 0, st));
+  CK(forward(s, s->blk, s->gb, st));
+  CK(head(s, st));
+  CK(launch_step_commit(D, S, s->st, s->blk, s->H, st));
+  CK(launch_merge_prep(D, S, s->st, s->M->W, st));
+  CK(launch_merge_sync(D, S, s->st, 0, st));
+  CK(launch_copy_pages(D, S, s->st, 1, st));
+  return BB_OK;
+}
+
+static int enqueue_refresh(Session* s, cudaStream_t st) {
+  const Dims& D = s->D;
+  const Sess& S = s->S;
+  CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
+  for (int k = 0; k < S.B; ++k) {
+    CK(cudaMemsetAsync(s->full.skip, 1, sizeof(int), st));
+    CK(launch_refresh_pack(D, S, s->st, s->full, s->blk, s->H, k, st));
+    CK(forward(s, s->full, s->gf, st));
+    CK(launch_gather_head(D, S, s->full, s->blk, s->H, k, st));
+  }
+  CK(head(s, st));
+  CK(launch_refresh_end(D, S, s->st, st));
+  return BB_OK;
+}
+
+static int capture(Session* s, bool with_refresh, cudaStream_t st, cudaGraphExec_t* out) {
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_block_step(s, st);
+  if (rc == BB_OK && with_refresh) rc = enqueue_refresh(s, st);
+  cudaError_t e = cudaStreamEndCapture(st, &g);
+  if (rc != BB_OK) return rc;
+  CK(e);
+  CK(cudaGraphInstantiate(out, g, 0));
+  cudaGraphDestroy(g);
+  return BB_OK;
+}
+
+}  // namespace bb
+
+using namespace bb;
+
+extern "C" {
+
+BB_API int bb_version(void) { return 1; }
+
+BB_API int bb_model_create(const bb_model_desc* desc, const bb_weights* w, void** out) {
+  if (!desc || !w || !out) return BB_ERR_CONTRACT;
+  int rc = validate_model(desc);
+  if (rc != BB_OK) return fail(rc, "invalid model desc");
+  Model* m = new Model();
+  m->desc = *desc;
+  m->D = make_dims(desc);
+  m->W.emb = w->emb;
+  m->W.pos = w->pos;
+  m->W.wqkv = w->wqkv;
+  m->W.bqkv = desc->qkv_bias ? w->bqkv : nullptr;
+  m->W.wo = w->wo;
+  m->W.wgu = w->wgu;
+  m->W.wd = w->wd;
+  m->W.ln1 = w->ln1;
+  m->W.ln2 = w->ln2;
+  m->W.lnf = w->lnf;
+  m->W.head = w->head;
+  if (desc->arch == BB_ARCH_LLADA) {
+    const int half = desc->head_dim / 2;
+    std::vector<float> tab((size_t)desc->max_len * half * 2);
+    for (int p = 0; p < desc->max_len; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow((double)desc->rope_theta, -2.0 * i / desc->head_dim);
+        const double a = (double)p * inv;
+        tab[((size_t)p * half + i) * 2] = (float)std::cos(a);
+        tab[((size_t)p * half + i) * 2 + 1] = (float)std::sin(a);
+      }
+    if (cudaMalloc(&m->rope, tab.size() * 4) != cudaSuccess) {
+      delete m;
+      return BB_ERR_CUDA;
+    }
+    cudaMemcpy(m->rope, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
+  }
+  m->W.rope = m->rope;
+  *out = m;
+  return BB_OK;
+}
+
+BB_API int bb_model_destroy(void* model) {
+  Model* m = (Model*)model;
+  if (!m) return BB_OK;
+  if (m->rope) cudaFree(m->rope);
+  delete m;
+  return BB_OK;
+}
+
+static int make_session(Model* M, const bb_session_desc* d, Session* s) {
+  s->M = M;
+  s->desc = *d;
+  s->D = M->D;
+  Sess& S = s->S;
+  memset(&S, 0, sizeof(S));
+  if (d->n_requests < 1 || d->n_branches < 1 || d->n_branches > MAXB) return BB_ERR_CONFIG;
+  if (d->prompt_len < 1 || d->gen_len < 1) return BB_ERR_CONFIG;
+  if (!(d->tau_conf >= 0.f && d->tau_conf <= 1.f) || !(d->tau_merge >= 0.f && d->tau_merge <= 1.f)) return BB_ERR_CONFIG;
+  if (d->tau_sync < 0 || d->refresh_interval < 1) return BB_ERR_CONFIG;
+  S.R = d->n_requests;
+  S.B = d->n_branches;
+  S.P = d->prompt_len;
+  S.G = d->gen_len;
+  S.L = S.P + S.G;
+  if (S.L > M->D.max_len) return BB_ERR_CONTRACT;  // model.py:286-287
+  int off = 0, maxb = 0;
+  for (int k = 0; k < S.B; ++k) {
+    if (d->block_sizes[k] < 1) return BB_ERR_CONFIG;
+    for (int j = 0; j < k; ++j)
+      if (d->block_sizes[j] == d->block_sizes[k]) return BB_ERR_CONFIG;
+    S.bs[k] = d->block_sizes[k];
+    S.off[k] = off;
+    off += S.bs[k];
+    maxb = maxb > S.bs[k] ? maxb : S.bs[k];
+  }
+  S.NRq = off;
+  S.NR = S.R * S.NRq;
+  S.NF = S.R * S.L;
+  S.tau_conf = d->tau_conf;
+  S.tau_merge = d->tau_merge;
+  S.tau_sync = d->tau_sync;
+  S.refresh_interval = d->refresh_interval;
+  S.merge_en = d->merge_enabled;
+  S.sync_en = d->sync_enabled;
+  S.ps = d->page_size > 0 ? d->page_size : 16;
+  if (S.ps > 32) return BB_ERR_CONFIG;
+  S.n_pp = (S.P + S.ps - 1) / S.ps;
+  S.n_gp = (S.G + S.ps - 1) / S.ps;
+  S.n_lp = S.n_pp + S.n_gp;
+  S.pool = S.B * S.n_lp;
+  S.ch_block = d->pages_per_item > 0 ? d->pages_per_item : 4;
+  S.max_items = S.B * ((S.n_lp + S.ch_block - 1) / S.ch_block) + 2 * S.B + 4;
+  S.ev_cap = d->event_capacity > 0 ? d->event_capacity : 32768;
+  S.trace = d->trace;
+  S.hard_cap = 4 * S.G * S.B + 16;  // scheduler.py:310
+  S.max_copies = S.B * (maxb / S.ps + 2);
+  const int NR = S.NR;
+  s->gb.BN = NR <= 64 ? 64 : (NR <= 128 ? 128 : 256);
+  s->gf.BN = S.NF >= 1024 ? 256 : 128;
+  return BB_OK;
+}
+
+BB_API int bb_session_workspace_bytes(const void* model, const bb_session_desc* d, size_t* bytes) {
+  if (!model || !d || !bytes) return BB_ERR_CONTRACT;
+  Session s;
+  int rc = make_session((Model*)model, d, &s);
+  if (rc != BB_OK) return rc;
+  plan(&s, nullptr, true);
+  *bytes = s.ws_bytes;
+  return BB_OK;
+}
+
+BB_API int bb_session_create(void* model, const bb_session_desc* d, void* workspace, size_t bytes, void** out) {
+  if (!model || !d || !workspace || !out) return BB_ERR_CONTRACT;
+  Session* s = new Session();
+  int rc = make_session((Model*)model, d, s);
+  if (rc != BB_OK) {
+    delete s;
+    return rc;
+  }
+  char* base = (char*)(((uintptr_t)workspace + 1023) & ~(uintptr_t)1023);
+  plan(s, nullptr, true);
+  if (s->ws_bytes > bytes) {
+    delete s;
+    return BB_ERR_NOMEM;
+  }
+  plan(s, base, false);
+  s->ws = (char*)workspace;
+  for (int i = 0; i < BB_VIEW_COUNT; ++i)
+    if (s->layout[i][1]) s->layout[i][0] += (long long)(base - (char*)workspace);
+  rc = setup_gemms(s);
+  if (rc != BB_OK) {
+    delete s;
+    return rc;
+  }
+  // static slot defaults (padding rows never change)
+  std::vector<int> neg(std::max(s->blk.rows_alloc, s->full.rows_alloc), -1);
+  std::vector<int> zero(neg.size(), 0);
+  cudaMemcpy(s->blk.slot_pos, neg.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(s->full.slot_pos, neg.data(), s->full.rows_alloc * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(s->H.masked, zero.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
+  if (cudaMallocHost(&s->host_ctrl, 4 * (size_t)s->S.R * C_WORDS * 4) != cudaSuccess) {
+    delete s;
+    return BB_ERR_CUDA;
+  }
+  for (int i = 0; i < 4; ++i) cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming);
+  *out = s;
+  return BB_OK;
+}
+
+BB_API int bb_session_destroy(void* sess) {
+  Session* s = (Session*)sess;
+  if (!s) return BB_OK;
+  if (s->g_iter) cudaGraphExecDestroy(s->g_iter);
+  if (s->g_iter_ref) cudaGraphExecDestroy(s->g_iter_ref);
+  if (s->host_ctrl) cudaFreeHost(s->host_ctrl);
+  for (int i = 0; i < 4; ++i)
+    if (s->ev[i]) cudaEventDestroy(s->ev[i]);
+  delete s;
+  return BB_OK;
+}
+
+BB_API int bb_session_view(const void* sess, int which, long long* offset, long long* bytes) {
+  const Session* s = (const Session*)sess;
+  if (!s || which < 0 || which >= BB_VIEW_COUNT) return BB_ERR_CONTRACT;
+  *offset = s->layout[which][0];
+  *bytes = s->layout[which][1];
+  return BB_OK;
+}
+
+BB_API int bb_session_info(const void* sess, int* out, int n) {
+  const Session* s = (const Session*)sess;
+  if (!s || !out) return BB_ERR_CONTRACT;
+  int v[16] = {s->S.R, s->S.B, s->S.L, s->S.ev_cap, EVW, C_WORDS, B_WORDS, s->S.n_lp, s->S.pool,
+               s->blk.rows_alloc, s->full.rows_alloc, s->gb.BN, s->gf.BN, s->S.max_items, s->S.NRq, s->S.ps};
+  for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
+  return BB_OK;
+}
+
+BB_API int bb_prefill(void* sess, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s) return BB_ERR_CONTRACT;
+  return enqueue_prefill(s, (cudaStream_t)stream);
+}
+
+BB_API int bb_block_step(void* sess, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s) return BB_ERR_CONTRACT;
+  return enqueue_block_step(s, (cudaStream_t)stream);
+}
+
+BB_API int bb_refresh(void* sess, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s) return BB_ERR_CONTRACT;
+  return enqueue_refresh(s, (cudaStream_t)stream);
+}
+
+BB_API int bb_iteration(void* sess, int with_refresh, int use_graph, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s) return BB_ERR_CONTRACT;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!use_graph) {
+    int rc = enqueue_block_step(s, st);
+    if (rc == BB_OK && with_refresh) rc = enqueue_refresh(s, st);
+    return rc;
+  }
+  cudaGraphExec_t* g = with_refresh ? &s->g_iter_ref : &s->g_iter;
+  if (!*g) {
+    int rc = capture(s, with_refresh != 0, st, g);
+    if (rc != BB_OK) return rc;
+  }
+  CK(cudaGraphLaunch(*g, st));
+  return BB_OK;
+}
+
+// Full run_blockbatch loop (scheduler.py:225-394) for every request of the
+// session: prefill, then iterations until all requests finished (status 1) or
+// failed (< 0).  Refresh is enqueued after every refresh_interval-th iteration
+// (the device asserts that it matches its own counter).  Status words are
+// polled asynchronously two iterations behind, so the host never stalls the
+// GPU; the (at most two) extra iterations are device-side no-ops.
+BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out) {
+  Session* s = (Session*)sess;
+  if (!s) return BB_ERR_CONTRACT;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = enqueue_prefill(s, st);
+  if (rc != BB_OK) return rc;
+  const int R = s->S.R;
+  const size_t cb = (size_t)R * C_WORDS * 4;
+  CK(cudaMemcpyAsync(s->host_ctrl, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(s->ev[0], st));
+  int it = 0;
+  bool finished = false;
+  const int lag = 2;
+  int checked = -1;
+  while (!finished && it < max_iterations) {
+    // check the status copied `lag` iterations ago
+    const int chk = it - lag;
+    if (chk >= 0 && chk > checked) {
+      CK(cudaEventSynchronize(s->ev[chk & 3]));
+      checked = chk;
+      const int32_t* c = s->host_ctrl + (size_t)(chk & 3) * R * C_WORDS;
+      finished = true;
+      for (int r = 0; r < R; ++r) finished &= c[r * C_WORDS + C_STATUS] != 0;
+      if (finished) break;
+    }
+    ++it;
+    rc = bb_iteration(s, it % s->S.refresh_interval == 0, use_graph, st);
+    if (rc != BB_OK) return rc;
+    CK(cudaMemcpyAsync(s->host_ctrl + (size_t)(it & 3) * R * C_WORDS, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s->ev[it & 3], st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (iterations_out) *iterations_out = it;
+  return BB_OK;
+}
+
+// host snapshot of the per-request control words (synchronous)
+BB_API int bb_session_ctrl(void* sess, int* host_out, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !host_out) return BB_ERR_CONTRACT;
+  CK(cudaMemcpyAsync(host_out, s->st.ctrl, (size_t)s->S.R * C_WORDS * 4, cudaMemcpyDeviceToHost,
+                     (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return BB_OK;
+}
+
+}  // extern "C"

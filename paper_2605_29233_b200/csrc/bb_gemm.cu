@@ -1,0 +1,403 @@
+// tcgen05 / TMEM / TMA weight-streaming GEMM (bf16 in, fp32 accumulate) and
+// the fp32 SIMT GEMM used by fp32 verification mode.
+//
+// CTA layout (192 threads, 1 CTA per SM):
+//   warp 0  lane 0 : TMA producer  (W tile 128x64 + X tile BNx64 per k-block)
+//   warp 1  lane 0 : MMA issuer    (4 x tcgen05.mma M128 N=BN K16 per k-block)
+//   warps 2-5      : epilogue      (tcgen05.ld TMEM -> regs -> global)
+// Two TMEM accumulators (2*BN columns) so the epilogue of one stream-K unit
+// overlaps the MMAs of the next.
+#include <cudaTypedefs.h>
+#include <stdio.h>
+
+#include "bb_common.cuh"
+#include "bb_gemm.cuh"
+
+namespace bb {
+
+struct Unit {
+  int tile, kb0, kb1, slot;
+};
+
+struct UnitIter {
+  long long x, end, T;
+  int KB, G, c, mode, n_tiles;
+  __device__ UnitIter(int c_, int G_, int KB_, int n_tiles_, int mode_)
+      : c(c_), G(G_), KB(KB_), n_tiles(n_tiles_), mode(mode_) {
+    T = (long long)n_tiles * KB;
+    if (mode == 0) {
+      x = (long long)c * T / G;
+      end = (long long)(c + 1) * T / G;
+    } else {
+      x = c;
+      end = n_tiles;
+    }
+  }
+  __device__ bool next(Unit& u) {
+    if (x >= end) return false;
+    if (mode != 0) {
+      u.tile = (int)x;
+      u.kb0 = 0;
+      u.kb1 = KB;
+      u.slot = 0;
+      x += G;
+      return true;
+    }
+    const int tile = (int)(x / KB);
+    const int kb0 = (int)(x % KB);
+    const long long rem = end - x;
+    const int kb1 = (int)((long long)kb0 + rem < KB ? kb0 + rem : KB);
+    u.tile = tile;
+    u.kb0 = kb0;
+    u.kb1 = kb1;
+    u.slot = c - sk_owner((long long)tile * KB, T, G);
+    x += kb1 - kb0;
+    return true;
+  }
+};
+
+template <int BN>
+struct TcCfg {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16 +
+                                 (size_t)3 * 4 * BN * 4;
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const GemmTcParams p) {
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* red = reinterpret_cast<float*>(tslot + 4);  // [3][4][BN]
+
+  if (p.skip != nullptr && *p.skip != 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows_valid = p.rows_valid != nullptr ? *p.rows_valid : p.rows_alloc;
+  const int n_tiles = p.n_ntiles * p.n_chunks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tslot, C::TCOLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+      Unit u;
+      while (it.next(u)) {
+        const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
+        if (chunk * BN >= rows_valid) continue;
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * 64, ntile * 128, pol_w);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * 64, chunk * BN, pol_x);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+      Unit u;
+      while (it.next(u)) {
+        const int chunk = u.tile % p.n_chunks;
+        if (chunk * BN >= rows_valid) continue;
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tbase + (uint32_t)(acc * BN);
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc_mma_bf16(dt, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), IDESC,
+                        (kb > u.kb0 || k > 0) ? 1u : 0u);
+          tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quadrant owned by this warp
+    const int et = threadIdx.x - 64;
+    int acc = 0;
+    uint32_t aphase = 0;
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+    Unit u;
+    while (it.next(u)) {
+      const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
+      if (chunk * BN >= rows_valid) continue;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int n = ntile * 128 + q * 32 + lane;
+      const int row0 = chunk * BN;
+      const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      if (p.mode == 0) {
+        float* dst = p.part + (long long)u.slot * p.plane + n;
+#pragma unroll 1
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + j0, v);
+          if (n < p.n_out) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int row = row0 + j0 + j;
+              if (row < rows_valid) dst[(long long)row * p.ldp] = v[j];
+            }
+          }
+        }
+      } else {
+        const float hs = p.head_scale, sc = p.spike_cut, sg = p.spike_gain;
+#pragma unroll 1
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + j0, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int row = row0 + j0 + j;
+            float l = -INFINITY;
+            if (n < p.n_out && row < p.rows_alloc) {
+              const float raw = v[j] * hs;
+              l = raw + sg * fmaxf(0.0f, raw - sc);
+              if (n == __ldg(&p.tgt[row])) l += __ldg(&p.boost[row]);
+            }
+            float m = l;
+            int a = n;
+            warp_argmax(m, a);
+            const float e = (m == -INFINITY) ? 0.0f : expf(l - m);
+            const float s = warp_sum(e);
+            if (lane == 0) {
+              red[(0 * 4 + q) * BN + j0 + j] = m;
+              red[(1 * 4 + q) * BN + j0 + j] = __int_as_float(a);
+              red[(2 * 4 + q) * BN + j0 + j] = s;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        epi_bar();
+        for (int r = et; r < BN; r += 128) {
+          const int row = row0 + r;
+          float m = red[r];
+          int a = __float_as_int(red[4 * BN + r]);
+          for (int qq = 1; qq < 4; ++qq) {
+            const float mq = red[qq * BN + r];
+            if (mq > m) {
+              m = mq;
+              a = __float_as_int(red[(4 + qq) * BN + r]);
+            }
+          }
+          float s = 0.0f;
+          if (m != -INFINITY)
+            for (int qq = 0; qq < 4; ++qq) {
+              const float mq = red[qq * BN + r];
+              if (mq != -INFINITY) s += red[(8 + qq) * BN + r] * expf(mq - m);
+            }
+          if (row < rows_valid) p.head_part[(long long)row * p.n_ntiles + ntile] = make_float4(m, __int_as_float(a), s, 0.0f);
+        }
+        epi_bar();
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+        continue;
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, C::TCOLS);
+  }
+}
+
+// ------------------------------------------------------------------ host
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static bool get_encode() {
+  if (g_encode) return true;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || fn == nullptr)
+    return false;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return true;
+}
+
+static bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+  if (!get_encode()) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN, int mode,
+                   int max_grid) {
+  if (BN != 64 && BN != 128 && BN != 256) return false;
+  if (K % 8 != 0) return false;  // 16-byte row stride for TMA
+  memset(&g, 0, sizeof(g));
+  g.BN = BN;
+  if (!make_tmap(&g.tmA, W, (uint64_t)K, (uint64_t)n_out, 128)) return false;
+  if (!make_tmap(&g.tmB, X, (uint64_t)K, (uint64_t)rows_alloc, (uint32_t)BN)) return false;
+  GemmTcParams& p = g.p;
+  p.n_out = n_out;
+  p.K = K;
+  p.n_ntiles = (n_out + 127) / 128;
+  p.n_chunks = (rows_alloc + BN - 1) / BN;
+  p.KB = (K + 63) / 64;
+  p.mode = mode;
+  p.rows_alloc = rows_alloc;
+  p.ldp = n_out;
+  p.plane = (long long)rows_alloc * n_out;
+  const long long n_tiles = (long long)p.n_ntiles * p.n_chunks;
+  const long long T = n_tiles * p.KB;
+  const int gmax = max_grid > 0 ? max_grid : kNumSMs;
+  g.grid = mode == 0 ? (int)(T < gmax ? T : gmax) : (int)(n_tiles < gmax ? n_tiles : gmax);
+  g.sk.T = mode == 0 ? T : 0;
+  g.sk.KB = p.KB;
+  g.sk.G = g.grid;
+  g.sk.n_chunks = p.n_chunks;
+  g.sk.BN = BN;
+  g.max_slots = 1;
+  if (mode == 0)
+    for (long long t = 0; t < n_tiles; ++t) {
+      const int ns = sk_owner(t * p.KB + p.KB - 1, T, g.grid) - sk_owner(t * p.KB, T, g.grid) + 1;
+      if (ns > g.max_slots) g.max_slots = ns;
+    }
+  g.smem = BN == 64 ? TcCfg<64>::SMEM : (BN == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM);
+  return true;
+}
+
+template <int BN>
+static cudaError_t launch_bn(const TcGemm& g, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)TcCfg<BN>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_gemm_tc<BN><<<g.grid, 192, TcCfg<BN>::SMEM, s>>>(g.tmA, g.tmB, g.p);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s) {
+  switch (g.BN) {
+    case 64: return launch_bn<64>(g, s);
+    case 128: return launch_bn<128>(g, s);
+    case 256: return launch_bn<256>(g, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ SIMT fp32
+// out[row][n] = sum_k X[row][k] * W[n][k]; 64x64 tile, 256 threads, 4x4 per thread.
+__global__ void __launch_bounds__(256) k_gemm_simt(SimtGemm g) {
+  if (g.skip != nullptr && *g.skip != 0) return;
+  const int rows = g.rows_valid != nullptr ? *g.rows_valid : g.rows_alloc;
+  const int r0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  if (r0 >= rows) return;
+  __shared__ float sX[16][64 + 4];
+  __shared__ float sW[16][64 + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < g.K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int rr = i / 16, kk = i % 16;
+      const int row = r0 + rr, n = n0 + rr, k = k0 + kk;
+      sX[kk][rr] = (row < rows && k < g.K) ? g.X[(long long)row * g.K + k] : 0.0f;
+      sW[kk][rr] = (n < g.n_out && k < g.K) ? g.W[(long long)n * g.K + k] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = sX[kk][ty * 4 + i];
+        b[i] = sW[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = r0 + ty * 4 + i;
+    if (row >= rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n < g.n_out) g.out[(long long)row * g.ldo + n] = acc[i][j];
+    }
+  }
+}
+
+cudaError_t simt_gemm_launch(const SimtGemm& g, cudaStream_t s) {
+  dim3 grid((g.n_out + 63) / 64, (g.rows_alloc + 63) / 64);
+  k_gemm_simt<<<grid, 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
+
+}  // namespace bb

@@ -1,0 +1,89 @@
+// GEMM interfaces shared by the launchers and the fused post-GEMM kernels.
+//
+// All projections are "weights-stationary, activations-streaming" TN GEMMs:
+//   out[row][n] = sum_k X[row][k] * W[n][k]      (W: [n_out][K], X: [rows][K], both K-major)
+// computed as D^T = W . X^T on tcgen05 (M = 128 weight rows per tile, N = BN
+// activation rows), so a decode step with only ~56 window rows still issues
+// full M=128 MMAs and every weight byte is read from HBM exactly once.
+//
+// Work is split stream-K over (tile, k-block): CTA c owns k-blocks
+// [c*T/G, (c+1)*T/G) of the flattened (tile-major) space and writes one fp32
+// partial "plane" per tile piece.  The consumer kernel (post-QKV / post-O /
+// ...) sums the pieces of a tile in slot order, so the reduction is
+// deterministic and no fp32 atomics are used.
+#pragma once
+#include <cuda.h>
+#include <stdint.h>
+
+namespace bb {
+
+struct SplitK {
+  long long T;   // total k-blocks (= n_tiles * KB); 0 => single slot (SIMT path)
+  int KB;        // k-blocks per tile
+  int G;         // CTAs
+  int n_chunks;  // row chunks per weight tile
+  int BN;        // rows per chunk
+};
+
+// owner CTA of flattened k-block y (largest c with floor(c*T/G) <= y)
+__host__ __device__ inline int sk_owner(long long y, long long T, int G) {
+  return (int)(((y + 1) * (long long)G - 1) / T);
+}
+__host__ __device__ inline int sk_nslots(const SplitK& s, int row, int n) {
+  if (s.T == 0) return 1;
+  const long long tile = (long long)(n >> 7) * s.n_chunks + row / s.BN;
+  const long long first = tile * s.KB, last = first + s.KB - 1;
+  return sk_owner(last, s.T, s.G) - sk_owner(first, s.T, s.G) + 1;
+}
+
+// Sum of the partial planes for output element (row, n).
+__device__ __forceinline__ float part_sum(const float* __restrict__ part, long long plane, int ldp,
+                                          const SplitK& s, int row, int n) {
+  const int ns = sk_nslots(s, row, n);
+  const float* p = part + (long long)row * ldp + n;
+  float acc = p[0];
+  for (int i = 1; i < ns; ++i) acc += p[(long long)i * plane];
+  return acc;
+}
+
+struct GemmTcParams {
+  int n_out, K, n_ntiles, n_chunks, KB, mode;  // mode 0: partial planes, 1: LM-head epilogue
+  int rows_alloc;
+  const int* rows_valid;  // device scalar or nullptr
+  const int* skip;        // device scalar or nullptr: nonzero => no-op
+  // mode 0
+  float* part;
+  long long plane;
+  int ldp;
+  // mode 1
+  float4* head_part;  // [rows_alloc][n_ntiles] = (max, argmax bits, sumexp, 0)
+  const float* boost;
+  const int* tgt;
+  float head_scale, spike_cut, spike_gain;
+};
+
+struct TcGemm {
+  CUtensorMap tmA, tmB;
+  GemmTcParams p;
+  SplitK sk;
+  int BN, grid, max_slots;
+  size_t smem;
+};
+
+// host API (bb_gemm.cu)
+bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN,
+                   int mode, int max_grid);
+cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s);
+
+struct SimtGemm {
+  const float* W;
+  const float* X;
+  int n_out, K, rows_alloc;
+  const int* rows_valid;
+  const int* skip;
+  float* out;
+  int ldo;
+};
+cudaError_t simt_gemm_launch(const SimtGemm& g, cudaStream_t s);
+
+}  // namespace bb

@@ -1,0 +1,318 @@
+// Per-layer fused kernels of the denoiser forward (model.py:278-319 semantics,
+// generalised to the LLaDA/Dream shape):
+//   embed            h = emb[tok] (+ pos[p]);  xn = RMSNorm(h) (arch 1) | h
+//   post_qkv         sum GEMM partial planes + bias, RoPE (arch 1), write q and
+//                    the window rows' K/V into the branch's KV pages (splice)
+//   post_residual    h += sum(partials);  xn = RMSNorm(h)*g | h   (next GEMM input)
+//   post_gu          act = silu(gate) * up   (SwiGLU)
+//   gather_head      full pass -> head slots (window rows only)
+//   head_tiles_f32   fp32 mode: per-128-column (max, argmax, sumexp) from logits
+//   head_reduce      combine column tiles -> conf = max prob, argmax, m, s and
+//                    update the branch's probability map (h, m, s, boost)
+#include "bb_common.cuh"
+#include "bb_layers.cuh"
+
+namespace bb {
+
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.0f;
+  if (w == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) sh[0] = t;
+  __syncthreads();
+  return sh[0];
+}
+
+// ------------------------------------------------------------------ embed
+template <typename T>
+__global__ void __launch_bounds__(256) k_embed(Dims D, Pass P, const T* __restrict__ emb,
+                                               const T* __restrict__ pos_emb, const float* __restrict__ ln) {
+  if (*P.skip) return;
+  __shared__ float sh[32];
+  const int row = blockIdx.x;
+  int pos = P.slot_pos[row], tok = P.slot_tok[row];
+  if (pos < 0) {
+    pos = 0;
+    tok = 0;
+  }
+  float* x = P.x + (long long)row * D.d;
+  T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
+  float ss = 0.0f;
+  for (int c = threadIdx.x; c < D.d; c += blockDim.x) {
+    float v = ldf(emb + (long long)tok * D.d + c);
+    if (D.arch == 0) v += ldf(pos_emb + (long long)pos * D.d + c);
+    x[c] = v;
+    ss += v * v;
+  }
+  float inv = 1.0f;
+  if (ln != nullptr) inv = 1.0f / sqrtf(block_sum(ss, sh) / (float)D.d + D.eps);
+  for (int c = threadIdx.x; c < D.d; c += blockDim.x)
+    stf(xn + c, ln != nullptr ? x[c] * inv * ln[c] : x[c]);
+}
+
+// ------------------------------------------------------------------ post QKV
+template <typename T>
+__global__ void __launch_bounds__(256) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
+                                                  const float* __restrict__ rope, int layer, PartRef pr) {
+  if (*P.skip) return;
+  extern __shared__ float vals[];  // [qkv_out]
+  const int row = blockIdx.x;
+  const int pos = P.slot_pos[row];
+  if (pos < 0) return;
+  for (int c = threadIdx.x; c < D.qkv_out; c += blockDim.x) {
+    float v = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c);
+    if (bias != nullptr) v += bias[c];
+    vals[c] = v;
+  }
+  __syncthreads();
+  const int r = P.slot_req[row], b = P.slot_br[row];
+  const int lp = lp_of(S, pos);
+  const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + b) * S.n_lp + lp];
+  const int off = pos - lp_start(S, lp);
+  const int half = D.hd >> 1;
+  const int nqk = D.nh + D.nkv;  // heads that get RoPE
+  T* q = reinterpret_cast<T*>(P.q) + (long long)row * D.attn_dim;
+  T* kk = reinterpret_cast<T*>(st.kv_k);
+  T* vv = reinterpret_cast<T*>(st.kv_v);
+  const long long lay = (long long)layer * S.R * S.pool;
+  // q and k heads: pairs (i, i + hd/2)
+  for (int t = threadIdx.x; t < nqk * half; t += blockDim.x) {
+    const int hh = t / half, i = t % half;
+    float a = vals[hh * D.hd + i], c2 = vals[hh * D.hd + i + half];
+    if (D.arch == 1) {
+      const float cs = rope[((long long)pos * half + i) * 2], sn = rope[((long long)pos * half + i) * 2 + 1];
+      const float a2 = a * cs - c2 * sn, b2 = c2 * cs + a * sn;
+      a = a2;
+      c2 = b2;
+    }
+    if (hh < D.nh) {
+      stf(q + hh * D.hd + i, a);
+      stf(q + hh * D.hd + i + half, c2);
+    } else {
+      const int kvh = hh - D.nh;
+      T* dst = kk + (((lay + gpage) * D.nkv + kvh) * S.ps + off) * D.hd;
+      stf(dst + i, a);
+      stf(dst + i + half, c2);
+    }
+  }
+  for (int c = threadIdx.x; c < D.kv_dim; c += blockDim.x) {
+    const int kvh = c / D.hd, i = c % D.hd;
+    T* dst = vv + (((lay + gpage) * D.nkv + kvh) * S.ps + off) * D.hd;
+    stf(dst + i, vals[(D.nh + D.nkv) * D.hd + c]);
+  }
+}
+
+// ------------------------------------------------------------------ residual (+ norm)
+template <typename T>
+__global__ void __launch_bounds__(256) k_post_residual(Dims D, Pass P, PartRef pr, const float* __restrict__ ln) {
+  if (*P.skip) return;
+  __shared__ float sh[32];
+  const int row = blockIdx.x;
+  if (P.slot_pos[row] < 0) return;
+  float* x = P.x + (long long)row * D.d;
+  T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
+  float ss = 0.0f;
+  for (int c = threadIdx.x; c < D.d; c += blockDim.x) {
+    const float v = x[c] + part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c);
+    x[c] = v;
+    ss += v * v;
+  }
+  float inv = 1.0f;
+  if (ln != nullptr) inv = 1.0f / sqrtf(block_sum(ss, sh) / (float)D.d + D.eps);
+  __syncthreads();
+  for (int c = threadIdx.x; c < D.d; c += blockDim.x)
+    stf(xn + c, ln != nullptr ? x[c] * inv * ln[c] : x[c]);
+}
+
+// ------------------------------------------------------------------ SwiGLU
+template <typename T>
+__global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
+  if (*P.skip) return;
+  const int row = blockIdx.y;
+  if (P.slot_pos[row] < 0) return;
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= D.dff) return;
+  const int cg = ((f >> 6) << 7) + (f & 63);
+  const float g = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, cg);
+  const float u = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, cg + 64);
+  stf(reinterpret_cast<T*>(P.act) + (long long)row * D.dff + f, g / (1.0f + expf(-g)) * u);
+}
+
+// ------------------------------------------------------------------ head side
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather_head(Dims D, Sess S, Pass full, Pass blk, Head H, int filter) {
+  if (*full.skip) return;
+  const int slot = blockIdx.x;
+  if (!H.masked[slot]) return;
+  if (filter >= 0 && blk.slot_br[slot] != filter) return;
+  const long long src = (long long)blk.slot_req[slot] * S.L + blk.slot_pos[slot];
+  const T* a = reinterpret_cast<const T*>(full.xn) + src * D.d;
+  T* o = reinterpret_cast<T*>(blk.xn) + (long long)slot * D.d;
+  for (int c = threadIdx.x; c < D.d; c += blockDim.x) o[c] = a[c];
+}
+
+__global__ void __launch_bounds__(128) k_head_tiles_f32(Dims D, Head H) {
+  if (*H.skip) return;
+  const int row = blockIdx.y, vt = blockIdx.x;
+  if (!H.masked[row]) return;
+  __shared__ float sm[4], ss[4];
+  __shared__ int sa[4];
+  const int n = vt * 128 + threadIdx.x;
+  float l = -INFINITY;
+  if (n < D.n_out) {
+    const float raw = H.logits[(long long)row * D.n_out + n] * D.head_scale;
+    l = raw + D.spike_gain * fmaxf(0.0f, raw - D.spike_cut);
+    if (n == H.tgt[row]) l += H.boost[row];
+  }
+  float m = l;
+  int a = n;
+  warp_argmax(m, a);
+  const float e = (m == -INFINITY) ? 0.0f : expf(l - m);
+  const float s = warp_sum(e);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sm[w] = m;
+    sa[w] = a;
+    ss[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = sm[0];
+    int A = sa[0];
+    for (int q = 1; q < 4; ++q)
+      if (sm[q] > M) {
+        M = sm[q];
+        A = sa[q];
+      }
+    float S2 = 0.0f;
+    if (M != -INFINITY)
+      for (int q = 0; q < 4; ++q)
+        if (sm[q] != -INFINITY) S2 += ss[q] * expf(sm[q] - M);
+    H.hpart[(long long)row * D.n_vtiles + vt] = make_float4(M, __int_as_float(A), S2, 0.0f);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, Head H, DevState st) {
+  if (*H.skip) return;
+  __shared__ float shm[256];
+  __shared__ int sht[256];
+  __shared__ float sh[32];
+  const int slot = blockIdx.x;
+  if (!H.masked[slot]) return;
+  const float4* hp = H.hpart + (long long)slot * D.n_vtiles;
+  float m = -INFINITY;
+  int t0 = 0x7fffffff;
+  for (int t = threadIdx.x; t < D.n_vtiles; t += blockDim.x) {
+    const float mt = hp[t].x;
+    if (mt > m) {
+      m = mt;
+      t0 = t;
+    }
+  }
+  shm[threadIdx.x] = m;
+  sht[threadIdx.x] = t0;
+  __syncthreads();
+  for (int o = blockDim.x >> 1; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const float m2 = shm[threadIdx.x + o];
+      const int t2 = sht[threadIdx.x + o];
+      if (m2 > shm[threadIdx.x] || (m2 == shm[threadIdx.x] && t2 < sht[threadIdx.x])) {
+        shm[threadIdx.x] = m2;
+        sht[threadIdx.x] = t2;
+      }
+    }
+    __syncthreads();
+  }
+  const float M = shm[0];
+  const int tb = sht[0];
+  float s = 0.0f;
+  for (int t = threadIdx.x; t < D.n_vtiles; t += blockDim.x) {
+    const float4 v = hp[t];
+    if (v.x != -INFINITY) s += v.z * expf(v.x - M);
+  }
+  const float Ssum = block_sum(s, sh);
+  const int r = blk.slot_req[slot], b = blk.slot_br[slot], pos = blk.slot_pos[slot];
+  const long long pm = ((long long)r * S.B + b) * S.L + pos;
+  if (threadIdx.x == 0) {
+    H.res_m[slot] = M;
+    H.res_s[slot] = Ssum;
+    H.res_conf[slot] = 1.0f / Ssum;
+    H.res_arg[slot] = __float_as_int(hp[tb].y);
+    st.pm_m[pm] = M;
+    st.pm_s[pm] = Ssum;
+    st.pm_boost[pm] = H.boost[slot];
+    st.covered[pm] = 1;
+  }
+  const T* src = reinterpret_cast<const T*>(blk.xn) + (long long)slot * D.d;
+  T* dst = reinterpret_cast<T*>(st.pm_h) + pm * D.d;
+  for (int c = threadIdx.x; c < D.d; c += blockDim.x) dst[c] = src[c];
+}
+
+// ------------------------------------------------------------------ launchers
+#define BB_DISPATCH(D, ...)                                  \
+  do {                                                       \
+    if ((D).dtype == 1) {                                    \
+      using T = __nv_bfloat16;                               \
+      __VA_ARGS__;                                           \
+    } else {                                                 \
+      using T = float;                                       \
+      __VA_ARGS__;                                           \
+    }                                                        \
+  } while (0)
+
+cudaError_t launch_embed(const Dims& D, const Sess& S, const Pass& P, const Weights& W, cudaStream_t s) {
+  BB_DISPATCH(D, (k_embed<T><<<P.rows_alloc, 256, 0, s>>>(D, P, (const T*)W.emb, (const T*)W.pos,
+                                                           D.arch == 1 ? W.ln1 : nullptr)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const Weights& W,
+                            int layer, const PartRef& pr, cudaStream_t s) {
+  const float* bias = W.bqkv != nullptr ? W.bqkv + (long long)layer * D.qkv_out : nullptr;
+  const size_t smem = (size_t)D.qkv_out * sizeof(float);
+  BB_DISPATCH(D, {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_post_qkv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    k_post_qkv<T><<<P.rows_alloc, 256, smem, s>>>(D, S, P, st, bias, W.rope, layer, pr);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s) {
+  BB_DISPATCH(D, (k_post_residual<T><<<P.rows_alloc, 256, 0, s>>>(D, P, pr, ln)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s) {
+  dim3 grid((D.dff + 255) / 256, P.rows_alloc);
+  BB_DISPATCH(D, (k_post_gu<T><<<grid, 256, 0, s>>>(D, P, pr)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_head(const Dims& D, const Sess& S, const Pass& full, const Pass& blk, const Head& H,
+                               int branch_filter, cudaStream_t s) {
+  BB_DISPATCH(D, (k_gather_head<T><<<blk.rows_alloc, 256, 0, s>>>(D, S, full, blk, H, branch_filter)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_head_tiles_f32(const Dims& D, const Pass& blk, const Head& H, cudaStream_t s) {
+  dim3 grid(D.n_vtiles, blk.rows_alloc);
+  k_head_tiles_f32<<<grid, 128, 0, s>>>(D, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_head_reduce(const Dims& D, const Sess& S, const Pass& blk, const Head& H, const DevState& st,
+                               cudaStream_t s) {
+  BB_DISPATCH(D, (k_head_reduce<T><<<blk.rows_alloc, 256, 0, s>>>(D, S, blk, H, st)));
+  return cudaGetLastError();
+}
+
+}  // namespace bb

@@ -1,0 +1,68 @@
+// Host-visible launch interfaces of the per-layer kernels (bb_layers.cu),
+// attention (bb_attn.cu) and control kernels (bb_control.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "bb_gemm.cuh"
+#include "bb_state.cuh"
+
+namespace bb {
+
+struct Weights {
+  const void* emb;    // [n_ext][d] T
+  const void* pos;    // [max_len][d] T (arch 0)
+  const void* wqkv;   // [layers][qkv_out][d] T
+  const float* bqkv;  // [layers][qkv_out] or null
+  const void* wo;     // [layers][d][attn_dim] T
+  const void* wgu;    // [layers][2*dff][d] T, gate/up interleaved in 64-row blocks
+  const void* wd;     // [layers][d][dff] T
+  const float* ln1;   // [layers][d] (arch 1)
+  const float* ln2;   // [layers][d]
+  const float* lnf;   // [d]
+  const void* head;   // [n_out][d] T
+  const float* rope;  // [max_len][hd/2][2] (cos, sin), arch 1
+};
+
+struct PartRef {      // where a GEMM left its fp32 partial planes
+  const float* part;
+  long long plane;
+  int ldp;
+  SplitK sk;
+};
+
+// ---- per-layer kernels (templated on storage type inside) ----
+cudaError_t launch_embed(const Dims& D, const Sess& S, const Pass& P, const Weights& W, cudaStream_t st);
+cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const Weights& W,
+                            int layer, const PartRef& pr, cudaStream_t s);
+cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s);
+cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s);
+cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, cudaStream_t s);
+cudaError_t launch_gather_head(const Dims& D, const Sess& S, const Pass& full, const Pass& blk, const Head& H,
+                               int branch_filter, cudaStream_t s);
+cudaError_t launch_head_tiles_f32(const Dims& D, const Pass& blk, const Head& H, cudaStream_t s);
+cudaError_t launch_head_reduce(const Dims& D, const Sess& S, const Pass& blk, const Head& H, const DevState& st,
+                               cudaStream_t s);
+
+// ---- control kernels ----
+cudaError_t launch_prefill_init(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
+                                const Head& H, cudaStream_t s);
+cudaError_t launch_prefill_post(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                                cudaStream_t s);
+cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                              cudaStream_t s);
+cudaError_t launch_copy_pages(const Dims& D, const Sess& S, const DevState& st, int with_pm, cudaStream_t s);
+cudaError_t launch_step_commit(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                               cudaStream_t s);
+cudaError_t launch_merge_prep(const Dims& D, const Sess& S, const DevState& st, const Weights& W, cudaStream_t s);
+cudaError_t launch_merge_sync(const Dims& D, const Sess& S, const DevState& st, int after_prefill, cudaStream_t s);
+cudaError_t launch_refresh_begin(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                                 cudaStream_t s);
+cudaError_t launch_refresh_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
+                                const Head& H, int branch, cudaStream_t s);
+cudaError_t launch_refresh_end(const Dims& D, const Sess& S, const DevState& st, cudaStream_t s);
+cudaError_t launch_debug_commit(const float* probs, int n, int n_out, const int* pos, int* row, float tau, int* out,
+                                int* count, cudaStream_t s);
+cudaError_t launch_debug_merge(const Dims& D, const Sess& S, const DevState& st, const float* probmaps, int n_out,
+                               cudaStream_t s);
+
+}  // namespace bb

@@ -1,0 +1,192 @@
+"""Device sessions: one workspace per (model, scheduler config, request count).
+
+A session owns a single caller-allocated device workspace (a torch uint8
+tensor — torch is only the allocator here) carved by the C library into the
+device state of R requests x B branches (rows, branch windows, paged KV,
+probability maps, trace ring) and the two forward passes.  ``run`` uploads
+prompts/targets, calls ``bb_run`` (prefill + the captured per-iteration
+CUDA graph until every request finished) and decodes the results.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, ContractError, RunawayError, StateError
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class Session:
+    def __init__(self, params, cfg, prompt_len: int, n_requests: int = 1, trace: bool = True,
+                 page_size: int = 16, pages_per_item: int = 4, event_capacity: int | None = None):
+        torch = _torch()
+        self.params = params
+        self.cfg = cfg
+        self.P, self.G, self.R = prompt_len, cfg.gen_len, n_requests
+        self.B = len(cfg.block_sizes)
+        if self.B > _lib.MAXB:
+            raise ConfigError(f"at most {_lib.MAXB} block sizes per request")
+        L = _lib.lib()
+        bs = (C.c_int * 8)(*(list(cfg.block_sizes) + [0] * (8 - self.B)))
+        if event_capacity is None:
+            event_capacity = 64 + 24 * (self.G + 4) * self.B
+        self.desc = _lib.SessionDesc(
+            n_requests=n_requests, n_branches=self.B, block_sizes=bs, prompt_len=prompt_len, gen_len=cfg.gen_len,
+            tau_conf=cfg.tau_conf, tau_merge=cfg.tau_merge, tau_sync=float(cfg.tau_sync),
+            refresh_interval=cfg.refresh_interval, merge_enabled=int(cfg.merge_enabled),
+            sync_enabled=int(cfg.sync_enabled), page_size=page_size, pages_per_item=pages_per_item,
+            trace=int(trace), event_capacity=event_capacity)
+        nbytes = C.c_size_t(0)
+        model = params.handle()
+        _lib.check(L.bb_session_workspace_bytes(model, C.byref(self.desc), C.byref(nbytes)),
+                   "bb_session_workspace_bytes")
+        self.ws = torch.zeros(nbytes.value + 2048, dtype=torch.uint8, device="cuda")
+        h = C.c_void_p()
+        _lib.check(L.bb_session_create(model, C.byref(self.desc), C.c_void_p(self.ws.data_ptr()),
+                                       self.ws.numel(), C.byref(h)), "bb_session_create")
+        self.h = h
+        info = (C.c_int * 16)()
+        L.bb_session_info(h, info, 16)
+        self.info = list(info)
+        self.Lseq = self.info[2]
+        self.ev_cap = self.info[3]
+        self.stream = torch.cuda.Stream()
+        self.v_tokens = self._view(_lib.VIEW_TOKENS, torch.int32, (self.R, self.B, self.Lseq))
+        self.v_target = self._view(_lib.VIEW_TARGET, torch.int32, (self.R, self.G))
+        self.v_prompt = self._view(_lib.VIEW_PROMPT, torch.int32, (self.R, self.P))
+        self.v_ctrl = self._view(_lib.VIEW_CTRL, torch.int32, (self.R, _lib.C_WORDS))
+        self.v_branch = self._view(_lib.VIEW_BRANCH, torch.int32, (self.R, self.B, _lib.B_WORDS))
+        self.v_events = self._view(_lib.VIEW_EVENTS, torch.int32, (self.R, self.ev_cap, _lib.EVW))
+        self.v_pages = self._view(_lib.VIEW_PAGES, torch.int32, (self.R, self.B, self.info[7]))
+        self.v_refc = self._view(_lib.VIEW_REFC, torch.int32, (self.R, self.info[8]))
+        self.h2d_bytes = self.d2h_bytes = 0
+
+    def _view(self, which, dtype, shape):
+        off, nb = C.c_longlong(0), C.c_longlong(0)
+        _lib.check(_lib.lib().bb_session_view(self.h, which, C.byref(off), C.byref(nb)), "bb_session_view")
+        n = int(np.prod(shape))
+        return self.ws[off.value:off.value + nb.value].view(dtype)[:n].view(*shape)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) is not None and _lib._lib is not None:
+                _lib._lib.bb_session_destroy(self.h)
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- inputs
+    def set_inputs(self, prompts, targets):
+        """prompts [R, P], targets [R, G]: host arrays (copied H2D on the session
+        stream) or CUDA tensors (copied D2D)."""
+        torch = _torch()
+        with torch.cuda.stream(self.stream):
+            for dst, src in ((self.v_prompt, prompts), (self.v_target, targets)):
+                if isinstance(src, torch.Tensor) and src.is_cuda:
+                    dst.copy_(src.to(torch.int32), non_blocking=True)
+                else:
+                    t = torch.from_numpy(np.ascontiguousarray(np.asarray(src), dtype=np.int32)).pin_memory()
+                    dst.copy_(t, non_blocking=True)
+                    self.h2d_bytes += t.numel() * 4
+
+    def max_iterations(self) -> int:
+        hard_cap = 4 * self.G * self.B + 16
+        return 10 * hard_cap + 4
+
+    def launch(self, use_graph: bool = True) -> int:
+        """Enqueue the whole run (bb_run) on the session stream; returns #iterations."""
+        it = C.c_int(0)
+        _lib.check(_lib.lib().bb_run(self.h, self.max_iterations(), int(use_graph),
+                                     C.c_void_p(self.stream.cuda_stream), C.byref(it)), "bb_run")
+        return it.value
+
+    def prefill(self):
+        _lib.check(_lib.lib().bb_prefill(self.h, C.c_void_p(self.stream.cuda_stream)), "bb_prefill")
+
+    def iteration(self, with_refresh: bool, use_graph: bool = True):
+        _lib.check(_lib.lib().bb_iteration(self.h, int(with_refresh), int(use_graph),
+                                           C.c_void_p(self.stream.cuda_stream)), "bb_iteration")
+
+    # ---------------------------------------------------------------- results
+    def fetch(self, trace: bool = True) -> dict:
+        torch = _torch()
+        self.stream.synchronize()
+        out = {"ctrl": self.v_ctrl.cpu().numpy(), "tokens": self.v_tokens.cpu().numpy(),
+               "branch": self.v_branch.cpu().numpy()}
+        self.d2h_bytes += out["ctrl"].nbytes + out["tokens"].nbytes + out["branch"].nbytes
+        if trace:
+            nmax = int(out["ctrl"][:, _lib.C_NEV].max())
+            out["events"] = self.v_events[:, :nmax].cpu().numpy()
+            self.d2h_bytes += out["events"].nbytes
+        return out
+
+    def results(self, tasks, vocab, single=False, fetched=None):
+        from .decoding import GenerationResult, NfeCounter
+        from .model import SequenceRow, exact_match
+        f = fetched if fetched is not None else self.fetch()
+        res = []
+        for r, task in enumerate(tasks):
+            c = f["ctrl"][r]
+            st = int(c[_lib.C_STATUS])
+            if st < 0:
+                if st == _lib.BB_ERR_RUNAWAY:
+                    raise RunawayError(f"blockbatch run exceeded the hard cap ({4 * self.G * self.B + 16})")
+                raise StateError(f"device session error {st} (request {r})")
+            if st != 1:
+                raise StateError(f"request {r} did not finish (status {st})")
+            if c[_lib.C_EV_OVERFLOW]:
+                raise StateError("trace event capacity exceeded")
+            w = int(c[_lib.C_WINNER])
+            eos = int(c[_lib.C_EOS])
+            row = SequenceRow(f["tokens"][r, w].astype(np.int64), self.P)
+            trace = decode_events(f["events"][r, :int(c[_lib.C_NEV])], self.B, single) if "events" in f else []
+            nfe = NfeCounter(int(c[_lib.C_NFE0]), int(c[_lib.C_NFE1]), int(c[_lib.C_NFE2]))
+            stats = {"iterations": int(c[_lib.C_ITER]), "merges": int(c[_lib.C_MERGES]),
+                     "syncs": int(c[_lib.C_SYNCS]), "commits": int(c[_lib.C_COMMITS]),
+                     "refreshes": int(c[_lib.C_REFRESHES]), "cow_pages": int(c[_lib.C_COW_PAGES])}
+            res.append(GenerationResult(row=row, branch_index=w, block_size=int(self.cfg.block_sizes[w]), nfe=nfe,
+                                        trace=trace, correct=exact_match(row, task, vocab),
+                                        tokens_decoded=int(f["branch"][r, w, _lib.B_DEC]),
+                                        eos_position=None if eos < 0 else eos, stats=stats))
+        return res
+
+
+def decode_events(ev: np.ndarray, n_branches: int, single: bool = False) -> list:
+    """Device trace records -> TraceEvent list (decoding.py:61-75 / scheduler.py emit order)."""
+    from .decoding import TraceEvent
+    out = []
+    for i, e in enumerate(ev):
+        kind = _lib.EV_KINDS[int(e[_lib.E_KIND])]
+        br = int(e[_lib.E_BRANCH])
+        branch = None if br < 0 else br
+        dec = tuple(int(x) for x in e[_lib.E_DEC:_lib.E_DEC + n_branches])
+        nfe = (int(e[_lib.E_NFE0]), int(e[_lib.E_NFE1]), int(e[_lib.E_NFE2]))
+        a0, a1, a2 = int(e[_lib.E_A0]), int(e[_lib.E_A1]), int(e[_lib.E_A2])
+        if kind == "init":
+            extra = {"extra_nfe": None}
+        elif kind in ("block_forward", "refresh"):
+            extra = {"active": [k for k in range(n_branches) if (a0 >> k) & 1]}
+        elif kind == "decode":
+            extra = {"commits": a0}
+        elif kind == "merge":
+            prob = float(np.array([e[_lib.E_PROB]], dtype=np.int32).view(np.float32)[0])
+            extra = {"source": a0, "pos": a1, "token": a2, "prob": prob}
+        elif kind == "sync":
+            extra = {"leader": a0, "gap": a1}
+        elif kind in ("eos_ready", "finish"):
+            extra = {"eos": None if a0 < 0 else a0}
+        else:
+            extra = {}
+        if single:  # single_branch_decode's record shapes (decoding.py:222-271)
+            branch = 0
+            if kind in ("init", "block_forward", "refresh", "finish"):
+                extra = {}
+        out.append(TraceEvent(i, kind, branch, dec, nfe, extra))
+    return out

@@ -1,0 +1,276 @@
+"""Branch-parallel decoding on the B200 (reference ``scheduler.py``).
+
+``run_blockbatch`` keeps the reference signature and result type.  The whole
+Alg. 1 loop runs on the device: one batched forward over every active
+branch's window rows per iteration (tcgen05 GEMMs with all windows stacked
+into the GEMM N dimension, paged shared-prefix attention, fused LM head +
+confidence), Eq. 1 commits, EOS cycle, Alg. 2 merge / leader sync and the
+periodic refresh — see csrc/bb_control.cu.  ``run_batch`` runs many
+requests in one session (request-level batching on one GPU).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .decoding import (BranchState, GenerationResult, TraceEvent, check_eos, EOS_READY)
+from .engine import Session
+from .errors import ConfigError, ContractError
+from .model import ModelParams, SequenceRow, Task, Vocab
+
+TRACE_SCHEMA = "blockbatch-trace-v1"
+DEFAULT_BLOCK_SIZES = (4, 8, 16, 32, 64, 128)
+HARD_CAP_FACTOR = 4
+
+
+@dataclass
+class SchedulerConfig:
+    """scheduler.py:32-63.  ``log_kv`` / ``log_consistency`` are KV-space
+    diagnostics (out of scope of the device path): only their defaults are
+    accepted by ``run_blockbatch``."""
+
+    block_sizes: tuple = DEFAULT_BLOCK_SIZES
+    tau_conf: float = 0.9
+    tau_merge: float = 0.5
+    tau_sync: int = 8
+    refresh_interval: int = 32
+    gen_len: int = 256
+    merge_enabled: bool = True
+    sync_enabled: bool = True
+    log_kv: str = "none"
+    log_consistency: bool = False
+
+    def validate(self) -> None:
+        if not self.block_sizes:
+            raise ConfigError("block_sizes must be non-empty")
+        if len(set(self.block_sizes)) != len(self.block_sizes):
+            raise ConfigError("block_sizes must be distinct")
+        if any(b < 1 for b in self.block_sizes):
+            raise ConfigError("block sizes must be positive")
+        if not 0.0 <= self.tau_conf <= 1.0:
+            raise ConfigError("tau_conf outside [0, 1]")
+        if not 0.0 <= self.tau_merge <= 1.0:
+            raise ConfigError("tau_merge outside [0, 1]")
+        if self.tau_sync < 0:
+            raise ConfigError("tau_sync must be non-negative")
+        if self.refresh_interval < 1:
+            raise ConfigError("refresh_interval must be >= 1")
+        if self.gen_len < 1:
+            raise ConfigError("gen_len must be >= 1")
+        if self.log_kv not in ("none", "norms", "full"):
+            raise ConfigError(f"unknown log_kv mode {self.log_kv!r}")
+
+
+@dataclass(frozen=True)
+class PackedQuery:
+    """scheduler.py:66-77 (the host view of a step's packed masked positions)."""
+    branch_order: tuple
+    positions: np.ndarray
+    offsets: tuple
+
+    def slice_for(self, branch_index: int) -> np.ndarray:
+        i = self.branch_order.index(branch_index)
+        return self.positions[self.offsets[i]:self.offsets[i + 1]]
+
+
+def get_active_branches(branches, rows, mask_id) -> list[int]:
+    """scheduler.py:92-100"""
+    return [b.index for b in branches
+            if not b.done and len(rows[b.index].masked_positions(mask_id, b.window))]
+
+
+def pack_active_blocks(rows, branches, active, mask_id) -> PackedQuery:
+    """scheduler.py:103-113"""
+    if not active:
+        raise ContractError("pack_active_blocks requires a non-empty active set")
+    chunks, offsets = [], [0]
+    for k in active:
+        pos = rows[k].masked_positions(mask_id, branches[k].window)
+        chunks.append(pos)
+        offsets.append(offsets[-1] + len(pos))
+    return PackedQuery(tuple(active), np.concatenate(chunks), tuple(offsets))
+
+
+def select_eos_winner(branches, rows, vocab: Vocab) -> BranchState:
+    """scheduler.py:216-222"""
+    ready = [b for b in branches if check_eos(b, rows[b.index], vocab) == EOS_READY]
+    if not ready:
+        raise ContractError("select_eos_winner requires an eos-ready branch")
+    return max(ready, key=lambda b: (b.tokens_decoded, -b.block_size))
+
+
+# -------------------------------------------------------------- sessions
+_SESSIONS: "weakref.WeakKeyDictionary[ModelParams, dict]" = weakref.WeakKeyDictionary()
+
+
+def _cfg_key(cfg: SchedulerConfig, P: int, R: int, trace: bool):
+    return (tuple(cfg.block_sizes), float(cfg.tau_conf), float(cfg.tau_merge), float(cfg.tau_sync),
+            int(cfg.refresh_interval), int(cfg.gen_len), bool(cfg.merge_enabled), bool(cfg.sync_enabled),
+            P, R, bool(trace))
+
+
+def get_session(params: ModelParams, cfg: SchedulerConfig, prompt_len: int, n_requests: int = 1,
+                trace: bool = True) -> Session:
+    """Cached device session for (params, cfg, prompt_len, n_requests)."""
+    cache = _SESSIONS.setdefault(params, {})
+    key = _cfg_key(cfg, prompt_len, n_requests, trace)
+    s = cache.get(key)
+    if s is None:
+        if len(cache) >= 4:
+            cache.pop(next(iter(cache)))
+        s = Session(params, cfg, prompt_len, n_requests, trace=trace)
+        cache[key] = s
+    return s
+
+
+def _check_call(params, cfg, tasks):
+    cfg.validate()
+    if cfg.log_kv != "none" or cfg.log_consistency:
+        raise ConfigError("KV-space logging (log_kv / log_consistency) is a CPU diagnostic, not on the device path")
+    P = tasks[0].prompt_len
+    for t in tasks:
+        if t.gen_len != cfg.gen_len:
+            raise ConfigError("cfg.gen_len does not match the task")
+        if t.prompt_len != P:
+            raise ConfigError("all tasks of a batch must share the prompt length")
+    if P + cfg.gen_len > params.dims.max_len:
+        raise ContractError(f"sequence length {P + cfg.gen_len} exceeds max_len {params.dims.max_len}")
+    return P
+
+
+def run_blockbatch(params: ModelParams, task: Task, cfg: SchedulerConfig, forward_hook=None,
+                   forward_observer=None, _single: bool = False) -> GenerationResult:
+    """scheduler.py:225-394 on the device: prefill, batched block denoising,
+    merge/sync, periodic refresh, early EOS return, final selection.
+
+    ``forward_hook(kind)`` is replayed once per charged NFE in charge order
+    from the device trace.  ``forward_observer`` needs host copies of every
+    branch's KV before/after each step (the reference's replay harness) and is
+    not supported on the device path."""
+    if forward_observer is not None:
+        raise NotImplementedError("forward_observer needs host KV snapshots; not supported on the device path")
+    return run_batch(params, [task], cfg, forward_hook=forward_hook, _single=_single)[0]
+
+
+def run_batch(params: ModelParams, tasks: list, cfg: SchedulerConfig, forward_hook=None, trace: bool = True,
+              use_graph: bool = True, _single: bool = False) -> list:
+    """Many independent requests (same P, G) in one device session: every
+    iteration runs one forward over all live requests' branch windows;
+    NFE, trace and termination stay per request."""
+    P = _check_call(params, cfg, tasks)
+    s = get_session(params, cfg, P, len(tasks), trace=trace or forward_hook is not None)
+    s.set_inputs(np.stack([t.prompt for t in tasks]), np.stack([t.target for t in tasks]))
+    s.launch(use_graph=use_graph)
+    res = s.results(tasks, params.vocab, single=_single)
+    if forward_hook is not None:
+        for r in res:
+            for ev in r.trace:
+                if ev.kind == "init":
+                    forward_hook("init")
+                elif ev.kind == "block_forward":
+                    forward_hook("block")
+                elif ev.kind == "refresh":
+                    forward_hook("refresh")
+    return res
+
+
+# -------------------------------------------------------------- merge/sync seam
+def merge_sync(rows: list, caches: list, branches: list, tau_merge: float, tau_sync: float, vocab: Vocab,
+               merge_enabled: bool = True, sync_enabled: bool = True) -> list[dict]:
+    """Alg. 2 (scheduler.py:144-209) on the GPU — the production merge/sync
+    core (csrc/bb_control.cu: merge_sync_core) fed with the caller's host
+    state; decisions are bit-exact given identical probabilities (fp32).
+    Mutates rows, caches (``.copy()`` on sync), branches like the reference."""
+    import torch
+    B = len(branches)
+    if B > _lib.MAXB:
+        raise ConfigError(f"at most {_lib.MAXB} branches")
+    L = len(rows[0])
+    P = rows[0].prompt_len
+    n_out = vocab.n_out
+    rt = torch.tensor(np.stack([r.tokens for r in rows]).astype(np.int32), device="cuda")
+    br = np.zeros((B, _lib.B_WORDS), np.int32)
+    for b in branches:
+        br[b.index] = [b.window.start, b.window.end, int(b.done), b.tokens_decoded, b.tokens_merged,
+                       b.block_size, 0, 0]
+    brt = torch.tensor(br, device="cuda")
+    cov = torch.tensor(np.stack([b.prob_covered for b in branches]).astype(np.uint8), device="cuda")
+    pm = torch.tensor(np.stack([b.prob_map for b in branches]).astype(np.float32), device="cuda")
+    cap = 8 * B * L + 64
+    ev = torch.zeros(cap, _lib.EVW, dtype=torch.int32, device="cuda")
+    ctrl = torch.zeros(_lib.C_WORDS, dtype=torch.int32, device="cuda")
+    ptab = torch.zeros(B * L * B, dtype=torch.float32, device="cuda")
+    pok = torch.zeros(B * L, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(_lib.lib().bb_merge_sync_maps(B, L, P, vocab.size, p(rt), p(brt), p(cov), p(pm), n_out,
+                                             float(tau_merge), float(tau_sync), int(merge_enabled),
+                                             int(sync_enabled), p(ev), cap, p(ctrl), p(ptab), p(pok),
+                                             C.c_void_p(s)), "bb_merge_sync_maps")
+    c = ctrl.cpu().numpy()
+    if c[_lib.C_STATUS] != 0:
+        raise ContractError(f"merge_sync device error {int(c[_lib.C_STATUS])}")
+    rows_out = rt.cpu().numpy()
+    br_out = brt.cpu().numpy()
+    cov_out = cov.cpu().numpy().astype(bool)
+    events = []
+    from .model import BlockWindow
+    for e in ev[:int(c[_lib.C_NEV])].cpu().numpy():
+        kind = _lib.EV_KINDS[int(e[_lib.E_KIND])]
+        d = int(e[_lib.E_BRANCH])
+        if kind == "merge":
+            prob = float(branches[d].prob_map[int(e[_lib.E_A1]), int(e[_lib.E_A2])])
+            events.append({"kind": "merge", "dest": d, "source": int(e[_lib.E_A0]), "pos": int(e[_lib.E_A1]),
+                           "token": int(e[_lib.E_A2]), "prob": prob})
+        else:
+            lead = int(e[_lib.E_A0])
+            rows[d] = rows[lead].copy()
+            caches[d] = caches[lead].copy()
+            branches[d].prob_map = branches[lead].prob_map.copy()
+            events.append({"kind": "sync", "dest": d, "leader": lead, "gap": int(e[_lib.E_A1])})
+    for b in branches:
+        k = b.index
+        rows[k].tokens[:] = rows_out[k]
+        b.window = BlockWindow(int(br_out[k, 0]), int(br_out[k, 1]))
+        b.done = bool(br_out[k, 2])
+        b.tokens_decoded = int(br_out[k, 3])
+        b.tokens_merged = int(br_out[k, 4])
+        b.prob_covered = cov_out[k].copy()
+    return events
+
+
+# -------------------------------------------------------------- trace IO
+def _jsonify(obj):
+    """scheduler.py:397-406"""
+    if isinstance(obj, dict):
+        return {str(k): _jsonify(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_jsonify(v) for v in obj]
+    if isinstance(obj, np.generic):
+        return obj.item()
+    if isinstance(obj, np.ndarray):
+        return obj.tolist()
+    return obj
+
+
+def write_trace(path, trace: list) -> None:
+    """scheduler.py:409-414: JSONL with a schema header line."""
+    with open(path, "w") as fh:
+        fh.write(json.dumps({"schema": TRACE_SCHEMA}) + "\n")
+        for event in trace:
+            fh.write(json.dumps(_jsonify(event.to_record())) + "\n")
+
+
+def read_trace(path) -> list[dict]:
+    """scheduler.py:417-422"""
+    with open(path) as fh:
+        header = json.loads(fh.readline())
+        if header.get("schema") != TRACE_SCHEMA:
+            raise ContractError(f"unknown trace schema: {header}")
+        return [json.loads(line) for line in fh if line.strip()]

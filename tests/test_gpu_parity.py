@@ -1,0 +1,183 @@
+"""GPU parity of the device path vs the reference (golden fixtures) — through
+the public API and the C-ABI library.  fp32 verification mode must be
+bit-exact on tokens, NFE, winner and the full trace (merge probabilities to
+1e-5 relative: fp32 vs the reference's float64)."""
+
+import numpy as np
+import pytest
+
+import fuzz
+import goldens
+
+pytestmark = pytest.mark.gpu
+
+bb = pytest.importorskip("paper_2605_29233_b200")
+
+REF = goldens.load("runs_ref.json")
+LLADA = goldens.load("runs_llada.json")
+KER = goldens.load("kernels.json")
+
+_MODELS = {}
+
+
+def ref_model(m, dtype="f32"):
+    key = (m["vocab_size"], m["layers"], m["d_model"], m["max_len"], m["head_scale"], dtype)
+    if key not in _MODELS:
+        vocab = bb.Vocab(size=m["vocab_size"])
+        dims = bb.ModelDims(layers=m["layers"], d_model=m["d_model"], max_len=m["max_len"])
+        _MODELS[key] = bb.build_model(m["seed"], vocab, dims, gamma=m["gamma"], radius=m["radius"],
+                                      head_scale=m["head_scale"], spike_cut=m["spike_cut"],
+                                      spike_gain=m["spike_gain"], dtype=dtype)
+    return _MODELS[key]
+
+
+def llada_model(g, dtype):
+    a = g["arch"]
+    key = ("llada", tuple(sorted(a.items())), dtype)
+    if key not in _MODELS:
+        vocab = bb.Vocab(size=a["vocab_size"])
+        dims = bb.ModelDims(layers=a["layers"], d_model=a["d_model"], max_len=a["max_len"], arch="llada",
+                            n_heads=a["n_heads"], n_kv_heads=a["n_kv_heads"], head_dim=a["head_dim"],
+                            d_ff=a["d_ff"], rope_theta=a["rope_theta"], norm_eps=a["norm_eps"],
+                            qkv_bias=a.get("qkv_bias", False))
+        _MODELS[key] = bb.build_model(0, vocab, dims, head_scale=a["head_scale"], dtype=dtype, init="hash")
+    return _MODELS[key]
+
+
+def cfg_from(c):
+    return bb.SchedulerConfig(block_sizes=tuple(c["block_sizes"]), tau_conf=c["tau_conf"],
+                              tau_merge=c["tau_merge"], tau_sync=c["tau_sync"],
+                              refresh_interval=c["refresh_interval"], gen_len=c["gen_len"],
+                              merge_enabled=c["merge_enabled"], sync_enabled=c["sync_enabled"])
+
+
+def record(r):
+    return {"tokens": [int(t) for t in r.row.tokens], "nfe": list(r.nfe.snapshot()),
+            "branch_index": r.branch_index, "block_size": r.block_size, "tokens_decoded": r.tokens_decoded,
+            "eos_position": r.eos_position, "correct": r.correct, "trace": [e.to_record() for e in r.trace]}
+
+
+@pytest.mark.parametrize("name", [k for k in REF if k != "single_branch_default"])
+def test_fp32_matches_reference_runs(name):
+    g = REF[name]
+    params = ref_model(g["model"])
+    vocab = params.vocab
+    cfg = cfg_from(g["config"])
+    for seed, want in zip(g["seeds"], g["runs"]):
+        task = bb.make_task(seed, g["prompt_len"], g["gen_len"], vocab)
+        got = record(bb.run_blockbatch(params, task, cfg))
+        err = goldens.compare_run(got, want, prob_tol=1e-5)
+        assert err is None, f"{name} seed {seed}: {err}"
+
+
+def test_fp32_batch_equals_single_requests():
+    g = REF["c1_hs2"]
+    params = ref_model(g["model"])
+    cfg = cfg_from(g["config"])
+    tasks = [bb.make_task(s, g["prompt_len"], g["gen_len"], params.vocab) for s in g["seeds"]]
+    got = bb.run_batch(params, tasks, cfg)
+    for r, want in zip(got, g["runs"]):
+        assert goldens.compare_run(record(r), want, prob_tol=1e-5) is None
+
+
+def test_single_branch_decode_matches_reference():
+    g = REF["single_branch_default"]
+    params = ref_model(REF["default_b4_128_g64"]["model"])
+    for want in g["runs"]:
+        task = bb.make_task(want["seed"], g["prompt_len"], g["gen_len"], params.vocab)
+        r = bb.single_branch_decode(params, task, bb.DecodeConfig(block_size=want["block"], gen_len=64))
+        assert [int(t) for t in r.row.tokens] == want["tokens"]
+        assert list(r.nfe.snapshot()) == want["nfe"]
+        assert goldens.diff_trace([e.to_record() for e in r.trace], want["trace"]) is None
+
+
+@pytest.mark.parametrize("name", [k for k in LLADA if k.endswith("_f32")])
+def test_fp32_llada_shape_matches_oracle(name):
+    g = LLADA[name]
+    params = llada_model(g, "f32")
+    cfg = cfg_from(g["config"])
+    for seed, want in zip(g["seeds"], g["runs"]):
+        task = bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab)
+        got = record(bb.run_blockbatch(params, task, cfg))
+        err = goldens.compare_run(got, want, prob_tol=1e-4)
+        assert err is None, f"{name} seed {seed}: {err}"
+
+
+@pytest.mark.parametrize("name", [k for k in LLADA if k.endswith("_bf16")])
+def test_bf16_llada_shape_nfe_agreement(name):
+    """bf16 tolerance regime: NFE identical on most prompts, tokens close."""
+    g = LLADA[name]
+    params = llada_model(g, "bf16")
+    cfg = cfg_from(g["config"])
+    same_nfe = 0
+    for seed, want in zip(g["seeds"], g["runs"]):
+        task = bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab)
+        r = bb.run_blockbatch(params, task, cfg)
+        same_nfe += list(r.nfe.snapshot()) == want["nfe"]
+    assert same_nfe >= len(g["seeds"]) - 1, f"{same_nfe}/{len(g['seeds'])} NFE matches"
+
+
+def test_commit_kernel_bit_exact_on_reference_fixtures():
+    for rec in KER["transition"]:
+        tokens, P, s, e, masked, probs, tau = fuzz.transition_instance(rec["seed"])
+        row = bb.SequenceRow(tokens.copy(), P)
+        out = bb.DenoiseOutput(masked, np.log(probs + 1e-300), probs)
+        got = bb.confidence_transition(out, row, bb.BlockWindow(s, e), tau)
+        assert [list(c) for c in got] == rec["commits"], rec["seed"]
+
+
+class _FC:
+    def __init__(self, tag):
+        self.tag = tag
+
+    def copy(self):
+        return _FC(self.tag)
+
+
+def test_merge_sync_kernel_bit_exact_on_reference_fixtures():
+    vocab = bb.Vocab()
+    for rec in KER["merge"]:
+        st = fuzz.merge_state(rec["seed"], n_branches=rec["n_branches"])
+        nb = rec["n_branches"]
+        rows = [bb.SequenceRow(st["rows"][i].copy(), st["prompt_len"]) for i in range(nb)]
+        branches = []
+        for i in range(nb):
+            b = bb.BranchState(index=i, block_size=int(st["block_sizes"][i]),
+                               window=bb.BlockWindow(int(st["starts"][i]), int(st["ends"][i])),
+                               done=bool(st["done"][i]), prob_map=st["prob_maps"][i].copy(),
+                               prob_covered=st["covered"][i].copy())
+            b.refresh_decoded(rows[i], vocab.mask_id)
+            branches.append(b)
+        caches = [_FC(i) for i in range(nb)]
+        ev = bb.merge_sync(rows, caches, branches, rec["tau_merge"], rec["tau_sync"], vocab,
+                           merge_enabled=rec["merge_enabled"], sync_enabled=rec["sync_enabled"])
+        assert ev == rec["events"], rec["seed"]
+        assert [[int(t) for t in r.tokens] for r in rows] == rec["rows"], rec["seed"]
+        assert [c.tag for c in caches] == rec["cache_tags"]
+        for b, w in zip(branches, rec["branches"]):
+            assert (b.window.start, b.window.end, b.done, b.tokens_decoded, b.tokens_merged) == \
+                (w["start"], w["end"], w["done"], w["tokens_decoded"], w["tokens_merged"]), rec["seed"]
+            assert [int(x) for x in b.prob_covered] == w["covered"]
+
+
+def test_deterministic_reruns():
+    g = REF["c1_hs2"]
+    params = ref_model(g["model"])
+    cfg = cfg_from(g["config"])
+    task = bb.make_task(1, g["prompt_len"], g["gen_len"], params.vocab)
+    a = bb.run_blockbatch(params, task, cfg)
+    b = bb.run_blockbatch(params, task, cfg)
+    assert [e.to_record() for e in a.trace] == [e.to_record() for e in b.trace]
+    assert np.array_equal(a.row.tokens, b.row.tokens)
+
+
+def test_forward_hook_counts():
+    g = REF["default_r4"]
+    params = ref_model(g["model"])
+    cfg = cfg_from(g["config"])
+    task = bb.make_task(4, g["prompt_len"], g["gen_len"], params.vocab)
+    calls = []
+    r = bb.run_blockbatch(params, task, cfg, forward_hook=calls.append)
+    assert len(calls) == r.nfe.total
+    assert calls.count("init") == 1 and calls.count("block") == r.nfe.nfe_block
+    assert calls.count("refresh") == r.nfe.nfe_refresh
