@@ -829,10 +829,23 @@ __global__ void k_merge_sync(Dims D, Sess S, DevState st, int after_prefill) {
   uint8_t* cov = reinterpret_cast<uint8_t*>(c.rows + S.B * S.L);
   const long long cb = (long long)c.r * S.B * S.L;
   for (int i = threadIdx.x; i < S.B * S.L; i += blockDim.x) cov[i] = st.covered[cb + i];
-  if (threadIdx.x == 0) c.ctrl[C_NPMCOPY] = 0;
+  __shared__ int s_ev0;
+  if (threadIdx.x == 0) {
+    c.ctrl[C_NPMCOPY] = 0;
+    s_ev0 = c.ctrl[C_NEV];
+  }
   __syncthreads();
   merge_sync_core(c, cov, true);
   __syncthreads();
+  // scheduler.py:370-372 emits merge/sync events after merge_sync returns:
+  // their `decoded` snapshot is the post-merge/sync state.
+  if (threadIdx.x == 0 && S.trace) {
+    const int n1 = min(c.ctrl[C_NEV], S.ev_cap);
+    for (int n = s_ev0; n < n1; ++n) {
+      int* e = st.events + ((long long)c.r * S.ev_cap + n) * EVW;
+      for (int k = 0; k < S.B; ++k) e[E_DEC + k] = c.B_(k, B_DEC);
+    }
+  }
   for (int i = threadIdx.x; i < S.B * S.L; i += blockDim.x) st.covered[cb + i] = cov[i];
   if (threadIdx.x == 0) {
     bool any_live = false;

@@ -1,0 +1,29 @@
+"""Run the C2 workload (LLaDA-8B shape, B={8,16,32}, P64, G256) and profile a
+window of block-step iterations (cudaProfilerStart/Stop around them) so that
+`ncu --profile-from-start off` captures exactly those kernels."""
+import os, sys
+sys.path.insert(0, '.')
+import torch
+import paper_2605_29233_b200 as bb
+from paper_2605_29233_b200.scheduler import get_session
+
+HS, GAMMA = float(os.environ.get("BB_HS", 0.4)), float(os.environ.get("BB_GAMMA", 8.0))
+N_PROF = int(os.environ.get("BB_PROF_ITERS", 2))
+P, G = 64, 256
+vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
+cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=G)
+params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=HS, gamma=GAMMA, dtype="bf16", init="hash")
+task = bb.make_task(2, P, G, vocab)
+s = get_session(params, cfg, P, 1)
+s.set_inputs(task.prompt[None], task.target[None])
+s.prefill()
+use_graph = os.environ.get("BB_GRAPH", "0") == "1"
+for it in range(1, 6):
+    s.iteration(it % cfg.refresh_interval == 0, use_graph)
+s.stream.synchronize()
+torch.cuda.profiler.start()
+for it in range(6, 6 + N_PROF):
+    s.iteration(it % cfg.refresh_interval == 0, use_graph)
+s.stream.synchronize()
+torch.cuda.profiler.stop()
+print("ctrl", s.v_ctrl[0, :24].tolist())
