@@ -114,6 +114,9 @@ BB_API int bb_iteration(void* sess, int with_refresh, int use_graph, void* strea
 /* run_blockbatch (scheduler.py:225-394) for all requests of the session */
 BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out);
 BB_API int bb_version(void);
+/* instrumentation: live per-launch GEMM timing and kernel-launch counters */
+BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream);
+BB_API int bb_session_counters(void* sess, long long* out);
 
 /* ---- debug / unit-test entry points (kernel-level) --------------------- */
 BB_API int bb_debug_gemm_tc(const void* W, const void* X, void* out, int n_out, int K, int rows, int BN, int mode,

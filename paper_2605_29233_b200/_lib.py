@@ -74,6 +74,8 @@ SIGNATURES = {
     "bb_session_view": (i32, [vp, i32, i64p, i64p]),
     "bb_session_info": (i32, [vp, i32p, i32]),
     "bb_session_ctrl": (i32, [vp, i32p, vp]),
+    "bb_session_gemm_stats": (i32, [vp, C.POINTER(C.c_ulonglong), i32, vp]),
+    "bb_session_counters": (i32, [vp, i64p]),
     "bb_prefill": (i32, [vp, vp]),
     "bb_block_step": (i32, [vp, vp]),
     "bb_refresh": (i32, [vp, vp]),

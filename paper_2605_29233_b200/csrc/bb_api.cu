@@ -47,7 +47,10 @@ struct Session {
   int* full_rows = nullptr;  // device scalar: rows of the full pass
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  cudaGraphExec_t g_iter = nullptr, g_iter_ref = nullptr;
+  cudaGraphExec_t g_iter = nullptr, g_iter_ref = nullptr, g_prefill = nullptr;
+  long long nodes_iter = 0, nodes_iter_ref = 0, nodes_prefill = 0;
+  long long kernel_launches = 0, graph_launches = 0;
+  unsigned long long* tstat = nullptr;  // [16][8] per-GEMM-kind live timing
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
   long long layout[BB_VIEW_COUNT][2];
@@ -208,6 +211,7 @@ static void plan(Session* s, char* base, bool dry) {
   H.res_s = c.take<float>(rb);
   H.skip = c.take<int>(1);
   s->full_rows = c.take<int>(1);
+  s->tstat = c.take<unsigned long long>(16 * 8);
   // GEMM partial planes: max over all stream-K GEMMs of (slots x rows x n_out)
   long long part = 1;
   if (D.dtype == BB_DTYPE_BF16) {
@@ -264,6 +268,7 @@ static int setup_gemms(Session* s) {
         }
         TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
+          all[g]->p.tstat = s->tstat + (size_t)(which * 8 + g) * 8;
           all[g]->p.part = s->part;
           all[g]->p.skip = P.skip;
           all[g]->p.rows_valid = which == 1 ? s->full_rows : nullptr;
@@ -293,6 +298,7 @@ static int setup_gemms(Session* s) {
     p.spike_cut = D.spike_cut;
     p.spike_gain = D.spike_gain;
     p.skip = s->H.skip;
+    p.tstat = s->tstat + (size_t)4 * 8;
   } else {
     s->head_simt = SimtGemm{(const float*)W.head, (const float*)s->blk.xn, D.n_out, D.d, s->blk.rows_alloc,
                             nullptr, s->H.skip, s->H.logits, D.n_out};
@@ -360,9 +366,6 @@ static cudaError_t head(Session* s, cudaStream_t st) {
 static int enqueue_prefill(Session* s, cudaStream_t st) {
   const Dims& D = s->D;
   const Sess& S = s->S;
-  CK(cudaMemsetAsync(s->full_rows, 0, sizeof(int), st));
-  const int nf = S.NF;
-  CK(cudaMemcpyAsync(s->full_rows, &nf, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(launch_prefill_init(D, S, s->st, s->full, s->blk, s->H, st));
   CK(forward(s, s->full, s->gf, st));
   CK(launch_gather_head(D, S, s->full, s->blk, s->H, -1, st));
@@ -405,14 +408,29 @@ static int enqueue_refresh(Session* s, cudaStream_t st) {
   return BB_OK;
 }
 
-static int capture(Session* s, bool with_refresh, cudaStream_t st, cudaGraphExec_t* out) {
+static long long count_kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return -1;
+  std::vector<cudaGraphNode_t> nodes(n);
+  cudaGraphGetNodes(g, nodes.data(), &n);
+  long long k = 0;
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
+// what: 0 = block step, 1 = block step + refresh, 2 = prefill
+static int capture(Session* s, int what, cudaStream_t st, cudaGraphExec_t* out, long long* nodes) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  int rc = enqueue_block_step(s, st);
-  if (rc == BB_OK && with_refresh) rc = enqueue_refresh(s, st);
+  int rc = what == 2 ? enqueue_prefill(s, st) : enqueue_block_step(s, st);
+  if (rc == BB_OK && what == 1) rc = enqueue_refresh(s, st);
   cudaError_t e = cudaStreamEndCapture(st, &g);
   if (rc != BB_OK) return rc;
   CK(e);
+  *nodes = count_kernel_nodes(g);
   CK(cudaGraphInstantiate(out, g, 0));
   cudaGraphDestroy(g);
   return BB_OK;
@@ -565,6 +583,12 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   cudaMemcpy(s->blk.slot_pos, neg.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->full.slot_pos, neg.data(), s->full.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->H.masked, zero.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(s->full_rows, &s->S.NF, sizeof(int), cudaMemcpyHostToDevice);
+  {
+    std::vector<unsigned long long> ts(16 * 8, 0ull);
+    for (int k = 0; k < 16; ++k) ts[k * 8] = ~0ull;
+    cudaMemcpy(s->tstat, ts.data(), ts.size() * 8, cudaMemcpyHostToDevice);
+  }
   if (cudaMallocHost(&s->host_ctrl, 4 * (size_t)s->S.R * C_WORDS * 4) != cudaSuccess) {
     delete s;
     return BB_ERR_CUDA;
@@ -579,6 +603,7 @@ BB_API int bb_session_destroy(void* sess) {
   if (!s) return BB_OK;
   if (s->g_iter) cudaGraphExecDestroy(s->g_iter);
   if (s->g_iter_ref) cudaGraphExecDestroy(s->g_iter_ref);
+  if (s->g_prefill) cudaGraphExecDestroy(s->g_prefill);
   if (s->host_ctrl) cudaFreeHost(s->host_ctrl);
   for (int i = 0; i < 4; ++i)
     if (s->ev[i]) cudaEventDestroy(s->ev[i]);
@@ -631,11 +656,14 @@ BB_API int bb_iteration(void* sess, int with_refresh, int use_graph, void* strea
     return rc;
   }
   cudaGraphExec_t* g = with_refresh ? &s->g_iter_ref : &s->g_iter;
+  long long* nn = with_refresh ? &s->nodes_iter_ref : &s->nodes_iter;
   if (!*g) {
-    int rc = capture(s, with_refresh != 0, st, g);
+    int rc = capture(s, with_refresh ? 1 : 0, st, g, nn);
     if (rc != BB_OK) return rc;
   }
   CK(cudaGraphLaunch(*g, st));
+  s->kernel_launches += *nn;
+  s->graph_launches += 1;
   return BB_OK;
 }
 
@@ -649,8 +677,19 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
   Session* s = (Session*)sess;
   if (!s) return BB_ERR_CONTRACT;
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = enqueue_prefill(s, st);
-  if (rc != BB_OK) return rc;
+  int rc = BB_OK;
+  if (use_graph) {
+    if (!s->g_prefill) {
+      rc = capture(s, 2, st, &s->g_prefill, &s->nodes_prefill);
+      if (rc != BB_OK) return rc;
+    }
+    CK(cudaGraphLaunch(s->g_prefill, st));
+    s->kernel_launches += s->nodes_prefill;
+    s->graph_launches += 1;
+  } else {
+    rc = enqueue_prefill(s, st);
+    if (rc != BB_OK) return rc;
+  }
   const int R = s->S.R;
   const size_t cb = (size_t)R * C_WORDS * 4;
   CK(cudaMemcpyAsync(s->host_ctrl, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
@@ -678,6 +717,41 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
   }
   CK(cudaStreamSynchronize(st));
   if (iterations_out) *iterations_out = it;
+  return BB_OK;
+}
+
+// live GEMM timing: out[16][5] = (unused min, unused max, unused, sum ns, launches)
+// kinds 0-3: block-pass QKV, O, gate/up, down; 4: LM head; 8-11: full-pass QKV..down
+BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !host_out) return BB_ERR_CONTRACT;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<unsigned long long> ts(16 * 8);
+  CK(cudaMemcpyAsync(ts.data(), s->tstat, ts.size() * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int k = 0; k < 16; ++k)
+    for (int j = 0; j < 5; ++j) host_out[k * 5 + j] = ts[k * 8 + j];
+  if (reset) {
+    for (int k = 0; k < 16; ++k) {
+      ts[k * 8 + 0] = ~0ull;
+      for (int j = 1; j < 8; ++j) ts[k * 8 + j] = 0;
+    }
+    CK(cudaMemcpyAsync(s->tstat, ts.data(), ts.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return BB_OK;
+}
+
+// out[0] = kernel launches enqueued through graphs, [1] graph launches,
+// [2] kernels per block-step graph, [3] per step+refresh graph, [4] per prefill graph
+BB_API int bb_session_counters(void* sess, long long* out) {
+  Session* s = (Session*)sess;
+  if (!s || !out) return BB_ERR_CONTRACT;
+  out[0] = s->kernel_launches;
+  out[1] = s->graph_launches;
+  out[2] = s->nodes_iter;
+  out[3] = s->nodes_iter_ref;
+  out[4] = s->nodes_prefill;
   return BB_OK;
 }
 

@@ -179,6 +179,260 @@ __global__ void __launch_bounds__(128) k_attn_combine(Dims D, Sess S, Pass P, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// bf16 tensor-core attention (mma.sync m16n8k16, fp32 accumulate), FA2-style:
+// 4 warps x 16 query rows, 64-key chunks staged in padded smem, online
+// softmax in the log2 domain, P reused from the S accumulators as the A
+// operand of P.V, V fragments via ldmatrix.trans.
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128) k_attn_mma(Dims D, Sess S, Pass P, DevState st, int layer, int max_items) {
+  if (*P.skip) return;
+  using bf = __nv_bfloat16;
+  constexpr int KC = 64, LD = HD + 8, QR = 64;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  bf* sQ = reinterpret_cast<bf*>(smraw);
+  bf* sK = sQ + QR * LD;
+  bf* sV = sK + KC * LD;
+  long long* sKey = reinterpret_cast<long long*>(sV + KC * LD);
+  __shared__ int sRow[QR];
+
+  const int r = blockIdx.x / max_items, it = blockIdx.x % max_items;
+  if (it >= P.n_items[r]) return;
+  const int* item = P.items + ((long long)r * max_items + it) * ITW;
+  const int mask = item[0], lp0 = item[1], lp1 = item[2], rep = item[3];
+  int n_rows = 0;
+  for (int k = 0; k < S.B; ++k)
+    if ((mask >> k) & 1) n_rows += P.rng_cnt[r * MAXB + k];
+  const int row0 = blockIdx.z * QR;
+  if (row0 >= n_rows) return;
+  const int h = blockIdx.y, kvh = h / (D.nh / D.nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+
+  const long long lay = (long long)layer * S.R * S.pool;
+  int n_keys = 0;
+  for (int lp = lp0; lp < lp1; ++lp) {
+    const int ks = lp_start(S, lp), ke = lp_end(S, lp);
+    const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + rep) * S.n_lp + lp];
+    const long long base = ((lay + gpage) * D.nkv + kvh) * S.ps * HD;
+    for (int j = threadIdx.x; j < ke - ks; j += blockDim.x) sKey[n_keys + j] = base + (long long)j * HD;
+    n_keys += ke - ks;
+  }
+  if (threadIdx.x < QR)
+    sRow[threadIdx.x] = (row0 + (int)threadIdx.x < n_rows) ? item_row_slot(P, S, r, mask, row0 + threadIdx.x) : -1;
+  __syncthreads();
+  constexpr int VPR = HD / 8;  // 16-byte vectors per row
+  const bf* Qg = reinterpret_cast<const bf*>(P.q);
+  for (int i = threadIdx.x; i < QR * VPR; i += blockDim.x) {
+    const int rr = i / VPR, v = i % VPR;
+    const int slot = sRow[rr];
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (slot >= 0) val = *reinterpret_cast<const uint4*>(Qg + (long long)slot * D.attn_dim + h * HD + v * 8);
+    *reinterpret_cast<uint4*>(sQ + rr * LD + v * 8) = val;
+  }
+  __syncthreads();
+  uint32_t qf[HD / 16][4];
+  {
+    const bf* q0 = sQ + (warp * 16 + g) * LD + 2 * t;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      qf[kk][0] = *reinterpret_cast<const uint32_t*>(q0 + 16 * kk);
+      qf[kk][1] = *reinterpret_cast<const uint32_t*>(q0 + 8 * LD + 16 * kk);
+      qf[kk][2] = *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + 8);
+      qf[kk][3] = *reinterpret_cast<const uint32_t*>(q0 + 8 * LD + 16 * kk + 8);
+    }
+  }
+  float o[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+  const float sl2 = D.attn_scale * 1.4426950408889634f;
+  const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
+  const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
+  const uint32_t sV_u = smem_u32(sV);
+  for (int k0 = 0; k0 < n_keys; k0 += KC) {
+    const int nk = min(KC, n_keys - k0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < KC * VPR; i += blockDim.x) {
+      const int j = i / VPR, v = i % VPR;
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      if (j < nk) {
+        const long long off = sKey[k0 + j] + v * 8;
+        kv = *reinterpret_cast<const uint4*>(Kg + off);
+        vv = *reinterpret_cast<const uint4*>(Vg + off);
+      }
+      *reinterpret_cast<uint4*>(sK + j * LD + v * 8) = kv;
+      *reinterpret_cast<uint4*>(sV + j * LD + v * 8) = vv;
+    }
+    __syncthreads();
+    float s[KC / 8][4];
+#pragma unroll
+    for (int nt = 0; nt < KC / 8; ++nt) {
+      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
+      const bf* k0p = sK + (8 * nt + g) * LD + 2 * t;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(k0p + 16 * kk);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(k0p + 16 * kk + 8);
+        mma16816(s[nt], qf[kk], b0, b1);
+      }
+    }
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < KC / 8; ++nt) {
+      const int j = 8 * nt + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool valid = (j + (e & 1)) < nk;
+        s[nt][e] = valid ? s[nt][e] * sl2 : -INFINITY;
+      }
+      mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
+      mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float c0 = m0 == -INFINITY ? 0.0f : exp2f(m0 - mn0);
+    const float c1 = m1 == -INFINITY ? 0.0f : exp2f(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    float ps0 = 0.0f, ps1 = 0.0f;
+#pragma unroll
+    for (int nt = 0; nt < KC / 8; ++nt) {
+      s[nt][0] = exp2f(s[nt][0] - mn0);
+      s[nt][1] = exp2f(s[nt][1] - mn0);
+      s[nt][2] = exp2f(s[nt][2] - mn1);
+      s[nt][3] = exp2f(s[nt][3] - mn1);
+      ps0 += s[nt][0] + s[nt][1];
+      ps1 += s[nt][2] + s[nt][3];
+    }
+    l0 = l0 * c0 + ps0;
+    l1 = l1 * c1 + ps1;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      o[i][0] *= c0;
+      o[i][1] *= c0;
+      o[i][2] *= c1;
+      o[i][3] *= c1;
+    }
+#pragma unroll
+    for (int kk = 0; kk < KC / 16; ++kk) {
+      uint32_t a[4];
+      a[0] = pack_bf2(s[2 * kk][0], s[2 * kk][1]);
+      a[1] = pack_bf2(s[2 * kk][2], s[2 * kk][3]);
+      a[2] = pack_bf2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+      a[3] = pack_bf2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+      const int mi = lane >> 3, rr = lane & 7;
+      const int key = 16 * kk + (mi & 1) * 8 + rr;
+#pragma unroll
+      for (int nt2 = 0; nt2 < HD / 8; nt2 += 2) {
+        const int dim = 8 * nt2 + (mi >> 1) * 8;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(b0, b1, b2, b3, sV_u + (uint32_t)((key * LD + dim) * 2));
+        mma16816(o[nt2], a, b0, b1);
+        mma16816(o[nt2 + 1], a, b2, b3);
+      }
+    }
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float LN2 = 0.6931471805599453f;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int lr = warp * 16 + g + 8 * half;
+    if (sRow[lr] < 0) continue;
+    float* op = P.apart + ((((long long)r * max_items + it) * P.item_rows + row0 + lr) * D.nh + h) * (HD + 2);
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt)
+      *reinterpret_cast<float2*>(op + 8 * nt + 2 * t) = make_float2(o[nt][2 * half], o[nt][2 * half + 1]);
+    if (t == 0) {
+      op[HD] = (half ? m1 : m0) * LN2;
+      op[HD + 1] = half ? l1 : l0;
+    }
+  }
+}
+
+// LSE-merge of the partials of the items covering (row, head).  CTA per
+// (row, head), one thread per head dim; fixed item order (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(256) k_attn_combine2(Dims D, Sess S, Pass P, int max_items) {
+  if (*P.skip) return;
+  const int row = blockIdx.x, h = blockIdx.y;
+  const int pos = P.slot_pos[row];
+  if (pos < 0) return;
+  const int r = P.slot_req[row], k = P.slot_br[row];
+  const int j = row - P.rng_off[r * MAXB + k];
+  if (j < 0 || j >= P.rng_cnt[r * MAXB + k]) return;
+  __shared__ int s_off[256];
+  __shared__ int s_n;
+  const int HD = D.hd;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    const int ni = P.n_items[r];
+    for (int it = 0; it < ni && n < 256; ++it) {
+      const int mask = P.items[((long long)r * max_items + it) * ITW];
+      if (!((mask >> k) & 1)) continue;
+      int rii = j;
+      for (int k2 = 0; k2 < k; ++k2)
+        if ((mask >> k2) & 1) rii += P.rng_cnt[r * MAXB + k2];
+      s_off[n++] = (int)((((long long)r * max_items + it) * P.item_rows + rii) * D.nh + h);
+    }
+    s_n = n;
+  }
+  __syncthreads();
+  const int n = s_n;
+  float M = -INFINITY;
+  for (int i = 0; i < n; ++i) M = fmaxf(M, P.apart[(long long)s_off[i] * (HD + 2) + HD]);
+  T* out = reinterpret_cast<T*>(P.attn) + (long long)row * D.attn_dim + h * HD;
+  for (int c = threadIdx.x; c < HD; c += blockDim.x) {
+    float acc = 0.0f, L = 0.0f;
+    for (int i = 0; i < n; ++i) {
+      const float* o = P.apart + (long long)s_off[i] * (HD + 2);
+      const float mi = o[HD];
+      if (mi == -INFINITY) continue;
+      const float w = expf(mi - M);
+      acc = fmaf(o[c], w, acc);
+      L = fmaf(o[HD + 1], w, L);
+    }
+    stf(out + c, acc / L);
+  }
+}
+
+template <int HD>
+static cudaError_t attn_mma_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
+                               int max_items, cudaStream_t s) {
+  const int max_keys = P.full ? S.L : S.ch_block * S.ps;
+  const size_t smem = (size_t)(64 + 2 * 64) * (HD + 8) * 2 + (size_t)max_keys * 8 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid(S.R * max_items, D.nh, (P.item_rows + 63) / 64);
+  k_attn_mma<HD><<<grid, 128, smem, s>>>(D, S, P, st, layer, max_items);
+  return cudaGetLastError();
+}
+
 template <typename T, int HD>
 static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                            int max_items, cudaStream_t s) {
@@ -198,14 +452,16 @@ static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const De
 cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, cudaStream_t s) {
   const int max_items = P.full ? 1 : S.max_items;
   cudaError_t e = cudaErrorInvalidValue;
+  dim3 cgrid(P.rows_alloc, D.nh);
+  const int cthreads = D.hd < 256 ? D.hd : 256;
   if (D.dtype == 1) {
     using T = __nv_bfloat16;
-    if (D.hd == 64) e = attn_hd<T, 64>(D, S, P, st, layer, max_items, s);
-    else if (D.hd == 128) e = attn_hd<T, 128>(D, S, P, st, layer, max_items, s);
+    if (D.hd == 64) e = attn_mma_hd<64>(D, S, P, st, layer, max_items, s);
+    else if (D.hd == 128) e = attn_mma_hd<128>(D, S, P, st, layer, max_items, s);
     else if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);
     else if (D.hd == 32) e = attn_hd<T, 32>(D, S, P, st, layer, max_items, s);
     if (e != cudaSuccess) return e;
-    k_attn_combine<T><<<P.rows_alloc, 128, 0, s>>>(D, S, P, max_items);
+    k_attn_combine2<T><<<cgrid, cthreads, 0, s>>>(D, S, P, max_items);
   } else {
     using T = float;
     if (D.hd == 64) e = attn_hd<T, 64>(D, S, P, st, layer, max_items, s);
@@ -213,7 +469,7 @@ cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevSt
     else if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);
     else if (D.hd == 32) e = attn_hd<T, 32>(D, S, P, st, layer, max_items, s);
     if (e != cudaSuccess) return e;
-    k_attn_combine<T><<<P.rows_alloc, 128, 0, s>>>(D, S, P, max_items);
+    k_attn_combine2<T><<<cgrid, cthreads, 0, s>>>(D, S, P, max_items);
   }
   return cudaGetLastError();
 }

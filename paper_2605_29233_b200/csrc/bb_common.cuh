@@ -145,6 +145,32 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Per-launch duration accounting: every CTA records its start/end; the last
+// CTA of the launch folds (max end - min start) into the running sum.
+__device__ __forceinline__ void tstat_begin(unsigned long long* ts) {
+  if (ts != nullptr && threadIdx.x == 0) atomicMin(&ts[0], globaltimer_ns());
+}
+__device__ __forceinline__ void tstat_end(unsigned long long* ts) {
+  if (ts == nullptr || threadIdx.x != 0) return;
+  atomicMax(&ts[1], globaltimer_ns());
+  __threadfence();
+  const unsigned long long done = atomicAdd(&ts[2], 1ull);
+  if (done == gridDim.x * gridDim.y * gridDim.z - 1) {
+    __threadfence();
+    const unsigned long long t0 = atomicAdd(&ts[0], 0ull), t1 = atomicAdd(&ts[1], 0ull);
+    atomicAdd(&ts[3], t1 - t0);
+    atomicAdd(&ts[4], 1ull);
+    atomicExch(&ts[0], ~0ull);
+    atomicExch(&ts[1], 0ull);
+    atomicExch(&ts[2], 0ull);
+  }
+}
+
 // ---------------------------------------------------------------- numerics
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
 __device__ __forceinline__ __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }

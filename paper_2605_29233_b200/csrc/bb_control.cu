@@ -942,10 +942,11 @@ __global__ void k_refresh_end(Dims D, Sess S, DevState st) {
 }
 
 // ------------------------------------------------------------------ copies
+// 16-byte vector copies; block-strided over (request, job, layer) units.
 template <typename T>
-__global__ void __launch_bounds__(256) k_copy_pages(Dims D, Sess S, DevState st, int with_pm) {
+__global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st, int with_pm) {
   if (!with_pm) {
-    const long long per = (long long)D.nkv * S.ps * D.hd;  // elements per (page, layer)
+    const long long vecs = (long long)D.nkv * S.ps * D.hd * sizeof(T) / 16;  // per (page, layer)
     const long long units = (long long)S.R * S.max_copies * D.layers;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
       const int layer = (int)(u % D.layers);
@@ -955,31 +956,35 @@ __global__ void __launch_bounds__(256) k_copy_pages(Dims D, Sess S, DevState st,
       const int src = st.copies[((long long)r * S.max_copies + j) * 2];
       const int dst = st.copies[((long long)r * S.max_copies + j) * 2 + 1];
       const long long lay = (long long)layer * S.R * S.pool;
-      const long long so = (lay + (long long)r * S.pool + src) * per, do_ = (lay + (long long)r * S.pool + dst) * per;
-      T* K = reinterpret_cast<T*>(st.kv_k);
-      T* V = reinterpret_cast<T*>(st.kv_v);
-      for (long long e = threadIdx.x; e < per; e += blockDim.x) {
-        K[do_ + e] = K[so + e];
-        V[do_ + e] = V[so + e];
+      const long long so = (lay + (long long)r * S.pool + src) * vecs, dof = (lay + (long long)r * S.pool + dst) * vecs;
+      uint4* K = reinterpret_cast<uint4*>(st.kv_k);
+      uint4* V = reinterpret_cast<uint4*>(st.kv_v);
+      for (long long e = threadIdx.x; e < vecs; e += blockDim.x) {
+        const uint4 a = K[so + e], b = V[so + e];
+        K[dof + e] = a;
+        V[dof + e] = b;
       }
     }
   } else {
-    const long long units = (long long)S.R * MAXB * S.L;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const int vecs = (int)(D.d * sizeof(T) / 16);
+    // (request, job, position) units
+    const long long total = (long long)S.R * MAXB * S.L;
+    for (long long u = blockIdx.x; u < total; u += gridDim.x) {
       const int pos = (int)(u % S.L);
       const int j = (int)((u / S.L) % MAXB);
       const int r = (int)(u / ((long long)S.L * MAXB));
       if (j >= st.ctrl[(long long)r * C_WORDS + C_NPMCOPY]) continue;
       const int src = st.pm_copies[((long long)r * MAXB + j) * 2];
       const int dst = st.pm_copies[((long long)r * MAXB + j) * 2 + 1];
-      const T* a = reinterpret_cast<const T*>(st.pm_h) + (((long long)r * S.B + src) * S.L + pos) * D.d;
-      T* b = reinterpret_cast<T*>(st.pm_h) + (((long long)r * S.B + dst) * S.L + pos) * D.d;
-      for (int e = threadIdx.x; e < D.d; e += blockDim.x) b[e] = a[e];
+      const uint4* a = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(st.pm_h) +
+                                                      (((long long)r * S.B + src) * S.L + pos) * D.d);
+      uint4* b = reinterpret_cast<uint4*>(reinterpret_cast<T*>(st.pm_h) + (((long long)r * S.B + dst) * S.L + pos) * D.d);
+      for (int e = threadIdx.x; e < vecs; e += blockDim.x) b[e] = a[e];
     }
   }
 }
 
-// ------------------------------------------------------------------ launchers
+// ------------------------------------------------------------------ launch helpers
 static size_t rc_smem(const Sess& S) { return (size_t)S.B * S.L * 4 + (size_t)S.B * S.L + 64; }
 
 template <typename K>
@@ -1089,8 +1094,8 @@ cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, 
   return cudaGetLastError();
 }
 cudaError_t launch_copy_pages(const Dims& D, const Sess& S, const DevState& st, int with_pm, cudaStream_t s) {
-  if (D.dtype == 1) k_copy_pages<__nv_bfloat16><<<2 * kNumSMs, 256, 0, s>>>(D, S, st, with_pm);
-  else k_copy_pages<float><<<2 * kNumSMs, 256, 0, s>>>(D, S, st, with_pm);
+  if (D.dtype == 1) k_copy_pages<__nv_bfloat16><<<2 * kNumSMs, 512, 0, s>>>(D, S, st, with_pm);
+  else k_copy_pages<float><<<2 * kNumSMs, 512, 0, s>>>(D, S, st, with_pm);
   return cudaGetLastError();
 }
 cudaError_t launch_step_commit(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,

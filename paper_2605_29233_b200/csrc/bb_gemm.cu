@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(192, 1)
   float* red = reinterpret_cast<float*>(tslot + 4);  // [3][4][BN]
 
   if (p.skip != nullptr && *p.skip != 0) return;
+  tstat_begin(p.tstat);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows_valid = p.rows_valid != nullptr ? *p.rows_valid : p.rows_alloc;
   const int n_tiles = p.n_ntiles * p.n_chunks;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     tmem_dealloc(tbase, C::TCOLS);
   }
+  tstat_end(p.tstat);
 }
 
 // ------------------------------------------------------------------ host

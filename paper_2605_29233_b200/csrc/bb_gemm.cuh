@@ -60,6 +60,8 @@ struct GemmTcParams {
   const float* boost;
   const int* tgt;
   float head_scale, spike_cut, spike_gain;
+  // live per-launch timing (%globaltimer): [min start, max end, CTAs done, sum ns, launches]
+  unsigned long long* tstat;
 };
 
 struct TcGemm {

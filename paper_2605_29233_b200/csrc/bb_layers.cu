@@ -55,60 +55,63 @@ __global__ void __launch_bounds__(256) k_embed(Dims D, Pass P, const T* __restri
 }
 
 // ------------------------------------------------------------------ post QKV
+// CTA = (row, head of the fused q|k|v output), one thread per (i, i+hd/2) pair.
 template <typename T>
-__global__ void __launch_bounds__(256) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
-                                                  const float* __restrict__ rope, int layer, PartRef pr) {
+__global__ void k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
+                           const float* __restrict__ rope, int layer, PartRef pr) {
   if (*P.skip) return;
-  extern __shared__ float vals[];  // [qkv_out]
-  const int row = blockIdx.x;
+  const int row = blockIdx.x, hh = blockIdx.y, i = threadIdx.x;
   const int pos = P.slot_pos[row];
   if (pos < 0) return;
-  for (int c = threadIdx.x; c < D.qkv_out; c += blockDim.x) {
-    float v = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c);
-    if (bias != nullptr) v += bias[c];
-    vals[c] = v;
-  }
-  __syncthreads();
-  const int r = P.slot_req[row], b = P.slot_br[row];
-  const int lp = lp_of(S, pos);
-  const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + b) * S.n_lp + lp];
-  const int off = pos - lp_start(S, lp);
   const int half = D.hd >> 1;
-  const int nqk = D.nh + D.nkv;  // heads that get RoPE
-  T* q = reinterpret_cast<T*>(P.q) + (long long)row * D.attn_dim;
-  T* kk = reinterpret_cast<T*>(st.kv_k);
-  T* vv = reinterpret_cast<T*>(st.kv_v);
+  const int c0 = hh * D.hd + i, c1 = c0 + half;
+  float a = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c0);
+  float b = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c1);
+  if (bias != nullptr) {
+    a += bias[c0];
+    b += bias[c1];
+  }
+  if (D.arch == 1 && hh < D.nh + D.nkv) {
+    const float2 cs = *reinterpret_cast<const float2*>(rope + ((long long)pos * half + i) * 2);
+    const float a2 = a * cs.x - b * cs.y, b2 = b * cs.x + a * cs.y;
+    a = a2;
+    b = b2;
+  }
+  if (hh < D.nh) {
+    T* q = reinterpret_cast<T*>(P.q) + (long long)row * D.attn_dim + hh * D.hd;
+    stf(q + i, a);
+    stf(q + i + half, b);
+    return;
+  }
+  const bool isk = hh < D.nh + D.nkv;
+  const int kvh = isk ? hh - D.nh : hh - D.nh - D.nkv;
+  const int r = P.slot_req[row], br = P.slot_br[row];
+  const int lp = lp_of(S, pos);
+  const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + br) * S.n_lp + lp];
+  const int off = pos - lp_start(S, lp);
   const long long lay = (long long)layer * S.R * S.pool;
-  // q and k heads: pairs (i, i + hd/2)
-  for (int t = threadIdx.x; t < nqk * half; t += blockDim.x) {
-    const int hh = t / half, i = t % half;
-    float a = vals[hh * D.hd + i], c2 = vals[hh * D.hd + i + half];
-    if (D.arch == 1) {
-      const float cs = rope[((long long)pos * half + i) * 2], sn = rope[((long long)pos * half + i) * 2 + 1];
-      const float a2 = a * cs - c2 * sn, b2 = c2 * cs + a * sn;
-      a = a2;
-      c2 = b2;
-    }
-    if (hh < D.nh) {
-      stf(q + hh * D.hd + i, a);
-      stf(q + hh * D.hd + i + half, c2);
-    } else {
-      const int kvh = hh - D.nh;
-      T* dst = kk + (((lay + gpage) * D.nkv + kvh) * S.ps + off) * D.hd;
-      stf(dst + i, a);
-      stf(dst + i + half, c2);
-    }
-  }
-  for (int c = threadIdx.x; c < D.kv_dim; c += blockDim.x) {
-    const int kvh = c / D.hd, i = c % D.hd;
-    T* dst = vv + (((lay + gpage) * D.nkv + kvh) * S.ps + off) * D.hd;
-    stf(dst + i, vals[(D.nh + D.nkv) * D.hd + c]);
-  }
+  T* dst = reinterpret_cast<T*>(isk ? st.kv_k : st.kv_v) + (((lay + gpage) * D.nkv + kvh) * S.ps + off) * D.hd;
+  stf(dst + i, a);
+  stf(dst + i + half, b);
 }
 
 // ------------------------------------------------------------------ residual (+ norm)
+template <typename T> struct Vec4;
+template <> struct Vec4<float> {
+  static __device__ __forceinline__ void st(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+};
+template <> struct Vec4<__nv_bfloat16> {
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, float4 v) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+};
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_post_residual(Dims D, Pass P, PartRef pr, const float* __restrict__ ln) {
+__global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef pr, const float* __restrict__ ln) {
   if (*P.skip) return;
   __shared__ float sh[32];
   const int row = blockIdx.x;
@@ -116,16 +119,38 @@ __global__ void __launch_bounds__(256) k_post_residual(Dims D, Pass P, PartRef p
   float* x = P.x + (long long)row * D.d;
   T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
   float ss = 0.0f;
-  for (int c = threadIdx.x; c < D.d; c += blockDim.x) {
-    const float v = x[c] + part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c);
-    x[c] = v;
-    ss += v * v;
+  for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<float4*>(x + c);
+    const int ns = sk_nslots(pr.sk, row, c);
+    const float* pp = pr.part + (long long)row * pr.ldp + c;
+    float4 acc = *reinterpret_cast<const float4*>(pp);
+    for (int i = 1; i < ns; ++i) {
+      const float4 w = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane);
+      acc.x += w.x;
+      acc.y += w.y;
+      acc.z += w.z;
+      acc.w += w.w;
+    }
+    v.x += acc.x;
+    v.y += acc.y;
+    v.z += acc.z;
+    v.w += acc.w;
+    *reinterpret_cast<float4*>(x + c) = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   float inv = 1.0f;
   if (ln != nullptr) inv = 1.0f / sqrtf(block_sum(ss, sh) / (float)D.d + D.eps);
-  __syncthreads();
-  for (int c = threadIdx.x; c < D.d; c += blockDim.x)
-    stf(xn + c, ln != nullptr ? x[c] * inv * ln[c] : x[c]);
+  for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<float4*>(x + c);
+    if (ln != nullptr) {
+      const float4 g = *reinterpret_cast<const float4*>(ln + c);
+      v.x *= inv * g.x;
+      v.y *= inv * g.y;
+      v.z *= inv * g.z;
+      v.w *= inv * g.w;
+    }
+    Vec4<T>::st(xn + c, v);
+  }
 }
 
 // ------------------------------------------------------------------ SwiGLU
@@ -275,19 +300,14 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
                             int layer, const PartRef& pr, cudaStream_t s) {
   const float* bias = W.bqkv != nullptr ? W.bqkv + (long long)layer * D.qkv_out : nullptr;
   const size_t smem = (size_t)D.qkv_out * sizeof(float);
-  BB_DISPATCH(D, {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_post_qkv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-    k_post_qkv<T><<<P.rows_alloc, 256, smem, s>>>(D, S, P, st, bias, W.rope, layer, pr);
-  });
+  (void)smem;
+  dim3 grid(P.rows_alloc, D.nh + 2 * D.nkv);
+  BB_DISPATCH(D, (k_post_qkv<T><<<grid, D.hd / 2, 0, s>>>(D, S, P, st, bias, W.rope, layer, pr)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s) {
-  BB_DISPATCH(D, (k_post_residual<T><<<P.rows_alloc, 256, 0, s>>>(D, P, pr, ln)));
+  BB_DISPATCH(D, (k_post_residual<T><<<P.rows_alloc, 512, 0, s>>>(D, P, pr, ln)));
   return cudaGetLastError();
 }
 

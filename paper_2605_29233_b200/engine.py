@@ -116,16 +116,39 @@ class Session:
 
     # ---------------------------------------------------------------- results
     def fetch(self, trace: bool = True) -> dict:
+        """D2H of the run's results on the session stream (ctrl words, branch
+        rows, branch states and — if traced — the event records)."""
         torch = _torch()
-        self.stream.synchronize()
-        out = {"ctrl": self.v_ctrl.cpu().numpy(), "tokens": self.v_tokens.cpu().numpy(),
-               "branch": self.v_branch.cpu().numpy()}
-        self.d2h_bytes += out["ctrl"].nbytes + out["tokens"].nbytes + out["branch"].nbytes
-        if trace:
-            nmax = int(out["ctrl"][:, _lib.C_NEV].max())
-            out["events"] = self.v_events[:, :nmax].cpu().numpy()
-            self.d2h_bytes += out["events"].nbytes
+        with torch.cuda.stream(self.stream):
+            ctrl = self.v_ctrl.to("cpu", non_blocking=False)
+            out = {"ctrl": ctrl.numpy(), "tokens": self.v_tokens.cpu().numpy(),
+                   "branch": self.v_branch.cpu().numpy()}
+            self.d2h_bytes += out["ctrl"].nbytes + out["tokens"].nbytes + out["branch"].nbytes
+            if trace:
+                nmax = int(out["ctrl"][:, _lib.C_NEV].max())
+                out["events"] = self.v_events[:, :nmax].cpu().numpy()
+                self.d2h_bytes += out["events"].nbytes
         return out
+
+    def snapshot(self, dst_ctrl, dst_branch):
+        """Device-side copy of the result words (ctrl, branch state) into
+        caller buffers — no host sync (used inside timed regions)."""
+        torch = _torch()
+        with torch.cuda.stream(self.stream):
+            dst_ctrl.copy_(self.v_ctrl, non_blocking=True)
+            dst_branch.copy_(self.v_branch, non_blocking=True)
+
+    def gemm_stats(self, reset: bool = False):
+        buf = (C.c_ulonglong * 80)()
+        _lib.check(_lib.lib().bb_session_gemm_stats(self.h, buf, int(reset), C.c_void_p(self.stream.cuda_stream)),
+                   "bb_session_gemm_stats")
+        return [[int(buf[k * 5 + j]) for j in range(5)] for k in range(16)]
+
+    def counters(self):
+        buf = (C.c_longlong * 5)()
+        _lib.check(_lib.lib().bb_session_counters(self.h, buf), "bb_session_counters")
+        return {"kernel_launches": buf[0], "graph_launches": buf[1], "kernels_per_step": buf[2],
+                "kernels_per_step_refresh": buf[3], "kernels_prefill": buf[4]}
 
     def results(self, tasks, vocab, single=False, fetched=None):
         from .decoding import GenerationResult, NfeCounter
