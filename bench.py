@@ -310,7 +310,7 @@ def main():
     value = tot_tokens / (t_max_ms / 1e3)
 
     # ---- e2e through the public API (host buffers) ----
-    e2e_tasks = [bb.make_task(base_seed + 50000 + i, P, G, vocab) for i in range(K)]
+    e2e_tasks = tasks[Wm:Wm + K]  # same prompts as the device-resident run
     h2d0, d2h0 = s.h2d_bytes, s.d2h_bytes
     torch.cuda.synchronize()
     if dist is not None:

@@ -51,6 +51,10 @@ struct Session {
   long long nodes_iter = 0, nodes_iter_ref = 0, nodes_prefill = 0;
   long long kernel_launches = 0, graph_launches = 0;
   unsigned long long* tstat = nullptr;  // [16][8] per-GEMM-kind live timing
+  int* tile_cnt = nullptr;              // fused-epilogue arrival counters (self-resetting)
+  float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
+  float* ss_full = nullptr;
+  int ss_ld = 1;
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
   long long layout[BB_VIEW_COUNT][2];
@@ -212,6 +216,10 @@ static void plan(Session* s, char* base, bool dry) {
   H.skip = c.take<int>(1);
   s->full_rows = c.take<int>(1);
   s->tstat = c.take<unsigned long long>(16 * 8);
+  s->tile_cnt = c.take<int>(8192);
+  s->ss_ld = (D.d + 127) / 128;
+  s->ss_blk = c.take<float>((long long)s->blk.rows_alloc * s->ss_ld);
+  s->ss_full = c.take<float>((long long)s->full.rows_alloc * s->ss_ld);
   // GEMM partial planes: max over all stream-K GEMMs of (slots x rows x n_out)
   long long part = 1;
   if (D.dtype == BB_DTYPE_BF16) {
@@ -268,6 +276,38 @@ static int setup_gemms(Session* s) {
         }
         TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
+          EpiArgs& E = all[g]->p.epi;
+          memset(&E, 0, sizeof(E));
+          E.kind = g == 0 ? 2 : (g == 2 ? 3 : 4);
+          E.tile_cnt = s->tile_cnt;
+          E.slot_pos = P.slot_pos;
+          E.slot_req = P.slot_req;
+          E.slot_br = P.slot_br;
+          E.nh = D.nh;
+          E.nkv = D.nkv;
+          E.hd = D.hd;
+          E.rope = D.arch == BB_ARCH_LLADA;
+          E.bias = W.bqkv != nullptr ? W.bqkv + (size_t)l * D.qkv_out : nullptr;
+          E.rope_tab = W.rope;
+          E.q = (__nv_bfloat16*)P.q;
+          E.attn_dim = D.attn_dim;
+          E.kv_k = (__nv_bfloat16*)s->st.kv_k;
+          E.kv_v = (__nv_bfloat16*)s->st.kv_v;
+          E.kv_layer_off = (long long)l * s->S.R * s->S.pool;
+          E.pt = s->st.pt;
+          E.ps = s->S.ps;
+          E.P = s->S.P;
+          E.n_pp = s->S.n_pp;
+          E.L = s->S.L;
+          E.pool = s->S.pool;
+          E.B = s->S.B;
+          E.n_lp = s->S.n_lp;
+          E.act = (__nv_bfloat16*)P.act;
+          E.dff = D.dff;
+          E.x = P.x;
+          E.d = D.d;
+          E.ss_part = which == 0 ? s->ss_blk : s->ss_full;
+          E.ss_ld = s->ss_ld;
           all[g]->p.tstat = s->tstat + (size_t)(which * 8 + g) * 8;
           all[g]->p.part = s->part;
           all[g]->p.skip = P.skip;
@@ -329,15 +369,30 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
   const Weights& W = s->M->W;
   cudaError_t e;
   if ((e = launch_embed(D, s->S, P, W, st)) != cudaSuccess) return e;
+  const bool fused = D.dtype == BB_DTYPE_BF16;
+  float* ss = &P == &s->full ? s->ss_full : s->ss_blk;
   for (int l = 0; l < D.layers; ++l) {
     LayerGemms& lg = G.layers[l];
+    const float* next_ln = l + 1 < D.layers ? (D.arch == BB_ARCH_LLADA ? W.ln1 + (size_t)(l + 1) * D.d : nullptr)
+                                            : (D.arch == BB_ARCH_LLADA ? W.lnf : nullptr);
+    if (fused) {
+      // QKV (+bias, RoPE, KV splice) -> attention -> O (+residual) -> norm -> GU (+SwiGLU) -> down (+residual) -> norm
+      if ((e = tc_gemm_launch(lg.qkv, st)) != cudaSuccess) return e;
+      if ((e = launch_attn(D, s->S, P, s->st, l, st)) != cudaSuccess) return e;
+      if ((e = tc_gemm_launch(lg.o, st)) != cudaSuccess) return e;
+      if (D.dff) {
+        if ((e = launch_norm(D, P, ss, s->ss_ld, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
+        if ((e = tc_gemm_launch(lg.gu, st)) != cudaSuccess) return e;
+        if ((e = tc_gemm_launch(lg.dn, st)) != cudaSuccess) return e;
+      }
+      if ((e = launch_norm(D, P, ss, s->ss_ld, next_ln, st)) != cudaSuccess) return e;
+      continue;
+    }
     PartRef pr;
     if ((e = run_gemm(s, lg.qkv, lg.sqkv, &pr, st)) != cudaSuccess) return e;
     if ((e = launch_post_qkv(D, s->S, P, s->st, W, l, pr, st)) != cudaSuccess) return e;
     if ((e = launch_attn(D, s->S, P, s->st, l, st)) != cudaSuccess) return e;
     if ((e = run_gemm(s, lg.o, lg.so, &pr, st)) != cudaSuccess) return e;
-    const float* next_ln = l + 1 < D.layers ? (D.arch == BB_ARCH_LLADA ? W.ln1 + (size_t)(l + 1) * D.d : nullptr)
-                                            : (D.arch == BB_ARCH_LLADA ? W.lnf : nullptr);
     if (D.dff) {
       if ((e = launch_post_residual(D, P, pr, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
       if ((e = run_gemm(s, lg.gu, lg.sgu, &pr, st)) != cudaSuccess) return e;

@@ -196,6 +196,16 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& 
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -208,9 +218,9 @@ __global__ void __launch_bounds__(128) k_attn_mma(Dims D, Sess S, Pass P, DevSta
   constexpr int KC = 64, LD = HD + 8, QR = 64;
   extern __shared__ __align__(16) uint8_t smraw[];
   bf* sQ = reinterpret_cast<bf*>(smraw);
-  bf* sK = sQ + QR * LD;
-  bf* sV = sK + KC * LD;
-  long long* sKey = reinterpret_cast<long long*>(sV + KC * LD);
+  bf* sKb = sQ + QR * LD;          // [2][KC][LD]
+  bf* sVb = sKb + 2 * KC * LD;     // [2][KC][LD]
+  long long* sKey = reinterpret_cast<long long*>(sVb + 2 * KC * LD);
   __shared__ int sRow[QR];
 
   const int r = blockIdx.x / max_items, it = blockIdx.x % max_items;
@@ -239,13 +249,31 @@ __global__ void __launch_bounds__(128) k_attn_mma(Dims D, Sess S, Pass P, DevSta
   __syncthreads();
   constexpr int VPR = HD / 8;  // 16-byte vectors per row
   const bf* Qg = reinterpret_cast<const bf*>(P.q);
+  const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
+  const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
   for (int i = threadIdx.x; i < QR * VPR; i += blockDim.x) {
     const int rr = i / VPR, v = i % VPR;
     const int slot = sRow[rr];
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (slot >= 0) val = *reinterpret_cast<const uint4*>(Qg + (long long)slot * D.attn_dim + h * HD + v * 8);
-    *reinterpret_cast<uint4*>(sQ + rr * LD + v * 8) = val;
+    cp_async16(sQ + rr * LD + v * 8, Qg + (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8, slot >= 0);
   }
+  cp_async_commit();
+  auto load_chunk = [&](int c, int buf) {
+    const int kb = c * KC;
+    const int nk = min(KC, n_keys - kb);
+    bf* dK = sKb + buf * KC * LD;
+    bf* dV = sVb + buf * KC * LD;
+    for (int i = threadIdx.x; i < KC * VPR; i += blockDim.x) {
+      const int j = i / VPR, v = i % VPR;
+      const bool ok = j < nk;
+      const long long off = (ok ? sKey[kb + j] : 0) + v * 8;
+      cp_async16(dK + j * LD + v * 8, Kg + off, ok);
+      cp_async16(dV + j * LD + v * 8, Vg + off, ok);
+    }
+    cp_async_commit();
+  };
+  const int n_chunks = (n_keys + KC - 1) / KC;
+  load_chunk(0, 0);
+  cp_async_wait<1>();  // Q landed
   __syncthreads();
   uint32_t qf[HD / 16][4];
   {
@@ -263,24 +291,18 @@ __global__ void __launch_bounds__(128) k_attn_mma(Dims D, Sess S, Pass P, DevSta
   for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
   const float sl2 = D.attn_scale * 1.4426950408889634f;
-  const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
-  const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
-  const uint32_t sV_u = smem_u32(sV);
-  for (int k0 = 0; k0 < n_keys; k0 += KC) {
+  for (int ci = 0; ci < n_chunks; ++ci) {
+    const int k0 = ci * KC;
     const int nk = min(KC, n_keys - k0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < KC * VPR; i += blockDim.x) {
-      const int j = i / VPR, v = i % VPR;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (j < nk) {
-        const long long off = sKey[k0 + j] + v * 8;
-        kv = *reinterpret_cast<const uint4*>(Kg + off);
-        vv = *reinterpret_cast<const uint4*>(Vg + off);
-      }
-      *reinterpret_cast<uint4*>(sK + j * LD + v * 8) = kv;
-      *reinterpret_cast<uint4*>(sV + j * LD + v * 8) = vv;
+    if (ci + 1 < n_chunks) {
+      load_chunk(ci + 1, (ci + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const bf* sK = sKb + (ci & 1) * KC * LD;
+    const uint32_t sV_u = smem_u32(sVb + (ci & 1) * KC * LD);
     float s[KC / 8][4];
 #pragma unroll
     for (int nt = 0; nt < KC / 8; ++nt) {
@@ -351,6 +373,7 @@ __global__ void __launch_bounds__(128) k_attn_mma(Dims D, Sess S, Pass P, DevSta
         mma16816(o[nt2 + 1], a, b2, b3);
       }
     }
+    __syncthreads();
   }
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -386,20 +409,41 @@ __global__ void __launch_bounds__(256) k_attn_combine2(Dims D, Sess S, Pass P, i
   __shared__ int s_off[256];
   __shared__ int s_n;
   const int HD = D.hd;
-  if (threadIdx.x == 0) {
-    int n = 0;
-    const int ni = P.n_items[r];
-    for (int it = 0; it < ni && n < 256; ++it) {
-      const int mask = P.items[((long long)r * max_items + it) * ITW];
-      if (!((mask >> k) & 1)) continue;
-      int rii = j;
-      for (int k2 = 0; k2 < k; ++k2)
-        if ((mask >> k2) & 1) rii += P.rng_cnt[r * MAXB + k2];
-      s_off[n++] = (int)((((long long)r * max_items + it) * P.item_rows + rii) * D.nh + h);
-    }
-    s_n = n;
-  }
+  // parallel scan of the request's items: which cover this row's branch, at which item row
+  const int ni = P.n_items[r];
+  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
+  for (int base = 0; base < ni; base += blockDim.x) {
+    const int it = base + threadIdx.x;
+    int cover = 0, off = 0;
+    if (it < ni) {
+      const int mask = P.items[((long long)r * max_items + it) * ITW];
+      if ((mask >> k) & 1) {
+        int rii = j;
+        for (int k2 = 0; k2 < k; ++k2)
+          if ((mask >> k2) & 1) rii += P.rng_cnt[r * MAXB + k2];
+        cover = 1;
+        off = (int)((((long long)r * max_items + it) * P.item_rows + rii) * D.nh + h);
+      }
+    }
+    // stable compaction (item order preserved -> deterministic merge order)
+    const unsigned ballot = __ballot_sync(0xffffffffu, cover);
+    __shared__ int s_wc[8];
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (ln == 0) s_wc[w] = __popc(ballot);
+    __syncthreads();
+    int pre = s_n;
+    for (int ww = 0; ww < w; ++ww) pre += s_wc[ww];
+    pre += __popc(ballot & ((1u << ln) - 1u));
+    if (cover && pre < 256) s_off[pre] = off;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) tot += s_wc[ww];
+      s_n = min(256, s_n + tot);
+    }
+    __syncthreads();
+  }
   const int n = s_n;
   float M = -INFINITY;
   for (int i = 0; i < n; ++i) M = fmaxf(M, P.apart[(long long)s_off[i] * (HD + 2) + HD]);
@@ -422,7 +466,7 @@ template <int HD>
 static cudaError_t attn_mma_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                int max_items, cudaStream_t s) {
   const int max_keys = P.full ? S.L : S.ch_block * S.ps;
-  const size_t smem = (size_t)(64 + 2 * 64) * (HD + 8) * 2 + (size_t)max_keys * 8 + 16;
+  const size_t smem = (size_t)(64 + 4 * 64) * (HD + 8) * 2 + (size_t)max_keys * 8 + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attn_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

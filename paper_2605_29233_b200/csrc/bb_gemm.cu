@@ -62,11 +62,128 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr size_t RED = (size_t)3 * 4 * BN * 4;            // head epilogue
+  static constexpr size_t STG = (size_t)(32 * 129 + 4 * 32) * 4;    // fused epilogue staging
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16 +
-                                 (size_t)3 * 4 * BN * 4;
+                                 (RED > STG ? RED : STG);
 };
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ int e_lp_of(const EpiArgs& E, int pos) {
+  return pos < E.P ? pos / E.ps : E.n_pp + (pos - E.P) / E.ps;
+}
+__device__ __forceinline__ int e_lp_start(const EpiArgs& E, int lp) {
+  return lp < E.n_pp ? lp * E.ps : E.P + (lp - E.n_pp) * E.ps;
+}
+// write one element of the fused q|k|v output (head hh, dim i) for `row`
+__device__ __forceinline__ void qkv_store(const EpiArgs& E, int row, int pos, int hh, int i, float val) {
+  const __nv_bfloat16 b = __float2bfloat16_rn(val);
+  if (hh < E.nh) {
+    E.q[(long long)row * E.attn_dim + hh * E.hd + i] = b;
+    return;
+  }
+  const bool isk = hh < E.nh + E.nkv;
+  const int kvh = isk ? hh - E.nh : hh - E.nh - E.nkv;
+  const int r = E.slot_req[row], br = E.slot_br[row];
+  const int lp = e_lp_of(E, pos);
+  const long long gpage = (long long)r * E.pool + E.pt[((long long)r * E.B + br) * E.n_lp + lp];
+  const int off = pos - e_lp_start(E, lp);
+  __nv_bfloat16* dst = isk ? E.kv_k : E.kv_v;
+  dst[(((E.kv_layer_off + gpage) * E.nkv + kvh) * E.ps + off) * E.hd + i] = b;
+}
+
+// Apply the fused consumer op to 32 rows [rbase, rbase+32) of this tile; v[j]
+// is this thread's column c (0..127).  Called by all 128 epilogue threads.
+__device__ void epi_apply(const EpiArgs& E, float (&v)[32], int n0, int c, int et, int rbase, int rows_valid,
+                          int n_out, int ntile, float* stage) {
+  const int n = n0 + c;
+  const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3;
+  if (E.kind == 2) {
+    if (E.bias != nullptr && n < n_out) {
+      const float bv = E.bias[n];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += bv;
+    }
+    if (E.rope) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stage[j * 129 + c] = v[j];
+      epi_bar();
+      const int hd2 = E.hd >> 1;
+      for (int k = et; k < 32 * 64; k += 128) {
+        const int r = k >> 6, pr = k & 63;
+        const int hl = pr / hd2, i = pr % hd2;
+        const int ca = hl * E.hd + i, cb = ca + hd2;
+        const int row = rbase + r;
+        if (row >= rows_valid) continue;
+        const int pos = E.slot_pos[row];
+        if (pos < 0) continue;
+        float a = stage[r * 129 + ca], b = stage[r * 129 + cb];
+        const int hh = (n0 + ca) / E.hd;
+        if (hh < E.nh + E.nkv) {
+          const float2 cs = *reinterpret_cast<const float2*>(E.rope_tab + ((long long)pos * hd2 + i) * 2);
+          const float a2 = a * cs.x - b * cs.y, b2 = b * cs.x + a * cs.y;
+          a = a2;
+          b = b2;
+        }
+        qkv_store(E, row, pos, hh, i, a);
+        qkv_store(E, row, pos, hh, i + hd2, b);
+      }
+      epi_bar();
+    } else if (n < n_out) {
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int row = rbase + j;
+        if (row >= rows_valid) continue;
+        const int pos = E.slot_pos[row];
+        if (pos < 0) continue;
+        qkv_store(E, row, pos, n / E.hd, n % E.hd, v[j]);
+      }
+    }
+  } else if (E.kind == 3) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stage[j * 129 + c] = v[j];
+    epi_bar();
+    for (int k = et; k < 32 * 64; k += 128) {
+      const int r = k >> 6, f = k & 63;
+      const int row = rbase + r;
+      if (row >= rows_valid || E.slot_pos[row] < 0) continue;
+      const float g = stage[r * 129 + f], u = stage[r * 129 + 64 + f];
+      E.act[(long long)row * E.dff + ntile * 64 + f] = __float2bfloat16_rn(g / (1.0f + expf(-g)) * u);
+    }
+    epi_bar();
+  } else if (E.kind == 4) {
+    float* rs = stage + 32 * 129;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int row = rbase + j;
+      float nv = 0.0f;
+      if (row < rows_valid && E.slot_pos[row] >= 0) {
+        float* xp = E.x + (long long)row * E.d + n;
+        nv = *xp + v[j];
+        *xp = nv;
+      }
+      const float sq = warp_sum(nv * nv);
+      if (lane == 0) rs[q * 32 + j] = sq;
+    }
+    epi_bar();
+    if (et < 32) {
+      const int row = rbase + et;
+      if (row < rows_valid) E.ss_part[(long long)row * E.ss_ld + ntile] = rs[et] + rs[32 + et] + rs[64 + et] + rs[96 + et];
+    }
+    epi_bar();
+  }
+}
+
+__device__ __forceinline__ SplitK sk_of(const GemmTcParams& p, int G) {
+  SplitK sk;
+  sk.KB = p.KB;
+  sk.n_chunks = p.n_chunks;
+  sk.BN = p.rows_alloc / p.n_chunks;
+  sk.G = G;
+  sk.T = (long long)p.n_ntiles * p.n_chunks * p.KB;
+  return sk;
+}
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
@@ -82,7 +199,9 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* red = reinterpret_cast<float*>(tslot + 4);  // [3][4][BN]
+  float* red = reinterpret_cast<float*>(tslot + 4);  // [3][4][BN] (head) / staging (fused epilogue)
+  float* stage = red;
+  __shared__ int s_last;
 
   if (p.skip != nullptr && *p.skip != 0) return;
   tstat_begin(p.tstat);
@@ -183,18 +302,60 @@ __global__ void __launch_bounds__(192, 1)
       const int row0 = chunk * BN;
       const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       if (p.mode == 0) {
-        float* dst = p.part + (long long)u.slot * p.plane + n;
+        const EpiArgs& E = p.epi;
+        const int ns = E.kind == 0 ? 2 : sk_nslots(sk_of(p, gridDim.x), row0, ntile * 128);
+        const bool direct = E.kind != 0 && ns == 1;
+        if (!direct) {
+          float* dst = p.part + (long long)u.slot * p.plane + n;
+#pragma unroll 1
+          for (int j0 = 0; j0 < BN; j0 += 32) {
+            float v[32];
+            tmem_ld32(taddr + j0, v);
+            if (n < p.n_out) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int row = row0 + j0 + j;
+                if (row < rows_valid) dst[(long long)row * p.ldp] = v[j];
+              }
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1;
+          if (E.kind == 0) continue;
+          __threadfence();
+          epi_bar();
+          if (et == 0) {
+            const int old = atomicAdd(&E.tile_cnt[u.tile], 1);
+            s_last = old == ns - 1;
+            if (s_last) atomicExch(&E.tile_cnt[u.tile], 0);
+          }
+          epi_bar();
+          if (!s_last) continue;
+          __threadfence();
+#pragma unroll 1
+          for (int j0 = 0; j0 < BN; j0 += 32) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int row = row0 + j0 + j;
+              float a = 0.0f;
+              if (row < rows_valid && n < p.n_out) {
+                const float* pp = p.part + (long long)row * p.ldp + n;
+                for (int sl = 0; sl < ns; ++sl) a += __ldcg(pp + (long long)sl * p.plane);
+              }
+              v[j] = a;
+            }
+            epi_apply(E, v, ntile * 128, q * 32 + lane, et, row0 + j0, rows_valid, p.n_out, ntile, stage);
+          }
+          continue;
+        }
 #pragma unroll 1
         for (int j0 = 0; j0 < BN; j0 += 32) {
           float v[32];
           tmem_ld32(taddr + j0, v);
-          if (n < p.n_out) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int row = row0 + j0 + j;
-              if (row < rows_valid) dst[(long long)row * p.ldp] = v[j];
-            }
-          }
+          epi_apply(E, v, ntile * 128, q * 32 + lane, et, row0 + j0, rows_valid, p.n_out, ntile, stage);
         }
       } else {
         const float hs = p.head_scale, sc = p.spike_cut, sg = p.spike_gain;

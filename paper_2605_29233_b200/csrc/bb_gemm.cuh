@@ -13,6 +13,7 @@
 // deterministic and no fp32 atomics are used.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace bb {
@@ -46,6 +47,38 @@ __device__ __forceinline__ float part_sum(const float* __restrict__ part, long l
   return acc;
 }
 
+// Fused stream-K epilogue.  The CTA that completes a tile's last k-piece
+// (per-tile arrival counter) sums the pieces in slot order (deterministic)
+// and applies the consumer op in place of a separate post-GEMM kernel:
+//   kind 2  QKV: + bias, RoPE (pairs (i, i+hd/2) are tile-local for hd <= 128),
+//           q -> q buffer, k/v -> the row's branch KV page (the window splice)
+//   kind 3  gate/up: act = silu(gate) * up (gate/up rows interleaved per tile)
+//   kind 4  residual: x += out, per-(row, tile) sum of squares for RMSNorm
+// kind 0 keeps the raw partial planes (tests).
+struct EpiArgs {
+  int kind;
+  int* tile_cnt;
+  const int* slot_pos;
+  const int* slot_req;
+  const int* slot_br;
+  int nh, nkv, hd, rope;
+  const float* bias;
+  const float* rope_tab;
+  __nv_bfloat16* q;
+  int attn_dim;
+  __nv_bfloat16* kv_k;
+  __nv_bfloat16* kv_v;
+  long long kv_layer_off;
+  const int* pt;
+  int ps, P, n_pp, L, pool, B, n_lp;
+  __nv_bfloat16* act;
+  int dff;
+  float* x;
+  int d;
+  float* ss_part;
+  int ss_ld;
+};
+
 struct GemmTcParams {
   int n_out, K, n_ntiles, n_chunks, KB, mode;  // mode 0: partial planes, 1: LM-head epilogue
   int rows_alloc;
@@ -62,6 +95,7 @@ struct GemmTcParams {
   float head_scale, spike_cut, spike_gain;
   // live per-launch timing (%globaltimer): [min start, max end, CTAs done, sum ns, launches]
   unsigned long long* tstat;
+  EpiArgs epi;
 };
 
 struct TcGemm {

@@ -153,6 +153,38 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
   }
 }
 
+// ------------------------------------------------------------------ RMSNorm (fused-epilogue path)
+// xn = x * rsqrt(mean(x^2) + eps) * g  with the row's sum of squares taken from
+// the per-(row, 128-column tile) partials the residual GEMM epilogue wrote
+// (summed in tile order: deterministic).  ln == nullptr -> xn = x.
+template <typename T>
+__global__ void __launch_bounds__(512) k_norm(Dims D, Pass P, const float* __restrict__ ss_part, int ss_ld,
+                                              const float* __restrict__ ln) {
+  if (*P.skip) return;
+  const int row = blockIdx.x;
+  if (P.slot_pos[row] < 0) return;
+  float inv = 1.0f;
+  if (ln != nullptr) {
+    const float* sp = ss_part + (long long)row * ss_ld;
+    float ss = 0.0f;
+    for (int t = 0; t < ss_ld; ++t) ss += sp[t];
+    inv = 1.0f / sqrtf(ss / (float)D.d + D.eps);
+  }
+  const float* x = P.x + (long long)row * D.d;
+  T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
+  for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    if (ln != nullptr) {
+      const float4 g = *reinterpret_cast<const float4*>(ln + c);
+      v.x *= inv * g.x;
+      v.y *= inv * g.y;
+      v.z *= inv * g.z;
+      v.w *= inv * g.w;
+    }
+    Vec4<T>::st(xn + c, v);
+  }
+}
+
 // ------------------------------------------------------------------ SwiGLU
 template <typename T>
 __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
@@ -308,6 +340,12 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
 
 cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s) {
   BB_DISPATCH(D, (k_post_residual<T><<<P.rows_alloc, 512, 0, s>>>(D, P, pr, ln)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int ss_ld, const float* ln,
+                        cudaStream_t s) {
+  BB_DISPATCH(D, (k_norm<T><<<P.rows_alloc, 512, 0, s>>>(D, P, ss_part, ss_ld, ln)));
   return cudaGetLastError();
 }
 

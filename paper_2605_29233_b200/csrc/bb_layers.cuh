@@ -36,6 +36,8 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
                             int layer, const PartRef& pr, cudaStream_t s);
 cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s);
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s);
+cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int ss_ld, const float* ln,
+                        cudaStream_t s);
 cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, cudaStream_t s);
 cudaError_t launch_gather_head(const Dims& D, const Sess& S, const Pass& full, const Pass& blk, const Head& H,
                                int branch_filter, cudaStream_t s);
