@@ -55,6 +55,7 @@ struct Session {
   float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
   float* ss_full = nullptr;
   int ss_ld = 1;
+  bool fuse_epi = false;  // BB_FUSE_EPI=1: GEMM-epilogue fusion (experimental)
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
   long long layout[BB_VIEW_COUNT][2];
@@ -188,6 +189,7 @@ static void plan(Session* s, char* base, bool dry) {
     P.slot_req = c.take<int>(rows_alloc);
     P.slot_br = c.take<int>(rows_alloc);
     P.slot_tok = c.take<int>(rows_alloc);
+    P.slot_kvoff = c.take<long long>(rows_alloc);
     P.rng_off = c.take<int>(R * MAXB);
     P.rng_cnt = c.take<int>(R * MAXB);
     P.items = c.take<int>(R * max_items * ITW);
@@ -278,7 +280,7 @@ static int setup_gemms(Session* s) {
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
           EpiArgs& E = all[g]->p.epi;
           memset(&E, 0, sizeof(E));
-          E.kind = g == 0 ? 2 : (g == 2 ? 3 : 4);
+          E.kind = !s->fuse_epi ? 0 : (g == 0 ? 2 : (g == 2 ? 3 : 4));
           E.tile_cnt = s->tile_cnt;
           E.slot_pos = P.slot_pos;
           E.slot_req = P.slot_req;
@@ -369,7 +371,7 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
   const Weights& W = s->M->W;
   cudaError_t e;
   if ((e = launch_embed(D, s->S, P, W, st)) != cudaSuccess) return e;
-  const bool fused = D.dtype == BB_DTYPE_BF16;
+  const bool fused = D.dtype == BB_DTYPE_BF16 && s->fuse_epi;
   float* ss = &P == &s->full ? s->ss_full : s->ss_blk;
   for (int l = 0; l < D.layers; ++l) {
     LayerGemms& lg = G.layers[l];
@@ -627,6 +629,7 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   s->ws = (char*)workspace;
   for (int i = 0; i < BB_VIEW_COUNT; ++i)
     if (s->layout[i][1]) s->layout[i][0] += (long long)(base - (char*)workspace);
+  s->fuse_epi = getenv("BB_FUSE_EPI") != nullptr && atoi(getenv("BB_FUSE_EPI")) != 0;
   rc = setup_gemms(s);
   if (rc != BB_OK) {
     delete s;

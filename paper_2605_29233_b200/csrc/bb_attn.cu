@@ -395,6 +395,277 @@ __global__ void __launch_bounds__(128) k_attn_mma(Dims D, Sess S, Pass P, DevSta
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-prefix attention without partials (bf16 mma.sync, HD <= 128).
+//
+// CTA = (request, q-head, 64-row tile of the request's rows).  The rows may
+// belong to several branches.  The CTA walks logical pages lp = 0..n_lp-1;
+// for each lp it loads every DISTINCT physical page among its rows' branches
+// once (a page aliased by k branches -- prompt after prefill, everything after
+// a sync -- is streamed once for all of them) and scores it against all rows
+// with a per-key branch mask: row r only sees keys whose page its own branch
+// maps at that lp.  Online softmax per row, one pass, normalised output
+// written directly (no split-K partials, no combine kernel).
+template <int HD>
+__global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
+  if (*P.skip) return;
+  using bf = __nv_bfloat16;
+  constexpr int KC = 64, LD = HD + 8, QR = 64;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  bf* sQ = reinterpret_cast<bf*>(smraw);
+  bf* sKb = sQ + QR * LD;       // [2][KC][LD]
+  bf* sVb = sKb + 2 * KC * LD;  // [2][KC][LD]
+  long long* sSegOff = reinterpret_cast<long long*>(sVb + 2 * KC * LD);  // [n_seg] page element base
+  int* sSegStart = reinterpret_cast<int*>(sSegOff + S.n_lp * S.B);       // [n_seg+1] prefix of key counts
+  int* sSegMask = sSegStart + S.n_lp * S.B + 1;                          // [n_seg]
+  __shared__ long long sKeyOff[2][KC];
+  __shared__ int sKeyMask[2][KC];
+  __shared__ int sRow[QR], sBr[QR];
+  __shared__ int s_bmask, s_nseg;
+
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int row0 = blockIdx.z * QR;
+  if (row0 >= rows_per_req) return;
+  const int kvh = h / (D.nh / D.nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  if (threadIdx.x == 0) s_bmask = 0;
+  __syncthreads();
+  if (threadIdx.x < QR) {
+    const int lr = row0 + threadIdx.x;
+    int slot = -1, br = 0;
+    if (lr < rows_per_req) {
+      const int sl = slot_base + lr;
+      if (P.slot_pos[sl] >= 0) {
+        slot = sl;
+        br = P.slot_br[sl];
+        atomicOr(&s_bmask, 1 << br);
+      }
+    }
+    sRow[threadIdx.x] = slot;
+    sBr[threadIdx.x] = br;
+  }
+  __syncthreads();
+  const int bmask = s_bmask;
+  if (bmask == 0) return;
+  // segments: (lp, distinct physical page, branch mask) in lp order
+  const long long lay = (long long)layer * S.R * S.pool;
+  if (threadIdx.x == 0) {
+    int n = 0, acc = 0;
+    const int* ptr = st.pt + (long long)r * S.B * S.n_lp;
+    for (int lp = 0; lp < S.n_lp; ++lp) {
+      int left = bmask;
+      const int nk = lp_end(S, lp) - lp_start(S, lp);
+      while (left) {
+        const int k = __ffs(left) - 1;
+        const int phys = ptr[k * S.n_lp + lp];
+        int m = 0;
+        for (int k2 = k; k2 < S.B; ++k2)
+          if (((left >> k2) & 1) && ptr[k2 * S.n_lp + lp] == phys) m |= 1 << k2;
+        left &= ~m;
+        sSegOff[n] = ((lay + (long long)r * S.pool + phys) * D.nkv + kvh) * S.ps * HD;
+        sSegMask[n] = m;
+        sSegStart[n] = acc;
+        acc += nk;
+        ++n;
+      }
+    }
+    sSegStart[n] = acc;
+    s_nseg = n;
+  }
+  __syncthreads();
+  const int n_seg = s_nseg;
+  const int n_keys = sSegStart[n_seg];
+  constexpr int VPR = HD / 8;
+  const bf* Qg = reinterpret_cast<const bf*>(P.q);
+  const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
+  const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
+  for (int i = threadIdx.x; i < QR * VPR; i += blockDim.x) {
+    const int rr = i / VPR, v = i % VPR;
+    const int slot = sRow[rr];
+    cp_async16(sQ + rr * LD + v * 8, Qg + (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8, slot >= 0);
+  }
+  cp_async_commit();
+  auto fill_keys = [&](int c, int tb) {  // threads < KC: key c*KC+j -> (offset, mask)
+    if (threadIdx.x < KC) {
+      const int key = c * KC + threadIdx.x;
+      long long off = 0;
+      int m = 0;
+      if (key < n_keys) {
+        int lo = 0, hi = n_seg - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sSegStart[mid] <= key) lo = mid;
+          else hi = mid - 1;
+        }
+        off = sSegOff[lo] + (long long)(key - sSegStart[lo]) * HD;
+        m = sSegMask[lo];
+      }
+      sKeyOff[tb][threadIdx.x] = off;
+      sKeyMask[tb][threadIdx.x] = m;
+    }
+  };
+  auto load_chunk = [&](int c, int buf) {
+    const int nk = min(KC, n_keys - c * KC);
+    bf* dK = sKb + buf * KC * LD;
+    bf* dV = sVb + buf * KC * LD;
+    for (int i = threadIdx.x; i < KC * VPR; i += blockDim.x) {
+      const int j = i / VPR, v = i % VPR;
+      const bool ok = j < nk;
+      const long long off = sKeyOff[buf][j] + v * 8;
+      cp_async16(dK + j * LD + v * 8, Kg + off, ok);
+      cp_async16(dV + j * LD + v * 8, Vg + off, ok);
+    }
+    cp_async_commit();
+  };
+  const int n_chunks = (n_keys + KC - 1) / KC;
+  fill_keys(0, 0);
+  __syncthreads();
+  load_chunk(0, 0);
+  cp_async_wait<1>();
+  __syncthreads();
+  uint32_t qf[HD / 16][4];
+  {
+    const bf* q0 = sQ + (warp * 16 + g) * LD + 2 * t;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      qf[kk][0] = *reinterpret_cast<const uint32_t*>(q0 + 16 * kk);
+      qf[kk][1] = *reinterpret_cast<const uint32_t*>(q0 + 8 * LD + 16 * kk);
+      qf[kk][2] = *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + 8);
+      qf[kk][3] = *reinterpret_cast<const uint32_t*>(q0 + 8 * LD + 16 * kk + 8);
+    }
+  }
+  const int rA = warp * 16 + g, rB = rA + 8;
+  const int bA = sRow[rA] >= 0 ? sBr[rA] : 31, bB = sRow[rB] >= 0 ? sBr[rB] : 31;
+  const bool warp_live = __any_sync(0xffffffffu, sRow[rA] >= 0 || sRow[rB] >= 0);
+  float o[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+  const float sl2 = D.attn_scale * 1.4426950408889634f;
+  for (int ci = 0; ci < n_chunks; ++ci) {
+    const int nk = min(KC, n_keys - ci * KC);
+    if (ci + 1 < n_chunks) {
+      fill_keys(ci + 1, (ci + 1) & 1);
+      __syncthreads();
+      load_chunk(ci + 1, (ci + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (warp_live) {
+      const int tb = ci & 1;
+      const bf* sK = sKb + tb * KC * LD;
+      const uint32_t sV_u = smem_u32(sVb + tb * KC * LD);
+      float s[KC / 8][4];
+#pragma unroll
+      for (int nt = 0; nt < KC / 8; ++nt) {
+        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
+        const bf* k0p = sK + (8 * nt + g) * LD + 2 * t;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(k0p + 16 * kk);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(k0p + 16 * kk + 8);
+          mma16816(s[nt], qf[kk], b0, b1);
+        }
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < KC / 8; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 8 * nt + 2 * t + e;
+          const int km = j < nk ? sKeyMask[tb][j] : 0;
+          s[nt][e] = ((km >> bA) & 1) ? s[nt][e] * sl2 : -INFINITY;
+          s[nt][2 + e] = ((km >> bB) & 1) ? s[nt][2 + e] * sl2 : -INFINITY;
+        }
+        mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
+        mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      // rows with no visible key in this chunk keep their state (mn == -inf)
+      const float c0 = (m0 == -INFINITY || mn0 == -INFINITY) ? (mn0 == -INFINITY ? 1.0f : 0.0f) : exp2f(m0 - mn0);
+      const float c1 = (m1 == -INFINITY || mn1 == -INFINITY) ? (mn1 == -INFINITY ? 1.0f : 0.0f) : exp2f(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      float ps0 = 0.0f, ps1 = 0.0f;
+#pragma unroll
+      for (int nt = 0; nt < KC / 8; ++nt) {
+        s[nt][0] = mn0 == -INFINITY ? 0.0f : exp2f(s[nt][0] - mn0);
+        s[nt][1] = mn0 == -INFINITY ? 0.0f : exp2f(s[nt][1] - mn0);
+        s[nt][2] = mn1 == -INFINITY ? 0.0f : exp2f(s[nt][2] - mn1);
+        s[nt][3] = mn1 == -INFINITY ? 0.0f : exp2f(s[nt][3] - mn1);
+        ps0 += s[nt][0] + s[nt][1];
+        ps1 += s[nt][2] + s[nt][3];
+      }
+      l0 = l0 * c0 + ps0;
+      l1 = l1 * c1 + ps1;
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        o[i][0] *= c0;
+        o[i][1] *= c0;
+        o[i][2] *= c1;
+        o[i][3] *= c1;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KC / 16; ++kk) {
+        uint32_t a[4];
+        a[0] = pack_bf2(s[2 * kk][0], s[2 * kk][1]);
+        a[1] = pack_bf2(s[2 * kk][2], s[2 * kk][3]);
+        a[2] = pack_bf2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+        a[3] = pack_bf2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+        const int mi = lane >> 3, rr = lane & 7;
+        const int key = 16 * kk + (mi & 1) * 8 + rr;
+#pragma unroll
+        for (int nt2 = 0; nt2 < HD / 8; nt2 += 2) {
+          const int dim = 8 * nt2 + (mi >> 1) * 8;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(b0, b1, b2, b3, sV_u + (uint32_t)((key * LD + dim) * 2));
+          mma16816(o[nt2], a, b0, b1);
+          mma16816(o[nt2 + 1], a, b2, b3);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int lr = warp * 16 + g + 8 * half;
+    const int slot = sRow[lr];
+    if (slot < 0) continue;
+    const float inv = 1.0f / (half ? l1 : l0);
+    bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD;
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt)
+      *reinterpret_cast<__nv_bfloat162*>(out + 8 * nt + 2 * t) =
+          __floats2bfloat162_rn(o[nt][2 * half] * inv, o[nt][2 * half + 1] * inv);
+  }
+}
+
+template <int HD>
+static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
+                               cudaStream_t s) {
+  const int rows = P.full ? S.L : S.NRq;
+  const size_t smem = (size_t)(64 + 4 * 64) * (HD + 8) * 2 + (size_t)S.n_lp * S.B * (8 + 4 + 4) + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_seg<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid(S.R, D.nh, (rows + 63) / 64);
+  k_attn_seg<HD><<<grid, 128, smem, s>>>(D, S, P, st, layer, rows);
+  return cudaGetLastError();
+}
+
 // LSE-merge of the partials of the items covering (row, head).  CTA per
 // (row, head), one thread per head dim; fixed item order (deterministic).
 template <typename T>
@@ -498,11 +769,12 @@ cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevSt
   cudaError_t e = cudaErrorInvalidValue;
   dim3 cgrid(P.rows_alloc, D.nh);
   const int cthreads = D.hd < 256 ? D.hd : 256;
+  if (D.dtype == 1 && (D.hd == 64 || D.hd == 128)) {
+    return D.hd == 64 ? attn_seg_hd<64>(D, S, P, st, layer, s) : attn_seg_hd<128>(D, S, P, st, layer, s);
+  }
   if (D.dtype == 1) {
     using T = __nv_bfloat16;
-    if (D.hd == 64) e = attn_mma_hd<64>(D, S, P, st, layer, max_items, s);
-    else if (D.hd == 128) e = attn_mma_hd<128>(D, S, P, st, layer, max_items, s);
-    else if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);
+    if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);
     else if (D.hd == 32) e = attn_hd<T, 32>(D, S, P, st, layer, max_items, s);
     if (e != cudaSuccess) return e;
     k_attn_combine2<T><<<cgrid, cthreads, 0, s>>>(D, S, P, max_items);

@@ -268,6 +268,13 @@ __device__ void store_request(RC& c) {
   c.mask_id = D.V + 1;                                               \
   c.eos_id = D.V;
 
+// element offset (within one layer) of the K/V row of (request r, branch k, pos)
+__device__ __forceinline__ long long kv_row_off(const Dims& D, const Sess& S, const DevState& st, int r, int k, int pos) {
+  const int lp = lp_of(S, pos);
+  const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + k) * S.n_lp + lp];
+  return (gpage * D.nkv * S.ps + (pos - lp_start(S, lp))) * D.hd;
+}
+
 // boost / target of a head slot at `pos` of row `rw` (model.py:258-275, 306-317)
 __device__ void slot_boost(const Dims& D, const Sess& S, const int* rw, const int* target, int pos, float* boost,
                            int* tgt) {
@@ -348,6 +355,7 @@ __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk,
     full.slot_req[row] = r;
     full.slot_br[row] = 0;
     full.slot_tok[row] = c.rows[p];
+    full.slot_kvoff[row] = kv_row_off(D, S, st, r, 0, p);
   }
   // head slots: each branch's initial window over the base row
   const int* target = st.target + (long long)r * S.G;
@@ -562,6 +570,7 @@ __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
     blk.slot_pos[slot] = pos;
     const int tok = pos >= 0 ? c.rows[k * S.L + pos] : 0;
     blk.slot_tok[slot] = tok;
+    blk.slot_kvoff[slot] = pos >= 0 ? kv_row_off(D, S, st, r, k, pos) : 0;
     const int msk = pos >= 0 && tok == c.mask_id;
     H.masked[slot] = msk;
     if (msk) slot_boost(D, S, c.rows + k * S.L, target, pos, &H.boost[slot], &H.tgt[slot]);
@@ -664,7 +673,14 @@ __global__ void __launch_bounds__(256) k_merge_prep(Dims D, Sess S, DevState st,
     const int v = rows[s * S.L + i];
     const T* w = head + (long long)v * D.d;
     float a = 0.0f;
-    for (int c = lane; c < D.d; c += 32) a = fmaf(ldf(h + c), ldf(w + c), a);
+    constexpr int VE = 16 / sizeof(T);  // elements per 16-byte vector
+    for (int c = lane * VE; c < D.d; c += 32 * VE) {
+      const uint4 hv = *reinterpret_cast<const uint4*>(h + c), wv = *reinterpret_cast<const uint4*>(w + c);
+      const T* hp = reinterpret_cast<const T*>(&hv);
+      const T* wp = reinterpret_cast<const T*>(&wv);
+#pragma unroll
+      for (int e = 0; e < VE; ++e) a = fmaf(ldf(hp + e), ldf(wp + e), a);
+    }
     a = warp_sum(a);
     const float raw = a * D.head_scale;
     float l = raw + D.spike_gain * fmaxf(0.0f, raw - D.spike_cut);
@@ -911,6 +927,7 @@ __global__ void k_refresh_pack(Dims D, Sess S, DevState st, Pass full, Pass blk,
     full.slot_req[row] = r;
     full.slot_br[row] = k;
     full.slot_tok[row] = c.rows[k * S.L + p];
+    full.slot_kvoff[row] = live ? kv_row_off(D, S, st, r, k, p) : 0;
   }
   const int* target = st.target + (long long)r * S.G;
   for (int j = threadIdx.x; j < S.bs[k]; j += blockDim.x) {

@@ -85,12 +85,8 @@ __global__ void k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __r
   }
   const bool isk = hh < D.nh + D.nkv;
   const int kvh = isk ? hh - D.nh : hh - D.nh - D.nkv;
-  const int r = P.slot_req[row], br = P.slot_br[row];
-  const int lp = lp_of(S, pos);
-  const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + br) * S.n_lp + lp];
-  const int off = pos - lp_start(S, lp);
-  const long long lay = (long long)layer * S.R * S.pool;
-  T* dst = reinterpret_cast<T*>(isk ? st.kv_k : st.kv_v) + (((lay + gpage) * D.nkv + kvh) * S.ps + off) * D.hd;
+  const long long lay = (long long)layer * S.R * S.pool * D.nkv * S.ps * D.hd;
+  T* dst = reinterpret_cast<T*>(isk ? st.kv_k : st.kv_v) + lay + P.slot_kvoff[row] + (long long)kvh * S.ps * D.hd;
   stf(dst + i, a);
   stf(dst + i + half, b);
 }
@@ -191,12 +187,24 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
   if (*P.skip) return;
   const int row = blockIdx.y;
   if (P.slot_pos[row] < 0) return;
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (f >= D.dff) return;
-  const int cg = ((f >> 6) << 7) + (f & 63);
-  const float g = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, cg);
-  const float u = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, cg + 64);
-  stf(reinterpret_cast<T*>(P.act) + (long long)row * D.dff + f, g / (1.0f + expf(-g)) * u);
+  const int cg = ((f >> 6) << 7) + (f & 63);  // 4 gate features in one 64-block; up at +64
+  const int ns = sk_nslots(pr.sk, row, cg);
+  const float* pp = pr.part + (long long)row * pr.ldp + cg;
+  float4 g = *reinterpret_cast<const float4*>(pp), u = *reinterpret_cast<const float4*>(pp + 64);
+  for (int i = 1; i < ns; ++i) {
+    const float4 g2 = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane);
+    const float4 u2 = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane + 64);
+    g.x += g2.x; g.y += g2.y; g.z += g2.z; g.w += g2.w;
+    u.x += u2.x; u.y += u2.y; u.z += u2.z; u.w += u2.w;
+  }
+  float4 a;
+  a.x = g.x / (1.0f + expf(-g.x)) * u.x;
+  a.y = g.y / (1.0f + expf(-g.y)) * u.y;
+  a.z = g.z / (1.0f + expf(-g.z)) * u.z;
+  a.w = g.w / (1.0f + expf(-g.w)) * u.w;
+  Vec4<T>::st(reinterpret_cast<T*>(P.act) + (long long)row * D.dff + f, a);
 }
 
 // ------------------------------------------------------------------ head side
@@ -350,7 +358,7 @@ cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int 
 }
 
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s) {
-  dim3 grid((D.dff + 255) / 256, P.rows_alloc);
+  dim3 grid((D.dff / 4 + 255) / 256, P.rows_alloc);
   BB_DISPATCH(D, (k_post_gu<T><<<grid, 256, 0, s>>>(D, P, pr)));
   return cudaGetLastError();
 }

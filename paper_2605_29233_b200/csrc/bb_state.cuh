@@ -95,6 +95,7 @@ struct Pass {
   int* slot_req;
   int* slot_br;
   int* slot_tok;
+  long long* slot_kvoff;  // [rows_alloc] KV element offset of the row's (page, slot) within a layer
   int* rng_off;       // [R][MAXB] slot range of (request, branch)
   int* rng_cnt;
   int* items;         // [R][max_items][ITW]
