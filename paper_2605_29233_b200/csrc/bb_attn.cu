@@ -11,6 +11,8 @@
 // per branch group.  CTA = (item, q-head, 32-query tile); it writes an
 // unnormalised (o, m, l) partial; k_attn_combine merges the partials of the
 // items covering each row (flash-decoding style LSE merge, fixed order).
+#include <cooperative_groups.h>
+
 #include "bb_common.cuh"
 #include "bb_layers.cuh"
 
@@ -135,55 +137,10 @@ __global__ void __launch_bounds__(128) k_attn(Dims D, Sess S, Pass P, DevState s
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_attn_combine(Dims D, Sess S, Pass P, int max_items) {
-  if (*P.skip) return;
-  const int row = blockIdx.x;
-  const int pos = P.slot_pos[row];
-  if (pos < 0) return;
-  const int r = P.slot_req[row], k = P.slot_br[row];
-  const int j = row - P.rng_off[r * MAXB + k];
-  if (j < 0 || j >= P.rng_cnt[r * MAXB + k]) return;
-  const int HD = D.hd;
-  const int ni = P.n_items[r];
-  T* out = reinterpret_cast<T*>(P.attn) + (long long)row * D.attn_dim;
-  for (int h = 0; h < D.nh; ++h) {
-    // max over items covering this row
-    float M = -INFINITY;
-    for (int it = 0; it < ni; ++it) {
-      const int mask = P.items[((long long)r * max_items + it) * ITW];
-      if (!((mask >> k) & 1)) continue;
-      int rii = j;
-      for (int k2 = 0; k2 < k; ++k2)
-        if ((mask >> k2) & 1) rii += P.rng_cnt[r * MAXB + k2];
-      const float* o = P.apart + ((((long long)r * max_items + it) * P.item_rows + rii) * D.nh + h) * (HD + 2);
-      M = fmaxf(M, o[HD]);
-    }
-    for (int c = threadIdx.x; c < HD; c += blockDim.x) {
-      float acc = 0.0f, L = 0.0f;
-      for (int it = 0; it < ni; ++it) {
-        const int mask = P.items[((long long)r * max_items + it) * ITW];
-        if (!((mask >> k) & 1)) continue;
-        int rii = j;
-        for (int k2 = 0; k2 < k; ++k2)
-          if ((mask >> k2) & 1) rii += P.rng_cnt[r * MAXB + k2];
-        const float* o = P.apart + ((((long long)r * max_items + it) * P.item_rows + rii) * D.nh + h) * (HD + 2);
-        const float mi = o[HD];
-        if (mi == -INFINITY) continue;
-        const float w = expf(mi - M);
-        acc = fmaf(o[c], w, acc);
-        L = fmaf(o[HD + 1], w, L);
-      }
-      stf(out + h * HD + c, acc / L);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
-// bf16 tensor-core attention (mma.sync m16n8k16, fp32 accumulate), FA2-style:
-// 4 warps x 16 query rows, 64-key chunks staged in padded smem, online
-// softmax in the log2 domain, P reused from the S accumulators as the A
-// operand of P.V, V fragments via ldmatrix.trans.
+// bf16 tensor-core helpers (mma.sync m16n8k16, fp32 accumulate), FA2-style
+// fragments: P reused from the S accumulators as the A operand of P.V, V
+// fragments via ldmatrix.trans, cp.async 16-byte staging.
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -211,204 +168,25 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int HD>
-__global__ void __launch_bounds__(128) k_attn_mma(Dims D, Sess S, Pass P, DevState st, int layer, int max_items) {
-  if (*P.skip) return;
-  using bf = __nv_bfloat16;
-  constexpr int KC = 64, LD = HD + 8, QR = 64;
-  extern __shared__ __align__(16) uint8_t smraw[];
-  bf* sQ = reinterpret_cast<bf*>(smraw);
-  bf* sKb = sQ + QR * LD;          // [2][KC][LD]
-  bf* sVb = sKb + 2 * KC * LD;     // [2][KC][LD]
-  long long* sKey = reinterpret_cast<long long*>(sVb + 2 * KC * LD);
-  __shared__ int sRow[QR];
-
-  const int r = blockIdx.x / max_items, it = blockIdx.x % max_items;
-  if (it >= P.n_items[r]) return;
-  const int* item = P.items + ((long long)r * max_items + it) * ITW;
-  const int mask = item[0], lp0 = item[1], lp1 = item[2], rep = item[3];
-  int n_rows = 0;
-  for (int k = 0; k < S.B; ++k)
-    if ((mask >> k) & 1) n_rows += P.rng_cnt[r * MAXB + k];
-  const int row0 = blockIdx.z * QR;
-  if (row0 >= n_rows) return;
-  const int h = blockIdx.y, kvh = h / (D.nh / D.nkv);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-
-  const long long lay = (long long)layer * S.R * S.pool;
-  int n_keys = 0;
-  for (int lp = lp0; lp < lp1; ++lp) {
-    const int ks = lp_start(S, lp), ke = lp_end(S, lp);
-    const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + rep) * S.n_lp + lp];
-    const long long base = ((lay + gpage) * D.nkv + kvh) * S.ps * HD;
-    for (int j = threadIdx.x; j < ke - ks; j += blockDim.x) sKey[n_keys + j] = base + (long long)j * HD;
-    n_keys += ke - ks;
-  }
-  if (threadIdx.x < QR)
-    sRow[threadIdx.x] = (row0 + (int)threadIdx.x < n_rows) ? item_row_slot(P, S, r, mask, row0 + threadIdx.x) : -1;
-  __syncthreads();
-  constexpr int VPR = HD / 8;  // 16-byte vectors per row
-  const bf* Qg = reinterpret_cast<const bf*>(P.q);
-  const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
-  const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
-  for (int i = threadIdx.x; i < QR * VPR; i += blockDim.x) {
-    const int rr = i / VPR, v = i % VPR;
-    const int slot = sRow[rr];
-    cp_async16(sQ + rr * LD + v * 8, Qg + (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8, slot >= 0);
-  }
-  cp_async_commit();
-  auto load_chunk = [&](int c, int buf) {
-    const int kb = c * KC;
-    const int nk = min(KC, n_keys - kb);
-    bf* dK = sKb + buf * KC * LD;
-    bf* dV = sVb + buf * KC * LD;
-    for (int i = threadIdx.x; i < KC * VPR; i += blockDim.x) {
-      const int j = i / VPR, v = i % VPR;
-      const bool ok = j < nk;
-      const long long off = (ok ? sKey[kb + j] : 0) + v * 8;
-      cp_async16(dK + j * LD + v * 8, Kg + off, ok);
-      cp_async16(dV + j * LD + v * 8, Vg + off, ok);
-    }
-    cp_async_commit();
-  };
-  const int n_chunks = (n_keys + KC - 1) / KC;
-  load_chunk(0, 0);
-  cp_async_wait<1>();  // Q landed
-  __syncthreads();
-  uint32_t qf[HD / 16][4];
-  {
-    const bf* q0 = sQ + (warp * 16 + g) * LD + 2 * t;
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      qf[kk][0] = *reinterpret_cast<const uint32_t*>(q0 + 16 * kk);
-      qf[kk][1] = *reinterpret_cast<const uint32_t*>(q0 + 8 * LD + 16 * kk);
-      qf[kk][2] = *reinterpret_cast<const uint32_t*>(q0 + 16 * kk + 8);
-      qf[kk][3] = *reinterpret_cast<const uint32_t*>(q0 + 8 * LD + 16 * kk + 8);
-    }
-  }
-  float o[HD / 8][4];
-#pragma unroll
-  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
-  const float sl2 = D.attn_scale * 1.4426950408889634f;
-  for (int ci = 0; ci < n_chunks; ++ci) {
-    const int k0 = ci * KC;
-    const int nk = min(KC, n_keys - k0);
-    if (ci + 1 < n_chunks) {
-      load_chunk(ci + 1, (ci + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const bf* sK = sKb + (ci & 1) * KC * LD;
-    const uint32_t sV_u = smem_u32(sVb + (ci & 1) * KC * LD);
-    float s[KC / 8][4];
-#pragma unroll
-    for (int nt = 0; nt < KC / 8; ++nt) {
-      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
-      const bf* k0p = sK + (8 * nt + g) * LD + 2 * t;
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(k0p + 16 * kk);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(k0p + 16 * kk + 8);
-        mma16816(s[nt], qf[kk], b0, b1);
-      }
-    }
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < KC / 8; ++nt) {
-      const int j = 8 * nt + 2 * t;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool valid = (j + (e & 1)) < nk;
-        s[nt][e] = valid ? s[nt][e] * sl2 : -INFINITY;
-      }
-      mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
-      mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float c0 = m0 == -INFINITY ? 0.0f : exp2f(m0 - mn0);
-    const float c1 = m1 == -INFINITY ? 0.0f : exp2f(m1 - mn1);
-    m0 = mn0;
-    m1 = mn1;
-    float ps0 = 0.0f, ps1 = 0.0f;
-#pragma unroll
-    for (int nt = 0; nt < KC / 8; ++nt) {
-      s[nt][0] = exp2f(s[nt][0] - mn0);
-      s[nt][1] = exp2f(s[nt][1] - mn0);
-      s[nt][2] = exp2f(s[nt][2] - mn1);
-      s[nt][3] = exp2f(s[nt][3] - mn1);
-      ps0 += s[nt][0] + s[nt][1];
-      ps1 += s[nt][2] + s[nt][3];
-    }
-    l0 = l0 * c0 + ps0;
-    l1 = l1 * c1 + ps1;
-#pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      o[i][0] *= c0;
-      o[i][1] *= c0;
-      o[i][2] *= c1;
-      o[i][3] *= c1;
-    }
-#pragma unroll
-    for (int kk = 0; kk < KC / 16; ++kk) {
-      uint32_t a[4];
-      a[0] = pack_bf2(s[2 * kk][0], s[2 * kk][1]);
-      a[1] = pack_bf2(s[2 * kk][2], s[2 * kk][3]);
-      a[2] = pack_bf2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-      a[3] = pack_bf2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-      const int mi = lane >> 3, rr = lane & 7;
-      const int key = 16 * kk + (mi & 1) * 8 + rr;
-#pragma unroll
-      for (int nt2 = 0; nt2 < HD / 8; nt2 += 2) {
-        const int dim = 8 * nt2 + (mi >> 1) * 8;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(b0, b1, b2, b3, sV_u + (uint32_t)((key * LD + dim) * 2));
-        mma16816(o[nt2], a, b0, b1);
-        mma16816(o[nt2 + 1], a, b2, b3);
-      }
-    }
-    __syncthreads();
-  }
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float LN2 = 0.6931471805599453f;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const int lr = warp * 16 + g + 8 * half;
-    if (sRow[lr] < 0) continue;
-    float* op = P.apart + ((((long long)r * max_items + it) * P.item_rows + row0 + lr) * D.nh + h) * (HD + 2);
-#pragma unroll
-    for (int nt = 0; nt < HD / 8; ++nt)
-      *reinterpret_cast<float2*>(op + 8 * nt + 2 * t) = make_float2(o[nt][2 * half], o[nt][2 * half + 1]);
-    if (t == 0) {
-      op[HD] = (half ? m1 : m0) * LN2;
-      op[HD + 1] = half ? l1 : l0;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Shared-prefix attention without partials (bf16 mma.sync, HD <= 128).
 //
-// CTA = (request, q-head, 64-row tile of the request's rows).  The rows may
-// belong to several branches.  The CTA walks logical pages lp = 0..n_lp-1;
+// Cluster of ATT_CS CTAs = (request, q-head, 64-row tile of the request's
+// rows); each CTA of the cluster takes 1/ATT_CS of the key chunks and the
+// partial softmax states are merged through distributed shared memory
+// (each CTA normalises 64/ATT_CS rows).  The rows may belong to several
+// branches.  The CTA walks logical pages lp = 0..n_lp-1;
 // for each lp it loads every DISTINCT physical page among its rows' branches
 // once (a page aliased by k branches -- prompt after prefill, everything after
 // a sync -- is streamed once for all of them) and scores it against all rows
 // with a per-key branch mask: row r only sees keys whose page its own branch
 // maps at that lp.  Online softmax per row, one pass, normalised output
 // written directly (no split-K partials, no combine kernel).
+constexpr int ATT_CS = 4;
+
 template <int HD>
-__global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
-  if (*P.skip) return;
+__global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
+    k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
   using bf = __nv_bfloat16;
   constexpr int KC = 64, LD = HD + 8, QR = 64;
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -423,9 +201,11 @@ __global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevSta
   __shared__ int sRow[QR], sBr[QR];
   __shared__ int s_bmask, s_nseg;
 
-  const int r = blockIdx.x, h = blockIdx.y;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int r = blockIdx.x / ATT_CS, h = blockIdx.y;
   const int row0 = blockIdx.z * QR;
-  if (row0 >= rows_per_req) return;
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int slot_base = P.full ? r * S.L : r * S.NRq;
@@ -434,7 +214,7 @@ __global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevSta
   if (threadIdx.x < QR) {
     const int lr = row0 + threadIdx.x;
     int slot = -1, br = 0;
-    if (lr < rows_per_req) {
+    if (lr < rows_per_req && !*P.skip) {
       const int sl = slot_base + lr;
       if (P.slot_pos[sl] >= 0) {
         slot = sl;
@@ -447,7 +227,6 @@ __global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevSta
   }
   __syncthreads();
   const int bmask = s_bmask;
-  if (bmask == 0) return;
   // segments: (lp, distinct physical page, branch mask) in lp order
   const long long lay = (long long)layer * S.R * S.pool;
   if (threadIdx.x == 0) {
@@ -518,11 +297,17 @@ __global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevSta
     }
     cp_async_commit();
   };
-  const int n_chunks = (n_keys + KC - 1) / KC;
-  fill_keys(0, 0);
-  __syncthreads();
-  load_chunk(0, 0);
-  cp_async_wait<1>();
+  const int n_all = bmask ? (n_keys + KC - 1) / KC : 0;
+  const int c_begin = (int)((long long)n_all * crank / ATT_CS), c_end = (int)((long long)n_all * (crank + 1) / ATT_CS);
+  const int n_chunks = c_end - c_begin;
+  if (n_chunks > 0) {
+    fill_keys(c_begin, 0);
+    __syncthreads();
+    load_chunk(c_begin, 0);
+    cp_async_wait<1>();
+  } else {
+    cp_async_wait<0>();
+  }
   __syncthreads();
   uint32_t qf[HD / 16][4];
   {
@@ -544,11 +329,11 @@ __global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevSta
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
   const float sl2 = D.attn_scale * 1.4426950408889634f;
   for (int ci = 0; ci < n_chunks; ++ci) {
-    const int nk = min(KC, n_keys - ci * KC);
+    const int nk = min(KC, n_keys - (c_begin + ci) * KC);
     if (ci + 1 < n_chunks) {
-      fill_keys(ci + 1, (ci + 1) & 1);
+      fill_keys(c_begin + ci + 1, (ci + 1) & 1);
       __syncthreads();
-      load_chunk(ci + 1, (ci + 1) & 1);
+      load_chunk(c_begin + ci + 1, (ci + 1) & 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -637,18 +422,58 @@ __global__ void __launch_bounds__(128) k_attn_seg(Dims D, Sess S, Pass P, DevSta
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  // partial state -> own smem (reuses the K buffers): o [QR][HD+4], m, l [QR]
+  constexpr int OLD = HD + 4;
+  float* sO = reinterpret_cast<float*>(sKb);
+  float* sM = sO + QR * OLD;
+  float* sL = sM + QR;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int lr = warp * 16 + g + 8 * half;
-    const int slot = sRow[lr];
-    if (slot < 0) continue;
-    const float inv = 1.0f / (half ? l1 : l0);
-    bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD;
 #pragma unroll
     for (int nt = 0; nt < HD / 8; ++nt)
-      *reinterpret_cast<__nv_bfloat162*>(out + 8 * nt + 2 * t) =
-          __floats2bfloat162_rn(o[nt][2 * half] * inv, o[nt][2 * half + 1] * inv);
+      *reinterpret_cast<float2*>(sO + lr * OLD + 8 * nt + 2 * t) = make_float2(o[nt][2 * half], o[nt][2 * half + 1]);
+    if (t == 0) {
+      sM[lr] = half ? m1 : m0;
+      sL[lr] = half ? l1 : l0;
+    }
   }
+  cluster.sync();
+  // merge: this CTA normalises rows [crank*QR/CS, (crank+1)*QR/CS) across the cluster
+  constexpr int RPC = QR / ATT_CS;
+  constexpr int V4 = HD / 4;
+  for (int i = threadIdx.x; i < RPC * V4; i += blockDim.x) {
+    const int lr = crank * RPC + i / V4, c4 = (i % V4) * 4;
+    const int slot = sRow[lr];
+    if (slot < 0) continue;
+    float mr[ATT_CS], M = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < ATT_CS; ++q) {
+      mr[q] = *cluster.map_shared_rank(sM + lr, q);
+      M = fmaxf(M, mr[q]);
+    }
+    float Lsum = 0.0f;
+    float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+    for (int q = 0; q < ATT_CS; ++q) {
+      if (mr[q] == -INFINITY) continue;
+      const float w = exp2f(mr[q] - M);
+      Lsum += w * *cluster.map_shared_rank(sL + lr, q);
+      const float4 v = *reinterpret_cast<const float4*>(cluster.map_shared_rank(sO + lr * OLD + c4, q));
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
+    }
+    const float inv = 1.0f / Lsum;
+    bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), p1 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&p0);
+    u.y = *reinterpret_cast<uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(out) = u;
+  }
+  cluster.sync();
 }
 
 template <int HD>
@@ -661,7 +486,7 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
     cudaFuncSetAttribute(k_attn_seg<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  dim3 grid(S.R, D.nh, (rows + 63) / 64);
+  dim3 grid(S.R * ATT_CS, D.nh, (rows + 63) / 64);
   k_attn_seg<HD><<<grid, 128, smem, s>>>(D, S, P, st, layer, rows);
   return cudaGetLastError();
 }
@@ -731,21 +556,6 @@ __global__ void __launch_bounds__(256) k_attn_combine2(Dims D, Sess S, Pass P, i
     }
     stf(out + c, acc / L);
   }
-}
-
-template <int HD>
-static cudaError_t attn_mma_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
-                               int max_items, cudaStream_t s) {
-  const int max_keys = P.full ? S.L : S.ch_block * S.ps;
-  const size_t smem = (size_t)(64 + 4 * 64) * (HD + 8) * 2 + (size_t)max_keys * 8 + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_attn_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  dim3 grid(S.R * max_items, D.nh, (P.item_rows + 63) / 64);
-  k_attn_mma<HD><<<grid, 128, smem, s>>>(D, S, P, st, layer, max_items);
-  return cudaGetLastError();
 }
 
 template <typename T, int HD>

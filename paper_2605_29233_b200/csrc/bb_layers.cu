@@ -55,15 +55,18 @@ __global__ void __launch_bounds__(256) k_embed(Dims D, Pass P, const T* __restri
 }
 
 // ------------------------------------------------------------------ post QKV
-// CTA = (row, head of the fused q|k|v output), one thread per (i, i+hd/2) pair.
+// CTA = (row, group of heads of the fused q|k|v output); one thread per
+// (i, i+hd/2) pair of one head.
 template <typename T>
-__global__ void k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
-                           const float* __restrict__ rope, int layer, PartRef pr) {
+__global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
+                                                  const float* __restrict__ rope, int layer, PartRef pr) {
   if (*P.skip) return;
-  const int row = blockIdx.x, hh = blockIdx.y, i = threadIdx.x;
+  const int half = D.hd >> 1;
+  const int row = blockIdx.x;
+  const int hh = blockIdx.y * (blockDim.x / half) + threadIdx.x / half, i = threadIdx.x % half;
+  if (hh >= D.nh + 2 * D.nkv) return;
   const int pos = P.slot_pos[row];
   if (pos < 0) return;
-  const int half = D.hd >> 1;
   const int c0 = hh * D.hd + i, c1 = c0 + half;
   float a = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c0);
   float b = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c1);
@@ -341,8 +344,10 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
   const float* bias = W.bqkv != nullptr ? W.bqkv + (long long)layer * D.qkv_out : nullptr;
   const size_t smem = (size_t)D.qkv_out * sizeof(float);
   (void)smem;
-  dim3 grid(P.rows_alloc, D.nh + 2 * D.nkv);
-  BB_DISPATCH(D, (k_post_qkv<T><<<grid, D.hd / 2, 0, s>>>(D, S, P, st, bias, W.rope, layer, pr)));
+  const int heads = D.nh + 2 * D.nkv, half = D.hd / 2;
+  const int hpb = half >= 512 ? 1 : 512 / half;  // heads per CTA
+  dim3 grid(P.rows_alloc, (heads + hpb - 1) / hpb);
+  BB_DISPATCH(D, (k_post_qkv<T><<<grid, hpb * half, 0, s>>>(D, S, P, st, bias, W.rope, layer, pr)));
   return cudaGetLastError();
 }
 
