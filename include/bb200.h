@@ -91,7 +91,13 @@ typedef struct {
 #define BB_VIEW_PM_S 8     /* fp32  [R][B][L]      prob-map sum-exp         */
 #define BB_VIEW_PAGES 9    /* int32 [R][B][n_lp]   KV page tables           */
 #define BB_VIEW_REFC 10    /* int32 [R][pool]      page refcounts           */
-#define BB_VIEW_COUNT 11
+#define BB_VIEW_HEAD_MASKED 11 /* int32 [NR]     head slot reports a masked position */
+#define BB_VIEW_HEAD_M 12  /* fp32  [NR]           max logit of the slot     */
+#define BB_VIEW_HEAD_S 13  /* fp32  [NR]           sum exp(logit - max)      */
+#define BB_VIEW_HEAD_ARG 14 /* int32 [NR]          argmax (lowest id)        */
+#define BB_VIEW_SLOT_POS 15 /* int32 [NR]          position of the slot      */
+#define BB_VIEW_SLOT_BR 16 /* int32 [NR]           branch of the slot        */
+#define BB_VIEW_COUNT 17
 
 BB_API int bb_session_workspace_bytes(const void* model, const bb_session_desc* d, size_t* bytes);
 BB_API int bb_session_create(void* model, const bb_session_desc* d, void* workspace, size_t bytes, void** sess);

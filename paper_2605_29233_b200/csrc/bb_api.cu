@@ -52,6 +52,8 @@ struct Session {
   long long kernel_launches = 0, graph_launches = 0;
   unsigned long long* tstat = nullptr;  // [16][8] per-GEMM-kind live timing
   int* tile_cnt = nullptr;              // fused-epilogue arrival counters (self-resetting)
+  unsigned char* ns_tabs = nullptr;     // per-GEMM-shape stream-K piece counts
+  size_t ns_used = 0, ns_cap = 0;
   float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
   float* ss_full = nullptr;
   int ss_ld = 1;
@@ -215,10 +217,18 @@ static void plan(Session* s, char* base, bool dry) {
   H.res_arg = c.take<int>(rb);
   H.res_m = c.take<float>(rb);
   H.res_s = c.take<float>(rb);
+  view(BB_VIEW_HEAD_MASKED, H.masked, (size_t)rb * 4);
+  view(BB_VIEW_HEAD_M, H.res_m, (size_t)rb * 4);
+  view(BB_VIEW_HEAD_S, H.res_s, (size_t)rb * 4);
+  view(BB_VIEW_HEAD_ARG, H.res_arg, (size_t)rb * 4);
+  view(BB_VIEW_SLOT_POS, s->blk.slot_pos, (size_t)rb * 4);
+  view(BB_VIEW_SLOT_BR, s->blk.slot_br, (size_t)rb * 4);
   H.skip = c.take<int>(1);
   s->full_rows = c.take<int>(1);
   s->tstat = c.take<unsigned long long>(16 * 8);
   s->tile_cnt = c.take<int>(8192);
+  s->ns_cap = 64 * 1024;
+  s->ns_tabs = c.take<unsigned char>(s->ns_cap);
   s->ss_ld = (D.d + 127) / 128;
   s->ss_blk = c.take<float>((long long)s->blk.rows_alloc * s->ss_ld);
   s->ss_full = c.take<float>((long long)s->full.rows_alloc * s->ss_ld);
@@ -255,6 +265,23 @@ static void plan(Session* s, char* base, bool dry) {
   s->ws_bytes = c.off + 1024;
 }
 
+static PartRef pref_tc(const TcGemm& g, const float* part) {
+  return PartRef{part, g.p.plane, g.p.ldp, g.sk};
+}
+
+// per-tile stream-K piece counts (avoids 64-bit divisions in consumers)
+static int attach_ns_table(Session* s, TcGemm& g) {
+  const long long tiles = (long long)g.p.n_ntiles * g.p.n_chunks;
+  if (s->ns_used + tiles > s->ns_cap) return BB_ERR_NOMEM;
+  std::vector<unsigned char> tab(tiles);
+  for (long long t = 0; t < tiles; ++t)
+    tab[t] = (unsigned char)(sk_owner(t * g.sk.KB + g.sk.KB - 1, g.sk.T, g.sk.G) - sk_owner(t * g.sk.KB, g.sk.T, g.sk.G) + 1);
+  unsigned char* dst = s->ns_tabs + s->ns_used;
+  if (cudaMemcpy(dst, tab.data(), tiles, cudaMemcpyHostToDevice) != cudaSuccess) return BB_ERR_CUDA;
+  g.sk.ns_tab = dst;
+  s->ns_used += (tiles + 15) / 16 * 16;
+  return BB_OK;
+}
 static int setup_gemms(Session* s) {
   const Dims& D = s->D;
   const Weights& W = s->M->W;
@@ -311,6 +338,7 @@ static int setup_gemms(Session* s) {
           E.ss_part = which == 0 ? s->ss_blk : s->ss_full;
           E.ss_ld = s->ss_ld;
           all[g]->p.tstat = s->tstat + (size_t)(which * 8 + g) * 8;
+          if (attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
           all[g]->p.part = s->part;
           all[g]->p.skip = P.skip;
           all[g]->p.rows_valid = which == 1 ? s->full_rows : nullptr;
@@ -348,9 +376,6 @@ static int setup_gemms(Session* s) {
   return BB_OK;
 }
 
-static PartRef pref_tc(const TcGemm& g, const float* part) {
-  return PartRef{part, g.p.plane, g.p.ldp, g.sk};
-}
 static PartRef pref_simt(const SimtGemm& g) {
   SplitK sk{};
   return PartRef{g.out, 0, g.ldo, sk};

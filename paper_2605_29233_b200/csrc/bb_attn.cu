@@ -227,11 +227,15 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   }
   __syncthreads();
   const int bmask = s_bmask;
-  // segments: (lp, distinct physical page, branch mask) in lp order
+  // segments: (lp, distinct physical page, branch mask) in lp order; the
+  // request's page tables are staged in smem first (one parallel load)
   const long long lay = (long long)layer * S.R * S.pool;
+  int* sPT = reinterpret_cast<int*>(sSegMask + S.n_lp * S.B);
+  for (int i = threadIdx.x; i < S.B * S.n_lp; i += blockDim.x) sPT[i] = st.pt[(long long)r * S.B * S.n_lp + i];
+  __syncthreads();
   if (threadIdx.x == 0) {
     int n = 0, acc = 0;
-    const int* ptr = st.pt + (long long)r * S.B * S.n_lp;
+    const int* ptr = sPT;
     for (int lp = 0; lp < S.n_lp; ++lp) {
       int left = bmask;
       const int nk = lp_end(S, lp) - lp_start(S, lp);
@@ -480,7 +484,7 @@ template <int HD>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                cudaStream_t s) {
   const int rows = P.full ? S.L : S.NRq;
-  const size_t smem = (size_t)(64 + 4 * 64) * (HD + 8) * 2 + (size_t)S.n_lp * S.B * (8 + 4 + 4) + 16;
+  const size_t smem = (size_t)(64 + 4 * 64) * (HD + 8) * 2 + (size_t)S.n_lp * S.B * (8 + 4 + 4 + 4) + 32;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attn_seg<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

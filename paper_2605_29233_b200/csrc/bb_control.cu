@@ -48,6 +48,34 @@ __device__ __forceinline__ int cta_min(int v, int* red) {
   return t;
 }
 
+// CTA-wide (max value, lowest index); invalid lanes pass v = -inf, idx = INT_MAX.
+__device__ __forceinline__ int cta_argmax_first(float v, int idx, float* redf, int* redi) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    redf[threadIdx.x >> 5] = v;
+    redi[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  float bv = redf[0];
+  int bi = redi[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+    if (redf[w] > bv || (redf[w] == bv && redi[w] < bi)) {
+      bv = redf[w];
+      bi = redi[w];
+    }
+  __syncthreads();
+  return bi;
+}
+
 struct RC {  // request context
   const Dims* D;
   const Sess* S;
@@ -413,10 +441,38 @@ __device__ int eq1_commit(const float* conf, const int* arg, const int* pos, con
   return cnt;
 }
 
+// Eq. 1 for branch k over its head slots, CTA-parallel: i* = first max conf
+// (lowest position), commit iff conf >= tau or i == i*.  All threads call;
+// returns #commits.
 __device__ int apply_commits(RC& c, const Pass& blk, const Head& H, int k, float tau) {
+  __shared__ float redf[32];
+  __shared__ int redi[32];
   const int slot0 = c.r * c.S->NRq + c.S->off[k];
-  return eq1_commit(H.res_conf + slot0, H.res_arg + slot0, blk.slot_pos + slot0, H.masked + slot0, c.S->bs[k], tau,
-                    c.row(k), nullptr);
+  const int n = c.S->bs[k];
+  int star = 0x7fffffff;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    const bool valid = j < n && H.masked[slot0 + j];
+    const float cf = valid ? H.res_conf[slot0 + j] : -INFINITY;
+    const int cand = cta_argmax_first(cf, valid ? j : 0x7fffffff, redf, redi);
+    if (cand != 0x7fffffff) {
+      // combine with previous bases (earlier j wins ties)
+      if (star == 0x7fffffff || H.res_conf[slot0 + cand] > H.res_conf[slot0 + star]) star = cand;
+    }
+  }
+  if (star == 0x7fffffff) return 0;
+  int cnt = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    bool commit = false;
+    if (j < n && H.masked[slot0 + j]) {
+      const int slot = slot0 + j;
+      commit = H.res_conf[slot] >= tau || j == star;
+      if (commit) c.row(k)[blk.slot_pos[slot]] = H.res_arg[slot];
+    }
+    cnt += __syncthreads_count(commit);
+  }
+  return cnt;
 }
 
 __global__ void k_prefill_post(Dims D, Sess S, DevState st, Pass blk, Head H) {
@@ -432,7 +488,10 @@ __global__ void k_prefill_post(Dims D, Sess S, DevState st, Pass blk, Head H) {
     if (threadIdx.x == 0) s_n = -1;
     __syncthreads();
     const bool any = c.has_mask(k, c.B_(k, B_START), c.B_(k, B_END));
-    if (any && threadIdx.x == 0) s_n = apply_commits(c, blk, H, k, S.tau_conf);
+    if (any) {
+      const int nc = apply_commits(c, blk, H, k, S.tau_conf);
+      if (threadIdx.x == 0) s_n = nc;
+    }
     __syncthreads();
     if (any) {
       const int dec = c.count_decoded(k);
@@ -488,11 +547,12 @@ __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
         const int lp0 = lp_of(S, c.B_(k, B_START)), lp1 = lp_of(S, c.B_(k, B_END) - 1);
         for (int lp = lp0; lp <= lp1; ++lp) c.write_intent(k, lp, true);
       }
-      // attention items: group active branches by physical page, runs of <= ch_block pages
+      // attention items (SIMT path): group active branches by physical page, runs of <= ch_block pages
       int n_items = 0;
+      const int n_lp_items = uses_items(D) ? S.n_lp : 0;
       int open_mask[MAXB], open_idx[MAXB], n_open = 0;
       int shared_pages = 0;
-      for (int lp = 0; lp < S.n_lp; ++lp) {
+      for (int lp = 0; lp < n_lp_items; ++lp) {
         int done_mask = 0;
         for (int k = 0; k < S.B; ++k) {
           if (!((active >> k) & 1) || ((done_mask >> k) & 1)) continue;
@@ -592,7 +652,10 @@ __global__ void k_step_commit(Dims D, Sess S, DevState st, Pass blk, Head H) {
   for (int k = 0; k < S.B; ++k) {
     if (!((active >> k) & 1)) continue;
     __syncthreads();
-    if (threadIdx.x == 0) s_n = apply_commits(c, blk, H, k, S.tau_conf);
+    {
+      const int nc = apply_commits(c, blk, H, k, S.tau_conf);
+      if (threadIdx.x == 0) s_n = nc;
+    }
     __syncthreads();
     const int dec = c.count_decoded(k);
     if (threadIdx.x == 0) {
@@ -706,7 +769,8 @@ __device__ float merge_prob(RC& c, int d, int i, int v) {
 }
 
 // Alg. 2 (scheduler.py:144-209).  `cov` = smem covered flags [B][L].
-__device__ void merge_sync_core(RC& c, uint8_t* cov, bool copy_device_state) {
+__device__ void merge_sync_core(RC& c, uint8_t* cov, bool copy_device_state, int* mfill, float* mpv,
+                                const float* mprob) {
   const Sess& S = *c.S;
   __shared__ int s_order[MAXB], s_srcs, s_leader, s_parts;
   int ld = c.leader();
@@ -745,40 +809,56 @@ __device__ void merge_sync_core(RC& c, uint8_t* cov, bool copy_device_state) {
         __syncthreads();
       }
       const int srcs = s_srcs;
-      if (srcs && threadIdx.x == 0) {
-        int lo = S.L, hi = 0;
-        for (int s = 0; s < S.B; ++s)
-          if ((srcs >> s) & 1) {
-            lo = min(lo, c.B_(s, B_START));
-            hi = max(hi, c.B_(s, B_END));
-          }
+      if (srcs) {
+        // positions of the union of the sources' windows are independent for one
+        // destination (a fill only changes drow[i]): evaluate them in parallel,
+        // then apply fills / emit events in position order.
+        __shared__ int s_lo, s_hi;
+        if (threadIdx.x == 0) {
+          int lo = S.L, hi = 0;
+          for (int s2 = 0; s2 < S.B; ++s2)
+            if ((srcs >> s2) & 1) {
+              lo = min(lo, c.B_(s2, B_START));
+              hi = max(hi, c.B_(s2, B_END));
+            }
+          s_lo = lo;
+          s_hi = hi;
+        }
+        __syncthreads();
+        const int lo = s_lo, hi = s_hi;
         int* rd = c.row(d);
-        for (int i = lo; i < hi; ++i) {
-          bool in_union = false;
-          for (int s = 0; s < S.B; ++s)
-            if (((srcs >> s) & 1) && c.B_(s, B_START) <= i && i < c.B_(s, B_END)) in_union = true;
-          if (!in_union) continue;
-          if (rd[i] != c.mask_id || !cov[d * S.L + i]) continue;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
           int best = -1;
           float bp = 0.0f;
-          for (int s = 0; s < S.B; ++s) {
-            if (!((srcs >> s) & 1)) continue;
-            const int v = c.row(s)[i];
-            if (v == c.mask_id) continue;
-            const float p = merge_prob(c, d, i, v);
-            if (best < 0 || p > bp) {
-              best = s;
-              bp = p;
+          bool in_union = false;
+          for (int s2 = 0; s2 < S.B; ++s2)
+            if (((srcs >> s2) & 1) && c.B_(s2, B_START) <= i && i < c.B_(s2, B_END)) in_union = true;
+          if (in_union && rd[i] == c.mask_id && cov[d * S.L + i]) {
+            for (int s2 = 0; s2 < S.B; ++s2) {
+              if (!((srcs >> s2) & 1)) continue;
+              const int v = c.row(s2)[i];
+              if (v == c.mask_id) continue;
+              const float p = mprob ? mprob[((long long)d * S.L + i) * S.B + s2] : merge_prob(c, d, i, v);
+              if (best < 0 || p > bp) {
+                best = s2;
+                bp = p;
+              }
             }
           }
-          if (best < 0) continue;
-          if (bp > S.tau_merge) {
+          mfill[i] = (best >= 0 && bp > S.tau_merge) ? best : -1;
+          mpv[i] = bp;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          for (int i = lo; i < hi; ++i) {
+            const int best = mfill[i];
+            if (best < 0) continue;
             const int tok = c.row(best)[i];
             rd[i] = tok;
             c.B_(d, B_MERGED) += 1;
             c.B_(d, B_DEC) += 1;  // i >= P: one gen mask became a token
             c.ctrl[C_MERGES] += 1;
-            c.emit(EV_MERGE, d, best, i, tok, 0, bp);
+            c.emit(EV_MERGE, d, best, i, tok, 0, mpv[i]);
           }
         }
       }
@@ -851,7 +931,8 @@ __global__ void k_merge_sync(Dims D, Sess S, DevState st, int after_prefill) {
     s_ev0 = c.ctrl[C_NEV];
   }
   __syncthreads();
-  merge_sync_core(c, cov, true);
+  int* mfill = reinterpret_cast<int*>(cov + ((S.B * S.L + 15) & ~15));
+  merge_sync_core(c, cov, true, mfill, reinterpret_cast<float*>(mfill + S.L), nullptr);
   __syncthreads();
   // scheduler.py:370-372 emits merge/sync events after merge_sync returns:
   // their `decoded` snapshot is the post-merge/sync state.
@@ -964,6 +1045,14 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st, int with_pm) {
   if (!with_pm) {
     const long long vecs = (long long)D.nkv * S.ps * D.hd * sizeof(T) / 16;  // per (page, layer)
+    __shared__ int s_any;
+    if (threadIdx.x == 0) {
+      int a = 0;
+      for (int r = 0; r < S.R && !a; ++r) a = st.ctrl[(long long)r * C_WORDS + C_NCOPY] > 0;
+      s_any = a;
+    }
+    __syncthreads();
+    if (!s_any) return;
     const long long units = (long long)S.R * S.max_copies * D.layers;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
       const int layer = (int)(u % D.layers);
@@ -984,6 +1073,14 @@ __global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st,
     }
   } else {
     const int vecs = (int)(D.d * sizeof(T) / 16);
+    __shared__ int s_any;
+    if (threadIdx.x == 0) {
+      int a = 0;
+      for (int r = 0; r < S.R && !a; ++r) a = st.ctrl[(long long)r * C_WORDS + C_NPMCOPY] > 0;
+      s_any = a;
+    }
+    __syncthreads();
+    if (!s_any) return;
     // (request, job, position) units
     const long long total = (long long)S.R * MAXB * S.L;
     for (long long u = blockIdx.x; u < total; u += gridDim.x) {
@@ -1002,7 +1099,7 @@ __global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st,
 }
 
 // ------------------------------------------------------------------ launch helpers
-static size_t rc_smem(const Sess& S) { return (size_t)S.B * S.L * 4 + (size_t)S.B * S.L + 64; }
+static size_t rc_smem(const Sess& S) { return (size_t)S.B * S.L * 4 + (size_t)S.B * S.L + 16 + (size_t)S.L * 8 + 64; }
 
 template <typename K>
 static void big_smem(K kern) {
@@ -1058,7 +1155,8 @@ __global__ void k_debug_merge(Dims D, Sess S, DevState st, const float* probmaps
   uint8_t* cov = reinterpret_cast<uint8_t*>(c.rows + S.B * S.L);
   for (int i = threadIdx.x; i < S.B * S.L; i += blockDim.x) cov[i] = st.covered[i];
   __syncthreads();
-  merge_sync_core(c, cov, false);
+  int* mfill = reinterpret_cast<int*>(cov + ((S.B * S.L + 15) & ~15));
+  merge_sync_core(c, cov, false, mfill, reinterpret_cast<float*>(mfill + S.L), nullptr);
   __syncthreads();
   for (int i = threadIdx.x; i < S.B * S.L; i += blockDim.x) st.covered[i] = cov[i];
   store_request(c);

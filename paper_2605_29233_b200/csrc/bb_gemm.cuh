@@ -24,6 +24,7 @@ struct SplitK {
   int G;         // CTAs
   int n_chunks;  // row chunks per weight tile
   int BN;        // rows per chunk
+  const unsigned char* ns_tab;  // optional [n_tiles] precomputed piece counts
 };
 
 // owner CTA of flattened k-block y (largest c with floor(c*T/G) <= y)
@@ -33,6 +34,9 @@ __host__ __device__ inline int sk_owner(long long y, long long T, int G) {
 __host__ __device__ inline int sk_nslots(const SplitK& s, int row, int n) {
   if (s.T == 0) return 1;
   const long long tile = (long long)(n >> 7) * s.n_chunks + row / s.BN;
+#ifdef __CUDA_ARCH__
+  if (s.ns_tab != nullptr) return s.ns_tab[tile];
+#endif
   const long long first = tile * s.KB, last = first + s.KB - 1;
   return sk_owner(last, s.T, s.G) - sk_owner(first, s.T, s.G) + 1;
 }

@@ -28,8 +28,29 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 }
 
 // ------------------------------------------------------------------ embed
+template <typename T> struct Vec4;
+template <> struct Vec4<float> {
+  static __device__ __forceinline__ void st(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+  static __device__ __forceinline__ float4 ld(const float* p) { return *reinterpret_cast<const float4*>(p); }
+};
+template <> struct Vec4<__nv_bfloat16> {
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, float4 v) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+  static __device__ __forceinline__ float4 ld(const __nv_bfloat16* p) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+};
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_embed(Dims D, Pass P, const T* __restrict__ emb,
+__global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restrict__ emb,
                                                const T* __restrict__ pos_emb, const float* __restrict__ ln) {
   if (*P.skip) return;
   __shared__ float sh[32];
@@ -42,16 +63,31 @@ __global__ void __launch_bounds__(256) k_embed(Dims D, Pass P, const T* __restri
   float* x = P.x + (long long)row * D.d;
   T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
   float ss = 0.0f;
-  for (int c = threadIdx.x; c < D.d; c += blockDim.x) {
-    float v = ldf(emb + (long long)tok * D.d + c);
-    if (D.arch == 0) v += ldf(pos_emb + (long long)pos * D.d + c);
-    x[c] = v;
-    ss += v * v;
+  for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
+    float4 v = Vec4<T>::ld(emb + (long long)tok * D.d + c);
+    if (D.arch == 0) {
+      const float4 p = Vec4<T>::ld(pos_emb + (long long)pos * D.d + c);
+      v.x += p.x;
+      v.y += p.y;
+      v.z += p.z;
+      v.w += p.w;
+    }
+    *reinterpret_cast<float4*>(x + c) = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   float inv = 1.0f;
   if (ln != nullptr) inv = 1.0f / sqrtf(block_sum(ss, sh) / (float)D.d + D.eps);
-  for (int c = threadIdx.x; c < D.d; c += blockDim.x)
-    stf(xn + c, ln != nullptr ? x[c] * inv * ln[c] : x[c]);
+  for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    if (ln != nullptr) {
+      const float4 g = *reinterpret_cast<const float4*>(ln + c);
+      v.x *= inv * g.x;
+      v.y *= inv * g.y;
+      v.z *= inv * g.z;
+      v.w *= inv * g.w;
+    }
+    Vec4<T>::st(xn + c, v);
+  }
 }
 
 // ------------------------------------------------------------------ post QKV
@@ -95,19 +131,6 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
 }
 
 // ------------------------------------------------------------------ residual (+ norm)
-template <typename T> struct Vec4;
-template <> struct Vec4<float> {
-  static __device__ __forceinline__ void st(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
-};
-template <> struct Vec4<__nv_bfloat16> {
-  static __device__ __forceinline__ void st(__nv_bfloat16* p, float4 v) {
-    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-    uint2 u;
-    u.x = *reinterpret_cast<uint32_t*>(&a);
-    u.y = *reinterpret_cast<uint32_t*>(&b);
-    *reinterpret_cast<uint2*>(p) = u;
-  }
-};
 
 template <typename T>
 __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef pr, const float* __restrict__ ln) {
@@ -334,7 +357,7 @@ __global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, H
   } while (0)
 
 cudaError_t launch_embed(const Dims& D, const Sess& S, const Pass& P, const Weights& W, cudaStream_t s) {
-  BB_DISPATCH(D, (k_embed<T><<<P.rows_alloc, 256, 0, s>>>(D, P, (const T*)W.emb, (const T*)W.pos,
+  BB_DISPATCH(D, (k_embed<T><<<P.rows_alloc, 512, 0, s>>>(D, P, (const T*)W.emb, (const T*)W.pos,
                                                            D.arch == 1 ? W.ln1 : nullptr)));
   return cudaGetLastError();
 }

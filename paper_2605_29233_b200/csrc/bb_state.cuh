@@ -124,6 +124,12 @@ struct Head {
   int* skip;
 };
 
+// the segment-masked tensor-core attention derives its work from the page
+// tables; only the SIMT (fp32 / head_dim 32,256) path needs planned items
+__host__ __device__ inline bool uses_items(const Dims& D) {
+  return !(D.dtype == 1 && (D.hd == 64 || D.hd == 128));
+}
+
 __host__ __device__ inline int lp_start(const Sess& s, int lp) {
   return lp < s.n_pp ? lp * s.ps : s.P + (lp - s.n_pp) * s.ps;
 }

@@ -67,6 +67,11 @@ class Session:
         self.v_events = self._view(_lib.VIEW_EVENTS, torch.int32, (self.R, self.ev_cap, _lib.EVW))
         self.v_pages = self._view(_lib.VIEW_PAGES, torch.int32, (self.R, self.B, self.info[7]))
         self.v_refc = self._view(_lib.VIEW_REFC, torch.int32, (self.R, self.info[8]))
+        nr = self.info[9]
+        self.v_head = {name: self._view(vid, dt, (nr,)) for name, vid, dt in (
+            ("masked", _lib.VIEW_HEAD_MASKED, torch.int32), ("m", _lib.VIEW_HEAD_M, torch.float32),
+            ("s", _lib.VIEW_HEAD_S, torch.float32), ("arg", _lib.VIEW_HEAD_ARG, torch.int32),
+            ("pos", _lib.VIEW_SLOT_POS, torch.int32), ("branch", _lib.VIEW_SLOT_BR, torch.int32))}
         self.h2d_bytes = self.d2h_bytes = 0
 
     def _view(self, which, dtype, shape):
@@ -129,6 +134,12 @@ class Session:
                 out["events"] = self.v_events[:, :nmax].cpu().numpy()
                 self.d2h_bytes += out["events"].nbytes
         return out
+
+    def head_results(self) -> dict:
+        """Per head slot of the last head pass: masked flag, max logit m, sum
+        exp s, argmax, position, branch (numerics tests)."""
+        self.stream.synchronize()
+        return {k: v.cpu().numpy() for k, v in self.v_head.items()}
 
     def snapshot(self, dst_ctrl, dst_branch):
         """Device-side copy of the result words (ctrl, branch state) into

@@ -183,3 +183,43 @@ def test_forward_hook_counts():
     assert len(calls) == r.nfe.total
     assert calls.count("init") == 1 and calls.count("block") == r.nfe.nfe_block
     assert calls.count("refresh") == r.nfe.nfe_refresh
+
+
+@pytest.mark.parametrize("name,dtype,tol", [("llada_tiny_bf16", "bf16", 2e-2), ("dream_tiny_bf16", "bf16", 2e-2),
+                                            ("llada_tiny_f32", "f32", 1e-4)])
+def test_prefill_head_numerics_match_oracle(name, dtype, tol):
+    """Fused LM-head + confidence of one prefill vs the oracle forward (same
+    weights; the oracle emulates the bf16 storage points): per masked window
+    position the max normalised logit (log max-prob = -log s), lse and argmax.
+    North-star tolerance: max-abs <= 2e-2 on normalised logits in bf16."""
+    from oracle import bb_oracle as O
+    from paper_2605_29233_b200.scheduler import get_session
+    g = LLADA[name]
+    params = llada_model(g, dtype)
+    cfg = cfg_from(g["config"])
+    arch = O.OArch(**g["arch"])
+    W = O.weights_as(O.hash_weights(arch, 0), dtype)
+    rnd = O.bf16_round if dtype == "bf16" else None
+    worst_lp, worst_lse, agree, n = 0.0, 0.0, 0, 0
+    for seed in g["seeds"][:3]:
+        task = bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab)
+        s = get_session(params, cfg, g["prompt_len"], 1)
+        s.set_inputs(task.prompt[None], task.target[None])
+        s.prefill()
+        hr = s.head_results()
+        row = np.full(g["prompt_len"] + g["gen_len"], arch.mask_id, dtype=np.int64)
+        row[:g["prompt_len"]] = task.prompt
+        out, _ = O.full_forward(arch, W, row, g["prompt_len"], task.target, rnd)
+        lse_ref = out.logits.max(1) + np.log(np.exp(out.logits - out.logits.max(1, keepdims=True)).sum(1))
+        idx = {int(p): i for i, p in enumerate(out.positions)}
+        for j in np.flatnonzero(hr["masked"]):
+            i = idx[int(hr["pos"][j])]
+            m, ssum = float(hr["m"][j]), float(hr["s"][j])
+            lse = m + np.log(ssum)
+            worst_lp = max(worst_lp, abs((m - lse) - (out.logits[i].max() - lse_ref[i])))
+            worst_lse = max(worst_lse, abs(lse - lse_ref[i]) / max(1.0, abs(lse_ref[i])))
+            agree += int(hr["arg"][j]) == int(out.probs[i].argmax())
+            n += 1
+    print(f"{name}: {n} positions, max|dlogp_max|={worst_lp:.2e}, rel dlse={worst_lse:.2e}, argmax agree {agree}/{n}")
+    assert worst_lp <= tol and worst_lse <= tol
+    assert agree >= n - max(1, n // 20)
