@@ -163,6 +163,13 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ void split_bf2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x - hf.x, y - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -182,7 +189,7 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 // with a per-key branch mask: row r only sees keys whose page its own branch
 // maps at that lp.  Online softmax per row, one pass, normalised output
 // written directly (no split-K partials, no combine kernel).
-constexpr int ATT_CS = 4;
+constexpr int ATT_CS = 8;
 
 template <int HD>
 __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
@@ -194,8 +201,8 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   bf* sKb = sQ + QR * LD;       // [2][KC][LD]
   bf* sVb = sKb + 2 * KC * LD;  // [2][KC][LD]
   long long* sSegOff = reinterpret_cast<long long*>(sVb + 2 * KC * LD);  // [n_seg] page element base
-  int* sSegStart = reinterpret_cast<int*>(sSegOff + S.n_lp * S.B);       // [n_seg+1] prefix of key counts
-  int* sSegMask = sSegStart + S.n_lp * S.B + 1;                          // [n_seg]
+  int* sSegStart = reinterpret_cast<int*>(sSegOff + S.n_lp * S.B);       // [n_lp] first key of lp
+  int* sSegMask = sSegStart + S.n_lp * S.B + 1;                          // [n_lp][B]
   __shared__ long long sKeyOff[2][KC];
   __shared__ int sKeyMask[2][KC];
   __shared__ int sRow[QR], sBr[QR];
@@ -227,38 +234,51 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   }
   __syncthreads();
   const int bmask = s_bmask;
-  // segments: (lp, distinct physical page, branch mask) in lp order; the
-  // request's page tables are staged in smem first (one parallel load)
+  // segments: per logical page lp, the distinct physical pages among the rows'
+  // branches (<= B each) with their branch masks; discovered in parallel over
+  // lp from the request's page tables staged in smem, then a block scan of
+  // the per-lp key counts gives every key's (lp, segment, offset).
   const long long lay = (long long)layer * S.R * S.pool;
   int* sPT = reinterpret_cast<int*>(sSegMask + S.n_lp * S.B);
   for (int i = threadIdx.x; i < S.B * S.n_lp; i += blockDim.x) sPT[i] = st.pt[(long long)r * S.B * S.n_lp + i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int n = 0, acc = 0;
-    const int* ptr = sPT;
-    for (int lp = 0; lp < S.n_lp; ++lp) {
-      int left = bmask;
-      const int nk = lp_end(S, lp) - lp_start(S, lp);
-      while (left) {
-        const int k = __ffs(left) - 1;
-        const int phys = ptr[k * S.n_lp + lp];
-        int m = 0;
-        for (int k2 = k; k2 < S.B; ++k2)
-          if (((left >> k2) & 1) && ptr[k2 * S.n_lp + lp] == phys) m |= 1 << k2;
-        left &= ~m;
-        sSegOff[n] = ((lay + (long long)r * S.pool + phys) * D.nkv + kvh) * S.ps * HD;
-        sSegMask[n] = m;
-        sSegStart[n] = acc;
-        acc += nk;
-        ++n;
-      }
+  for (int lp = threadIdx.x; lp < S.n_lp; lp += blockDim.x) {
+    int left = bmask, n = 0;
+    while (left) {
+      const int k = __ffs(left) - 1;
+      const int phys = sPT[k * S.n_lp + lp];
+      int m = 0;
+      for (int k2 = k; k2 < S.B; ++k2)
+        if (((left >> k2) & 1) && sPT[k2 * S.n_lp + lp] == phys) m |= 1 << k2;
+      left &= ~m;
+      sSegOff[lp * S.B + n] = ((lay + (long long)r * S.pool + phys) * D.nkv + kvh) * S.ps * HD;
+      sSegMask[lp * S.B + n] = m;
+      ++n;
     }
-    sSegStart[n] = acc;
-    s_nseg = n;
+    sSegStart[lp] = n * (lp_end(S, lp) - lp_start(S, lp));  // keys contributed by lp
   }
   __syncthreads();
-  const int n_seg = s_nseg;
-  const int n_keys = sSegStart[n_seg];
+  if (threadIdx.x < 32) {  // exclusive scan over lp (one warp, n_lp <= 32 * per-lane chunk)
+    const int per = (S.n_lp + 31) / 32;
+    const int b0 = threadIdx.x * per, b1 = min(S.n_lp, b0 + per);
+    int tot = 0;
+    for (int i = b0; i < b1; ++i) tot += sSegStart[i];
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (threadIdx.x >= o) incl += v;
+    }
+    int run = incl - tot;
+    for (int i = b0; i < b1; ++i) {
+      const int v = sSegStart[i];
+      sSegStart[i] = run;
+      run += v;
+    }
+    if (threadIdx.x == 31) s_nseg = incl;  // total keys
+  }
+  __syncthreads();
+  const int n_keys = s_nseg;
   constexpr int VPR = HD / 8;
   const bf* Qg = reinterpret_cast<const bf*>(P.q);
   const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
@@ -275,14 +295,17 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       long long off = 0;
       int m = 0;
       if (key < n_keys) {
-        int lo = 0, hi = n_seg - 1;
+        int lo = 0, hi = S.n_lp - 1;  // last lp with start <= key
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (sSegStart[mid] <= key) lo = mid;
           else hi = mid - 1;
         }
-        off = sSegOff[lo] + (long long)(key - sSegStart[lo]) * HD;
-        m = sSegMask[lo];
+        const int nk = lp_end(S, lo) - lp_start(S, lo);
+        const int rel = key - sSegStart[lo];
+        const int j = rel / nk;
+        off = sSegOff[lo * S.B + j] + (long long)(rel - j * nk) * HD;
+        m = sSegMask[lo * S.B + j];
       }
       sKeyOff[tb][threadIdx.x] = off;
       sKeyMask[tb][threadIdx.x] = m;
@@ -403,11 +426,13 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       }
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk) {
-        uint32_t a[4];
-        a[0] = pack_bf2(s[2 * kk][0], s[2 * kk][1]);
-        a[1] = pack_bf2(s[2 * kk][2], s[2 * kk][3]);
-        a[2] = pack_bf2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-        a[3] = pack_bf2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+        // P = hi + lo (two bf16 parts): P.V to ~fp32 accuracy (the spike
+        // epilogue amplifies attention error ~34x)
+        uint32_t a[4], al[4];
+        split_bf2(s[2 * kk][0], s[2 * kk][1], a[0], al[0]);
+        split_bf2(s[2 * kk][2], s[2 * kk][3], a[1], al[1]);
+        split_bf2(s[2 * kk + 1][0], s[2 * kk + 1][1], a[2], al[2]);
+        split_bf2(s[2 * kk + 1][2], s[2 * kk + 1][3], a[3], al[3]);
         const int mi = lane >> 3, rr = lane & 7;
         const int key = 16 * kk + (mi & 1) * 8 + rr;
 #pragma unroll
@@ -417,6 +442,8 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
           ldsm_x4_t(b0, b1, b2, b3, sV_u + (uint32_t)((key * LD + dim) * 2));
           mma16816(o[nt2], a, b0, b1);
           mma16816(o[nt2 + 1], a, b2, b3);
+          mma16816(o[nt2], al, b0, b1);
+          mma16816(o[nt2 + 1], al, b2, b3);
         }
       }
     }
