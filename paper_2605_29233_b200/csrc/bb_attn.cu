@@ -14,6 +14,7 @@
 #include <cooperative_groups.h>
 
 #include "bb_common.cuh"
+#include "bb_launch.cuh"
 #include "bb_layers.cuh"
 
 namespace bb {
@@ -31,6 +32,7 @@ __device__ __forceinline__ int item_row_slot(const Pass& P, const Sess& S, int r
 
 template <typename T, int HD>
 __global__ void __launch_bounds__(128) k_attn(Dims D, Sess S, Pass P, DevState st, int layer, int max_items) {
+  pdl_enter();
   if (*P.skip) return;
   constexpr int NPL = HD / 32;  // dims per lane
   extern __shared__ float sm[];
@@ -194,6 +196,7 @@ constexpr int ATT_CS = 8;
 template <int HD>
 __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
+  pdl_enter();
   using bf = __nv_bfloat16;
   constexpr int KC = 64, LD = HD + 8, QR = 64;
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -518,7 +521,7 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
     attr = true;
   }
   dim3 grid(S.R * ATT_CS, D.nh, (rows + 63) / 64);
-  k_attn_seg<HD><<<grid, 128, smem, s>>>(D, S, P, st, layer, rows);
+  launch_k(k_attn_seg<HD>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
   return cudaGetLastError();
 }
 
@@ -526,6 +529,7 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
 // (row, head), one thread per head dim; fixed item order (deterministic).
 template <typename T>
 __global__ void __launch_bounds__(256) k_attn_combine2(Dims D, Sess S, Pass P, int max_items) {
+  pdl_enter();
   if (*P.skip) return;
   const int row = blockIdx.x, h = blockIdx.y;
   const int pos = P.slot_pos[row];
@@ -601,7 +605,7 @@ static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const De
   }
   const int max_rows = P.item_rows;
   dim3 grid(S.R * max_items, D.nh, (max_rows + QT - 1) / QT);
-  k_attn<T, HD><<<grid, 128, smem, s>>>(D, S, P, st, layer, max_items);
+  launch_k(k_attn<T, HD>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, max_items);
   return cudaGetLastError();
 }
 
@@ -618,7 +622,7 @@ cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevSt
     if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);
     else if (D.hd == 32) e = attn_hd<T, 32>(D, S, P, st, layer, max_items, s);
     if (e != cudaSuccess) return e;
-    k_attn_combine2<T><<<cgrid, cthreads, 0, s>>>(D, S, P, max_items);
+    launch_k(k_attn_combine2<T>, dim3(cgrid), dim3(cthreads), (size_t)(0), s, D, S, P, max_items);
   } else {
     using T = float;
     if (D.hd == 64) e = attn_hd<T, 64>(D, S, P, st, layer, max_items, s);
@@ -626,7 +630,7 @@ cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevSt
     else if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);
     else if (D.hd == 32) e = attn_hd<T, 32>(D, S, P, st, layer, max_items, s);
     if (e != cudaSuccess) return e;
-    k_attn_combine2<T><<<cgrid, cthreads, 0, s>>>(D, S, P, max_items);
+    launch_k(k_attn_combine2<T>, dim3(cgrid), dim3(cthreads), (size_t)(0), s, D, S, P, max_items);
   }
   return cudaGetLastError();
 }

@@ -20,6 +20,7 @@
 //   k_copy_pages     executes page copy-on-write and prob-map copy jobs
 #include "bb200.h"
 #include "bb_common.cuh"
+#include "bb_launch.cuh"
 #include "bb_layers.cuh"
 
 namespace bb {
@@ -325,6 +326,7 @@ __device__ void slot_boost(const Dims& D, const Sess& S, const int* rw, const in
 
 // ------------------------------------------------------------------ prefill
 __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk, Head H) {
+  pdl_enter();
   RC_SETUP();
   const int r = c.r;
   const int* prompt = st.prompt + (long long)r * S.P;
@@ -476,6 +478,7 @@ __device__ int apply_commits(RC& c, const Pass& blk, const Head& H, int k, float
 }
 
 __global__ void k_prefill_post(Dims D, Sess S, DevState st, Pass blk, Head H) {
+  pdl_enter();
   RC_SETUP();
   load_request(c);
   if (c.ctrl[C_STATUS] != 0) return;
@@ -509,6 +512,7 @@ __global__ void k_prefill_post(Dims D, Sess S, DevState st, Pass blk, Head H) {
 
 // ------------------------------------------------------------------ block step
 __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
+  pdl_enter();
   RC_SETUP();
   const int r = c.r;
   __shared__ int s_active, s_live;
@@ -643,6 +647,7 @@ __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
 }
 
 __global__ void k_step_commit(Dims D, Sess S, DevState st, Pass blk, Head H) {
+  pdl_enter();
   RC_SETUP();
   load_request(c);
   if (c.ctrl[C_STATUS] != 0) return;
@@ -705,6 +710,7 @@ __global__ void k_step_commit(Dims D, Sess S, DevState st, Pass blk, Head H) {
 // P_d(i, v) for merge candidates (scheduler.py:180-184 reads dest.prob_map[i, v]).
 template <typename T>
 __global__ void __launch_bounds__(256) k_merge_prep(Dims D, Sess S, DevState st, const T* __restrict__ head) {
+  pdl_enter();
   const int nch = (S.G + 7) / 8;
   const int r = blockIdx.x / (S.B * nch);
   const int d = (blockIdx.x / nch) % S.B;
@@ -919,6 +925,7 @@ __device__ void merge_sync_core(RC& c, uint8_t* cov, bool copy_device_state, int
 }
 
 __global__ void k_merge_sync(Dims D, Sess S, DevState st, int after_prefill) {
+  pdl_enter();
   RC_SETUP();
   load_request(c);
   if (c.ctrl[C_STATUS] != 0) return;
@@ -980,6 +987,7 @@ __global__ void k_merge_sync(Dims D, Sess S, DevState st, int after_prefill) {
 
 // ------------------------------------------------------------------ refresh
 __global__ void k_refresh_pack(Dims D, Sess S, DevState st, Pass full, Pass blk, Head H, int k) {
+  pdl_enter();
   RC_SETUP();
   const int r = c.r;
   load_request(c);
@@ -1028,6 +1036,7 @@ __global__ void k_refresh_pack(Dims D, Sess S, DevState st, Pass full, Pass blk,
 }
 
 __global__ void k_refresh_end(Dims D, Sess S, DevState st) {
+  pdl_enter();
   RC_SETUP();
   load_request(c);
   if (threadIdx.x == 0 && c.ctrl[C_STATUS] == 0 && c.ctrl[C_REFRESH_DUE]) {
@@ -1043,6 +1052,7 @@ __global__ void k_refresh_end(Dims D, Sess S, DevState st) {
 // 16-byte vector copies; block-strided over (request, job, layer) units.
 template <typename T>
 __global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st, int with_pm) {
+  pdl_enter();
   if (!with_pm) {
     const long long vecs = (long long)D.nkv * S.ps * D.hd * sizeof(T) / 16;  // per (page, layer)
     __shared__ int s_any;
@@ -1110,6 +1120,7 @@ static void big_smem(K kern) {
 // confidence_transition on given probabilities (decoding.py:108-129).
 __global__ void k_debug_commit(const float* probs, int n, int n_out, const int* pos, int* row, float tau, int* out,
                                int* count) {
+  pdl_enter();
   extern __shared__ float sconf[];
   int* sarg = reinterpret_cast<int*>(sconf + n);
   int* sval = sarg + n;
@@ -1139,6 +1150,7 @@ __global__ void k_debug_commit(const float* probs, int n, int n_out, const int* 
 // (scheduler.py:144-209): the production merge core, fed from a table built
 // out of the caller's prob maps instead of the stored head rows.
 __global__ void k_debug_merge(Dims D, Sess S, DevState st, const float* probmaps, int n_out) {
+  pdl_enter();
   RC_SETUP();
   const int mask_id = D.V + 1;
   for (int idx = threadIdx.x; idx < S.B * S.L; idx += blockDim.x) {
@@ -1164,7 +1176,7 @@ __global__ void k_debug_merge(Dims D, Sess S, DevState st, const float* probmaps
 
 cudaError_t launch_debug_commit(const float* probs, int n, int n_out, const int* pos, int* row, float tau, int* out,
                                 int* count, cudaStream_t s) {
-  k_debug_commit<<<1, 256, (size_t)n * 12 + 16, s>>>(probs, n, n_out, pos, row, tau, out, count);
+  launch_k(k_debug_commit, dim3(1), dim3(256), (size_t)((size_t)n * 12 + 16), s, probs, n, n_out, pos, row, tau, out, count);
   return cudaGetLastError();
 }
 cudaError_t launch_debug_merge(const Dims& D, const Sess& S, const DevState& st, const float* probmaps, int n_out,
@@ -1174,7 +1186,7 @@ cudaError_t launch_debug_merge(const Dims& D, const Sess& S, const DevState& st,
     big_smem(k_debug_merge);
     a = true;
   }
-  k_debug_merge<<<1, 256, rc_smem(S), s>>>(D, S, st, probmaps, n_out);
+  launch_k(k_debug_merge, dim3(1), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, probmaps, n_out);
   return cudaGetLastError();
 }
 
@@ -1185,7 +1197,7 @@ cudaError_t launch_prefill_init(const Dims& D, const Sess& S, const DevState& st
     big_smem(k_prefill_init);
     a = true;
   }
-  k_prefill_init<<<S.R, 256, rc_smem(S), s>>>(D, S, st, full, blk, H);
+  launch_k(k_prefill_init, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, full, blk, H);
   return cudaGetLastError();
 }
 cudaError_t launch_prefill_post(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
@@ -1195,7 +1207,7 @@ cudaError_t launch_prefill_post(const Dims& D, const Sess& S, const DevState& st
     big_smem(k_prefill_post);
     a = true;
   }
-  k_prefill_post<<<S.R, 256, rc_smem(S), s>>>(D, S, st, blk, H);
+  launch_k(k_prefill_post, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
   return cudaGetLastError();
 }
 cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
@@ -1205,12 +1217,12 @@ cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, 
     big_smem(k_block_pack);
     a = true;
   }
-  k_block_pack<<<S.R, 256, rc_smem(S), s>>>(D, S, st, blk, H);
+  launch_k(k_block_pack, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
   return cudaGetLastError();
 }
 cudaError_t launch_copy_pages(const Dims& D, const Sess& S, const DevState& st, int with_pm, cudaStream_t s) {
-  if (D.dtype == 1) k_copy_pages<__nv_bfloat16><<<2 * kNumSMs, 512, 0, s>>>(D, S, st, with_pm);
-  else k_copy_pages<float><<<2 * kNumSMs, 512, 0, s>>>(D, S, st, with_pm);
+  if (D.dtype == 1) launch_k(k_copy_pages<__nv_bfloat16>, dim3(2 * kNumSMs), dim3(512), (size_t)(0), s, D, S, st, with_pm);
+  else launch_k(k_copy_pages<float>, dim3(2 * kNumSMs), dim3(512), (size_t)(0), s, D, S, st, with_pm);
   return cudaGetLastError();
 }
 cudaError_t launch_step_commit(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
@@ -1220,13 +1232,13 @@ cudaError_t launch_step_commit(const Dims& D, const Sess& S, const DevState& st,
     big_smem(k_step_commit);
     a = true;
   }
-  k_step_commit<<<S.R, 256, rc_smem(S), s>>>(D, S, st, blk, H);
+  launch_k(k_step_commit, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
   return cudaGetLastError();
 }
 cudaError_t launch_merge_prep(const Dims& D, const Sess& S, const DevState& st, const Weights& W, cudaStream_t s) {
   const int nch = (S.G + 7) / 8;
-  if (D.dtype == 1) k_merge_prep<__nv_bfloat16><<<S.R * S.B * nch, 256, 0, s>>>(D, S, st, (const __nv_bfloat16*)W.head);
-  else k_merge_prep<float><<<S.R * S.B * nch, 256, 0, s>>>(D, S, st, (const float*)W.head);
+  if (D.dtype == 1) launch_k(k_merge_prep<__nv_bfloat16>, dim3(S.R * S.B * nch), dim3(256), (size_t)(0), s, D, S, st, (const __nv_bfloat16*)W.head);
+  else launch_k(k_merge_prep<float>, dim3(S.R * S.B * nch), dim3(256), (size_t)(0), s, D, S, st, (const float*)W.head);
   return cudaGetLastError();
 }
 cudaError_t launch_merge_sync(const Dims& D, const Sess& S, const DevState& st, int after_prefill, cudaStream_t s) {
@@ -1235,7 +1247,7 @@ cudaError_t launch_merge_sync(const Dims& D, const Sess& S, const DevState& st, 
     big_smem(k_merge_sync);
     a = true;
   }
-  k_merge_sync<<<S.R, 256, rc_smem(S), s>>>(D, S, st, after_prefill);
+  launch_k(k_merge_sync, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, after_prefill);
   return cudaGetLastError();
 }
 cudaError_t launch_refresh_begin(const Dims&, const Sess&, const DevState&, const Pass&, const Head&, cudaStream_t) {
@@ -1248,7 +1260,7 @@ cudaError_t launch_refresh_pack(const Dims& D, const Sess& S, const DevState& st
     big_smem(k_refresh_pack);
     a = true;
   }
-  k_refresh_pack<<<S.R, 256, rc_smem(S), s>>>(D, S, st, full, blk, H, branch);
+  launch_k(k_refresh_pack, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, full, blk, H, branch);
   return cudaGetLastError();
 }
 cudaError_t launch_refresh_end(const Dims& D, const Sess& S, const DevState& st, cudaStream_t s) {
@@ -1257,7 +1269,7 @@ cudaError_t launch_refresh_end(const Dims& D, const Sess& S, const DevState& st,
     big_smem(k_refresh_end);
     a = true;
   }
-  k_refresh_end<<<S.R, 256, rc_smem(S), s>>>(D, S, st);
+  launch_k(k_refresh_end, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st);
   return cudaGetLastError();
 }
 

@@ -4,12 +4,14 @@
 #include <string.h>
 
 #include "bb_common.cuh"
+#include "bb_launch.cuh"
 #include "bb_gemm.cuh"
 #include "bb200.h"
 
 namespace bb {
 __global__ void k_reduce_planes(const float* part, long long plane, int ldp, SplitK sk, int rows, int n_out,
                                 float* out) {
+  pdl_enter();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)rows * n_out) return;
   const int row = (int)(i / n_out), n = (int)(i % n_out);
@@ -47,7 +49,7 @@ BB_API int bb_debug_gemm_tc(const void* W, const void* X, void* out, int n_out, 
   if (tc_gemm_launch(g, s) != cudaSuccess) return -10;
   if (mode == 0) {
     const long long n = (long long)rows * n_out;
-    k_reduce_planes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(work, g.p.plane, g.p.ldp, g.sk, rows, n_out,
+    launch_k(k_reduce_planes, dim3((unsigned)((n + 255) / 256)), dim3(256), (size_t)(0), s, work, g.p.plane, g.p.ldp, g.sk, rows, n_out,
                                                                  (float*)out);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -10;

@@ -11,6 +11,7 @@
 #include <stdio.h>
 
 #include "bb_common.cuh"
+#include "bb_launch.cuh"
 #include "bb_gemm.cuh"
 
 namespace bb {
@@ -203,11 +204,9 @@ __global__ void __launch_bounds__(192, 1)
   float* stage = red;
   __shared__ int s_last;
 
-  if (p.skip != nullptr && *p.skip != 0) return;
-  tstat_begin(p.tstat);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rows_valid = p.rows_valid != nullptr ? *p.rows_valid : p.rows_alloc;
   const int n_tiles = p.n_ntiles * p.n_chunks;
+  __shared__ int s_pre;  // stages whose weight tile was issued before the dependency wait
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -228,22 +227,69 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
+  // PDL: let the next kernel launch, then stream the first weight tiles (which
+  // no predecessor writes) while the previous kernel drains; activations (the
+  // B tiles) are only touched after the dependency wait.
+  pdl_launch();
+  if (warp == 0 && lane == 0) {
+    const uint64_t pol_w = policy_evict_first();
+    int pre = 0;
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+    Unit u;
+    while (pre < C::STAGES && it.next(u)) {
+      const int ntile = u.tile / p.n_chunks;
+      for (int kb = u.kb0; kb < u.kb1 && pre < C::STAGES; ++kb, ++pre) {
+        mbar_expect_tx_only(&full[pre], C::A_BYTES);
+        tma_load_2d(sA + pre * C::A_BYTES, &tmA, &full[pre], kb * 64, ntile * 128, pol_w);
+      }
+    }
+    s_pre = pre;
+  }
+  pdl_wait();
+  tstat_begin(p.tstat);
+  const bool skipped = p.skip != nullptr && *p.skip != 0;
+  const int rows_valid = skipped ? 0 : (p.rows_valid != nullptr ? *p.rows_valid : p.rows_alloc);
+  if (skipped) {
+    // drain the prefetched weight tiles before exiting (async copies into our smem)
+    __syncthreads();
+    if (warp == 0 && lane == 0)
+      for (int st = 0; st < s_pre; ++st) {
+        mbar_arrive(&full[st]);
+        mbar_wait(&full[st], 0);
+      }
+    __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc(tbase, C::TCOLS);
+    }
+    tstat_end(p.tstat);
+    return;
+  }
+
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      int issued = 0;  // global k-block counter (matches the prefetch order)
+      const int pre = s_pre;
       UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
       Unit u;
       while (it.next(u)) {
         const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
-        if (chunk * BN >= rows_valid) continue;
-        for (int kb = u.kb0; kb < u.kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * 64, ntile * 128, pol_w);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * 64, chunk * BN, pol_x);
+        // (row chunks are never fully padding: rows_alloc = round_up(rows, BN))
+        for (int kb = u.kb0; kb < u.kb1; ++kb, ++issued) {
+          if (issued < pre) {
+            // weight tile already in flight: add the activation tile
+            mbar_expect_tx(&full[stage], C::B_BYTES);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * 64, chunk * BN, pol_x);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * 64, ntile * 128, pol_w);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * 64, chunk * BN, pol_x);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -261,8 +307,6 @@ __global__ void __launch_bounds__(192, 1)
       UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
       Unit u;
       while (it.next(u)) {
-        const int chunk = u.tile % p.n_chunks;
-        if (chunk * BN >= rows_valid) continue;
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t dt = tbase + (uint32_t)(acc * BN);
@@ -295,7 +339,6 @@ __global__ void __launch_bounds__(192, 1)
     Unit u;
     while (it.next(u)) {
       const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
-      if (chunk * BN >= rows_valid) continue;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int n = ntile * 128 + q * 32 + lane;
@@ -498,7 +541,7 @@ static cudaError_t launch_bn(const TcGemm& g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_gemm_tc<BN><<<g.grid, 192, TcCfg<BN>::SMEM, s>>>(g.tmA, g.tmB, g.p);
+  launch_k(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.tmA, g.tmB, g.p);
   return cudaGetLastError();
 }
 
@@ -514,6 +557,7 @@ cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s) {
 // ------------------------------------------------------------------ SIMT fp32
 // out[row][n] = sum_k X[row][k] * W[n][k]; 64x64 tile, 256 threads, 4x4 per thread.
 __global__ void __launch_bounds__(256) k_gemm_simt(SimtGemm g) {
+  pdl_enter();
   if (g.skip != nullptr && *g.skip != 0) return;
   const int rows = g.rows_valid != nullptr ? *g.rows_valid : g.rows_alloc;
   const int r0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
@@ -559,7 +603,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(SimtGemm g) {
 
 cudaError_t simt_gemm_launch(const SimtGemm& g, cudaStream_t s) {
   dim3 grid((g.n_out + 63) / 64, (g.rows_alloc + 63) / 64);
-  k_gemm_simt<<<grid, 256, 0, s>>>(g);
+  launch_k(k_gemm_simt, dim3(grid), dim3(256), (size_t)(0), s, g);
   return cudaGetLastError();
 }
 

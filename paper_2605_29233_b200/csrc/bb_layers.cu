@@ -10,6 +10,7 @@
 //   head_reduce      combine column tiles -> conf = max prob, argmax, m, s and
 //                    update the branch's probability map (h, m, s, boost)
 #include "bb_common.cuh"
+#include "bb_launch.cuh"
 #include "bb_layers.cuh"
 
 namespace bb {
@@ -52,6 +53,7 @@ template <> struct Vec4<__nv_bfloat16> {
 template <typename T>
 __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restrict__ emb,
                                                const T* __restrict__ pos_emb, const float* __restrict__ ln) {
+  pdl_enter();
   if (*P.skip) return;
   __shared__ float sh[32];
   const int row = blockIdx.x;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restri
 template <typename T>
 __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
                                                   const float* __restrict__ rope, int layer, PartRef pr) {
+  pdl_enter();
   if (*P.skip) return;
   const int half = D.hd >> 1;
   const int row = blockIdx.x;
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
 
 template <typename T>
 __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef pr, const float* __restrict__ ln) {
+  pdl_enter();
   if (*P.skip) return;
   __shared__ float sh[32];
   const int row = blockIdx.x;
@@ -182,6 +186,7 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
 template <typename T>
 __global__ void __launch_bounds__(512) k_norm(Dims D, Pass P, const float* __restrict__ ss_part, int ss_ld,
                                               const float* __restrict__ ln) {
+  pdl_enter();
   if (*P.skip) return;
   const int row = blockIdx.x;
   if (P.slot_pos[row] < 0) return;
@@ -210,6 +215,7 @@ __global__ void __launch_bounds__(512) k_norm(Dims D, Pass P, const float* __res
 // ------------------------------------------------------------------ SwiGLU
 template <typename T>
 __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
+  pdl_enter();
   if (*P.skip) return;
   const int row = blockIdx.y;
   if (P.slot_pos[row] < 0) return;
@@ -236,6 +242,7 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
 // ------------------------------------------------------------------ head side
 template <typename T>
 __global__ void __launch_bounds__(256) k_gather_head(Dims D, Sess S, Pass full, Pass blk, Head H, int filter) {
+  pdl_enter();
   if (*full.skip) return;
   const int slot = blockIdx.x;
   if (!H.masked[slot]) return;
@@ -247,6 +254,7 @@ __global__ void __launch_bounds__(256) k_gather_head(Dims D, Sess S, Pass full, 
 }
 
 __global__ void __launch_bounds__(128) k_head_tiles_f32(Dims D, Head H) {
+  pdl_enter();
   if (*H.skip) return;
   const int row = blockIdx.y, vt = blockIdx.x;
   if (!H.masked[row]) return;
@@ -289,6 +297,7 @@ __global__ void __launch_bounds__(128) k_head_tiles_f32(Dims D, Head H) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, Head H, DevState st) {
+  pdl_enter();
   if (*H.skip) return;
   __shared__ float shm[256];
   __shared__ int sht[256];
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, H
   } while (0)
 
 cudaError_t launch_embed(const Dims& D, const Sess& S, const Pass& P, const Weights& W, cudaStream_t s) {
-  BB_DISPATCH(D, (k_embed<T><<<P.rows_alloc, 512, 0, s>>>(D, P, (const T*)W.emb, (const T*)W.pos,
+  BB_DISPATCH(D, (launch_k(k_embed<T>, dim3(P.rows_alloc), dim3(512), (size_t)(0), s, D, P, (const T*)W.emb, (const T*)W.pos,
                                                            D.arch == 1 ? W.ln1 : nullptr)));
   return cudaGetLastError();
 }
@@ -370,42 +379,42 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
   const int heads = D.nh + 2 * D.nkv, half = D.hd / 2;
   const int hpb = half >= 512 ? 1 : 512 / half;  // heads per CTA
   dim3 grid(P.rows_alloc, (heads + hpb - 1) / hpb);
-  BB_DISPATCH(D, (k_post_qkv<T><<<grid, hpb * half, 0, s>>>(D, S, P, st, bias, W.rope, layer, pr)));
+  BB_DISPATCH(D, (launch_k(k_post_qkv<T>, dim3(grid), dim3(hpb * half), (size_t)(0), s, D, S, P, st, bias, W.rope, layer, pr)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s) {
-  BB_DISPATCH(D, (k_post_residual<T><<<P.rows_alloc, 512, 0, s>>>(D, P, pr, ln)));
+  BB_DISPATCH(D, (launch_k(k_post_residual<T>, dim3(P.rows_alloc), dim3(512), (size_t)(0), s, D, P, pr, ln)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int ss_ld, const float* ln,
                         cudaStream_t s) {
-  BB_DISPATCH(D, (k_norm<T><<<P.rows_alloc, 512, 0, s>>>(D, P, ss_part, ss_ld, ln)));
+  BB_DISPATCH(D, (launch_k(k_norm<T>, dim3(P.rows_alloc), dim3(512), (size_t)(0), s, D, P, ss_part, ss_ld, ln)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s) {
   dim3 grid((D.dff / 4 + 255) / 256, P.rows_alloc);
-  BB_DISPATCH(D, (k_post_gu<T><<<grid, 256, 0, s>>>(D, P, pr)));
+  BB_DISPATCH(D, (launch_k(k_post_gu<T>, dim3(grid), dim3(256), (size_t)(0), s, D, P, pr)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_gather_head(const Dims& D, const Sess& S, const Pass& full, const Pass& blk, const Head& H,
                                int branch_filter, cudaStream_t s) {
-  BB_DISPATCH(D, (k_gather_head<T><<<blk.rows_alloc, 256, 0, s>>>(D, S, full, blk, H, branch_filter)));
+  BB_DISPATCH(D, (launch_k(k_gather_head<T>, dim3(blk.rows_alloc), dim3(256), (size_t)(0), s, D, S, full, blk, H, branch_filter)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_head_tiles_f32(const Dims& D, const Pass& blk, const Head& H, cudaStream_t s) {
   dim3 grid(D.n_vtiles, blk.rows_alloc);
-  k_head_tiles_f32<<<grid, 128, 0, s>>>(D, H);
+  launch_k(k_head_tiles_f32, dim3(grid), dim3(128), (size_t)(0), s, D, H);
   return cudaGetLastError();
 }
 
 cudaError_t launch_head_reduce(const Dims& D, const Sess& S, const Pass& blk, const Head& H, const DevState& st,
                                cudaStream_t s) {
-  BB_DISPATCH(D, (k_head_reduce<T><<<blk.rows_alloc, 256, 0, s>>>(D, S, blk, H, st)));
+  BB_DISPATCH(D, (launch_k(k_head_reduce<T>, dim3(blk.rows_alloc), dim3(256), (size_t)(0), s, D, S, blk, H, st)));
   return cudaGetLastError();
 }
 
