@@ -123,6 +123,7 @@ BB_API int bb_version(void);
 /* instrumentation: live per-launch GEMM timing and kernel-launch counters */
 BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream);
 BB_API int bb_session_counters(void* sess, long long* out);
+BB_API int bb_session_klog(void* sess, unsigned long long* host_out, int cap, int reset, long long* n, void* stream);
 
 /* ---- debug / unit-test entry points (kernel-level) --------------------- */
 BB_API int bb_debug_gemm_tc(const void* W, const void* X, void* out, int n_out, int K, int rows, int BN, int mode,

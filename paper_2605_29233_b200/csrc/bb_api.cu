@@ -58,6 +58,7 @@ struct Session {
   float* ss_full = nullptr;
   int ss_ld = 1;
   bool fuse_epi = false;  // BB_FUSE_EPI=1: GEMM-epilogue fusion (experimental)
+  unsigned long long* klog = nullptr;  // BB_KLOG=1: kernel timeline (cudaMalloc'd)
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
   long long layout[BB_VIEW_COUNT][2];
@@ -338,6 +339,9 @@ static int setup_gemms(Session* s) {
           E.ss_part = which == 0 ? s->ss_blk : s->ss_full;
           E.ss_ld = s->ss_ld;
           all[g]->p.tstat = s->tstat + (size_t)(which * 8 + g) * 8;
+          all[g]->p.klog = s->D.klog;
+          all[g]->p.klog_cap = s->D.klog_cap;
+          all[g]->p.klog_id = 100 + which * 8 + g;
           if (attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
           all[g]->p.part = s->part;
           all[g]->p.skip = P.skip;
@@ -369,6 +373,9 @@ static int setup_gemms(Session* s) {
     p.spike_gain = D.spike_gain;
     p.skip = s->H.skip;
     p.tstat = s->tstat + (size_t)4 * 8;
+    p.klog = s->D.klog;
+    p.klog_cap = s->D.klog_cap;
+    p.klog_id = 104;
   } else {
     s->head_simt = SimtGemm{(const float*)W.head, (const float*)s->blk.xn, D.n_out, D.d, s->blk.rows_alloc,
                             nullptr, s->H.skip, s->H.logits, D.n_out};
@@ -655,6 +662,14 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   for (int i = 0; i < BB_VIEW_COUNT; ++i)
     if (s->layout[i][1]) s->layout[i][0] += (long long)(base - (char*)workspace);
   s->fuse_epi = getenv("BB_FUSE_EPI") != nullptr && atoi(getenv("BB_FUSE_EPI")) != 0;
+  if (getenv("BB_KLOG") != nullptr && atoi(getenv("BB_KLOG")) != 0) {
+    const int cap = 1 << 20;
+    if (cudaMalloc(&s->klog, (1 + 2 * (size_t)cap) * 8) == cudaSuccess) {
+      cudaMemset(s->klog, 0, 8);
+      s->D.klog = s->klog;
+      s->D.klog_cap = cap;
+    }
+  }
   rc = setup_gemms(s);
   if (rc != BB_OK) {
     delete s;
@@ -687,6 +702,7 @@ BB_API int bb_session_destroy(void* sess) {
   if (s->g_iter) cudaGraphExecDestroy(s->g_iter);
   if (s->g_iter_ref) cudaGraphExecDestroy(s->g_iter_ref);
   if (s->g_prefill) cudaGraphExecDestroy(s->g_prefill);
+  if (s->klog) cudaFree(s->klog);
   if (s->host_ctrl) cudaFreeHost(s->host_ctrl);
   for (int i = 0; i < 4; ++i)
     if (s->ev[i]) cudaEventDestroy(s->ev[i]);
@@ -835,6 +851,30 @@ BB_API int bb_session_counters(void* sess, long long* out) {
   out[2] = s->nodes_iter;
   out[3] = s->nodes_iter_ref;
   out[4] = s->nodes_prefill;
+  return BB_OK;
+}
+
+// kernel timeline (BB_KLOG=1 sessions): copies up to `cap` (id, t_ns) pairs,
+// returns the number recorded in *n (and resets the log if reset != 0)
+BB_API int bb_session_klog(void* sess, unsigned long long* host_out, int cap, int reset, long long* n, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !n) return BB_ERR_CONTRACT;
+  cudaStream_t st = (cudaStream_t)stream;
+  *n = 0;
+  if (!s->klog) return BB_OK;
+  unsigned long long cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, s->klog, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const long long m = (long long)(cnt < (unsigned long long)cap ? cnt : (unsigned long long)cap);
+  if (host_out && m > 0) {
+    CK(cudaMemcpyAsync(host_out, s->klog + 1, (size_t)m * 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  *n = m;
+  if (reset) {
+    CK(cudaMemsetAsync(s->klog, 0, 8, st));
+    CK(cudaStreamSynchronize(st));
+  }
   return BB_OK;
 }
 

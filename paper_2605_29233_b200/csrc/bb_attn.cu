@@ -33,6 +33,7 @@ __device__ __forceinline__ int item_row_slot(const Pass& P, const Sess& S, int r
 template <typename T, int HD>
 __global__ void __launch_bounds__(128) k_attn(Dims D, Sess S, Pass P, DevState st, int layer, int max_items) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 21);
   if (*P.skip) return;
   constexpr int NPL = HD / 32;  // dims per lane
   extern __shared__ float sm[];
@@ -197,6 +198,7 @@ template <int HD>
 __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 3);
   using bf = __nv_bfloat16;
   constexpr int KC = 64, LD = HD + 8, QR = 64;
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -530,6 +532,7 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
 template <typename T>
 __global__ void __launch_bounds__(256) k_attn_combine2(Dims D, Sess S, Pass P, int max_items) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 22);
   if (*P.skip) return;
   const int row = blockIdx.x, h = blockIdx.y;
   const int pos = P.slot_pos[row];

@@ -188,6 +188,18 @@ __device__ __forceinline__ void tstat_end(unsigned long long* ts) {
   }
 }
 
+// Kernel timeline: CTA 0 stamps (id, %globaltimer) right after its PDL wait,
+// i.e. when its predecessor completed; consecutive stamps give each kernel's
+// slot in the real (graph, PDL) timeline including launch gaps.
+__device__ __forceinline__ void klog_mark(unsigned long long* log, int cap, int id) {
+  if (log == nullptr || threadIdx.x != 0 || blockIdx.x != 0 || blockIdx.y != 0 || blockIdx.z != 0) return;
+  const unsigned long long i = atomicAdd(&log[0], 1ull);
+  if (i < (unsigned long long)cap) {
+    log[1 + 2 * i] = (unsigned long long)id;
+    log[2 + 2 * i] = globaltimer_ns();
+  }
+}
+
 // ---------------------------------------------------------------- numerics
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
 __device__ __forceinline__ __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }

@@ -327,6 +327,7 @@ __device__ void slot_boost(const Dims& D, const Sess& S, const int* rw, const in
 // ------------------------------------------------------------------ prefill
 __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk, Head H) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 10);
   RC_SETUP();
   const int r = c.r;
   const int* prompt = st.prompt + (long long)r * S.P;
@@ -479,6 +480,7 @@ __device__ int apply_commits(RC& c, const Pass& blk, const Head& H, int k, float
 
 __global__ void k_prefill_post(Dims D, Sess S, DevState st, Pass blk, Head H) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 11);
   RC_SETUP();
   load_request(c);
   if (c.ctrl[C_STATUS] != 0) return;
@@ -513,6 +515,7 @@ __global__ void k_prefill_post(Dims D, Sess S, DevState st, Pass blk, Head H) {
 // ------------------------------------------------------------------ block step
 __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 12);
   RC_SETUP();
   const int r = c.r;
   __shared__ int s_active, s_live;
@@ -648,6 +651,7 @@ __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
 
 __global__ void k_step_commit(Dims D, Sess S, DevState st, Pass blk, Head H) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 13);
   RC_SETUP();
   load_request(c);
   if (c.ctrl[C_STATUS] != 0) return;
@@ -711,6 +715,7 @@ __global__ void k_step_commit(Dims D, Sess S, DevState st, Pass blk, Head H) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_merge_prep(Dims D, Sess S, DevState st, const T* __restrict__ head) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 14);
   const int nch = (S.G + 7) / 8;
   const int r = blockIdx.x / (S.B * nch);
   const int d = (blockIdx.x / nch) % S.B;
@@ -926,6 +931,7 @@ __device__ void merge_sync_core(RC& c, uint8_t* cov, bool copy_device_state, int
 
 __global__ void k_merge_sync(Dims D, Sess S, DevState st, int after_prefill) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 15);
   RC_SETUP();
   load_request(c);
   if (c.ctrl[C_STATUS] != 0) return;
@@ -988,6 +994,7 @@ __global__ void k_merge_sync(Dims D, Sess S, DevState st, int after_prefill) {
 // ------------------------------------------------------------------ refresh
 __global__ void k_refresh_pack(Dims D, Sess S, DevState st, Pass full, Pass blk, Head H, int k) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 16);
   RC_SETUP();
   const int r = c.r;
   load_request(c);
@@ -1037,6 +1044,7 @@ __global__ void k_refresh_pack(Dims D, Sess S, DevState st, Pass full, Pass blk,
 
 __global__ void k_refresh_end(Dims D, Sess S, DevState st) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 17);
   RC_SETUP();
   load_request(c);
   if (threadIdx.x == 0 && c.ctrl[C_STATUS] == 0 && c.ctrl[C_REFRESH_DUE]) {
@@ -1053,6 +1061,7 @@ __global__ void k_refresh_end(Dims D, Sess S, DevState st) {
 template <typename T>
 __global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st, int with_pm) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 18);
   if (!with_pm) {
     const long long vecs = (long long)D.nkv * S.ps * D.hd * sizeof(T) / 16;  // per (page, layer)
     __shared__ int s_any;

@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(192, 1)
     s_pre = pre;
   }
   pdl_wait();
+  klog_mark(p.klog, p.klog_cap, p.klog_id);
   tstat_begin(p.tstat);
   const bool skipped = p.skip != nullptr && *p.skip != 0;
   const int rows_valid = skipped ? 0 : (p.rows_valid != nullptr ? *p.rows_valid : p.rows_alloc);

@@ -99,6 +99,8 @@ struct GemmTcParams {
   float head_scale, spike_cut, spike_gain;
   // live per-launch timing (%globaltimer): [min start, max end, CTAs done, sum ns, launches]
   unsigned long long* tstat;
+  unsigned long long* klog;
+  int klog_cap, klog_id;
   EpiArgs epi;
 };
 

@@ -54,6 +54,7 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restrict__ emb,
                                                const T* __restrict__ pos_emb, const float* __restrict__ ln) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 1);
   if (*P.skip) return;
   __shared__ float sh[32];
   const int row = blockIdx.x;
@@ -99,6 +100,7 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
                                                   const float* __restrict__ rope, int layer, PartRef pr) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 2);
   if (*P.skip) return;
   const int half = D.hd >> 1;
   const int row = blockIdx.x;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
 template <typename T>
 __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef pr, const float* __restrict__ ln) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 4);
   if (*P.skip) return;
   __shared__ float sh[32];
   const int row = blockIdx.x;
@@ -187,6 +190,7 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_norm(Dims D, Pass P, const float* __restrict__ ss_part, int ss_ld,
                                               const float* __restrict__ ln) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 6);
   if (*P.skip) return;
   const int row = blockIdx.x;
   if (P.slot_pos[row] < 0) return;
@@ -216,6 +220,7 @@ __global__ void __launch_bounds__(512) k_norm(Dims D, Pass P, const float* __res
 template <typename T>
 __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 5);
   if (*P.skip) return;
   const int row = blockIdx.y;
   if (P.slot_pos[row] < 0) return;
@@ -243,6 +248,7 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_gather_head(Dims D, Sess S, Pass full, Pass blk, Head H, int filter) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 7);
   if (*full.skip) return;
   const int slot = blockIdx.x;
   if (!H.masked[slot]) return;
@@ -255,6 +261,7 @@ __global__ void __launch_bounds__(256) k_gather_head(Dims D, Sess S, Pass full, 
 
 __global__ void __launch_bounds__(128) k_head_tiles_f32(Dims D, Head H) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 8);
   if (*H.skip) return;
   const int row = blockIdx.y, vt = blockIdx.x;
   if (!H.masked[row]) return;
@@ -298,6 +305,7 @@ __global__ void __launch_bounds__(128) k_head_tiles_f32(Dims D, Head H) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, Head H, DevState st) {
   pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 9);
   if (*H.skip) return;
   __shared__ float shm[256];
   __shared__ int sht[256];

@@ -47,6 +47,8 @@ struct Dims {
   int qkv_out, attn_dim, kv_dim, n_vtiles;
   float eps, gamma, head_scale, spike_cut, spike_gain, attn_scale;
   int radius;
+  unsigned long long* klog;  // kernel timeline log ([0] count, then (id, t_ns) pairs) or null
+  int klog_cap;
 };
 
 struct Sess {

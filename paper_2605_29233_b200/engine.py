@@ -155,6 +155,23 @@ class Session:
                    "bb_session_gemm_stats")
         return [[int(buf[k * 5 + j]) for j in range(5)] for k in range(16)]
 
+    KLOG_NAMES = {1: "embed", 2: "post_qkv", 3: "attn_seg", 4: "post_residual", 5: "post_gu", 6: "norm",
+                  7: "gather_head", 8: "head_tiles_f32", 9: "head_reduce", 10: "prefill_init", 11: "prefill_post",
+                  12: "block_pack", 13: "step_commit", 14: "merge_prep", 15: "merge_sync", 16: "refresh_pack",
+                  17: "refresh_end", 18: "copy_pages", 20: "gemm_simt", 21: "attn_simt", 22: "attn_combine",
+                  100: "gemm_qkv", 101: "gemm_o", 102: "gemm_gate_up", 103: "gemm_down", 104: "gemm_head",
+                  108: "gemm_qkv_full", 109: "gemm_o_full", 110: "gemm_gate_up_full", 111: "gemm_down_full"}
+
+    def klog(self, reset: bool = False):
+        """Kernel timeline of a BB_KLOG=1 session: list of (name, t_ns)."""
+        cap = 1 << 20
+        buf = (C.c_ulonglong * (2 * cap))()
+        n = C.c_longlong(0)
+        _lib.check(_lib.lib().bb_session_klog(self.h, buf, cap, int(reset), C.byref(n),
+                                              C.c_void_p(self.stream.cuda_stream)), "bb_session_klog")
+        return [(self.KLOG_NAMES.get(int(buf[2 * i]), str(int(buf[2 * i]))), int(buf[2 * i + 1]))
+                for i in range(n.value)]
+
     def counters(self):
         buf = (C.c_longlong * 5)()
         _lib.check(_lib.lib().bb_session_counters(self.h, buf), "bb_session_counters")

@@ -1,0 +1,47 @@
+"""Real (graph + PDL) per-kernel timeline of one C2 request from the device
+kernel log (BB_KLOG=1): each kernel's slot = time from its predecessor's
+completion to its own completion (next kernel's stamp)."""
+import collections, json, os, sys
+os.environ["BB_KLOG"] = "1"
+sys.path.insert(0, '.')
+import numpy as np
+import torch
+import paper_2605_29233_b200 as bb
+from paper_2605_29233_b200.scheduler import get_session
+
+P, G = 64, 256
+vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
+cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=G)
+params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=0.4, gamma=8.0, dtype="bf16")
+s = get_session(params, cfg, P, 1, trace=False)
+for seed in (1000, 1001):
+    t = bb.make_task(seed, P, G, vocab)
+    s.set_inputs(t.prompt[None], t.target[None]); s.launch()
+s.stream.synchronize()
+s.klog(reset=True)
+t = bb.make_task(1002, P, G, vocab)
+s.set_inputs(t.prompt[None], t.target[None])
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ev0.record(s.stream); it = s.launch(); ev1.record(s.stream); ev1.synchronize()
+log = s.klog()
+c = s.v_ctrl[0].cpu().numpy()
+nfe = int(c[5] + c[6] + c[7])
+names = [n for n, _ in log]
+ts = np.array([t for _, t in log], dtype=np.int64)
+agg = collections.defaultdict(lambda: [0, 0])
+for i in range(len(log) - 1):
+    agg[names[i]][0] += 1
+    agg[names[i]][1] += int(ts[i + 1] - ts[i])
+tot = ts[-1] - ts[0]
+print(f"request: {ev0.elapsed_time(ev1):.2f} ms event-timed, {tot/1e6:.2f} ms logged span, {len(log)} kernels, "
+      f"{it} iterations, nfe {nfe} (split {c[5]},{c[6]},{c[7]})")
+rows = sorted(agg.items(), key=lambda x: -x[1][1])
+print(f"{'kernel':22s} {'n':>6s} {'total ms':>9s} {'per NFE us':>10s} {'avg us':>8s} {'share':>6s}")
+for k, (n, ns) in rows:
+    print(f"{k:22s} {n:6d} {ns/1e6:9.3f} {ns/1e3/nfe:10.1f} {ns/1e3/n:8.2f} {100*ns/tot:5.1f}%")
+# largest gaps (host/graph boundaries)
+d = np.diff(ts)
+big = np.argsort(-d)[:8]
+print("largest slots:", [(names[i], round(d[i] / 1e3, 1)) for i in big])
+json.dump({"kernels": {k: {"n": n, "ns": ns} for k, (n, ns) in rows}, "nfe": nfe, "span_ns": int(tot)},
+          open("gpurun_out/timeline_c2.json", "w"))
