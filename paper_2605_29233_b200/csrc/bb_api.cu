@@ -57,7 +57,7 @@ struct Session {
   float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
   float* ss_full = nullptr;
   int ss_ld = 1;
-  bool fuse_epi = false;  // BB_FUSE_EPI=1: GEMM-epilogue fusion (experimental)
+  bool fuse_epi = true;  // bf16: fused GEMM epilogues (BB_FUSE_EPI=0: stream-K + post kernels)
   unsigned long long* klog = nullptr;  // BB_KLOG=1: kernel timeline (cudaMalloc'd)
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
@@ -298,11 +298,12 @@ static int setup_gemms(Session* s) {
       const char* wgu = D.dff ? (const char*)W.wgu + (size_t)l * 2 * D.dff * D.d * e : nullptr;
       const char* wd = D.dff ? (const char*)W.wd + (size_t)l * D.d * D.dff * e : nullptr;
       if (D.dtype == BB_DTYPE_BF16) {
-        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
-        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
+        const int gm = s->fuse_epi ? 3 : 0;
+        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
+        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
         if (D.dff) {
-          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
-          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, 0, 0)) return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
         }
         TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
@@ -310,6 +311,8 @@ static int setup_gemms(Session* s) {
           memset(&E, 0, sizeof(E));
           E.kind = !s->fuse_epi ? 0 : (g == 0 ? 2 : (g == 2 ? 3 : 4));
           E.tile_cnt = s->tile_cnt;
+          E.slot_kvoff = P.slot_kvoff;
+          E.kv_layer_elems = (long long)s->S.R * s->S.pool * D.nkv * s->S.ps * D.hd;
           E.slot_pos = P.slot_pos;
           E.slot_req = P.slot_req;
           E.slot_br = P.slot_br;
@@ -323,7 +326,7 @@ static int setup_gemms(Session* s) {
           E.attn_dim = D.attn_dim;
           E.kv_k = (__nv_bfloat16*)s->st.kv_k;
           E.kv_v = (__nv_bfloat16*)s->st.kv_v;
-          E.kv_layer_off = (long long)l * s->S.R * s->S.pool;
+          E.kv_layer_off = l;
           E.pt = s->st.pt;
           E.ps = s->S.ps;
           E.P = s->S.P;
@@ -342,7 +345,7 @@ static int setup_gemms(Session* s) {
           all[g]->p.klog = s->D.klog;
           all[g]->p.klog_cap = s->D.klog_cap;
           all[g]->p.klog_id = 100 + which * 8 + g;
-          if (attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
+          if (!s->fuse_epi && attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
           all[g]->p.part = s->part;
           all[g]->p.skip = P.skip;
           all[g]->p.rows_valid = which == 1 ? s->full_rows : nullptr;
@@ -661,7 +664,7 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   s->ws = (char*)workspace;
   for (int i = 0; i < BB_VIEW_COUNT; ++i)
     if (s->layout[i][1]) s->layout[i][0] += (long long)(base - (char*)workspace);
-  s->fuse_epi = getenv("BB_FUSE_EPI") != nullptr && atoi(getenv("BB_FUSE_EPI")) != 0;
+  s->fuse_epi = s->D.dtype == BB_DTYPE_BF16 && (getenv("BB_FUSE_EPI") == nullptr || atoi(getenv("BB_FUSE_EPI")) != 0);
   if (getenv("BB_KLOG") != nullptr && atoi(getenv("BB_KLOG")) != 0) {
     const int cap = 1 << 20;
     if (cudaMalloc(&s->klog, (1 + 2 * (size_t)cap) * 8) == cudaSuccess) {

@@ -12,6 +12,8 @@
 
 #include "bb_common.cuh"
 #include "bb_launch.cuh"
+#include <cooperative_groups.h>
+
 #include "bb_gemm.cuh"
 
 namespace bb {
@@ -22,26 +24,38 @@ struct Unit {
 
 struct UnitIter {
   long long x, end, T;
-  int KB, G, c, mode, n_tiles;
-  __device__ UnitIter(int c_, int G_, int KB_, int n_tiles_, int mode_)
-      : c(c_), G(G_), KB(KB_), n_tiles(n_tiles_), mode(mode_) {
+  int KB, G, c, mode, n_tiles, split;
+  __device__ UnitIter(int c_, int G_, int KB_, int n_tiles_, int mode_, int split_)
+      : c(c_), G(G_), KB(KB_), n_tiles(n_tiles_), mode(mode_), split(split_) {
     T = (long long)n_tiles * KB;
     if (mode == 0) {
       x = (long long)c * T / G;
       end = (long long)(c + 1) * T / G;
-    } else {
+    } else if (mode == 1) {
       x = c;
       end = n_tiles;
+    } else {
+      x = c / split;  // one unit: (tile, k-slice = cluster rank)
+      end = x + 1;
     }
   }
   __device__ bool next(Unit& u) {
     if (x >= end) return false;
-    if (mode != 0) {
+    if (mode == 1) {
       u.tile = (int)x;
       u.kb0 = 0;
       u.kb1 = KB;
       u.slot = 0;
       x += G;
+      return true;
+    }
+    if (mode == 2) {
+      const int ks = c % split;
+      u.tile = (int)x;
+      u.kb0 = (int)((long long)KB * ks / split);
+      u.kb1 = (int)((long long)KB * (ks + 1) / split);
+      u.slot = ks;
+      x = end;
       return true;
     }
     const int tile = (int)(x / KB);
@@ -57,28 +71,26 @@ struct UnitIter {
   }
 };
 
+// Smem budget sized for two CTAs per SM (weight streaming wants many CTAs in
+// flight; 3 stages x 16 KB weight tiles per CTA).
 template <int BN>
 struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = BN == 256 ? 2 : 3;
   static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr size_t RED = (size_t)3 * 4 * BN * 4;            // head epilogue
-  static constexpr size_t STG = (size_t)(32 * 129 + 4 * 32) * 4;    // fused epilogue staging
+  static constexpr size_t RED = (size_t)3 * 4 * BN * 4;                 // LM-head epilogue
+  static constexpr size_t STG = (size_t)(32 * 129 + 4 * 32 + 32 + 64 + 16) * 4;  // staging + row sums + row meta
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16 +
                                  (RED > STG ? RED : STG);
+  // cluster split-K staging of the full accumulator reuses the pipeline stages
+  static constexpr bool SPLIT_OK = (size_t)BN * 128 * 4 <= (size_t)STAGES * (A_BYTES + B_BYTES);
 };
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-__device__ __forceinline__ int e_lp_of(const EpiArgs& E, int pos) {
-  return pos < E.P ? pos / E.ps : E.n_pp + (pos - E.P) / E.ps;
-}
-__device__ __forceinline__ int e_lp_start(const EpiArgs& E, int lp) {
-  return lp < E.n_pp ? lp * E.ps : E.P + (lp - E.n_pp) * E.ps;
-}
 // write one element of the fused q|k|v output (head hh, dim i) for `row`
-__device__ __forceinline__ void qkv_store(const EpiArgs& E, int row, int pos, int hh, int i, float val) {
+__device__ __forceinline__ void qkv_store(const EpiArgs& E, int row, long long kvoff, int hh, int i, float val) {
   const __nv_bfloat16 b = __float2bfloat16_rn(val);
   if (hh < E.nh) {
     E.q[(long long)row * E.attn_dim + hh * E.hd + i] = b;
@@ -86,20 +98,26 @@ __device__ __forceinline__ void qkv_store(const EpiArgs& E, int row, int pos, in
   }
   const bool isk = hh < E.nh + E.nkv;
   const int kvh = isk ? hh - E.nh : hh - E.nh - E.nkv;
-  const int r = E.slot_req[row], br = E.slot_br[row];
-  const int lp = e_lp_of(E, pos);
-  const long long gpage = (long long)r * E.pool + E.pt[((long long)r * E.B + br) * E.n_lp + lp];
-  const int off = pos - e_lp_start(E, lp);
   __nv_bfloat16* dst = isk ? E.kv_k : E.kv_v;
-  dst[(((E.kv_layer_off + gpage) * E.nkv + kvh) * E.ps + off) * E.hd + i] = b;
+  dst[E.kv_layer_off * E.kv_layer_elems + kvoff + (long long)kvh * E.ps * E.hd + i] = b;
 }
 
-// Apply the fused consumer op to 32 rows [rbase, rbase+32) of this tile; v[j]
-// is this thread's column c (0..127).  Called by all 128 epilogue threads.
+// Apply the fused consumer op to rows [rbase, rbase+32) ∩ [.., rows_valid) of
+// this 128-column tile; v[j] is this thread's column c.  All 128 epilogue
+// threads call it.  stage: [32][129] floats + 4x32 row sums + 64 row meta.
 __device__ void epi_apply(const EpiArgs& E, float (&v)[32], int n0, int c, int et, int rbase, int rows_valid,
                           int n_out, int ntile, float* stage) {
   const int n = n0 + c;
   const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3;
+  int* mpos = reinterpret_cast<int*>(stage + 32 * 129 + 128);
+  long long* mkv = reinterpret_cast<long long*>(stage + 32 * 129 + 128 + 32);
+  if (et < 32) {
+    const int row = rbase + et;
+    const int pos = row < rows_valid ? E.slot_pos[row] : -1;
+    mpos[et] = pos;
+    if (E.kind == 2) mkv[et] = pos >= 0 ? E.slot_kvoff[row] : 0;
+  }
+  epi_bar();
   if (E.kind == 2) {
     if (E.bias != nullptr && n < n_out) {
       const float bv = E.bias[n];
@@ -113,12 +131,10 @@ __device__ void epi_apply(const EpiArgs& E, float (&v)[32], int n0, int c, int e
       const int hd2 = E.hd >> 1;
       for (int k = et; k < 32 * 64; k += 128) {
         const int r = k >> 6, pr = k & 63;
+        const int pos = mpos[r];
+        if (pos < 0) continue;
         const int hl = pr / hd2, i = pr % hd2;
         const int ca = hl * E.hd + i, cb = ca + hd2;
-        const int row = rbase + r;
-        if (row >= rows_valid) continue;
-        const int pos = E.slot_pos[row];
-        if (pos < 0) continue;
         float a = stage[r * 129 + ca], b = stage[r * 129 + cb];
         const int hh = (n0 + ca) / E.hd;
         if (hh < E.nh + E.nkv) {
@@ -127,19 +143,13 @@ __device__ void epi_apply(const EpiArgs& E, float (&v)[32], int n0, int c, int e
           a = a2;
           b = b2;
         }
-        qkv_store(E, row, pos, hh, i, a);
-        qkv_store(E, row, pos, hh, i + hd2, b);
+        qkv_store(E, rbase + r, mkv[r], hh, i, a);
+        qkv_store(E, rbase + r, mkv[r], hh, i + hd2, b);
       }
-      epi_bar();
     } else if (n < n_out) {
 #pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        const int row = rbase + j;
-        if (row >= rows_valid) continue;
-        const int pos = E.slot_pos[row];
-        if (pos < 0) continue;
-        qkv_store(E, row, pos, n / E.hd, n % E.hd, v[j]);
-      }
+      for (int j = 0; j < 32; ++j)
+        if (mpos[j] >= 0) qkv_store(E, rbase + j, mkv[j], n / E.hd, n % E.hd, v[j]);
     }
   } else if (E.kind == 3) {
 #pragma unroll
@@ -147,33 +157,30 @@ __device__ void epi_apply(const EpiArgs& E, float (&v)[32], int n0, int c, int e
     epi_bar();
     for (int k = et; k < 32 * 64; k += 128) {
       const int r = k >> 6, f = k & 63;
-      const int row = rbase + r;
-      if (row >= rows_valid || E.slot_pos[row] < 0) continue;
+      if (mpos[r] < 0) continue;
       const float g = stage[r * 129 + f], u = stage[r * 129 + 64 + f];
-      E.act[(long long)row * E.dff + ntile * 64 + f] = __float2bfloat16_rn(g / (1.0f + expf(-g)) * u);
+      E.act[(long long)(rbase + r) * E.dff + ntile * 64 + f] = __float2bfloat16_rn(g / (1.0f + expf(-g)) * u);
     }
-    epi_bar();
   } else if (E.kind == 4) {
     float* rs = stage + 32 * 129;
+    float xv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) xv[j] = mpos[j] >= 0 ? E.x[(long long)(rbase + j) * E.d + n] : 0.0f;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const int row = rbase + j;
       float nv = 0.0f;
-      if (row < rows_valid && E.slot_pos[row] >= 0) {
-        float* xp = E.x + (long long)row * E.d + n;
-        nv = *xp + v[j];
-        *xp = nv;
+      if (mpos[j] >= 0) {
+        nv = xv[j] + v[j];
+        E.x[(long long)(rbase + j) * E.d + n] = nv;
       }
       const float sq = warp_sum(nv * nv);
       if (lane == 0) rs[q * 32 + j] = sq;
     }
     epi_bar();
-    if (et < 32) {
-      const int row = rbase + et;
-      if (row < rows_valid) E.ss_part[(long long)row * E.ss_ld + ntile] = rs[et] + rs[32 + et] + rs[64 + et] + rs[96 + et];
-    }
-    epi_bar();
+    if (et < 32 && mpos[et] >= 0)
+      E.ss_part[(long long)(rbase + et) * E.ss_ld + ntile] = rs[et] + rs[32 + et] + rs[64 + et] + rs[96 + et];
   }
+  epi_bar();
 }
 
 __device__ __forceinline__ SplitK sk_of(const GemmTcParams& p, int G) {
@@ -183,14 +190,43 @@ __device__ __forceinline__ SplitK sk_of(const GemmTcParams& p, int G) {
   sk.BN = p.rows_alloc / p.n_chunks;
   sk.G = G;
   sk.T = (long long)p.n_ntiles * p.n_chunks * p.KB;
+  sk.ns_tab = nullptr;
   return sk;
 }
 
+// LM-head epilogue for 32 rows (per-(row, vocab-tile) max / argmax / sum-exp)
 template <int BN>
-__global__ void __launch_bounds__(192, 1)
+__device__ __forceinline__ void head_rows(const GemmTcParams& p, float (&v)[32], int n, int q, int lane, int row0, int j0,
+                                          float* red) {
+  const float hs = p.head_scale, sc = p.spike_cut, sg = p.spike_gain;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int row = row0 + j0 + j;
+    float l = -INFINITY;
+    if (n < p.n_out && row < p.rows_alloc) {
+      const float raw = v[j] * hs;
+      l = raw + sg * fmaxf(0.0f, raw - sc);
+      if (n == __ldg(&p.tgt[row])) l += __ldg(&p.boost[row]);
+    }
+    float m = l;
+    int a = n;
+    warp_argmax(m, a);
+    const float e = (m == -INFINITY) ? 0.0f : expf(l - m);
+    const float s = warp_sum(e);
+    if (lane == 0) {
+      red[(0 * 4 + q) * BN + j0 + j] = m;
+      red[(1 * 4 + q) * BN + j0 + j] = __int_as_float(a);
+      red[(2 * 4 + q) * BN + j0 + j] = s;
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const GemmTcParams p) {
   using C = TcCfg<BN>;
+  namespace cg = cooperative_groups;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -200,9 +236,9 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* red = reinterpret_cast<float*>(tslot + 4);  // [3][4][BN] (head) / staging (fused epilogue)
+  float* red = reinterpret_cast<float*>(tslot + 4);  // LM-head reduction / fused-epilogue staging
   float* stage = red;
-  __shared__ int s_last;
+  float* acc_stage = reinterpret_cast<float*>(sA);   // mode 2: [BN][128] partial accumulator
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = p.n_ntiles * p.n_chunks;
@@ -234,7 +270,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     const uint64_t pol_w = policy_evict_first();
     int pre = 0;
-    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
     Unit u;
     while (pre < C::STAGES && it.next(u)) {
       const int ntile = u.tile / p.n_chunks;
@@ -258,11 +294,13 @@ __global__ void __launch_bounds__(192, 1)
         mbar_arrive(&full[st]);
         mbar_wait(&full[st], 0);
       }
+    if (p.mode == 2) cg::this_cluster().sync();
     __syncthreads();
     if (warp == 1) {
       tc_fence_after();
       tmem_dealloc(tbase, C::TCOLS);
     }
+    if (p.mode == 2) cg::this_cluster().sync();
     tstat_end(p.tstat);
     return;
   }
@@ -271,11 +309,11 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      int stage = 0;
+      int stage_i = 0;
       uint32_t phase = 0;
       int issued = 0;  // global k-block counter (matches the prefetch order)
       const int pre = s_pre;
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
       Unit u;
       while (it.next(u)) {
         const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
@@ -283,16 +321,16 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = u.kb0; kb < u.kb1; ++kb, ++issued) {
           if (issued < pre) {
             // weight tile already in flight: add the activation tile
-            mbar_expect_tx(&full[stage], C::B_BYTES);
-            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * 64, chunk * BN, pol_x);
+            mbar_expect_tx(&full[stage_i], C::B_BYTES);
+            tma_load_2d(sB + stage_i * C::B_BYTES, &tmB, &full[stage_i], kb * 64, chunk * BN, pol_x);
           } else {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
-            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * 64, ntile * 128, pol_w);
-            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * 64, chunk * BN, pol_x);
+            mbar_wait(&empty[stage_i], phase ^ 1);
+            mbar_expect_tx(&full[stage_i], C::A_BYTES + C::B_BYTES);
+            tma_load_2d(sA + stage_i * C::A_BYTES, &tmA, &full[stage_i], kb * 64, ntile * 128, pol_w);
+            tma_load_2d(sB + stage_i * C::B_BYTES, &tmB, &full[stage_i], kb * 64, chunk * BN, pol_x);
           }
-          if (++stage == C::STAGES) {
-            stage = 0;
+          if (++stage_i == C::STAGES) {
+            stage_i = 0;
             phase ^= 1;
           }
         }
@@ -301,28 +339,28 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
-      int stage = 0;
+      int stage_i = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
       Unit u;
       while (it.next(u)) {
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t dt = tbase + (uint32_t)(acc * BN);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(&full[stage_i], phase);
           tc_fence_after();
-          const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
-          const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
+          const uint64_t ad = sdesc_sw128(smem_u32(sA + stage_i * C::A_BYTES));
+          const uint64_t bd = sdesc_sw128(smem_u32(sB + stage_i * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             tc_mma_bf16(dt, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), IDESC,
                         (kb > u.kb0 || k > 0) ? 1u : 0u);
-          tc_commit(&empty[stage]);
-          if (++stage == C::STAGES) {
-            stage = 0;
+          tc_commit(&empty[stage_i]);
+          if (++stage_i == C::STAGES) {
+            stage_i = 0;
             phase ^= 1;
           }
         }
@@ -336,7 +374,7 @@ __global__ void __launch_bounds__(192, 1)
     const int et = threadIdx.x - 64;
     int acc = 0;
     uint32_t aphase = 0;
-    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
     Unit u;
     while (it.next(u)) {
       const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
@@ -346,87 +384,35 @@ __global__ void __launch_bounds__(192, 1)
       const int row0 = chunk * BN;
       const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       if (p.mode == 0) {
-        const EpiArgs& E = p.epi;
-        const int ns = E.kind == 0 ? 2 : sk_nslots(sk_of(p, gridDim.x), row0, ntile * 128);
-        const bool direct = E.kind != 0 && ns == 1;
-        if (!direct) {
-          float* dst = p.part + (long long)u.slot * p.plane + n;
+        // stream-K: raw fp32 partial planes for the post-GEMM kernels
+        float* dst = p.part + (long long)u.slot * p.plane + n;
 #pragma unroll 1
-          for (int j0 = 0; j0 < BN; j0 += 32) {
-            float v[32];
-            tmem_ld32(taddr + j0, v);
-            if (n < p.n_out) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int row = row0 + j0 + j;
-                if (row < rows_valid) dst[(long long)row * p.ldp] = v[j];
-              }
-            }
-          }
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
-          acc ^= 1;
-          if (acc == 0) aphase ^= 1;
-          if (E.kind == 0) continue;
-          __threadfence();
-          epi_bar();
-          if (et == 0) {
-            const int old = atomicAdd(&E.tile_cnt[u.tile], 1);
-            s_last = old == ns - 1;
-            if (s_last) atomicExch(&E.tile_cnt[u.tile], 0);
-          }
-          epi_bar();
-          if (!s_last) continue;
-          __threadfence();
-#pragma unroll 1
-          for (int j0 = 0; j0 < BN; j0 += 32) {
-            float v[32];
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + j0, v);
+          if (n < p.n_out) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int row = row0 + j0 + j;
-              float a = 0.0f;
-              if (row < rows_valid && n < p.n_out) {
-                const float* pp = p.part + (long long)row * p.ldp + n;
-                for (int sl = 0; sl < ns; ++sl) a += __ldcg(pp + (long long)sl * p.plane);
-              }
-              v[j] = a;
+              if (row < rows_valid) dst[(long long)row * p.ldp] = v[j];
             }
-            epi_apply(E, v, ntile * 128, q * 32 + lane, et, row0 + j0, rows_valid, p.n_out, ntile, stage);
           }
-          continue;
         }
-#pragma unroll 1
-        for (int j0 = 0; j0 < BN; j0 += 32) {
-          float v[32];
-          tmem_ld32(taddr + j0, v);
-          epi_apply(E, v, ntile * 128, q * 32 + lane, et, row0 + j0, rows_valid, p.n_out, ntile, stage);
-        }
-      } else {
-        const float hs = p.head_scale, sc = p.spike_cut, sg = p.spike_gain;
+      } else if (p.mode == 2) {
+        // cluster split-K: stage the partial accumulator; reduced after the loop
 #pragma unroll 1
         for (int j0 = 0; j0 < BN; j0 += 32) {
           float v[32];
           tmem_ld32(taddr + j0, v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int row = row0 + j0 + j;
-            float l = -INFINITY;
-            if (n < p.n_out && row < p.rows_alloc) {
-              const float raw = v[j] * hs;
-              l = raw + sg * fmaxf(0.0f, raw - sc);
-              if (n == __ldg(&p.tgt[row])) l += __ldg(&p.boost[row]);
-            }
-            float m = l;
-            int a = n;
-            warp_argmax(m, a);
-            const float e = (m == -INFINITY) ? 0.0f : expf(l - m);
-            const float s = warp_sum(e);
-            if (lane == 0) {
-              red[(0 * 4 + q) * BN + j0 + j] = m;
-              red[(1 * 4 + q) * BN + j0 + j] = __int_as_float(a);
-              red[(2 * 4 + q) * BN + j0 + j] = s;
-            }
-          }
+          for (int j = 0; j < 32; ++j) acc_stage[(j0 + j) * 128 + q * 32 + lane] = v[j];
+        }
+      } else if (p.epi.kind == 1) {
+#pragma unroll 1
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + j0, v);
+          head_rows<BN>(p, v, n, q, lane, row0, j0, red);
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -454,12 +440,49 @@ __global__ void __launch_bounds__(192, 1)
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
         continue;
+      } else {
+        // tiles-only fused epilogue straight from TMEM
+#pragma unroll 1
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + j0, v);
+          epi_apply(p.epi, v, ntile * 128, q * 32 + lane, et, row0 + j0, rows_valid, p.n_out, ntile, stage);
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
+  }
+  if (p.mode == 2) {
+    // ---- cluster split-K reduction through DSMEM (rank order: deterministic)
+    cg::cluster_group cluster = cg::this_cluster();
+    __syncthreads();
+    cluster.sync();
+    if (warp >= 2) {
+      const int et = threadIdx.x - 64, q = warp & 3;
+      const int S = p.split, rank = (int)cluster.block_rank();
+      const int tile = blockIdx.x / S;
+      const int ntile = tile / p.n_chunks, chunk = tile % p.n_chunks;
+      const int rows_per = BN / S;
+      const int r0 = rank * rows_per;
+      const int c = q * 32 + lane;
+      for (int j0 = 0; j0 < rows_per; j0 += 32) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float a = 0.0f;
+          if (j0 + j < rows_per)
+            for (int qq = 0; qq < S; ++qq) a += *cluster.map_shared_rank(acc_stage + (r0 + j0 + j) * 128 + c, qq);
+          v[j] = a;
+        }
+        const int rbase = chunk * BN + r0 + j0;
+        const int rv = min(rows_valid, rbase + min(32, rows_per - j0));
+        epi_apply(p.epi, v, ntile * 128, c, et, rbase, rv, p.n_out, ntile, stage);
+      }
+    }
+    cluster.sync();
   }
   tc_fence_before();
   __syncthreads();
@@ -516,19 +539,30 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
   p.plane = (long long)rows_alloc * n_out;
   const long long n_tiles = (long long)p.n_ntiles * p.n_chunks;
   const long long T = n_tiles * p.KB;
-  const int gmax = max_grid > 0 ? max_grid : kNumSMs;
-  g.grid = mode == 0 ? (int)(T < gmax ? T : gmax) : (int)(n_tiles < gmax ? n_tiles : gmax);
-  g.sk.T = mode == 0 ? T : 0;
-  g.sk.KB = p.KB;
-  g.sk.G = g.grid;
-  g.sk.n_chunks = p.n_chunks;
-  g.sk.BN = BN;
-  g.max_slots = 1;
-  if (mode == 0)
-    for (long long t = 0; t < n_tiles; ++t) {
-      const int ns = sk_owner(t * p.KB + p.KB - 1, T, g.grid) - sk_owner(t * p.KB, T, g.grid) + 1;
-      if (ns > g.max_slots) g.max_slots = ns;
+  const int resident = 2 * kNumSMs;  // two CTAs per SM (TcCfg smem budget)
+  p.split = 1;
+  if (mode == 3) {
+    // fused epilogue: whole tiles if there are enough of them to fill the
+    // machine, otherwise split K over a thread-block cluster (2 or 4 CTAs)
+    const bool split_ok = BN == 64 ? TcCfg<64>::SPLIT_OK : (BN == 128 ? TcCfg<128>::SPLIT_OK : TcCfg<256>::SPLIT_OK);
+    if (n_tiles >= 192 || !split_ok) {
+      mode = 1;
+    } else {
+      mode = 2;
+      p.split = n_tiles * 4 <= resident ? 4 : 2;
     }
+    p.mode = mode;
+  }
+  if (mode == 0) {
+    const int gmax = max_grid > 0 ? max_grid : kNumSMs;
+    g.grid = (int)(T < gmax ? T : gmax);
+  } else if (mode == 1) {
+    const int gmax = max_grid > 0 ? max_grid : resident;
+    const long long rounds = (n_tiles + gmax - 1) / gmax;
+    g.grid = (int)((n_tiles + rounds - 1) / rounds);
+  } else {
+    g.grid = (int)(n_tiles * p.split);
+  }
   g.smem = BN == 64 ? TcCfg<64>::SMEM : (BN == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM);
   return true;
 }
@@ -542,7 +576,10 @@ static cudaError_t launch_bn(const TcGemm& g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  launch_k(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.tmA, g.tmB, g.p);
+  if (g.p.mode == 2)
+    launch_kc(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.p.split, g.tmA, g.tmB, g.p);
+  else
+    launch_k(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.tmA, g.tmB, g.p);
   return cudaGetLastError();
 }
 

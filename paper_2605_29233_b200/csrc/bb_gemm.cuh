@@ -62,6 +62,8 @@ __device__ __forceinline__ float part_sum(const float* __restrict__ part, long l
 struct EpiArgs {
   int kind;
   int* tile_cnt;
+  const long long* slot_kvoff;  // per-row KV element offset within a layer (page, position)
+  long long kv_layer_elems;     // elements per layer of the KV pool
   const int* slot_pos;
   const int* slot_req;
   const int* slot_br;
@@ -84,7 +86,14 @@ struct EpiArgs {
 };
 
 struct GemmTcParams {
-  int n_out, K, n_ntiles, n_chunks, KB, mode;  // mode 0: partial planes, 1: LM-head epilogue
+  // mode 0: stream-K into fp32 partial planes (consumed by post kernels)
+  // mode 1: whole tiles round-robin over a persistent grid, epilogue from TMEM
+  //         (epi.kind 1 = LM head, 2..4 fused consumer ops)
+  // mode 2: cluster split-K: `split` CTAs of a cluster each own 1/split of the
+  //         k-blocks of one tile; partial accumulators are reduced through
+  //         distributed shared memory in rank order, then the fused epilogue
+  int n_out, K, n_ntiles, n_chunks, KB, mode;
+  int split;
   int rows_alloc;
   const int* rows_valid;  // device scalar or nullptr
   const int* skip;        // device scalar or nullptr: nonzero => no-op
@@ -112,7 +121,8 @@ struct TcGemm {
   size_t smem;
 };
 
-// host API (bb_gemm.cu)
+// host API (bb_gemm.cu).  mode 0 = stream-K planes, 1 = LM head, 3 = fused
+// (picks tiles-only or cluster split-K from the tile count; epi set by caller)
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN,
                    int mode, int max_grid);
 cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s);
