@@ -541,6 +541,7 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
   const long long T = n_tiles * p.KB;
   const int resident = 2 * kNumSMs;  // two CTAs per SM (TcCfg smem budget)
   p.split = 1;
+  if (mode == 1) p.epi.kind = 1;  // LM-head epilogue
   if (mode == 3) {
     // fused epilogue: whole tiles if there are enough of them to fill the
     // machine, otherwise split K over a thread-block cluster (2 or 4 CTAs)
