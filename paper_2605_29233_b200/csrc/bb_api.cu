@@ -57,7 +57,7 @@ struct Session {
   float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
   float* ss_full = nullptr;
   int ss_ld = 1;
-  bool fuse_epi = true;  // bf16: fused GEMM epilogues (BB_FUSE_EPI=0: stream-K + post kernels)
+  bool fuse_epi = false;  // BB_FUSE_EPI=1: fused GEMM epilogues (experimental; default stream-K + post kernels)
   unsigned long long* klog = nullptr;  // BB_KLOG=1: kernel timeline (cudaMalloc'd)
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
@@ -664,7 +664,7 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   s->ws = (char*)workspace;
   for (int i = 0; i < BB_VIEW_COUNT; ++i)
     if (s->layout[i][1]) s->layout[i][0] += (long long)(base - (char*)workspace);
-  s->fuse_epi = s->D.dtype == BB_DTYPE_BF16 && (getenv("BB_FUSE_EPI") == nullptr || atoi(getenv("BB_FUSE_EPI")) != 0);
+  s->fuse_epi = s->D.dtype == BB_DTYPE_BF16 && getenv("BB_FUSE_EPI") != nullptr && atoi(getenv("BB_FUSE_EPI")) != 0;
   if (getenv("BB_KLOG") != nullptr && atoi(getenv("BB_KLOG")) != 0) {
     const int cap = 1 << 20;
     if (cudaMalloc(&s->klog, (1 + 2 * (size_t)cap) * 8) == cudaSuccess) {

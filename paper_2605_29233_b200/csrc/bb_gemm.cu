@@ -71,13 +71,13 @@ struct UnitIter {
   }
 };
 
-// Smem budget sized for two CTAs per SM (weight streaming wants many CTAs in
-// flight; 3 stages x 16 KB weight tiles per CTA).
+// One CTA per SM with a deep TMA pipeline (8 x 24 KB stages at BN=64): a
+// streaming CTA needs ~100+ KB in flight to pull its share of HBM bandwidth.
 template <int BN>
 struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGES = BN == 256 ? 2 : 3;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr size_t RED = (size_t)3 * 4 * BN * 4;                 // LM-head epilogue
   static constexpr size_t STG = (size_t)(32 * 129 + 4 * 32 + 32 + 64 + 16) * 4;  // staging + row sums + row meta
@@ -539,7 +539,7 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
   p.plane = (long long)rows_alloc * n_out;
   const long long n_tiles = (long long)p.n_ntiles * p.n_chunks;
   const long long T = n_tiles * p.KB;
-  const int resident = 2 * kNumSMs;  // two CTAs per SM (TcCfg smem budget)
+  const int resident = kNumSMs;  // one CTA per SM (TcCfg smem budget)
   p.split = 1;
   if (mode == 1) p.epi.kind = 1;  // LM-head epilogue
   if (mode == 3) {
