@@ -564,6 +564,18 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
   } else {
     g.grid = (int)(n_tiles * p.split);
   }
+  g.sk.T = mode == 0 ? T : 0;
+  g.sk.KB = p.KB;
+  g.sk.G = g.grid;
+  g.sk.n_chunks = p.n_chunks;
+  g.sk.BN = BN;
+  g.sk.ns_tab = nullptr;
+  g.max_slots = 1;
+  if (mode == 0)
+    for (long long t = 0; t < n_tiles; ++t) {
+      const int ns = sk_owner(t * p.KB + p.KB - 1, T, g.grid) - sk_owner(t * p.KB, T, g.grid) + 1;
+      if (ns > g.max_slots) g.max_slots = ns;
+    }
   g.smem = BN == 64 ? TcCfg<64>::SMEM : (BN == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM);
   return true;
 }
