@@ -255,17 +255,24 @@ def main():
     vocab = params.vocab
     s = get_session(params, cfg, P, 1, trace=False)
     K, Wm = args.steps, max(args.warmup, 1)
-    base_seed = 1000 + rank * 100000
-    tasks = [bb.make_task(base_seed + i, P, G, vocab) for i in range(Wm + K)]
+    from paper_2605_29233_b200 import dp
+    # prompts: global request g -> seed 1000 + g, sharded round-robin over ranks
+    mine = dp.shard(K * world, rank, world)
+    tasks = ([bb.make_task(900000 + rank * 1000 + i, P, G, vocab) for i in range(Wm)]
+             + [bb.make_task(1000 + g, P, G, vocab) for g in mine])
     dev_p = torch.tensor(np.stack([t.prompt for t in tasks]).astype(np.int32), device="cuda")
     dev_t = torch.tensor(np.stack([t.target for t in tasks]).astype(np.int32), device="cuda")
+    nb = len(cfgd["bs"])
     snap_c = torch.zeros(Wm + K, 1, 32, dtype=torch.int32, device="cuda")
-    snap_b = torch.zeros(Wm + K, 1, len(cfgd["bs"]), 8, dtype=torch.int32, device="cuda")
+    snap_b = torch.zeros(Wm + K, 1, nb, 8, dtype=torch.int32, device="cuda")
+    snap_tok = torch.zeros(Wm + K, 1, nb, P + G, dtype=torch.int32, device="cuda")
 
     def one(i):
         s.set_inputs(dev_p[i:i + 1], dev_t[i:i + 1])
         s.launch(use_graph=True)
         s.snapshot(snap_c[i], snap_b[i])
+        with torch.cuda.stream(s.stream):
+            snap_tok[i].copy_(s.v_tokens, non_blocking=True)
 
     log(f"[bench] rank {rank}: warmup {Wm} requests")
     for i in range(Wm):
@@ -291,22 +298,32 @@ def main():
     gst = s.gemm_stats(reset=False)
     ctrl = snap_c[Wm:].cpu().numpy()
     brs = snap_b[Wm:].cpu().numpy()
+    toks = snap_tok[Wm:].cpu().numpy()
     status = ctrl[:, 0, 0]
     if not (status == 1).all():
         raise RuntimeError(f"requests did not finish: status {status.tolist()}")
     winners = ctrl[:, 0, 1]
     tokens = np.array([brs[i, 0, winners[i], 3] for i in range(K)], dtype=np.int64)
     nfe = ctrl[:, 0, 5:8].astype(np.int64)
-    local_stats = torch.tensor([float(tokens.sum()), t_ms, float(nfe.sum()), float(nfe[:, 1].sum())],
-                               dtype=torch.float64, device="cuda")
+    # one all-gather of the per-request results at the end (no per-step collective)
+    L = P + G
+    packed = np.full((K, L + 6), -1, dtype=np.int64)
+    for i in range(K):
+        packed[i, :L] = toks[i, 0, winners[i]]
+        packed[i, L:L + 3] = nfe[i]
+        packed[i, L + 3] = winners[i]
+        packed[i, L + 4] = tokens[i]
+        packed[i, L + 5] = ctrl[i, 0, 2]
     if dist is not None:
-        allst = [torch.zeros_like(local_stats) for _ in range(world)]
-        dist.all_gather(allst, local_stats)
-        allst = torch.stack(allst).cpu().numpy()
+        all_res = dp.gather_results(packed, K * world, rank, world, device="cuda")
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        allt = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(allt, tt)
+        t_max_ms = max(float(x.item()) for x in allt)
     else:
-        allst = local_stats.cpu().numpy()[None]
-    tot_tokens = allst[:, 0].sum()
-    t_max_ms = allst[:, 1].max()
+        all_res = packed
+        t_max_ms = t_ms
+    tot_tokens = float(all_res[:, L + 4].sum())
     value = tot_tokens / (t_max_ms / 1e3)
 
     # ---- e2e through the public API (host buffers) ----
@@ -379,7 +396,10 @@ def main():
     trf = os.path.join(HERE, "profiles", "gemm_traffic.json")
     if os.path.exists(trf):
         try:
-            roof["traffic"] = json.load(open(trf)).get("dram_bytes_per_launch")
+            tj = json.load(open(trf))
+            roof["traffic"] = tj.get("dram_bytes_per_launch")
+            roof["traffic_algorithmic_bytes_per_launch"] = tot_bytes / launches if launches else None
+            roof["traffic_source"] = tj.get("source")
         except Exception:
             pass
     with open(os.path.join(HERE, "profiles", "nfe_split_c2.json") if args.config == "c2" else os.devnull, "w") as fh:
@@ -400,7 +420,8 @@ def main():
                    "refresh_interval": cfgd["R"], "head_scale": cfgd["head_scale"], "gamma": cfgd["gamma"],
                    "requests_per_gpu_per_step": 1, "parallelism": f"request-parallel dp{world}",
                    "l2": "inputs larger than L2 (16 GB of weights streamed per block step)"},
-        "nfe_per_request": float(nfe.sum(axis=1).mean()), "nfe_split": nfe_mean.tolist(),
+        "nfe_per_request": float(all_res[:, L:L + 3].sum(axis=1).mean()), "nfe_split": nfe_mean.tolist(),
+        "requests": int(len(all_res)),
         "tokens_per_request": float(tokens.mean()), "ms_per_nfe": ms_per_nfe,
         "e2e": {"value": e2e_value, "unit": "decoded tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

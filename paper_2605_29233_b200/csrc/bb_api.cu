@@ -632,7 +632,8 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.max_copies = S.B * (maxb / S.ps + 2);
   const int NR = S.NR;
   s->gb.BN = NR <= 64 ? 64 : (NR <= 128 ? 128 : 256);
-  s->gf.BN = S.NF >= 1024 ? 256 : 128;
+  // full pass (prefill / refresh): tile rows exactly when possible (L = 320 -> 5 x 64)
+  s->gf.BN = S.NF >= 1024 ? 256 : (S.NF % 128 == 0 ? 128 : 64);
   return BB_OK;
 }
 
