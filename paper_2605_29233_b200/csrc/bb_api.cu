@@ -54,6 +54,11 @@ struct Session {
   int* tile_cnt = nullptr;              // fused-epilogue arrival counters (self-resetting)
   unsigned char* ns_tabs = nullptr;     // per-GEMM-shape stream-K piece counts
   size_t ns_used = 0, ns_cap = 0;
+  struct NsShape {
+    int ntiles, nchunks, KB, G;
+    unsigned char* tab;
+  };
+  std::vector<NsShape> ns_shapes;
   float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
   float* ss_full = nullptr;
   int ss_ld = 1;
@@ -270,9 +275,15 @@ static PartRef pref_tc(const TcGemm& g, const float* part) {
   return PartRef{part, g.p.plane, g.p.ldp, g.sk};
 }
 
-// per-tile stream-K piece counts (avoids 64-bit divisions in consumers)
+// per-tile stream-K piece counts (avoids 64-bit divisions in consumers);
+// one table per distinct GEMM shape (all layers share them)
 static int attach_ns_table(Session* s, TcGemm& g) {
   const long long tiles = (long long)g.p.n_ntiles * g.p.n_chunks;
+  for (auto& e : s->ns_shapes)
+    if (e.ntiles == g.p.n_ntiles && e.nchunks == g.p.n_chunks && e.KB == g.sk.KB && e.G == g.sk.G) {
+      g.sk.ns_tab = e.tab;
+      return BB_OK;
+    }
   if (s->ns_used + tiles > s->ns_cap) return BB_ERR_NOMEM;
   std::vector<unsigned char> tab(tiles);
   for (long long t = 0; t < tiles; ++t)
@@ -281,8 +292,10 @@ static int attach_ns_table(Session* s, TcGemm& g) {
   if (cudaMemcpy(dst, tab.data(), tiles, cudaMemcpyHostToDevice) != cudaSuccess) return BB_ERR_CUDA;
   g.sk.ns_tab = dst;
   s->ns_used += (tiles + 15) / 16 * 16;
+  s->ns_shapes.push_back({g.p.n_ntiles, g.p.n_chunks, g.sk.KB, g.sk.G, dst});
   return BB_OK;
 }
+
 static int setup_gemms(Session* s) {
   const Dims& D = s->D;
   const Weights& W = s->M->W;
