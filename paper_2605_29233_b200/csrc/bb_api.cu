@@ -645,8 +645,23 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.max_copies = S.B * (maxb / S.ps + 2);
   const int NR = S.NR;
   s->gb.BN = NR <= 64 ? 64 : (NR <= 128 ? 128 : 256);
-  // full pass (prefill / refresh): tile rows exactly when possible (L = 320 -> 5 x 64)
-  s->gf.BN = S.NF >= 1024 ? 256 : (S.NF % 128 == 0 ? 128 : 64);
+  // full pass (prefill / refresh): row chunks as wide as possible with little
+  // padding (L = 320 -> 2 x 160, L = 192 -> 1 x 192, L = 3072 -> 12 x 256)
+  {
+    const int cands[5] = {256, 192, 160, 128, 64};
+    int best = 128;
+    long long best_cost = -1;
+    for (int i = 0; i < 5; ++i) {
+      const int bn = cands[i];
+      const long long chunks = (S.NF + bn - 1) / bn;
+      const long long cost = chunks * bn + chunks * 32;  // padded rows + per-chunk weight re-read penalty
+      if (best_cost < 0 || cost < best_cost) {
+        best_cost = cost;
+        best = bn;
+      }
+    }
+    s->gf.BN = best;
+  }
   return BB_OK;
 }
 

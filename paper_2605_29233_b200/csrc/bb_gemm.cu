@@ -77,7 +77,7 @@ template <int BN>
 struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = BN >= 192 ? 4 : (BN >= 128 ? 5 : 8);
   static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr size_t RED = (size_t)3 * 4 * BN * 4;                 // LM-head epilogue
   static constexpr size_t STG = (size_t)(32 * 129 + 4 * 32 + 32 + 64 + 16) * 4;  // staging + row sums + row meta
@@ -105,7 +105,7 @@ __device__ __forceinline__ void qkv_store(const EpiArgs& E, int row, long long k
 // Apply the fused consumer op to rows [rbase, rbase+32) ∩ [.., rows_valid) of
 // this 128-column tile; v[j] is this thread's column c.  All 128 epilogue
 // threads call it.  stage: [32][129] floats + 4x32 row sums + 64 row meta.
-__device__ void epi_apply(const EpiArgs& E, float (&v)[32], int n0, int c, int et, int rbase, int rows_valid,
+__device__ __forceinline__ void epi_apply(const EpiArgs& E, float (&v)[32], int n0, int c, int et, int rbase, int rows_valid,
                           int n_out, int ntile, float* stage) {
   const int n = n0 + c;
   const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3;
@@ -521,7 +521,7 @@ static bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t
 
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN, int mode,
                    int max_grid) {
-  if (BN != 64 && BN != 128 && BN != 256) return false;
+  if (BN != 64 && BN != 128 && BN != 160 && BN != 192 && BN != 256) return false;
   if (K % 8 != 0) return false;  // 16-byte row stride for TMA
   memset(&g, 0, sizeof(g));
   g.BN = BN;
@@ -543,14 +543,17 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
   p.split = 1;
   if (mode == 1) p.epi.kind = 1;  // LM-head epilogue
   if (mode == 3) {
-    // fused epilogue: whole tiles if there are enough of them to fill the
-    // machine, otherwise split K over a thread-block cluster (2 or 4 CTAs)
-    const bool split_ok = BN == 64 ? TcCfg<64>::SPLIT_OK : (BN == 128 ? TcCfg<128>::SPLIT_OK : TcCfg<256>::SPLIT_OK);
-    if (n_tiles >= 192 || !split_ok) {
+    // fused epilogue: whole tiles when there are enough to keep ~100 SMs
+    // streaming (96 CTAs reach ~97% of the 148-CTA bandwidth), otherwise split
+    // K over a thread-block cluster of up to 4 CTAs (DSMEM reduction)
+    const bool split_ok = BN == 64 ? TcCfg<64>::SPLIT_OK : (BN == 128 ? TcCfg<128>::SPLIT_OK : false);
+    if (n_tiles >= 96 || !split_ok) {
       mode = 1;
     } else {
       mode = 2;
-      p.split = n_tiles * 4 <= resident ? 4 : 2;
+      int sp = (int)(resident / n_tiles);
+      p.split = sp >= 4 ? 4 : (sp >= 2 ? 2 : 1);
+      if (p.split == 1) mode = 1;
     }
     p.mode = mode;
   }
@@ -576,7 +579,11 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
       const int ns = sk_owner(t * p.KB + p.KB - 1, T, g.grid) - sk_owner(t * p.KB, T, g.grid) + 1;
       if (ns > g.max_slots) g.max_slots = ns;
     }
-  g.smem = BN == 64 ? TcCfg<64>::SMEM : (BN == 128 ? TcCfg<128>::SMEM : TcCfg<256>::SMEM);
+  g.smem = BN == 64 ? TcCfg<64>::SMEM
+           : BN == 128 ? TcCfg<128>::SMEM
+           : BN == 160 ? TcCfg<160>::SMEM
+           : BN == 192 ? TcCfg<192>::SMEM
+                       : TcCfg<256>::SMEM;
   return true;
 }
 
@@ -600,6 +607,8 @@ cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s) {
   switch (g.BN) {
     case 64: return launch_bn<64>(g, s);
     case 128: return launch_bn<128>(g, s);
+    case 160: return launch_bn<160>(g, s);
+    case 192: return launch_bn<192>(g, s);
     case 256: return launch_bn<256>(g, s);
   }
   return cudaErrorInvalidValue;
