@@ -122,6 +122,11 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
 BB_API int bb_version(void);
 /* instrumentation: live per-launch GEMM timing and kernel-launch counters */
 BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream);
+/* Timeline sessions (BB_KLOG=1): phase offsets of the fused-QKV block
+ * attention, out[8] = (CTAs, then summed ns from the PDL release to: rows and
+ * keys loaded, phase-A loads issued, splice stored, cluster barrier passed,
+ * chunk 0 landed, chunk loop done, end).  Averages = out[i] / out[0]. */
+BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset, void* stream);
 BB_API int bb_session_counters(void* sess, long long* out);
 BB_API int bb_session_klog(void* sess, unsigned long long* host_out, int cap, int reset, long long* n, void* stream);
 
@@ -129,6 +134,10 @@ BB_API int bb_session_klog(void* sess, unsigned long long* host_out, int cap, in
 BB_API int bb_debug_gemm_tc(const void* W, const void* X, void* out, int n_out, int K, int rows, int BN, int mode,
                             int max_grid, float* work, long long* work_floats, const int* tgt, const float* boost,
                             float head_scale, float spike_cut, float spike_gain, void* stream);
+/* Debug: prefetch a whole [n_out][K] bf16 weight matrix into L2 (kind 0 =
+ * the GEMM's tensor-tile prefetch over all stream-K ranges, 1 = contiguous
+ * 64 KB bulk prefetches).  Measurement hook for the next-GEMM prefetch. */
+BB_API int bb_debug_l2_prefetch(const void* W, int n_out, int K, int kind, void* stream);
 BB_API int bb_debug_gemm_simt(const float* W, const float* X, float* out, int n_out, int K, int rows,
                               void* stream);
 

@@ -76,6 +76,7 @@ SIGNATURES = {
     "bb_session_info": (i32, [vp, i32p, i32]),
     "bb_session_ctrl": (i32, [vp, i32p, vp]),
     "bb_session_gemm_stats": (i32, [vp, C.POINTER(C.c_ulonglong), i32, vp]),
+    "bb_session_phase_stats": (i32, [vp, vp, i32, vp]),
     "bb_session_counters": (i32, [vp, i64p]),
     "bb_session_klog": (i32, [vp, C.POINTER(C.c_ulonglong), i32, i32, i64p, vp]),
     "bb_prefill": (i32, [vp, vp]),
@@ -89,6 +90,7 @@ SIGNATURES = {
     "bb_fill_hash_uniform": (i32, [vp, i32, i64, C.c_ulonglong, i32, f32, i64, i32, i32, vp]),
     "bb_debug_gemm_tc": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp, i64p, vp, vp, f32, f32, f32, vp]),
     "bb_debug_gemm_simt": (i32, [vp, vp, vp, i32, i32, i32, vp]),
+    "bb_debug_l2_prefetch": (i32, [vp, i32, i32, i32, vp]),
 }
 
 

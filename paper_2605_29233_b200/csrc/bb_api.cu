@@ -62,7 +62,11 @@ struct Session {
   float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
   float* ss_full = nullptr;
   int ss_ld = 1;
-  bool fuse_epi = false;  // BB_FUSE_EPI=1: fused GEMM epilogues (experimental; default stream-K + post kernels)
+  bool fuse_epi = false;     // BB_FUSE_EPI=1: fused GEMM epilogues (experimental; default stream-K + post kernels)
+  bool no_fq = true;         // BB_FQ=1: block-pass attention finalizes QKV in its prologue (opt-in; slower today)
+  long long l2pf_bytes = 0;  // BB_L2PF_MB: next-GEMM weight prefetch budget per GEMM (0 = off)
+  CUtensorMap* tmaps = nullptr;  // device copies of the GEMM weight tensor maps (prefetch operands)
+  long long tmap_cap = 0;
   unsigned long long* klog = nullptr;  // BB_KLOG=1: kernel timeline (cudaMalloc'd)
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
@@ -209,6 +213,10 @@ static void plan(Session* s, char* base, bool dry) {
     P.attn = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
     P.act = c.take<char>((long long)rows_alloc * (D.dff > 0 ? D.dff : 1) * e, 1024);
     P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
+    P.n_kz = full ? 1 : (item_rows + 63) / 64;
+    P.akey_cap = B * S.L;
+    P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
+    P.akey_n = c.take<int>((long long)R * P.n_kz * 2);
   };
   pass(s->blk, round_up(S.NR, s->gb.BN), S.max_items, S.NRq, 0);
   pass(s->full, round_up(S.NF, s->gf.BN), 1, S.L, 1);
@@ -231,7 +239,11 @@ static void plan(Session* s, char* base, bool dry) {
   view(BB_VIEW_SLOT_BR, s->blk.slot_br, (size_t)rb * 4);
   H.skip = c.take<int>(1);
   s->full_rows = c.take<int>(1);
+  s->tmap_cap = 8LL * D.layers + 1;
+  s->tmaps = c.take<CUtensorMap>((size_t)s->tmap_cap, 128);
   s->tstat = c.take<unsigned long long>(16 * 8);
+  s->blk.atstat = s->tstat + 5 * 8;   // slots 5/6: block-pass attention (duration, start spread)
+  s->full.atstat = s->tstat + 13 * 8; // slots 13/14: full-pass attention
   s->tile_cnt = c.take<int>(8192);
   s->ns_cap = 64 * 1024;
   s->ns_tabs = c.take<unsigned char>(s->ns_cap);
@@ -396,6 +408,50 @@ static int setup_gemms(Session* s) {
     s->head_simt = SimtGemm{(const float*)W.head, (const float*)s->blk.xn, D.n_out, D.d, s->blk.rows_alloc,
                             nullptr, s->H.skip, s->H.logits, D.n_out};
   }
+  // L2 prefetch chain: each GEMM's producer warp, after its last TMA load,
+  // prefetches the first part of the next GEMM's per-CTA weight ranges
+  // (qkv -> o -> gate/up -> down -> next layer's qkv; last block-pass down ->
+  // LM head), so HBM streams through the attention / post kernels between.
+  if (D.dtype == BB_DTYPE_BF16 && !s->fuse_epi && s->l2pf_bytes > 0) {
+    // device copies of every GEMM's weight tensor map (the prefetch operand)
+    std::vector<const TcGemm*> gl;
+    for (int which = 0; which < 2; ++which)
+      for (auto& lg : (which == 0 ? s->gb : s->gf).layers) {
+        gl.push_back(&lg.qkv);
+        gl.push_back(&lg.o);
+        if (D.dff) {
+          gl.push_back(&lg.gu);
+          gl.push_back(&lg.dn);
+        }
+      }
+    gl.push_back(&s->head_tc);
+    if ((long long)gl.size() > s->tmap_cap) return BB_ERR_NOMEM;
+    std::vector<CUtensorMap> maps(gl.size());
+    for (size_t i = 0; i < gl.size(); ++i) maps[i] = gl[i]->tmA;
+    if (cudaMemcpy(s->tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess)
+      return BB_ERR_CUDA;
+    auto dev_map = [&](const TcGemm* g) -> const CUtensorMap* {
+      for (size_t i = 0; i < gl.size(); ++i)
+        if (gl[i] == g) return s->tmaps + i;
+      return nullptr;
+    };
+    for (int which = 0; which < 2; ++which) {
+      PassGemms& G = which == 0 ? s->gb : s->gf;
+      for (int l = 0; l < D.layers; ++l) {
+        LayerGemms& lg = G.layers[l];
+        std::vector<TcGemm*> chain = {&lg.qkv, &lg.o};
+        if (D.dff) {
+          chain.push_back(&lg.gu);
+          chain.push_back(&lg.dn);
+        }
+        for (size_t i = 0; i < chain.size(); ++i) {
+          const TcGemm* next = i + 1 < chain.size() ? chain[i + 1]
+                               : (l + 1 < D.layers ? &G.layers[l + 1].qkv : (which == 0 ? &s->head_tc : nullptr));
+          if (next != nullptr) chain[i]->p.pf = tc_gemm_l2pf(*next, dev_map(next), s->l2pf_bytes);
+        }
+      }
+    }
+  }
   return BB_OK;
 }
 
@@ -428,7 +484,7 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
     if (fused) {
       // QKV (+bias, RoPE, KV splice) -> attention -> O (+residual) -> norm -> GU (+SwiGLU) -> down (+residual) -> norm
       if ((e = tc_gemm_launch(lg.qkv, st)) != cudaSuccess) return e;
-      if ((e = launch_attn(D, s->S, P, s->st, l, st)) != cudaSuccess) return e;
+      if ((e = launch_attn(D, s->S, P, s->st, l, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
       if ((e = tc_gemm_launch(lg.o, st)) != cudaSuccess) return e;
       if (D.dff) {
         if ((e = launch_norm(D, P, ss, s->ss_ld, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
@@ -440,8 +496,13 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
     }
     PartRef pr;
     if ((e = run_gemm(s, lg.qkv, lg.sqkv, &pr, st)) != cudaSuccess) return e;
-    if ((e = launch_post_qkv(D, s->S, P, s->st, W, l, pr, st)) != cudaSuccess) return e;
-    if ((e = launch_attn(D, s->S, P, s->st, l, st)) != cudaSuccess) return e;
+    if (D.dtype == BB_DTYPE_BF16 && attn_fuses_qkv(D, s->S, P) && !s->no_fq) {
+      const float* bias = W.bqkv != nullptr ? W.bqkv + (size_t)l * D.qkv_out : nullptr;
+      if ((e = launch_attn(D, s->S, P, s->st, l, &pr, bias, W.rope, st)) != cudaSuccess) return e;
+    } else {
+      if ((e = launch_post_qkv(D, s->S, P, s->st, W, l, pr, st)) != cudaSuccess) return e;
+      if ((e = launch_attn(D, s->S, P, s->st, l, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
+    }
     if ((e = run_gemm(s, lg.o, lg.so, &pr, st)) != cudaSuccess) return e;
     if (D.dff) {
       if ((e = launch_post_residual(D, P, pr, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
@@ -472,6 +533,7 @@ static int enqueue_prefill(Session* s, cudaStream_t st) {
   const Dims& D = s->D;
   const Sess& S = s->S;
   CK(launch_prefill_init(D, S, s->st, s->full, s->blk, s->H, st));
+  CK(launch_attn_keys(D, S, s->full, s->st, st));
   CK(forward(s, s->full, s->gf, st));
   CK(launch_gather_head(D, S, s->full, s->blk, s->H, -1, st));
   CK(head(s, st));
@@ -489,6 +551,7 @@ static int enqueue_block_step(Session* s, cudaStream_t st) {
   CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
   CK(launch_block_pack(D, S, s->st, s->blk, s->H, st));
   CK(launch_copy_pages(D, S, s->st, 0, st));
+  CK(launch_attn_keys(D, S, s->blk, s->st, st));
   CK(forward(s, s->blk, s->gb, st));
   CK(head(s, st));
   CK(launch_step_commit(D, S, s->st, s->blk, s->H, st));
@@ -505,6 +568,7 @@ static int enqueue_refresh(Session* s, cudaStream_t st) {
   for (int k = 0; k < S.B; ++k) {
     CK(cudaMemsetAsync(s->full.skip, 1, sizeof(int), st));
     CK(launch_refresh_pack(D, S, s->st, s->full, s->blk, s->H, k, st));
+    CK(launch_attn_keys(D, S, s->full, s->st, st));
     CK(forward(s, s->full, s->gf, st));
     CK(launch_gather_head(D, S, s->full, s->blk, s->H, k, st));
   }
@@ -694,6 +758,8 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   for (int i = 0; i < BB_VIEW_COUNT; ++i)
     if (s->layout[i][1]) s->layout[i][0] += (long long)(base - (char*)workspace);
   s->fuse_epi = s->D.dtype == BB_DTYPE_BF16 && getenv("BB_FUSE_EPI") != nullptr && atoi(getenv("BB_FUSE_EPI")) != 0;
+  s->no_fq = !(getenv("BB_FQ") != nullptr && atoi(getenv("BB_FQ")) != 0);
+  s->l2pf_bytes = (long long)(getenv("BB_L2PF_MB") != nullptr ? atof(getenv("BB_L2PF_MB")) : 0.0) * (1 << 20);
   if (getenv("BB_KLOG") != nullptr && atoi(getenv("BB_KLOG")) != 0) {
     const int cap = 1 << 20;
     if (cudaMalloc(&s->klog, (1 + 2 * (size_t)cap) * 8) == cudaSuccess) {
@@ -851,8 +917,10 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
   return BB_OK;
 }
 
-// live GEMM timing: out[16][5] = (unused min, unused max, unused, sum ns, launches)
-// kinds 0-3: block-pass QKV, O, gate/up, down; 4: LM head; 8-11: full-pass QKV..down
+// live kernel timing: out[16][5] = (unused min, unused max, unused, sum ns, launches)
+// kinds 0-3: block-pass QKV, O, gate/up, down; 4: LM head; 8-11: full-pass QKV..down;
+// 5/13: block/full-pass tensor-core attention duration after its PDL wait,
+// 6/14: spread of that attention's CTA start times (cluster placement)
 BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream) {
   Session* s = (Session*)sess;
   if (!s || !host_out) return BB_ERR_CONTRACT;
@@ -868,6 +936,22 @@ BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int r
       for (int j = 1; j < 8; ++j) ts[k * 8 + j] = 0;
     }
     CK(cudaMemcpyAsync(s->tstat, ts.data(), ts.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return BB_OK;
+}
+
+// timeline sessions (BB_KLOG=1): fused-QKV block attention phase offsets,
+// out[8] = (CTAs, sum ns to: rows/keys loaded, phase-A loads issued, splice
+// stored, cluster barrier, q gathered + chunk 0 landed, chunk loop done, end)
+BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !out) return BB_ERR_CONTRACT;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(out, s->tstat + 7 * 8, 8 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (reset) {
+    CK(cudaMemsetAsync(s->tstat + 7 * 8, 0, 8 * 8, st));
     CK(cudaStreamSynchronize(st));
   }
   return BB_OK;

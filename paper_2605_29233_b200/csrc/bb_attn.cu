@@ -12,6 +12,7 @@
 // unnormalised (o, m, l) partial; k_attn_combine merges the partials of the
 // items covering each row (flash-decoding style LSE merge, fixed order).
 #include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "bb_common.cuh"
 #include "bb_launch.cuh"
@@ -179,74 +180,37 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 }
 
 // ---------------------------------------------------------------------------
-// Shared-prefix attention without partials (bf16 mma.sync, HD <= 128).
+// Key lists of the tensor-core attention, built once per pass.
 //
-// Cluster of ATT_CS CTAs = (request, q-head, 64-row tile of the request's
-// rows); each CTA of the cluster takes 1/ATT_CS of the key chunks and the
-// partial softmax states are merged through distributed shared memory
-// (each CTA normalises 64/ATT_CS rows).  The rows may belong to several
-// branches.  The CTA walks logical pages lp = 0..n_lp-1;
-// for each lp it loads every DISTINCT physical page among its rows' branches
-// once (a page aliased by k branches -- prompt after prefill, everything after
-// a sync -- is streamed once for all of them) and scores it against all rows
-// with a per-key branch mask: row r only sees keys whose page its own branch
-// maps at that lp.  Online softmax per row, one pass, normalised output
-// written directly (no split-K partials, no combine kernel).
-constexpr int ATT_CS = 8;
+// The page tables do not change between the layers of a pass, so the walk
+// over logical pages that finds, per lp, the DISTINCT physical pages among a
+// key tile's branches (a page aliased by k branches -- prompt after prefill,
+// everything after a sync -- is one segment with a k-bit branch mask) runs
+// here once instead of in every (layer, head) attention cluster.  One CTA per
+// (request, key tile); keys are emitted lp-major as (global page * ps + row,
+// branch mask); akey_n = (n_keys, first key of the generation pages).
+constexpr int KEY_WIN = 1 << 30;  // key-list flag: position rewritten by this step's splice
 
-template <int HD>
-__global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
-    k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
+__global__ void __launch_bounds__(256) k_attn_keys(Sess S, Pass P, DevState st, int rows_per_req) {
   pdl_enter();
-  klog_mark(D.klog, D.klog_cap, 3);
-  using bf = __nv_bfloat16;
-  constexpr int KC = 64, LD = HD + 8, QR = 64;
-  extern __shared__ __align__(16) uint8_t smraw[];
-  bf* sQ = reinterpret_cast<bf*>(smraw);
-  bf* sKb = sQ + QR * LD;       // [2][KC][LD]
-  bf* sVb = sKb + 2 * KC * LD;  // [2][KC][LD]
-  long long* sSegOff = reinterpret_cast<long long*>(sVb + 2 * KC * LD);  // [n_seg] page element base
-  int* sSegStart = reinterpret_cast<int*>(sSegOff + S.n_lp * S.B);       // [n_lp] first key of lp
-  int* sSegMask = sSegStart + S.n_lp * S.B + 1;                          // [n_lp][B]
-  __shared__ long long sKeyOff[2][KC];
-  __shared__ int sKeyMask[2][KC];
-  __shared__ int sRow[QR], sBr[QR];
-  __shared__ int s_bmask, s_nseg;
-
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int crank = (int)cluster.block_rank();
-  const int r = blockIdx.x / ATT_CS, h = blockIdx.y;
-  const int row0 = blockIdx.z * QR;
-  const int kvh = h / (D.nh / D.nkv);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  extern __shared__ __align__(16) int ksm[];
+  int* sPT = ksm;                         // [B][n_lp]
+  int* sCnt = sPT + S.B * S.n_lp;         // [n_lp] keys per lp -> exclusive start
+  int* sSeg = sCnt + S.n_lp + 1;          // [n_lp][B] physical page of segment
+  int* sMsk = sSeg + S.n_lp * S.B;        // [n_lp][B] branch mask of segment
+  __shared__ int s_bmask, s_tot, s_gen0;
+  const int r = blockIdx.x, kz = blockIdx.y;
   const int slot_base = P.full ? r * S.L : r * S.NRq;
   if (threadIdx.x == 0) s_bmask = 0;
   __syncthreads();
-  if (threadIdx.x < QR) {
-    const int lr = row0 + threadIdx.x;
-    int slot = -1, br = 0;
-    if (lr < rows_per_req && !*P.skip) {
-      const int sl = slot_base + lr;
-      if (P.slot_pos[sl] >= 0) {
-        slot = sl;
-        br = P.slot_br[sl];
-        atomicOr(&s_bmask, 1 << br);
-      }
-    }
-    sRow[threadIdx.x] = slot;
-    sBr[threadIdx.x] = br;
+  const bool skip = *P.skip != 0;
+  for (int lr = kz * 64 + (int)threadIdx.x; lr < min(rows_per_req, kz * 64 + 64) && !skip; lr += blockDim.x) {
+    const int sl = slot_base + lr;
+    if (P.slot_pos[sl] >= 0) atomicOr(&s_bmask, 1 << P.slot_br[sl]);
   }
-  __syncthreads();
-  const int bmask = s_bmask;
-  // segments: per logical page lp, the distinct physical pages among the rows'
-  // branches (<= B each) with their branch masks; discovered in parallel over
-  // lp from the request's page tables staged in smem, then a block scan of
-  // the per-lp key counts gives every key's (lp, segment, offset).
-  const long long lay = (long long)layer * S.R * S.pool;
-  int* sPT = reinterpret_cast<int*>(sSegMask + S.n_lp * S.B);
   for (int i = threadIdx.x; i < S.B * S.n_lp; i += blockDim.x) sPT[i] = st.pt[(long long)r * S.B * S.n_lp + i];
   __syncthreads();
+  const int bmask = s_bmask;
   for (int lp = threadIdx.x; lp < S.n_lp; lp += blockDim.x) {
     int left = bmask, n = 0;
     while (left) {
@@ -256,89 +220,361 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       for (int k2 = k; k2 < S.B; ++k2)
         if (((left >> k2) & 1) && sPT[k2 * S.n_lp + lp] == phys) m |= 1 << k2;
       left &= ~m;
-      sSegOff[lp * S.B + n] = ((lay + (long long)r * S.pool + phys) * D.nkv + kvh) * S.ps * HD;
-      sSegMask[lp * S.B + n] = m;
+      sSeg[lp * S.B + n] = phys;
+      sMsk[lp * S.B + n] = m;
       ++n;
     }
-    sSegStart[lp] = n * (lp_end(S, lp) - lp_start(S, lp));  // keys contributed by lp
+    sCnt[lp] = n * (lp_end(S, lp) - lp_start(S, lp));
   }
   __syncthreads();
-  if (threadIdx.x < 32) {  // exclusive scan over lp (one warp, n_lp <= 32 * per-lane chunk)
+  if (threadIdx.x < 32) {  // exclusive scan over lp, one warp, per-lane runs
     const int per = (S.n_lp + 31) / 32;
     const int b0 = threadIdx.x * per, b1 = min(S.n_lp, b0 + per);
     int tot = 0;
-    for (int i = b0; i < b1; ++i) tot += sSegStart[i];
+    for (int i = b0; i < b1; ++i) tot += sCnt[i];
     int incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (threadIdx.x >= o) incl += v;
+      if ((int)threadIdx.x >= o) incl += v;
     }
     int run = incl - tot;
     for (int i = b0; i < b1; ++i) {
-      const int v = sSegStart[i];
-      sSegStart[i] = run;
+      const int v = sCnt[i];
+      sCnt[i] = run;
+      if (i == S.n_pp) s_gen0 = run;
       run += v;
     }
-    if (threadIdx.x == 31) s_nseg = incl;  // total keys
+    if (threadIdx.x == 31) {
+      s_tot = incl;
+      if (S.n_pp >= S.n_lp) s_gen0 = incl;
+    }
   }
   __syncthreads();
-  const int n_keys = s_nseg;
+  const long long kb = (long long)r * P.n_kz + kz;
+  int* out = P.akeys + kb * P.akey_cap * 2;
+  // block pass: keys at a window position of one of their branches are
+  // rewritten by this step's splice (KEY_WIN) -- the attention loads every
+  // other key before the splice is published
+  __shared__ int s_ws[MAXB], s_we[MAXB];
+  if (threadIdx.x < MAXB) {
+    const int k = threadIdx.x;
+    const bool on = !P.full && k < S.B && ((bmask >> k) & 1);
+    s_ws[k] = on ? st.br[(r * S.B + k) * B_WORDS + B_START] : 0;
+    s_we[k] = on ? st.br[(r * S.B + k) * B_WORDS + B_END] : 0;
+  }
+  __syncthreads();
+  // one thread per (lp, segment, row): lp-major emission
+  for (int lp = threadIdx.x / 32; lp < S.n_lp; lp += blockDim.x / 32) {
+    const int s0 = lp_start(S, lp), nk = lp_end(S, lp) - s0;
+    const int base = sCnt[lp];
+    const int nseg = (lp + 1 < S.n_lp ? sCnt[lp + 1] : s_tot) - base;
+    for (int e = threadIdx.x & 31; e < nseg; e += 32) {
+      const int j = e / nk, row = e - j * nk;
+      const int pg = r * S.pool + sSeg[lp * S.B + j];
+      const int m = sMsk[lp * S.B + j], pos = s0 + row;
+      bool win = false;
+      for (int k = 0; k < S.B; ++k) win |= ((m >> k) & 1) && pos >= s_ws[k] && pos < s_we[k];
+      out[2 * (base + e)] = pg * S.ps + row;
+      out[2 * (base + e) + 1] = m | (win ? KEY_WIN : 0);
+    }
+  }
+  if (threadIdx.x == 0) {
+    P.akey_n[2 * kb] = s_tot;
+    P.akey_n[2 * kb + 1] = s_gen0;
+  }
+}
+
+cudaError_t launch_attn_keys(const Dims& D, const Sess& S, const Pass& P, const DevState& st, cudaStream_t s) {
+  if (uses_items(D)) return cudaSuccess;
+  const int rows = P.full ? S.L : S.NRq;
+  const size_t smem = (size_t)(S.B * S.n_lp + S.n_lp + 1 + 2 * S.n_lp * S.B) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  launch_k(k_attn_keys, dim3(S.R, P.n_kz), dim3(256), smem, s, S, P, st, rows);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Shared-prefix attention without partials (bf16 mma.sync, HD <= 128).
+//
+// Cluster of ATT_CS CTAs = (request, q-head, 64-row tile of the request's
+// rows); each CTA of the cluster takes 1/ATT_CS of the key chunks of the
+// tile's key list (k_attn_keys) and the partial softmax states are merged
+// through distributed shared memory (each CTA normalises 64/ATT_CS rows).
+// The rows may belong to several branches: a shared page is one run of keys
+// carrying a branch mask, and row r only sees keys whose mask holds its own
+// branch.  Online softmax per row, one pass, normalised output written
+// directly (no split-K partials, no combine kernel).
+//
+// FQ (block pass, all rows of a request in one tile): the QKV finalize
+// (model.py:283-293: + bias, RoPE, splice of the window's fresh K/V into the
+// branch's pages) runs in the prologue instead of a separate post kernel.
+// CTA c of the cluster sums the stream-K partial planes for rows
+// [8c, 8c+8) of its head's q and its kv-head's k/v, writes k/v into the
+// pages, and the q rows are exchanged through distributed shared memory.
+// Chunks made only of prompt keys are prefetched before the splice; chunks
+// that may hold window keys are loaded after the cluster barrier that
+// publishes the splice.
+// timeline runs only: per-CTA phase offsets from the PDL release, summed into
+// ph[1..7] with ph[0] = CTAs (bb_session_phase_stats)
+__device__ __forceinline__ void phase_mark(unsigned long long* ph, int i, unsigned long long t0) {
+  if (ph != nullptr && threadIdx.x == 0) atomicAdd(&ph[i], globaltimer_ns() - t0);
+}
+
+template <int HD, bool FQ, int ATT_CS>
+__global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
+    k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req, PartRef pr,
+               const float* __restrict__ bias, const float* __restrict__ rope) {
+  pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 3);
+  unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;  // timeline runs only
+  tstat_begin(ats);
+  tstat_begin(ats != nullptr ? ats + 8 : nullptr);
+  tstat_end(ats != nullptr ? ats + 8 : nullptr);
+  unsigned long long* const ph = (ats != nullptr && FQ) ? ats + 16 : nullptr;  // slot 7
+  const unsigned long long t0 = ph != nullptr ? globaltimer_ns() : 0ull;
+  if (ph != nullptr && threadIdx.x == 0) atomicAdd(&ph[0], 1ull);
+  using bf = __nv_bfloat16;
+  constexpr int KC = 64, LD = HD + 8, QR = 64;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  bf* sQ = reinterpret_cast<bf*>(smraw);
+  bf* sKb = sQ + QR * LD;       // [2][KC][LD]
+  bf* sVb = sKb + 2 * KC * LD;  // [2][KC][LD]
+  int2* sKeys = reinterpret_cast<int2*>(sVb + 2 * KC * LD);  // this CTA's keys
+  __shared__ int sRow[QR], sBr[QR], sPos[QR];
+  __shared__ long long sKvo[QR];
+  __shared__ int s_nk, s_gen0;
+  __shared__ int sNS[FQ ? 3 * (QR / ATT_CS) : 1];  // FQ: partial planes per (q|k|v, row)
+
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int r = blockIdx.x / ATT_CS, h = blockIdx.y;
+  const int row0 = blockIdx.z * QR;
+  const int kvh = h / (D.nh / D.nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : blockIdx.z);
+  if (threadIdx.x < QR) {
+    const int lr = row0 + threadIdx.x;
+    int slot = -1, br = 0, pos = -1;
+    long long kvo = 0;
+    if (lr < rows_per_req) {
+      const int sl = slot_base + lr;
+      pos = P.slot_pos[sl];
+      br = P.slot_br[sl];
+      if (FQ) kvo = P.slot_kvoff[sl];
+      if (pos >= 0 && !*P.skip) slot = sl;
+    }
+    sRow[threadIdx.x] = slot;
+    sBr[threadIdx.x] = br;
+    sPos[threadIdx.x] = pos;
+    sKvo[threadIdx.x] = kvo;
+  } else if (threadIdx.x == QR) {
+    s_nk = P.akey_n[2 * kb];
+    s_gen0 = P.akey_n[2 * kb + 1];
+  } else if (FQ && threadIdx.x > QR && threadIdx.x <= QR + 3 * (QR / ATT_CS)) {
+    // stream-K piece count of the (q|k|v column tile, row) pairs this CTA finalizes
+    const int e = threadIdx.x - QR - 1, which = e / (QR / ATT_CS), rr = e % (QR / ATT_CS);
+    const int hh = which == 0 ? h : (which == 1 ? D.nh + kvh : D.nh + D.nkv + kvh);
+    const int row = slot_base + row0 + crank * (QR / ATT_CS) + rr;
+    sNS[e] = row < P.rows_alloc ? sk_nslots(pr.sk, row, hh * HD) : 1;
+  }
+  __syncthreads();
+  const int n_keys = s_nk;
+  phase_mark(ph, 1, t0);
+  const long long lay = (long long)layer * S.R * S.pool;
   constexpr int VPR = HD / 8;
-  const bf* Qg = reinterpret_cast<const bf*>(P.q);
   const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
   const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
-  for (int i = threadIdx.x; i < QR * VPR; i += blockDim.x) {
-    const int rr = i / VPR, v = i % VPR;
-    const int slot = sRow[rr];
-    cp_async16(sQ + rr * LD + v * 8, Qg + (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8, slot >= 0);
-  }
-  cp_async_commit();
-  auto fill_keys = [&](int c, int tb) {  // threads < KC: key c*KC+j -> (offset, mask)
-    if (threadIdx.x < KC) {
-      const int key = c * KC + threadIdx.x;
-      long long off = 0;
-      int m = 0;
-      if (key < n_keys) {
-        int lo = 0, hi = S.n_lp - 1;  // last lp with start <= key
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (sSegStart[mid] <= key) lo = mid;
-          else hi = mid - 1;
-        }
-        const int nk = lp_end(S, lo) - lp_start(S, lo);
-        const int rel = key - sSegStart[lo];
-        const int j = rel / nk;
-        off = sSegOff[lo * S.B + j] + (long long)(rel - j * nk) * HD;
-        m = sSegMask[lo * S.B + j];
-      }
-      sKeyOff[tb][threadIdx.x] = off;
-      sKeyMask[tb][threadIdx.x] = m;
+  const int n_all = (n_keys + KC - 1) / KC;
+  const int c_begin = (int)((long long)n_all * crank / ATT_CS), c_end = (int)((long long)n_all * (crank + 1) / ATT_CS);
+  const int n_chunks = c_end - c_begin;
+  // this CTA's keys -> registers now, smem after the phase-A loads are out
+  // (keeps the two L2 round trips overlapped)
+  constexpr int KREG = 4;
+  int2 kr[KREG];
+  const int nkc = n_chunks * KC;
+  {
+    const int2* src = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + (long long)c_begin * KC;
+    const int nk_cta = min(nkc, n_keys - c_begin * KC);
+#pragma unroll
+    for (int u = 0; u < KREG; ++u) {
+      const int i = threadIdx.x + u * 128;
+      kr[u] = i < nk_cta ? src[i] : make_int2(0, 0);
     }
+    for (int i = threadIdx.x + KREG * 128; i < nkc; i += blockDim.x) sKeys[i] = i < nk_cta ? src[i] : make_int2(0, 0);
+  }
+  auto store_keys = [&]() {
+#pragma unroll
+    for (int u = 0; u < KREG; ++u)
+      if (threadIdx.x + u * 128 < nkc) sKeys[threadIdx.x + u * 128] = kr[u];
   };
-  auto load_chunk = [&](int c, int buf) {
-    const int nk = min(KC, n_keys - c * KC);
+  const long long kvstride = (long long)S.ps * HD;
+  // ci: chunk index relative to c_begin; part 0 = all keys, 1 = all but the
+  // window keys (before the splice), 2 = only the window keys (after it)
+  auto load_chunk = [&](int ci, int buf, int part) {
     bf* dK = sKb + buf * KC * LD;
     bf* dV = sVb + buf * KC * LD;
+    const int nk = min(KC, n_keys - (c_begin + ci) * KC);
     for (int i = threadIdx.x; i < KC * VPR; i += blockDim.x) {
       const int j = i / VPR, v = i % VPR;
+      const int2 e = sKeys[ci * KC + j];
       const bool ok = j < nk;
-      const long long off = sKeyOff[buf][j] + v * 8;
-      cp_async16(dK + j * LD + v * 8, Kg + off, ok);
-      cp_async16(dV + j * LD + v * 8, Vg + off, ok);
+      const bool win = ok && (e.y & KEY_WIN) != 0;
+      if ((part == 1 && win) || (part == 2 && !win)) continue;
+      const int pg = e.x / S.ps;
+      const long long off = ((lay + pg) * D.nkv + kvh) * kvstride + (long long)(e.x - pg * S.ps) * HD + v * 8;
+      cp_async16(dK + j * LD + v * 8, Kg + (ok ? off : 0), ok);
+      cp_async16(dV + j * LD + v * 8, Vg + (ok ? off : 0), ok);
     }
     cp_async_commit();
   };
-  const int n_all = bmask ? (n_keys + KC - 1) / KC : 0;
-  const int c_begin = (int)((long long)n_all * crank / ATT_CS), c_end = (int)((long long)n_all * (crank + 1) / ATT_CS);
-  const int n_chunks = c_end - c_begin;
-  if (n_chunks > 0) {
-    fill_keys(c_begin, 0);
-    __syncthreads();
-    load_chunk(c_begin, 0);
-    cp_async_wait<1>();
+  if (FQ) {
+    // QKV finalize for rows [8*crank, 8*crank+8) of this tile.  Items are
+    // (row, q|k|v, 4 consecutive pair indices); the plane loop is outside
+    // the item loop so every item's plane-q loads are independent (one L2
+    // round trip per plane level, no stores in between), then math + stores.
+    constexpr int RPC = QR / ATT_CS, HALF = HD / 2, I4 = HALF / 4;
+    constexpr int TOT = RPC * 3 * I4, NIT = (TOT + 127) / 128;
+    const long long lay_el = (long long)layer * S.R * S.pool * D.nkv * kvstride;
+    float4 va[NIT], vb[NIT], ba[NIT], bb4[NIT], c01[NIT], c23[NIT];
+    const float* pk[NIT];
+    int nsk[NIT];
+#pragma unroll
+    for (int k = 0; k < NIT; ++k) {
+      const int it = threadIdx.x + k * 128;
+      const int rr = it / (3 * I4), rem = it - rr * 3 * I4;
+      const int which = rem / I4, i = (rem - which * I4) * 4;
+      const int lr = crank * RPC + rr;
+      const int slot = it < TOT ? sRow[lr] : -1;
+      const int hh = which == 0 ? h : (which == 1 ? D.nh + kvh : D.nh + D.nkv + kvh);
+      const int c0 = hh * HD + i;
+      nsk[k] = slot >= 0 ? sNS[which * RPC + rr] : 0;
+      pk[k] = pr.part + (long long)(slot >= 0 ? slot : 0) * pr.ldp + c0;
+      va[k] = vb[k] = ba[k] = bb4[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      c01[k] = c23[k] = make_float4(1.0f, 0.0f, 1.0f, 0.0f);
+      if (slot >= 0 && bias != nullptr) {
+        ba[k] = __ldg(reinterpret_cast<const float4*>(bias + c0));
+        bb4[k] = __ldg(reinterpret_cast<const float4*>(bias + c0 + HALF));
+      }
+      if (slot >= 0 && D.arch == 1 && which < 2) {
+        const float4* cp = reinterpret_cast<const float4*>(rope + ((long long)sPos[lr] * HALF + i) * 2);
+        c01[k] = __ldg(cp);
+        c23[k] = __ldg(cp + 1);
+      }
+    }
+    auto add4 = [](float4& acc, const float4 v) {
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    };
+    // all plane levels in one batch (one L2 round trip), then the keys to
+    // smem and the splice-independent part of the first chunk
+    float4 ta[4][NIT], tb[4][NIT];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        ta[q][k] = tb[q][k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (q < nsk[k]) {
+          ta[q][k] = __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane));
+          tb[q][k] = __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane + HALF));
+        }
+      }
+    store_keys();
+    __syncthreads();  // sKeys
+    if (n_chunks > 0) load_chunk(0, 0, 1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        add4(va[k], ta[q][k]);
+        add4(vb[k], tb[q][k]);
+      }
+#pragma unroll
+    for (int k = 0; k < NIT; ++k)
+      for (int q = 4; q < nsk[k]; ++q) {
+        add4(va[k], __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane)));
+        add4(vb[k], __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane + HALF)));
+      }
+    phase_mark(ph, 2, t0);  // (issue order only: the adds below wait for the loads)
+#pragma unroll
+    for (int k = 0; k < NIT; ++k) {  // bias after the planes: part_sum's rounding order
+      add4(va[k], ba[k]);
+      add4(vb[k], bb4[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < NIT; ++k) {
+      const int it = threadIdx.x + k * 128;
+      if (it >= TOT) continue;
+      const int rr = it / (3 * I4), rem = it - rr * 3 * I4;
+      const int which = rem / I4, i = (rem - which * I4) * 4;
+      const int lr = crank * RPC + rr;
+      const float ax[4] = {va[k].x, va[k].y, va[k].z, va[k].w}, bx[4] = {vb[k].x, vb[k].y, vb[k].z, vb[k].w};
+      const float cx[4] = {c01[k].x, c01[k].z, c23[k].x, c23[k].z}, sx[4] = {c01[k].y, c01[k].w, c23[k].y, c23[k].w};
+      __align__(8) bf oa[4], ob[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        oa[e] = __float2bfloat16(ax[e] * cx[e] - bx[e] * sx[e]);
+        ob[e] = __float2bfloat16(bx[e] * cx[e] + ax[e] * sx[e]);
+      }
+      bf* dst;
+      if (which == 0) {
+        dst = sQ + lr * LD;
+      } else {
+        if (sRow[lr] < 0) continue;
+        dst = reinterpret_cast<bf*>(which == 1 ? st.kv_k : st.kv_v) + lay_el + sKvo[lr] + (long long)kvh * kvstride;
+      }
+      *reinterpret_cast<uint2*>(dst + i) = *reinterpret_cast<const uint2*>(oa);
+      *reinterpret_cast<uint2*>(dst + i + HALF) = *reinterpret_cast<const uint2*>(ob);
+    }
+    phase_mark(ph, 3, t0);
+    cluster.sync();  // publishes the K/V splice and every CTA's q rows
+    phase_mark(ph, 4, t0);
+    constexpr int QV = HD / 8;  // 16-byte vectors per q row
+    constexpr int NG = QR * QV / 128;
+    uint4 qv[NG];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      const int idx = threadIdx.x + k * 128;
+      const int lr = idx / QV, v = idx - lr * QV;
+      const int owner = lr / RPC;
+      const bf* src = owner == crank ? sQ + lr * LD : cluster.map_shared_rank(sQ + lr * LD, owner);
+      qv[k] = reinterpret_cast<const uint4*>(src)[v];
+    }
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      const int idx = threadIdx.x + k * 128;
+      const int lr = idx / QV, v = idx - lr * QV;
+      if (lr / RPC != crank) reinterpret_cast<uint4*>(sQ + lr * LD)[v] = qv[k];
+    }
+    if (n_chunks > 0) {
+      load_chunk(0, 0, 2);  // the window keys just spliced
+      cp_async_wait<0>();
+    }
+    phase_mark(ph, 5, t0);
   } else {
-    cp_async_wait<0>();
+    const bf* Qg = reinterpret_cast<const bf*>(P.q);
+    for (int i = threadIdx.x; i < QR * VPR; i += blockDim.x) {
+      const int rr = i / VPR, v = i % VPR;
+      const int slot = sRow[rr];
+      cp_async16(sQ + rr * LD + v * 8, Qg + (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8, slot >= 0);
+    }
+    cp_async_commit();
+    store_keys();
+    __syncthreads();  // sKeys
+    if (n_chunks > 0) {
+      load_chunk(0, 0, 0);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
   }
   __syncthreads();
   uint32_t qf[HD / 16][4];
@@ -363,9 +599,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   for (int ci = 0; ci < n_chunks; ++ci) {
     const int nk = min(KC, n_keys - (c_begin + ci) * KC);
     if (ci + 1 < n_chunks) {
-      fill_keys(c_begin + ci + 1, (ci + 1) & 1);
-      __syncthreads();
-      load_chunk(c_begin + ci + 1, (ci + 1) & 1);
+      load_chunk(ci + 1, (ci + 1) & 1, 0);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -375,6 +609,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       const int tb = ci & 1;
       const bf* sK = sKb + tb * KC * LD;
       const uint32_t sV_u = smem_u32(sVb + tb * KC * LD);
+      const int2* kmask = sKeys + ci * KC;
       float s[KC / 8][4];
 #pragma unroll
       for (int nt = 0; nt < KC / 8; ++nt) {
@@ -393,7 +628,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int j = 8 * nt + 2 * t + e;
-          const int km = j < nk ? sKeyMask[tb][j] : 0;
+          const int km = j < nk ? kmask[j].y : 0;
           s[nt][e] = ((km >> bA) & 1) ? s[nt][e] * sl2 : -INFINITY;
           s[nt][2 + e] = ((km >> bB) & 1) ? s[nt][2 + e] * sl2 : -INFINITY;
         }
@@ -454,6 +689,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     }
     __syncthreads();
   }
+  phase_mark(ph, 6, t0);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
@@ -475,31 +711,45 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     }
   }
   cluster.sync();
-  // merge: this CTA normalises rows [crank*QR/CS, (crank+1)*QR/CS) across the cluster
+  // merge: this CTA normalises rows [crank*QR/CS, (crank+1)*QR/CS) across the
+  // cluster; every rank's (m, l, o) is gathered into registers first
   constexpr int RPC = QR / ATT_CS;
   constexpr int V4 = HD / 4;
-  for (int i = threadIdx.x; i < RPC * V4; i += blockDim.x) {
+  constexpr int NMI = (RPC * V4 + 127) / 128;
+  float mr[NMI][ATT_CS], lv[NMI][ATT_CS];
+  float4 ov[NMI][ATT_CS];
+#pragma unroll
+  for (int k = 0; k < NMI; ++k) {
+    const int i = threadIdx.x + k * 128;
+    const int lr = crank * RPC + (i < RPC * V4 ? i / V4 : 0), c4 = (i % V4) * 4;
+#pragma unroll
+    for (int q = 0; q < ATT_CS; ++q) {
+      mr[k][q] = *cluster.map_shared_rank(sM + lr, q);
+      lv[k][q] = *cluster.map_shared_rank(sL + lr, q);
+      ov[k][q] = *reinterpret_cast<const float4*>(cluster.map_shared_rank(sO + lr * OLD + c4, q));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NMI; ++k) {
+    const int i = threadIdx.x + k * 128;
+    if (i >= RPC * V4) continue;
     const int lr = crank * RPC + i / V4, c4 = (i % V4) * 4;
     const int slot = sRow[lr];
     if (slot < 0) continue;
-    float mr[ATT_CS], M = -INFINITY;
+    float M = -INFINITY;
 #pragma unroll
-    for (int q = 0; q < ATT_CS; ++q) {
-      mr[q] = *cluster.map_shared_rank(sM + lr, q);
-      M = fmaxf(M, mr[q]);
-    }
+    for (int q = 0; q < ATT_CS; ++q) M = fmaxf(M, mr[k][q]);
     float Lsum = 0.0f;
     float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
     for (int q = 0; q < ATT_CS; ++q) {
-      if (mr[q] == -INFINITY) continue;
-      const float w = exp2f(mr[q] - M);
-      Lsum += w * *cluster.map_shared_rank(sL + lr, q);
-      const float4 v = *reinterpret_cast<const float4*>(cluster.map_shared_rank(sO + lr * OLD + c4, q));
-      acc.x += w * v.x;
-      acc.y += w * v.y;
-      acc.z += w * v.z;
-      acc.w += w * v.w;
+      if (mr[k][q] == -INFINITY) continue;
+      const float w = exp2f(mr[k][q] - M);
+      Lsum += w * lv[k][q];
+      acc.x += w * ov[k][q].x;
+      acc.y += w * ov[k][q].y;
+      acc.z += w * ov[k][q].z;
+      acc.w += w * ov[k][q].w;
     }
     const float inv = 1.0f / Lsum;
     bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4;
@@ -510,21 +760,40 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     *reinterpret_cast<uint2*>(out) = u;
   }
   cluster.sync();
+  phase_mark(ph, 7, t0);
+  tstat_end(ats);
 }
 
-template <int HD>
-static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
-                               cudaStream_t s) {
+template <int HD, bool FQ, int CS>
+static cudaError_t attn_seg_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
+                                   const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
   const int rows = P.full ? S.L : S.NRq;
-  const size_t smem = (size_t)(64 + 4 * 64) * (HD + 8) * 2 + (size_t)S.n_lp * S.B * (8 + 4 + 4 + 4) + 32;
+  const int max_ck = (P.akey_cap + 64 * CS - 1) / (64 * CS);  // chunks per CTA, upper bound
+  const size_t smem = (size_t)(64 + 4 * 64) * (HD + 8) * 2 + (size_t)max_ck * 64 * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_seg<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_attn_seg<HD, FQ, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  dim3 grid(S.R * ATT_CS, D.nh, (rows + 63) / 64);
-  launch_k(k_attn_seg<HD>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  dim3 grid(S.R * CS, D.nh, (rows + 63) / 64);
+  launch_k(k_attn_seg<HD, FQ, CS>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows, pr, bias, rope);
   return cudaGetLastError();
+}
+
+// cluster size: 8 CTAs per (request, head, row tile) by default; BB_ATT_CS=4
+// halves the cluster (fewer, longer CTAs; faster cluster placement)
+static int att_cs() {
+  static int cs = -1;
+  if (cs < 0) cs = (getenv("BB_ATT_CS") != nullptr && atoi(getenv("BB_ATT_CS")) == 4) ? 4 : 8;
+  return cs;
+}
+
+template <int HD, bool FQ>
+static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
+                               const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
+  return att_cs() == 4 ? attn_seg_launch<HD, FQ, 4>(D, S, P, st, layer, pr, bias, rope, s)
+                       : attn_seg_launch<HD, FQ, 8>(D, S, P, st, layer, pr, bias, rope, s);
 }
 
 // LSE-merge of the partials of the items covering (row, head).  CTA per
@@ -612,14 +881,27 @@ static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const De
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, cudaStream_t s) {
+bool attn_fuses_qkv(const Dims& D, const Sess& S, const Pass& P) {
+  return !uses_items(D) && !P.full && S.NRq <= 64;
+}
+
+cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
+                        const PartRef* qkv, const float* bias, const float* rope, cudaStream_t s) {
   const int max_items = P.full ? 1 : S.max_items;
   cudaError_t e = cudaErrorInvalidValue;
   dim3 cgrid(P.rows_alloc, D.nh);
   const int cthreads = D.hd < 256 ? D.hd : 256;
   if (D.dtype == 1 && (D.hd == 64 || D.hd == 128)) {
-    return D.hd == 64 ? attn_seg_hd<64>(D, S, P, st, layer, s) : attn_seg_hd<128>(D, S, P, st, layer, s);
+    PartRef none{};
+    if (qkv != nullptr) {
+      if (!attn_fuses_qkv(D, S, P)) return cudaErrorInvalidValue;
+      return D.hd == 64 ? attn_seg_hd<64, true>(D, S, P, st, layer, *qkv, bias, rope, s)
+                        : attn_seg_hd<128, true>(D, S, P, st, layer, *qkv, bias, rope, s);
+    }
+    return D.hd == 64 ? attn_seg_hd<64, false>(D, S, P, st, layer, none, nullptr, nullptr, s)
+                      : attn_seg_hd<128, false>(D, S, P, st, layer, none, nullptr, nullptr, s);
   }
+  if (qkv != nullptr) return cudaErrorInvalidValue;
   if (D.dtype == 1) {
     using T = __nv_bfloat16;
     if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);

@@ -221,6 +221,37 @@ __device__ __forceinline__ void head_rows(const GemmTcParams& p, float (&v)[32],
   }
 }
 
+__device__ __forceinline__ void l2_prefetch_tile(const CUtensorMap* tm, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(tm)),
+               "r"(x), "r"(y)
+               : "memory");
+}
+
+// Issued by the 32 lanes of one warp of CTA `c` of a grid of `g_cur` CTAs:
+// one tensor prefetch per 128 x 64 weight k-block, covering the next GEMM's
+// CTA ranges c, c + g_cur, ...
+__device__ void l2pf_issue(const L2Pf& f, int c, int g_cur, int lane) {
+  if (f.tm == nullptr || f.nkb <= 0) return;
+  for (int cn = c; cn < f.G; cn += g_cur) {
+    if (f.mode == 0) {
+      const long long y0 = (long long)cn * f.T / f.G, hi = (long long)(cn + 1) * f.T / f.G;
+      const long long yend = y0 + f.nkb < hi ? y0 + f.nkb : hi;
+      for (long long y = y0 + lane; y < yend; y += 32) {
+        const long long tile = y / f.KB;
+        const int kb = (int)(y - tile * f.KB);
+        l2_prefetch_tile(f.tm, kb * 64, (int)(tile / f.n_chunks) * 128);
+      }
+    } else {
+      // tiles cn, cn + G, ... with KB k-blocks each, first nkb of that sequence
+      for (int j = lane; j < f.nkb; j += 32) {
+        const long long t = cn + (long long)(j / f.KB) * f.G;
+        if (t >= f.T) break;
+        l2_prefetch_tile(f.tm, (j % f.KB) * 64, (int)(t / f.n_chunks) * 128);
+      }
+    }
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(192)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -336,6 +367,8 @@ __global__ void __launch_bounds__(192)
         }
       }
     }
+    __syncwarp();
+    l2pf_issue(p.pf, blockIdx.x, gridDim.x, lane);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
@@ -519,12 +552,60 @@ static bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t
   return r == CUDA_SUCCESS;
 }
 
+L2Pf tc_gemm_l2pf(const TcGemm& next, const CUtensorMap* tm_dev, long long bytes) {
+  L2Pf f;
+  memset(&f, 0, sizeof(f));
+  const GemmTcParams& p = next.p;
+  if (bytes <= 0 || tm_dev == nullptr || (p.mode != 0 && p.mode != 1) || next.grid <= 0) return f;
+  f.tm = tm_dev;
+  f.G = next.grid;
+  f.KB = p.KB;
+  f.n_chunks = p.n_chunks;
+  f.mode = p.mode;
+  const long long n_tiles = (long long)p.n_ntiles * p.n_chunks;
+  f.T = p.mode == 0 ? n_tiles * p.KB : n_tiles;
+  const long long per_cta = p.mode == 0 ? (f.T + f.G - 1) / f.G : ((n_tiles + f.G - 1) / f.G) * p.KB;
+  long long nkb = bytes / ((long long)f.G * 128 * 128);
+  if (nkb > per_cta) nkb = per_cta;
+  f.nkb = (int)nkb;
+  if (f.nkb <= 0) f.tm = nullptr;
+  return f;
+}
+
+__global__ void k_l2pf_debug(L2Pf f, const char* w, long long bytes, int kind) {
+  if (kind == 0) {
+    if (threadIdx.x < 32) l2pf_issue(f, blockIdx.x, gridDim.x, threadIdx.x);
+  } else {
+    const long long chunk = 64 << 10;
+    for (long long o = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * chunk; o < bytes;
+         o += (long long)gridDim.x * blockDim.x * chunk) {
+      const long long n = bytes - o < chunk ? bytes - o : chunk;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w + o), "r"((uint32_t)n) : "memory");
+    }
+  }
+}
+
+// debug: prefetch a whole [n_out][K] bf16 weight into L2 -- kind 0 = the
+// GEMM's own tensor-tile prefetch over all its stream-K ranges, 1 = contiguous
+// 64 KB bulk prefetches
+int tc_debug_l2_prefetch(const void* W, int n_out, int K, int kind, cudaStream_t s) {
+  TcGemm g;
+  if (!tc_gemm_setup(g, W, n_out, K, W, 64, 64, 0, 0)) return -3;
+  static CUtensorMap* dmap = nullptr;
+  if (dmap == nullptr && cudaMalloc(&dmap, sizeof(CUtensorMap)) != cudaSuccess) return -10;
+  if (cudaMemcpy(dmap, &g.tmA, sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess) return -10;
+  L2Pf f = tc_gemm_l2pf(g, dmap, 1LL << 40);
+  k_l2pf_debug<<<g.grid, 128, 0, s>>>(f, (const char*)W, (long long)n_out * K * 2, kind);
+  return cudaGetLastError() == cudaSuccess ? 0 : -10;
+}
+
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN, int mode,
                    int max_grid) {
   if (BN != 64 && BN != 128 && BN != 160 && BN != 192 && BN != 256) return false;
   if (K % 8 != 0) return false;  // 16-byte row stride for TMA
   memset(&g, 0, sizeof(g));
   g.BN = BN;
+  g.W = W;
   if (!make_tmap(&g.tmA, W, (uint64_t)K, (uint64_t)n_out, 128)) return false;
   if (!make_tmap(&g.tmB, X, (uint64_t)K, (uint64_t)rows_alloc, (uint32_t)BN)) return false;
   GemmTcParams& p = g.p;

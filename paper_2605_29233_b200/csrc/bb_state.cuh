@@ -110,6 +110,14 @@ struct Pass {
   void* attn;         // [rows_alloc][attn_dim] T
   void* act;          // [rows_alloc][dff] T
   float* apart;       // [R][max_items][item_rows][nh][hd+2]
+  // key lists of the tensor-core attention, built once per pass (the page
+  // tables do not change between layers): per (request, key tile) the keys
+  // in lp-major order as (page_global * ps + row_in_page, branch mask)
+  int* akeys;         // [R][n_kz][akey_cap][2]
+  int* akey_n;        // [R][n_kz][2] (n_keys, first key of the generation pages)
+  int akey_cap;
+  int n_kz;           // key tiles per request (block pass: 64-row tiles; full pass: 1)
+  unsigned long long* atstat;  // live attention timing: [0..7] duration, [8..15] CTA start spread
 };
 
 // Head (LM head + confidence) works on block-pass slots.

@@ -18,7 +18,8 @@ for seed in (1000, 1001):
     t = bb.make_task(seed, P, G, vocab)
     s.set_inputs(t.prompt[None], t.target[None]); s.launch()
 s.stream.synchronize()
-s.klog(reset=True)
+s.klog(reset=True); s.gemm_stats(reset=True)
+import ctypes as _C; from paper_2605_29233_b200 import _lib as _L; _L.lib().bb_session_phase_stats(s.h, (_C.c_ulonglong * 8)(), 1, _C.c_void_p(s.stream.cuda_stream))
 t = bb.make_task(1002, P, G, vocab)
 s.set_inputs(t.prompt[None], t.target[None])
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -45,3 +46,17 @@ big = np.argsort(-d)[:8]
 print("largest slots:", [(names[i], round(d[i] / 1e3, 1)) for i in big])
 json.dump({"kernels": {k: {"n": n, "ns": ns} for k, (n, ns) in rows}, "nfe": nfe, "span_ns": int(tot)},
           open("gpurun_out/timeline_c2.json", "w"))
+gs = s.gemm_stats()
+for k, name in ((5, "attn block: duration after PDL wait"), (6, "attn block: CTA start spread"),
+                (0, "gemm qkv"), (1, "gemm o"), (2, "gemm gate_up"), (3, "gemm down")):
+    if gs[k][4]:
+        print(f"live {name:40s} {gs[k][3] / gs[k][4] / 1e3:8.2f} us avg over {gs[k][4]} launches")
+import ctypes as C
+from paper_2605_29233_b200 import _lib
+ph = (C.c_ulonglong * 8)()
+_lib.lib().bb_session_phase_stats(s.h, ph, 0, C.c_void_p(s.stream.cuda_stream))
+if ph[0]:
+    names_ph = ["rows+keys loaded", "phase-A loads issued", "splice stored", "cluster barrier",
+                "chunk0 landed", "chunk loop done", "end"]
+    print("FQ attention phase offsets (avg us from PDL release): " +
+          ", ".join(f"{n} {ph[i + 1] / ph[0] / 1e3:.2f}" for i, n in enumerate(names_ph)))

@@ -234,3 +234,91 @@ def test_prefill_head_numerics_match_oracle(name, dtype, spike_gain, tol):
           f"argmax agree {agree}/{n}")
     assert worst_lp <= tol and worst_lse <= tol
     assert agree >= n - max(1, n // 20)
+
+
+def _llada_params(g, dtype, spike_gain):
+    a = dict(g["arch"], spike_gain=spike_gain)
+    vocab = bb.Vocab(size=a["vocab_size"])
+    dims = bb.ModelDims(layers=a["layers"], d_model=a["d_model"], max_len=a["max_len"], arch="llada",
+                        n_heads=a["n_heads"], n_kv_heads=a["n_kv_heads"], head_dim=a["head_dim"], d_ff=a["d_ff"],
+                        rope_theta=a["rope_theta"], norm_eps=a["norm_eps"], qkv_bias=a.get("qkv_bias", False))
+    return a, bb.build_model(0, vocab, dims, head_scale=a["head_scale"], spike_gain=spike_gain, dtype=dtype)
+
+
+@pytest.mark.parametrize("name,dtype,spike_gain,tol", [
+    ("llada_tiny_bf16", "bf16", 0.0, 2e-2), ("dream_tiny_bf16", "bf16", 0.0, 2e-2),
+    ("llada_tiny_bf16", "bf16", 33.0, 1e-1), ("dream_tiny_bf16", "bf16", 33.0, 1e-1),
+    ("llada_tiny_f32", "f32", 33.0, 1e-4)])
+def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol):
+    """One block step after prefill (the block pass: window KV splice into the
+    branches' aliased prefill pages, segment-masked attention over shared
+    pages, LM head) vs the oracle's block_forward of every active branch on
+    the prefill cache (model.py:331-343).  Same tolerances as the prefill
+    test."""
+    from oracle import bb_oracle as O
+    from paper_2605_29233_b200.engine import Session
+    g = LLADA[name]
+    a, params = _llada_params(g, dtype, spike_gain)
+    cfg = cfg_from(g["config"])
+    arch = O.OArch(**a)
+    W = O.weights_as(O.hash_weights(arch, 0), dtype)
+    rnd = O.bf16_round if dtype == "bf16" else None
+    P, G = g["prompt_len"], g["gen_len"]
+    worst_lp, worst_lse, agree, n = 0.0, 0.0, 0, 0
+    for seed in g["seeds"][:3]:
+        task = bb.make_task(seed, P, G, params.vocab)
+        s = Session(params, cfg, P, 1)
+        s.set_inputs(task.prompt[None], task.target[None])
+        s.prefill()
+        st = s.fetch(trace=False)
+        if st["ctrl"][0, 0] != 0:
+            continue  # finished at prefill: no block step
+        s.iteration(with_refresh=False)
+        hr = s.head_results()
+        row0 = np.full(P + G, arch.mask_id, dtype=np.int64)
+        row0[:P] = task.prompt
+        _, cache = O.full_forward(arch, W, row0, P, task.target, rnd)
+        for k in range(len(cfg.block_sizes)):
+            sel = np.flatnonzero((hr["masked"] != 0) & (hr["branch"] == k) & (hr["pos"] >= 0))
+            if len(sel) == 0:
+                continue
+            tok = st["tokens"][0, k].astype(np.int64)
+            start, end = int(st["branch"][0, k, 0]), int(st["branch"][0, k, 1])
+            out, _ = O.block_forward(arch, W, tok, P, cache, start, end, task.target, rnd)
+            idx = {int(p): i for i, p in enumerate(out.positions)}
+            lse_ref = out.logits.max(1) + np.log(np.exp(out.logits - out.logits.max(1, keepdims=True)).sum(1))
+            for j in sel:
+                i = idx[int(hr["pos"][j])]
+                m, ssum = float(hr["m"][j]), float(hr["s"][j])
+                lse = m + np.log(ssum)
+                worst_lp = max(worst_lp, abs((m - lse) - (out.logits[i].max() - lse_ref[i])))
+                worst_lse = max(worst_lse, abs(lse - lse_ref[i]) / max(1.0, abs(lse_ref[i])))
+                agree += int(hr["arg"][j]) == int(out.probs[i].argmax())
+                n += 1
+    print(f"{name} gain {spike_gain}: {n} block positions, max|dlogp_max|={worst_lp:.2e}, "
+          f"rel dlse={worst_lse:.2e}, argmax agree {agree}/{n}")
+    assert n > 0
+    assert worst_lp <= tol and worst_lse <= tol
+    assert agree >= n - max(1, n // 20)
+
+
+@pytest.mark.parametrize("name", ["llada_tiny_bf16", "dream_tiny_bf16"])
+def test_fused_qkv_attention_equals_separate_finalize(name, monkeypatch):
+    """The block-pass attention that finalizes the QKV partial planes in its
+    prologue (bias, RoPE, KV splice, q through DSMEM) is bit-identical to the
+    separate post_qkv kernel + attention (the default; BB_FQ=1 selects the
+    fused prologue): same rounding points, same key order."""
+    from paper_2605_29233_b200.engine import Session
+    g = LLADA[name]
+    params = llada_model(g, "bf16")
+    cfg = cfg_from(g["config"])
+    outs = []
+    for fq in ("1", "0"):
+        monkeypatch.setenv("BB_FQ", fq)
+        s = Session(params, cfg, g["prompt_len"], 2)
+        tasks = [bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab) for seed in g["seeds"][:2]]
+        s.set_inputs(np.stack([t.prompt for t in tasks]), np.stack([t.target for t in tasks]))
+        s.launch()
+        outs.append(s.fetch())
+    for key in ("ctrl", "tokens", "branch", "events"):
+        assert np.array_equal(outs[0][key], outs[1][key]), key
