@@ -127,6 +127,9 @@ BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int r
  * keys loaded, phase-A loads issued, splice stored, cluster barrier passed,
  * chunk 0 landed, chunk loop done, end).  Averages = out[i] / out[0]. */
 BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset, void* stream);
+/* layer-stream kernel phase profile (BB_KLOG=1 sessions), out[64]: CTA 0's
+   summed ns from release to each phase event, [63] = launches */
+BB_API int bb_session_lsk_prof(void* sess, unsigned long long* out, int reset, void* stream);
 BB_API int bb_session_counters(void* sess, long long* out);
 BB_API int bb_session_klog(void* sess, unsigned long long* host_out, int cap, int reset, long long* n, void* stream);
 

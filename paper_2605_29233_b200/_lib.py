@@ -77,6 +77,7 @@ SIGNATURES = {
     "bb_session_ctrl": (i32, [vp, i32p, vp]),
     "bb_session_gemm_stats": (i32, [vp, C.POINTER(C.c_ulonglong), i32, vp]),
     "bb_session_phase_stats": (i32, [vp, vp, i32, vp]),
+    "bb_session_lsk_prof": (i32, [vp, vp, i32, vp]),
     "bb_session_counters": (i32, [vp, i64p]),
     "bb_session_klog": (i32, [vp, C.POINTER(C.c_ulonglong), i32, i32, i64p, vp]),
     "bb_prefill": (i32, [vp, vp]),

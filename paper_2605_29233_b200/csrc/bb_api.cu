@@ -12,6 +12,7 @@
 #include "bb_common.cuh"
 #include "bb_gemm.cuh"
 #include "bb_layers.cuh"
+#include "bb_stream.cuh"
 
 namespace bb {
 
@@ -68,6 +69,12 @@ struct Session {
   CUtensorMap* tmaps = nullptr;  // device copies of the GEMM weight tensor maps (prefetch operands)
   long long tmap_cap = 0;
   unsigned long long* klog = nullptr;  // BB_KLOG=1: kernel timeline (cudaMalloc'd)
+  // layer-stream kernels of the block pass (bf16, BN 64): [0] = QKV(0),
+  // [l+1] = O(l) .. down(l) + QKV(l+1); empty = per-GEMM kernels
+  std::vector<LskParams> lsk;
+  unsigned int* lsk_bar = nullptr;  // [(layers+1)][16] grid-barrier counters
+  unsigned long long* lsk_prof = nullptr;  // [64] CTA-0 phase profile (BB_KLOG)
+  int lsk_grid = 0;
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
   long long layout[BB_VIEW_COUNT][2];
@@ -213,6 +220,7 @@ static void plan(Session* s, char* base, bool dry) {
     P.attn = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
     P.act = c.take<char>((long long)rows_alloc * (D.dff > 0 ? D.dff : 1) * e, 1024);
     P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
+    P.row_rope = (!full && D.arch == BB_ARCH_LLADA) ? c.take<float>((long long)rows_alloc * D.hd) : nullptr;
     P.n_kz = full ? 1 : (item_rows + 63) / 64;
     P.akey_cap = B * S.L;
     P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
@@ -245,6 +253,8 @@ static void plan(Session* s, char* base, bool dry) {
   s->blk.atstat = s->tstat + 5 * 8;   // slots 5/6: block-pass attention (duration, start spread)
   s->full.atstat = s->tstat + 13 * 8; // slots 13/14: full-pass attention
   s->tile_cnt = c.take<int>(8192);
+  s->lsk_bar = c.take<unsigned int>((size_t)(D.layers + 1) * 16);
+  s->lsk_prof = c.take<unsigned long long>(64);
   s->ns_cap = 64 * 1024;
   s->ns_tabs = c.take<unsigned char>(s->ns_cap);
   s->ss_ld = (D.d + 127) / 128;
@@ -455,6 +465,65 @@ static int setup_gemms(Session* s) {
   return BB_OK;
 }
 
+// Layer-stream kernels for the block pass (opt-in, BB_LSK=1; default: one
+// kernel per GEMM and per consumer op)
+static int setup_lsk(Session* s) {
+  const Dims& D = s->D;
+  const Weights& W = s->M->W;
+  s->lsk.clear();
+  const char* env = getenv("BB_LSK");  // opt-in (BB_LSK=1): slower than the per-GEMM kernels today
+  if (env == nullptr || atoi(env) == 0) return BB_OK;
+  if (D.dtype != BB_DTYPE_BF16 || s->fuse_epi || s->gb.BN != 64 || D.d % 128 != 0 || D.hd % 8 != 0) return BB_OK;
+  int dev = 0, sms = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  s->lsk_grid = sms;
+  PassGemms& G = s->gb;
+  auto base = [&](int idx) {
+    LskParams p;
+    memset(&p, 0, sizeof(p));
+    p.c.D = D;
+    p.c.S = s->S;
+    p.c.P = s->blk;
+    p.c.st = s->st;
+    p.c.part = s->part;
+    p.c.rows = s->S.NR;
+    p.c.flags = getenv("BB_LSK_FLAGS") != nullptr ? atoi(getenv("BB_LSK_FLAGS")) : 0;
+    p.c.ss = s->ss_blk;
+    p.c.rope = W.rope;
+    p.c.bar = s->lsk_bar + (size_t)idx * 16;
+    p.c.tstat = s->tstat + 12 * 8;
+    p.c.prof = D.klog != nullptr ? s->lsk_prof : nullptr;
+    return p;
+  };
+  auto bias = [&](int l) -> const float* { return W.bqkv != nullptr ? W.bqkv + (size_t)l * D.qkv_out : nullptr; };
+  LskParams p0 = base(0);
+  if (!lsk_add_gemm(p0, G.layers[0].qkv, LSK_POST_QKV, nullptr, bias(0), 0, s->tstat + 0 * 8)) return BB_OK;
+  std::vector<LskParams> all = {p0};
+  for (int l = 0; l < D.layers; ++l) {
+    LayerGemms& lg = G.layers[l];
+    const float* next_ln = l + 1 < D.layers ? (D.arch == BB_ARCH_LLADA ? W.ln1 + (size_t)(l + 1) * D.d : nullptr)
+                                            : (D.arch == BB_ARCH_LLADA ? W.lnf : nullptr);
+    LskParams p = base(l + 1);
+    bool ok = true;
+    if (D.dff) {
+      ok &= lsk_add_gemm(p, lg.o, LSK_POST_RESIDUAL, W.ln2 + (size_t)l * D.d, nullptr, l, s->tstat + 1 * 8);
+      ok &= lsk_add_gemm(p, lg.gu, LSK_POST_SWIGLU, nullptr, nullptr, l, s->tstat + 2 * 8);
+      ok &= lsk_add_gemm(p, lg.dn, LSK_POST_RESIDUAL, next_ln, nullptr, l, s->tstat + 3 * 8);
+    } else {
+      ok &= lsk_add_gemm(p, lg.o, LSK_POST_RESIDUAL, next_ln, nullptr, l, s->tstat + 1 * 8);
+    }
+    if (l + 1 < D.layers)
+      ok &= lsk_add_gemm(p, G.layers[l + 1].qkv, LSK_POST_QKV, nullptr, bias(l + 1), l + 1, s->tstat + 0 * 8);
+    if (!ok) return BB_OK;  // shape not supported: per-GEMM kernels
+    all.push_back(p);
+  }
+  CK(cudaMemset(s->lsk_bar, 0, (size_t)(D.layers + 1) * 16 * sizeof(unsigned int)));
+  CK(cudaMemset(s->lsk_prof, 0, 64 * sizeof(unsigned long long)));
+  s->lsk = all;
+  return BB_OK;
+}
+
 static PartRef pref_simt(const SimtGemm& g) {
   SplitK sk{};
   return PartRef{g.out, 0, g.ldo, sk};
@@ -475,6 +544,15 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
   const Weights& W = s->M->W;
   cudaError_t e;
   if ((e = launch_embed(D, s->S, P, W, st)) != cudaSuccess) return e;
+  if (&P == &s->blk && !s->lsk.empty()) {
+    // attention(l) -> layer-stream kernel (O .. down of layer l, QKV of l+1)
+    if ((e = lsk_launch(s->lsk[0], s->lsk_grid, st)) != cudaSuccess) return e;
+    for (int l = 0; l < D.layers; ++l) {
+      if ((e = launch_attn(D, s->S, P, s->st, l, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
+      if ((e = lsk_launch(s->lsk[l + 1], s->lsk_grid, st)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   const bool fused = D.dtype == BB_DTYPE_BF16 && s->fuse_epi;
   float* ss = &P == &s->full ? s->ss_full : s->ss_blk;
   for (int l = 0; l < D.layers; ++l) {
@@ -769,6 +847,7 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
     }
   }
   rc = setup_gemms(s);
+  if (rc == BB_OK) rc = setup_lsk(s);
   if (rc != BB_OK) {
     delete s;
     return rc;
@@ -952,6 +1031,23 @@ BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset
   CK(cudaStreamSynchronize(st));
   if (reset) {
     CK(cudaMemsetAsync(s->tstat + 7 * 8, 0, 8 * 8, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return BB_OK;
+}
+
+// layer-stream kernel phase profile of CTA 0 (BB_KLOG=1 sessions): out[64],
+// [8i + k] summed ns from the epilogue's release to: k=0 GEMM i planes written,
+// 1 step-1 barrier passed, 2 step 1 done, 3 step-2 barrier passed, 4 step 2
+// done, 5 (activation producer) GEMM i inputs released; [63] launches
+BB_API int bb_session_lsk_prof(void* sess, unsigned long long* out, int reset, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !out) return BB_ERR_CONTRACT;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(out, s->lsk_prof, 64 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (reset) {
+    CK(cudaMemsetAsync(s->lsk_prof, 0, 64 * 8, st));
     CK(cudaStreamSynchronize(st));
   }
   return BB_OK;

@@ -52,7 +52,8 @@ template <> struct Vec4<__nv_bfloat16> {
 
 template <typename T>
 __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restrict__ emb,
-                                               const T* __restrict__ pos_emb, const float* __restrict__ ln) {
+                                               const T* __restrict__ pos_emb, const float* __restrict__ ln,
+                                               const float* __restrict__ rope) {
   pdl_enter();
   klog_mark(D.klog, D.klog_cap, 1);
   if (*P.skip) return;
@@ -65,6 +66,10 @@ __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restri
   }
   float* x = P.x + (long long)row * D.d;
   T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
+  if (P.row_rope != nullptr && rope != nullptr)  // per-row RoPE table for the layer-stream QKV finalize
+    for (int i = threadIdx.x; i < (D.hd >> 1); i += blockDim.x)
+      *reinterpret_cast<float2*>(P.row_rope + ((long long)row * (D.hd >> 1) + i) * 2) =
+          *reinterpret_cast<const float2*>(rope + ((long long)pos * (D.hd >> 1) + i) * 2);
   float ss = 0.0f;
   for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
     float4 v = Vec4<T>::ld(emb + (long long)tok * D.d + c);
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, H
 
 cudaError_t launch_embed(const Dims& D, const Sess& S, const Pass& P, const Weights& W, cudaStream_t s) {
   BB_DISPATCH(D, (launch_k(k_embed<T>, dim3(P.rows_alloc), dim3(512), (size_t)(0), s, D, P, (const T*)W.emb, (const T*)W.pos,
-                                                           D.arch == 1 ? W.ln1 : nullptr)));
+                                                           D.arch == 1 ? W.ln1 : nullptr, D.arch == 1 ? W.rope : nullptr)));
   return cudaGetLastError();
 }
 

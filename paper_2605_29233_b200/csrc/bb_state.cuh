@@ -110,6 +110,7 @@ struct Pass {
   void* attn;         // [rows_alloc][attn_dim] T
   void* act;          // [rows_alloc][dff] T
   float* apart;       // [R][max_items][item_rows][nh][hd+2]
+  float* row_rope;    // [rows_alloc][hd/2][2] RoPE (cos, sin) of each row's position (block pass, arch 1) or null
   // key lists of the tensor-core attention, built once per pass (the page
   // tables do not change between layers): per (request, key tile) the keys
   // in lp-major order as (page_global * ps + row_in_page, branch mask)

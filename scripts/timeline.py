@@ -19,6 +19,7 @@ for seed in (1000, 1001):
     s.set_inputs(t.prompt[None], t.target[None]); s.launch()
 s.stream.synchronize()
 s.klog(reset=True); s.gemm_stats(reset=True)
+import ctypes as _C0; from paper_2605_29233_b200 import _lib as _L0; _L0.lib().bb_session_lsk_prof(s.h, (_C0.c_ulonglong * 64)(), 1, _C0.c_void_p(s.stream.cuda_stream))
 import ctypes as _C; from paper_2605_29233_b200 import _lib as _L; _L.lib().bb_session_phase_stats(s.h, (_C.c_ulonglong * 8)(), 1, _C.c_void_p(s.stream.cuda_stream))
 t = bb.make_task(1002, P, G, vocab)
 s.set_inputs(t.prompt[None], t.target[None])
@@ -48,7 +49,7 @@ json.dump({"kernels": {k: {"n": n, "ns": ns} for k, (n, ns) in rows}, "nfe": nfe
           open("gpurun_out/timeline_c2.json", "w"))
 gs = s.gemm_stats()
 for k, name in ((5, "attn block: duration after PDL wait"), (6, "attn block: CTA start spread"),
-                (0, "gemm qkv"), (1, "gemm o"), (2, "gemm gate_up"), (3, "gemm down")):
+                (0, "gemm qkv"), (1, "gemm o"), (2, "gemm gate_up"), (3, "gemm down"), (12, "layer_stream kernel")):
     if gs[k][4]:
         print(f"live {name:40s} {gs[k][3] / gs[k][4] / 1e3:8.2f} us avg over {gs[k][4]} launches")
 import ctypes as C
@@ -60,3 +61,18 @@ if ph[0]:
                 "chunk0 landed", "chunk loop done", "end"]
     print("FQ attention phase offsets (avg us from PDL release): " +
           ", ".join(f"{n} {ph[i + 1] / ph[0] / 1e3:.2f}" for i, n in enumerate(names_ph)))
+
+pr = (C.c_ulonglong * 64)()
+_lib.lib().bb_session_lsk_prof(s.h, pr, 0, C.c_void_p(s.stream.cuda_stream))
+if pr[63]:
+    n = pr[63]
+    ev = ["planes written", "step1 barrier", "step1 done", "step2 barrier", "step2 done", "inputs released",
+          "step1 op returned", "step1 fenced"]
+    for gi in range(4):
+        vals = [pr[8 * gi + k] / n / 1e3 for k in range(8)]
+        if any(vals):
+            print(f"lsk gemm {gi}: " + ", ".join(f"{e} {v:.2f}" for e, v in zip(ev, vals)))
+    print(f"in-situ load latency (CTA0 norm, cycles): x {pr[40] / n:.0f}, part {pr[41] / n:.0f}")
+    for gi in (0, 2):
+        if pr[44 + gi]:
+            print(f"gemm {gi} norm: 1st call ends {pr[44 + gi] / n / 1e3:.2f}, 2nd call ends {pr[48 + gi] / n / 1e3:.2f}, 2nd call thread-0 cycles {pr[52 + gi] / n:.0f}")

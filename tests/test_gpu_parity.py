@@ -249,12 +249,15 @@ def _llada_params(g, dtype, spike_gain):
     ("llada_tiny_bf16", "bf16", 0.0, 2e-2), ("dream_tiny_bf16", "bf16", 0.0, 2e-2),
     ("llada_tiny_bf16", "bf16", 33.0, 1e-1), ("dream_tiny_bf16", "bf16", 33.0, 1e-1),
     ("llada_tiny_f32", "f32", 33.0, 1e-4)])
-def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol):
+@pytest.mark.parametrize("lsk", ["0", "1"])
+def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol, lsk, monkeypatch):
     """One block step after prefill (the block pass: window KV splice into the
     branches' aliased prefill pages, segment-masked attention over shared
     pages, LM head) vs the oracle's block_forward of every active branch on
     the prefill cache (model.py:331-343).  Same tolerances as the prefill
-    test."""
+    test.  lsk=1: the block pass runs the layer-stream kernels (BB_LSK=1,
+    bf16 only; fp32 mode has no tensor-core path and ignores it)."""
+    monkeypatch.setenv("BB_LSK", lsk)
     from oracle import bb_oracle as O
     from paper_2605_29233_b200.engine import Session
     g = LLADA[name]
