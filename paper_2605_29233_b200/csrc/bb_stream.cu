@@ -42,15 +42,15 @@ __device__ __forceinline__ void grid_wait(const unsigned* p, unsigned target) {
   if (ld_relaxed_u32(p) < target) {
     const long long t0 = clock64();
     while (ld_relaxed_u32(p) < target) {
-      __nanosleep(64);
+      __nanosleep(16);
       if (clock64() - t0 > 20000000000LL) __trap();
     }
   }
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+// release-add without a returned value (no full fence, no L1 invalidation)
 __device__ __forceinline__ void grid_arrive(unsigned* p) {
-  __threadfence();
-  atomicAdd(p, 1u);
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void lsk_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -104,6 +104,12 @@ struct LskUnits {
 };
 
 constexpr int LSK_POST_THREADS = 256;  // warps 7-14: consumer ops
+#ifndef LSK_RB_RES
+#define LSK_RB_RES 1
+#endif
+#ifndef LSK_RB_SW
+#define LSK_RB_SW 2
+#endif
 #ifndef LSK_NS_RES
 #define LSK_NS_RES 8
 #endif
@@ -437,9 +443,9 @@ __device__ __forceinline__ void lsk_qkv(const LskCore& p, const LskGemm& g, int 
 __device__ __forceinline__ void lsk_post(const LskCore& p, const LskGemm& g, int step, int et) {
   if (g.post == LSK_POST_RESIDUAL) {
     if (step == 1) lsk_norm<2>(p, g, et);
-    else lsk_accum<LSK_NS_RES, 1>(p, g, et);
+    else lsk_accum<LSK_NS_RES, LSK_RB_RES>(p, g, et);
   } else if (g.post == LSK_POST_SWIGLU) {
-    lsk_swiglu<LSK_NS_SW, 2>(p, g, et);
+    lsk_swiglu<LSK_NS_SW, LSK_RB_SW>(p, g, et);
   } else {
     lsk_qkv<LSK_NS_QKV, 1>(p, g, et);
   }
