@@ -158,8 +158,8 @@ class Session:
     KLOG_NAMES = {1: "embed", 2: "post_qkv", 3: "attn_seg", 4: "post_residual", 5: "post_gu", 6: "norm",
                   7: "gather_head", 8: "head_tiles_f32", 9: "head_reduce", 10: "prefill_init", 11: "prefill_post",
                   12: "block_pack", 13: "step_commit", 14: "merge_prep", 15: "merge_sync", 16: "refresh_pack",
-                  17: "refresh_end", 18: "copy_pages", 20: "gemm_simt", 21: "attn_simt", 22: "attn_combine", 23: "layer_stream",
-                  100: "gemm_qkv", 101: "gemm_o", 102: "gemm_gate_up", 103: "gemm_down", 104: "gemm_head",
+                  17: "refresh_end", 18: "copy_pages", 20: "gemm_simt", 21: "attn_simt", 22: "attn_combine", 23: "layer_stream", 24: "attn_seg_pre",
+                  100: "gemm_qkv", 101: "gemm_o", 102: "gemm_gate_up", 103: "gemm_down", 104: "gemm_head", 151: "gemm_o_pre",
                   108: "gemm_qkv_full", 109: "gemm_o_full", 110: "gemm_gate_up_full", 111: "gemm_down_full"}
 
     def klog(self, reset: bool = False):

@@ -59,7 +59,7 @@ _lib.lib().bb_session_phase_stats(s.h, ph, 0, C.c_void_p(s.stream.cuda_stream))
 if ph[0]:
     names_ph = ["rows+keys loaded", "phase-A loads issued", "splice stored", "cluster barrier",
                 "chunk0 landed", "chunk loop done", "end"]
-    print("FQ attention phase offsets (avg us from PDL release): " +
+    print("attention phase offsets (avg us from PDL release): " +
           ", ".join(f"{n} {ph[i + 1] / ph[0] / 1e3:.2f}" for i, n in enumerate(names_ph)))
 
 pr = (C.c_ulonglong * 64)()
