@@ -119,6 +119,11 @@ BB_API int bb_refresh(void* sess, void* stream);
 BB_API int bb_iteration(void* sess, int with_refresh, int use_graph, void* stream);
 /* run_blockbatch (scheduler.py:225-394) for all requests of the session */
 BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out);
+/* vanilla_decode (decoding.py:279-321) for all requests of a session that has
+   one branch of block size gen_len: one full forward per round, tau 1.0.
+   Replaces the reference's vanilla_decode (the baseline decoder of the
+   paper's NFE comparison, test_acceptance.py:300-325). */
+BB_API int bb_run_vanilla(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out);
 BB_API int bb_version(void);
 /* instrumentation: live per-launch GEMM timing and kernel-launch counters */
 BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream);

@@ -9,7 +9,7 @@ anything that computes needs the library and a B200.
 """
 
 from .decoding import (DecodeConfig, GenerationResult, NfeCounter, TraceEvent, BranchState,
-                       confidence_transition, single_branch_decode)
+                       confidence_transition, single_branch_decode, vanilla_decode)
 from .errors import ConfigError, ContractError, RunawayError, StateError
 from .model import (BlockWindow, DenoiseOutput, KvCache, ModelDims, ModelParams, SequenceRow, Task, Vocab,
                     build_model, make_task, exact_match, serialize_params, LLADA_8B, LLADA_8B_VOCAB, DREAM_7B,

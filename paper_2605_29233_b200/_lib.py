@@ -85,6 +85,7 @@ SIGNATURES = {
     "bb_refresh": (i32, [vp, vp]),
     "bb_iteration": (i32, [vp, i32, i32, vp]),
     "bb_run": (i32, [vp, i32, i32, vp, i32p]),
+    "bb_run_vanilla": (i32, [vp, i32, i32, vp, i32p]),
     "bb_commit_probs": (i32, [vp, i32, i32, vp, vp, f32, vp, vp, vp]),
     "bb_merge_sync_maps": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, f32, f32, i32, i32, vp, i32, vp, vp, vp,
                                  vp]),

@@ -48,8 +48,8 @@ struct Session {
   int* full_rows = nullptr;  // device scalar: rows of the full pass
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  cudaGraphExec_t g_iter = nullptr, g_iter_ref = nullptr, g_prefill = nullptr;
-  long long nodes_iter = 0, nodes_iter_ref = 0, nodes_prefill = 0;
+  cudaGraphExec_t g_iter = nullptr, g_iter_ref = nullptr, g_prefill = nullptr, g_vanilla = nullptr;
+  long long nodes_iter = 0, nodes_iter_ref = 0, nodes_prefill = 0, nodes_vanilla = 0;
   long long kernel_launches = 0, graph_launches = 0;
   unsigned long long* tstat = nullptr;  // [16][8] per-GEMM-kind live timing
   int* tile_cnt = nullptr;              // fused-epilogue arrival counters (self-resetting)
@@ -655,6 +655,22 @@ static int enqueue_refresh(Session* s, cudaStream_t st) {
   return BB_OK;
 }
 
+// one vanilla_decode round (decoding.py:279-321): full forward of branch 0,
+// head over the masked positions before the first eos, Eq. 1 with tau 1.0
+static int enqueue_vanilla(Session* s, cudaStream_t st) {
+  const Dims& D = s->D;
+  const Sess& S = s->S;
+  CK(cudaMemsetAsync(s->full.skip, 1, sizeof(int), st));
+  CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
+  CK(launch_vanilla_pack(D, S, s->st, s->full, s->blk, s->H, st));
+  CK(launch_attn_keys(D, S, s->full, s->st, st));
+  CK(forward(s, s->full, s->gf, st));
+  CK(launch_gather_head(D, S, s->full, s->blk, s->H, 0, st));
+  CK(head(s, st));
+  CK(launch_vanilla_commit(D, S, s->st, s->blk, s->H, st));
+  return BB_OK;
+}
+
 static long long count_kernel_nodes(cudaGraph_t g) {
   size_t n = 0;
   if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return -1;
@@ -668,11 +684,11 @@ static long long count_kernel_nodes(cudaGraph_t g) {
   return k;
 }
 
-// what: 0 = block step, 1 = block step + refresh, 2 = prefill
+// what: 0 = block step, 1 = block step + refresh, 2 = prefill, 3 = vanilla round
 static int capture(Session* s, int what, cudaStream_t st, cudaGraphExec_t* out, long long* nodes) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  int rc = what == 2 ? enqueue_prefill(s, st) : enqueue_block_step(s, st);
+  int rc = what == 2 ? enqueue_prefill(s, st) : (what == 3 ? enqueue_vanilla(s, st) : enqueue_block_step(s, st));
   if (rc == BB_OK && what == 1) rc = enqueue_refresh(s, st);
   cudaError_t e = cudaStreamEndCapture(st, &g);
   if (rc != BB_OK) return rc;
@@ -879,6 +895,7 @@ BB_API int bb_session_destroy(void* sess) {
   if (s->g_iter) cudaGraphExecDestroy(s->g_iter);
   if (s->g_iter_ref) cudaGraphExecDestroy(s->g_iter_ref);
   if (s->g_prefill) cudaGraphExecDestroy(s->g_prefill);
+  if (s->g_vanilla) cudaGraphExecDestroy(s->g_vanilla);
   if (s->klog) cudaFree(s->klog);
   if (s->host_ctrl) cudaFreeHost(s->host_ctrl);
   for (int i = 0; i < 4; ++i)
@@ -988,6 +1005,55 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
     ++it;
     rc = bb_iteration(s, it % s->S.refresh_interval == 0, use_graph, st);
     if (rc != BB_OK) return rc;
+    CK(cudaMemcpyAsync(s->host_ctrl + (size_t)(it & 3) * R * C_WORDS, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s->ev[it & 3], st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (iterations_out) *iterations_out = it;
+  return BB_OK;
+}
+
+// vanilla_decode (decoding.py:279-321) for every request of a session with
+// one branch of block size gen_len: initial rows, then rounds (one full
+// forward each, captured once into a graph) until every request finished;
+// status polled two rounds behind like bb_run.
+BB_API int bb_run_vanilla(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out) {
+  Session* s = (Session*)sess;
+  if (!s) return BB_ERR_CONTRACT;
+  if (s->S.B != 1 || s->S.bs[0] != s->S.G) return fail(BB_ERR_CONFIG, "vanilla: one branch of block size gen_len");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(launch_prefill_init(s->D, s->S, s->st, s->full, s->blk, s->H, st));
+  const int R = s->S.R;
+  const size_t cb = (size_t)R * C_WORDS * 4;
+  // slot 0 = the initial state (the polling below reads slot (it - lag) & 3)
+  CK(cudaMemcpyAsync(s->host_ctrl, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(s->ev[0], st));
+  int it = 0, checked = -1;
+  bool finished = false;
+  const int lag = 2;
+  while (!finished && it < max_iterations) {
+    const int chk = it - lag;
+    if (chk >= 0 && chk > checked) {
+      CK(cudaEventSynchronize(s->ev[chk & 3]));
+      checked = chk;
+      const int32_t* c = s->host_ctrl + (size_t)(chk & 3) * R * C_WORDS;
+      finished = true;
+      for (int r = 0; r < R; ++r) finished &= c[r * C_WORDS + C_STATUS] != 0;
+      if (finished) break;
+    }
+    ++it;
+    if (use_graph) {
+      if (!s->g_vanilla) {
+        const int rc = capture(s, 3, st, &s->g_vanilla, &s->nodes_vanilla);
+        if (rc != BB_OK) return rc;
+      }
+      CK(cudaGraphLaunch(s->g_vanilla, st));
+      s->kernel_launches += s->nodes_vanilla;
+      s->graph_launches += 1;
+    } else {
+      const int rc = enqueue_vanilla(s, st);
+      if (rc != BB_OK) return rc;
+    }
     CK(cudaMemcpyAsync(s->host_ctrl + (size_t)(it & 3) * R * C_WORDS, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(s->ev[it & 3], st));
   }

@@ -1056,6 +1056,120 @@ __global__ void k_refresh_end(Dims D, Sess S, DevState st) {
   }
 }
 
+// ------------------------------------------------------------------ vanilla decode
+// decoding.py:279-321, the baseline decoder of SURVEY 8(f3): one FULL forward
+// per round over the whole row (no cache reuse), then Eq. 1 with tau = 1.0 over
+// the masked positions of [P, first eos or L) -- the most confident position
+// commits -- charged as nfe_block.  The session has one branch of block size G,
+// so its G head slots cover the span.  k_prefill_init sets the initial state;
+// each round: k_vanilla_pack -> full pass of branch 0 -> head -> k_vanilla_commit.
+__global__ void k_vanilla_pack(Dims D, Sess S, DevState st, Pass full, Pass blk, Head H) {
+  pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 19);
+  RC_SETUP();
+  const int r = c.r;
+  __shared__ int s_live;
+  load_request(c);
+  if (threadIdx.x == 0) {
+    s_live = c.ctrl[C_STATUS] == 0;
+    if (s_live) {
+      c.ctrl[C_ITER] += 1;
+      const int total = c.ctrl[C_NFE0] + c.ctrl[C_NFE1] + c.ctrl[C_NFE2];
+      if (total > S.hard_cap) {  // decoding.py:296-297
+        c.ctrl[C_STATUS] = BB_ERR_RUNAWAY;
+        s_live = 0;
+      }
+    }
+  }
+  __syncthreads();
+  int end = S.L;
+  bool any = false;
+  if (s_live) {
+    const int eos = c.earliest_eos(0);
+    end = eos >= 0 ? eos : S.L;
+    any = c.has_mask(0, S.P, end);
+    if (!any) {  // no mask before the first eos: finished (decoding.py:302-305, 317-321)
+      const int dec = c.count_decoded(0);
+      if (threadIdx.x == 0) {
+        c.B_(0, B_DEC) = dec;
+        c.emit(EV_FINISH, 0, eos);
+        c.ctrl[C_WINNER] = 0;
+        c.ctrl[C_EOS] = eos;
+        c.ctrl[C_STATUS] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  const bool live = s_live && any;
+  if (threadIdx.x == 0) {
+    c.B_(0, B_START) = S.P;
+    c.B_(0, B_END) = end;
+    for (int kk = 0; kk < MAXB; ++kk) {
+      full.rng_off[r * MAXB + kk] = r * S.L;
+      full.rng_cnt[r * MAXB + kk] = (live && kk == 0) ? S.L : 0;
+    }
+    full.n_items[r] = live ? 1 : 0;
+    if (live) {
+      int* it = full.items + (long long)r * ITW;
+      it[0] = 1;
+      it[1] = 0;
+      it[2] = S.n_lp;
+      it[3] = 0;
+      *full.skip = 0;
+      *H.skip = 0;
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < S.L; p += blockDim.x) {
+    const int row = r * S.L + p;
+    full.slot_pos[row] = live ? p : -1;
+    full.slot_req[row] = r;
+    full.slot_br[row] = 0;
+    full.slot_tok[row] = c.rows[p];
+    full.slot_kvoff[row] = live ? kv_row_off(D, S, st, r, 0, p) : 0;
+  }
+  const int* target = st.target + (long long)r * S.G;
+  for (int j = threadIdx.x; j < S.NRq; j += blockDim.x) {
+    const int slot = r * S.NRq + j;
+    const int pos = S.P + j;
+    const bool in = live && pos < end && c.rows[pos] == c.mask_id;
+    blk.slot_req[slot] = r;
+    blk.slot_br[slot] = 0;
+    blk.slot_pos[slot] = in ? pos : -1;
+    H.masked[slot] = in ? 1 : 0;
+    if (in) slot_boost(D, S, c.rows, target, pos, &H.boost[slot], &H.tgt[slot]);
+    else {
+      H.boost[slot] = 0.0f;
+      H.tgt[slot] = -1;
+    }
+  }
+  store_request(c);
+}
+
+__global__ void k_vanilla_commit(Dims D, Sess S, DevState st, Pass blk, Head H) {
+  pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 13);
+  RC_SETUP();
+  load_request(c);
+  __shared__ int s_live;
+  if (threadIdx.x == 0) s_live = c.ctrl[C_STATUS] == 0 && c.B_(0, B_END) > S.P && *H.skip == 0;
+  __syncthreads();
+  if (!s_live) return;
+  // only this request's slots are masked when its round is live
+  bool any = false;
+  for (int j = threadIdx.x; j < S.NRq; j += blockDim.x) any |= H.masked[c.r * S.NRq + j] != 0;
+  if (!__syncthreads_or(any)) return;
+  const int n = apply_commits(c, blk, H, 0, 1.0f);  // tau 1.0: the most confident position (decoding.py:311)
+  const int dec = c.count_decoded(0);
+  if (threadIdx.x == 0) {
+    c.B_(0, B_DEC) = dec;
+    c.ctrl[C_NFE1] += 1;
+    c.ctrl[C_COMMITS] += n;
+    c.emit(EV_BLOCK, 0, 1);
+  }
+  store_request(c);
+}
+
 // ------------------------------------------------------------------ copies
 // 16-byte vector copies; block-strided over (request, job, layer) units.
 template <typename T>
@@ -1279,6 +1393,27 @@ cudaError_t launch_refresh_end(const Dims& D, const Sess& S, const DevState& st,
     a = true;
   }
   launch_k(k_refresh_end, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vanilla_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
+                                const Head& H, cudaStream_t s) {
+  static bool a = false;
+  if (!a) {
+    big_smem(k_vanilla_pack);
+    a = true;
+  }
+  launch_k(k_vanilla_pack, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, full, blk, H);
+  return cudaGetLastError();
+}
+cudaError_t launch_vanilla_commit(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                                  cudaStream_t s) {
+  static bool a = false;
+  if (!a) {
+    big_smem(k_vanilla_commit);
+    a = true;
+  }
+  launch_k(k_vanilla_commit, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
   return cudaGetLastError();
 }
 

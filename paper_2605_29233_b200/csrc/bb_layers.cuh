@@ -67,6 +67,11 @@ cudaError_t launch_refresh_begin(const Dims& D, const Sess& S, const DevState& s
 cudaError_t launch_refresh_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
                                 const Head& H, int branch, cudaStream_t s);
 cudaError_t launch_refresh_end(const Dims& D, const Sess& S, const DevState& st, cudaStream_t s);
+// vanilla_decode (decoding.py:279-321): round = pack -> full pass -> head -> commit
+cudaError_t launch_vanilla_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
+                                const Head& H, cudaStream_t s);
+cudaError_t launch_vanilla_commit(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                                  cudaStream_t s);
 cudaError_t launch_debug_commit(const float* probs, int n, int n_out, const int* pos, int* row, float tau, int* out,
                                 int* count, cudaStream_t s);
 cudaError_t launch_debug_merge(const Dims& D, const Sess& S, const DevState& st, const float* probmaps, int n_out,

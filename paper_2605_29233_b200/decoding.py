@@ -212,3 +212,25 @@ def single_branch_decode(params, task, cfg: DecodeConfig, preset=None):
                                                         refresh_interval=cfg.refresh_interval,
                                                         gen_len=cfg.gen_len, merge_enabled=False,
                                                         sync_enabled=False), _single=True)
+
+
+def vanilla_decode(params, task, cfg: DecodeConfig):
+    """decoding.py:279-321 — the reference's baseline decoder: one full forward
+    per round over the whole row (no cache reuse) and exactly one committed
+    token per round (Eq. 1 with tau 1.0 over the masked positions before the
+    first eos), so a generation costs about gen_len forwards.
+
+    Runs on the device (bb_run_vanilla: full pass + LM head + commit kernels,
+    one captured graph per round) in a one-branch session of block size
+    gen_len; returns the reference's GenerationResult and trace records."""
+    from .scheduler import SchedulerConfig, _check_call, get_session
+    cfg.validate()
+    if cfg.gen_len != task.gen_len:
+        raise ConfigError("cfg.gen_len does not match the task")
+    scfg = SchedulerConfig(block_sizes=(cfg.gen_len,), gen_len=cfg.gen_len, tau_conf=1.0,
+                           merge_enabled=False, sync_enabled=False)
+    P = _check_call(params, scfg, [task])
+    s = get_session(params, scfg, P, 1, trace=True)
+    s.set_inputs(task.prompt[None], task.target[None])
+    s.launch_vanilla()
+    return s.results([task], params.vocab, single=True)[0]

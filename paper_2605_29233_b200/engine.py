@@ -112,6 +112,14 @@ class Session:
                                      C.c_void_p(self.stream.cuda_stream), C.byref(it)), "bb_run")
         return it.value
 
+    def launch_vanilla(self, use_graph: bool = True) -> int:
+        """vanilla_decode rounds (bb_run_vanilla) on the session stream; the
+        session must have one branch of block size gen_len."""
+        it = C.c_int(0)
+        _lib.check(_lib.lib().bb_run_vanilla(self.h, self.max_iterations(), int(use_graph),
+                                             C.c_void_p(self.stream.cuda_stream), C.byref(it)), "bb_run_vanilla")
+        return it.value
+
     def prefill(self):
         _lib.check(_lib.lib().bb_prefill(self.h, C.c_void_p(self.stream.cuda_stream)), "bb_prefill")
 

@@ -3,7 +3,7 @@
 Run in the build container (needs /root/reference; it does not travel to the
 GPU box — the fixtures it writes do):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [--vanilla-only]
 
 Outputs (all under tests/golden/):
   runs_ref.json     full-run results (tokens, NFE, winner, complete trace) of
@@ -15,6 +15,8 @@ Outputs (all under tests/golden/):
                     the scheduler's module-level forward seams
                     (scheduler.py:23-25) — pins the oracle's scheduler on a
                     second architecture; fp32-weight and bf16-emulating runs.
+  runs_vanilla.json the reference's vanilla_decode baseline (decoding.py:279-321)
+                    on its own model (default dims, and C1 at head_scale 2).
   kernels.json      reference confidence_transition / merge_sync outputs on
                     the fuzzed inputs of fuzz.py (inputs rebuilt from seeds).
   forward_c1.npz    reference full_forward / block_forward numerics (C1, seed 0).
@@ -112,6 +114,34 @@ def gen_ref_runs():
             rec.update(seed=s, block=b)
             sb.append(rec)
     out["single_branch_default"] = {"prompt_len": 16, "gen_len": 64, "runs": sb}
+    return out
+
+
+# ---- vanilla_decode (decoding.py:279-321), the baseline decoder of row f(3) --
+
+VANILLA_CONFIGS = [
+    ("default_g32", dict(), 16, 32, range(6)),
+    ("default_g64", dict(), 16, 64, range(4)),
+    ("c1_hs2_g128", dict(vocab=4096, layers=4, d_model=256, max_len=192, head_scale=2.0), 64, 128, range(2)),
+]
+
+
+def gen_vanilla_runs():
+    out = {}
+    for name, mk, P, G, seeds in VANILLA_CONFIGS:
+        t0 = time.time()
+        params, vocab = ref_params(mk)
+        runs = []
+        for s in seeds:
+            task = bbm.make_task(s, P, G, vocab)
+            runs.append(result_record(bbd.vanilla_decode(params, task, bbd.DecodeConfig(block_size=G, gen_len=G))))
+        out[name] = {"model": {"vocab_size": vocab.size, "layers": params.dims.layers,
+                               "d_model": params.dims.d_model, "max_len": params.dims.max_len,
+                               "head_scale": params.head_scale, "gamma": params.gamma,
+                               "radius": params.radius, "spike_cut": params.spike_cut,
+                               "spike_gain": params.spike_gain, "seed": 0},
+                     "prompt_len": P, "gen_len": G, "seeds": list(seeds), "runs": runs}
+        print(f"vanilla {name}: {time.time() - t0:.1f}s", flush=True)
     return out
 
 
@@ -252,6 +282,11 @@ def gen_forward_c1():
 
 def main():
     t0 = time.time()
+    with open(os.path.join(HERE, "runs_vanilla.json"), "w") as fh:
+        json.dump(gen_vanilla_runs(), fh, separators=(",", ":"))
+    if "--vanilla-only" in sys.argv:
+        print(f"done in {time.time() - t0:.1f}s")
+        return
     with open(os.path.join(HERE, "runs_ref.json"), "w") as fh:
         json.dump(gen_ref_runs(), fh, separators=(",", ":"))
     with open(os.path.join(HERE, "runs_llada.json"), "w") as fh:

@@ -16,6 +16,7 @@ bb = pytest.importorskip("paper_2605_29233_b200")
 REF = goldens.load("runs_ref.json")
 LLADA = goldens.load("runs_llada.json")
 KER = goldens.load("kernels.json")
+VANILLA = goldens.load("runs_vanilla.json")
 
 _MODELS = {}
 
@@ -325,3 +326,17 @@ def test_fused_qkv_attention_equals_separate_finalize(name, monkeypatch):
         outs.append(s.fetch())
     for key in ("ctrl", "tokens", "branch", "events"):
         assert np.array_equal(outs[0][key], outs[1][key]), key
+
+
+@pytest.mark.parametrize("name", list(VANILLA))
+def test_vanilla_decode_matches_reference_runs(name):
+    """vanilla_decode (decoding.py:279-321) on the device — full pass + LM head
+    + tau-1.0 commit per round — bit-exact vs the reference's own runs in fp32
+    verification mode: tokens, NFE, eos position and every trace record."""
+    g = VANILLA[name]
+    params = ref_model(g["model"])
+    for seed, want in zip(g["seeds"], g["runs"]):
+        task = bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab)
+        got = record(bb.vanilla_decode(params, task, bb.DecodeConfig(block_size=g["gen_len"], gen_len=g["gen_len"])))
+        err = goldens.compare_run(got, want)
+        assert err is None, f"{name} seed {seed}: {err}"
