@@ -13,21 +13,28 @@ P, G = 64, 256
 vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
 cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=G)
 params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=0.4, gamma=8.0, dtype="bf16")
-s = get_session(params, cfg, P, 1, trace=False)
+R = int(os.environ.get("BB_TL_R", "1"))  # requests per session (multi-request batching)
+s = get_session(params, cfg, P, R, trace=False)
+
+
+def inputs(seed0):
+    ts = [bb.make_task(seed0 + i, P, G, vocab) for i in range(R)]
+    return np.stack([t.prompt for t in ts]), np.stack([t.target for t in ts])
+
+
 for seed in (1000, 1001):
-    t = bb.make_task(seed, P, G, vocab)
-    s.set_inputs(t.prompt[None], t.target[None]); s.launch()
+    s.set_inputs(*inputs(seed * 100)); s.launch()
 s.stream.synchronize()
 s.klog(reset=True); s.gemm_stats(reset=True)
 import ctypes as _C0; from paper_2605_29233_b200 import _lib as _L0; _L0.lib().bb_session_lsk_prof(s.h, (_C0.c_ulonglong * 64)(), 1, _C0.c_void_p(s.stream.cuda_stream))
 import ctypes as _C; from paper_2605_29233_b200 import _lib as _L; _L.lib().bb_session_phase_stats(s.h, (_C.c_ulonglong * 8)(), 1, _C.c_void_p(s.stream.cuda_stream))
-t = bb.make_task(1002, P, G, vocab)
-s.set_inputs(t.prompt[None], t.target[None])
+s.set_inputs(*inputs(100200))
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 ev0.record(s.stream); it = s.launch(); ev1.record(s.stream); ev1.synchronize()
 log = s.klog()
 c = s.v_ctrl[0].cpu().numpy()
 nfe = int(c[5] + c[6] + c[7])
+nfe = max(nfe, it)  # (R > 1: iterations of the batch)
 names = [n for n, _ in log]
 ts = np.array([t for _, t in log], dtype=np.int64)
 agg = collections.defaultdict(lambda: [0, 0])
