@@ -788,19 +788,35 @@ static cudaError_t attn_seg_launch(const Dims& D, const Sess& S, const Pass& P, 
   return cudaGetLastError();
 }
 
-// cluster size: 8 CTAs per (request, head, row tile) by default; BB_ATT_CS=4
-// halves the cluster (fewer, longer CTAs; faster cluster placement)
-static int att_cs() {
-  static int cs = -1;
-  if (cs < 0) cs = (getenv("BB_ATT_CS") != nullptr && atoi(getenv("BB_ATT_CS")) == 4) ? 4 : 8;
-  return cs;
+// Cluster size: the largest of 8 / 4 / 2 / 1 CTAs per (request, head, row
+// tile) whose grid still fits one wave (2 CTAs of 89 KB / 238 registers per
+// SM): at one request (C2 block pass, 32 heads) 8-CTA clusters split the keys;
+// with several requests per session, fewer CTAs per cluster (more keys each)
+// avoid running the grid in waves.  BB_ATT_CS forces.
+static int att_cs(const Dims& D, const Sess& S, const Pass& P, bool fq) {
+  static const int forced = getenv("BB_ATT_CS") != nullptr ? atoi(getenv("BB_ATT_CS")) : 0;
+  if (forced == 8 || forced == 4 || (!fq && (forced == 2 || forced == 1))) return forced;
+  if (P.full) return 8;  // full passes: 1-CTA clusters measured 1.3% slower per C2 request
+  const int rows = S.NRq;
+  const long long per = (long long)S.R * D.nh * ((rows + 63) / 64);
+  const long long wave = 2LL * kNumSMs;
+  if (per * 8 <= wave) return 8;
+  if (fq || per * 4 <= wave) return 4;
+  return per * 2 <= wave ? 2 : 1;
 }
 
 template <int HD, bool FQ>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
-  return att_cs() == 4 ? attn_seg_launch<HD, FQ, 4>(D, S, P, st, layer, pr, bias, rope, s)
-                       : attn_seg_launch<HD, FQ, 8>(D, S, P, st, layer, pr, bias, rope, s);
+  switch (att_cs(D, S, P, FQ)) {
+    case 8: return attn_seg_launch<HD, FQ, 8>(D, S, P, st, layer, pr, bias, rope, s);
+    case 4: return attn_seg_launch<HD, FQ, 4>(D, S, P, st, layer, pr, bias, rope, s);
+  }
+  if constexpr (!FQ) {
+    if (att_cs(D, S, P, FQ) == 2) return attn_seg_launch<HD, false, 2>(D, S, P, st, layer, pr, bias, rope, s);
+    return attn_seg_launch<HD, false, 1>(D, S, P, st, layer, pr, bias, rope, s);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // LSE-merge of the partials of the items covering (row, head).  CTA per
