@@ -322,6 +322,14 @@ static int setup_gemms(Session* s) {
   const Dims& D = s->D;
   const Weights& W = s->M->W;
   const size_t e = esz(D);
+  // block pass: the attention prefetches the O projection's weights into L2
+  // (BB_ATT_L2PF=0 disables)
+  s->blk.pf_base = nullptr;
+  s->full.pf_base = nullptr;
+  if (D.dtype == BB_DTYPE_BF16 && !(getenv("BB_ATT_L2PF") != nullptr && atoi(getenv("BB_ATT_L2PF")) == 0)) {
+    s->blk.pf_base = (const char*)W.wo;
+    s->blk.pf_layer_bytes = (long long)D.d * D.attn_dim * (long long)e;
+  }
   for (int which = 0; which < 2; ++which) {
     Pass& P = which == 0 ? s->blk : s->full;
     PassGemms& G = which == 0 ? s->gb : s->gf;

@@ -333,6 +333,18 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req, PartRef pr,
                const float* __restrict__ bias, const float* __restrict__ rope) {
   klog_mark(D.klog, D.klog_cap, 24);  // (timeline) CTA 0 resident, before the dependency wait
+  if (P.pf_base != nullptr && threadIdx.x == 0) {
+    // this CTA's slice of the O projection's weights -> L2 (constant data: no
+    // dependency; the O GEMM's TMA loads then hit L2)
+    const long long n_cta = (long long)gridDim.x * gridDim.y * gridDim.z;
+    const long long cta = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+    const long long per = ((P.pf_layer_bytes + n_cta - 1) / n_cta + 127) & ~127LL;
+    const char* base = P.pf_base + (long long)layer * P.pf_layer_bytes;
+    for (long long o = cta * per; o < min((cta + 1) * per, P.pf_layer_bytes); o += 65536) {
+      const long long n = min(65536LL, min((cta + 1) * per, P.pf_layer_bytes) - o);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"((uint32_t)n) : "memory");
+    }
+  }
   pdl_enter();
   klog_mark(D.klog, D.klog_cap, 3);
   unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;  // timeline runs only

@@ -119,6 +119,10 @@ struct Pass {
   int akey_cap;
   int n_kz;           // key tiles per request (block pass: 64-row tiles; full pass: 1)
   unsigned long long* atstat;  // live attention timing: [0..7] duration, [8..15] CTA start spread
+  // L2 prefetch of the next GEMM's weights issued by the attention CTAs (HBM is
+  // idle during the attention): layer l's bytes at pf_base + l * pf_layer_bytes
+  const char* pf_base;
+  long long pf_layer_bytes;
 };
 
 // Head (LM head + confidence) works on block-pass slots.
