@@ -78,6 +78,7 @@ typedef struct {
   int pages_per_item;  /* attention split (pages per work item, def. 4)  */
   int trace;           /* record trace events (TraceEvent, decoding.py:61-75) */
   int event_capacity;  /* events per request                              */
+  int diagnostics;     /* 1: reserve scratch KV pages for bb_fresh_kv (log_consistency) */
 } bb_session_desc;
 
 #define BB_VIEW_TOKENS 0   /* int32 [R][B][L]      branch rows              */
@@ -124,6 +125,25 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
    Replaces the reference's vanilla_decode (the baseline decoder of the
    paper's NFE comparison, test_acceptance.py:300-325). */
 BB_API int bb_run_vanilla(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out);
+
+/* ---- KV-space diagnostics (scheduler.py:268-281, 332-347, 376-390; the
+   run_blockbatch log_kv / log_consistency modes).  The host runs the step in
+   parts so the diagnostics see the caches between the forward and the
+   commit/merge/sync that follows it. */
+/* part 0: init + full forward + head; part 1: first commits, merge/sync, copies */
+BB_API int bb_prefill_part(void* sess, int part, void* stream);
+/* part 0: pack + copy-on-write copies (ctrl then holds the active set);
+   part 1: forward + head; part 2: commit, EOS, merge/sync, copies */
+BB_API int bb_block_step_part(void* sess, int part, void* stream);
+/* kv_vectorize (model.py:346-352) of branch k of request r: fp32
+   [layers][L][2][n_kv*head_dim] (keys before values) into dst (device) */
+BB_API int bb_kv_gather(void* sess, int r, int k, float* dst, void* stream);
+/* full_forward(row_k).cache vectorized the same way, without changing any
+   session state (the pass writes into reserved scratch pages; needs
+   diagnostics = 1 in the session desc) */
+BB_API int bb_fresh_kv(void* sess, int r, int k, float* dst, void* stream);
+/* out[0] = ||a - b||_2 (b may be NULL), fp64 accumulation in a fixed order */
+BB_API int bb_sqdiff_norm(const float* a, const float* b, long long n, double* out, void* stream);
 BB_API int bb_version(void);
 /* instrumentation: live per-launch GEMM timing and kernel-launch counters */
 BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream);

@@ -44,7 +44,8 @@ class SessionDesc(C.Structure):
                 ("prompt_len", C.c_int), ("gen_len", C.c_int), ("tau_conf", C.c_float),
                 ("tau_merge", C.c_float), ("tau_sync", C.c_float), ("refresh_interval", C.c_int),
                 ("merge_enabled", C.c_int), ("sync_enabled", C.c_int), ("page_size", C.c_int),
-                ("pages_per_item", C.c_int), ("trace", C.c_int), ("event_capacity", C.c_int)]
+                ("pages_per_item", C.c_int), ("trace", C.c_int), ("event_capacity", C.c_int),
+                ("diagnostics", C.c_int)]
 
 
 ARCH_REF, ARCH_LLADA = 0, 1
@@ -86,6 +87,11 @@ SIGNATURES = {
     "bb_iteration": (i32, [vp, i32, i32, vp]),
     "bb_run": (i32, [vp, i32, i32, vp, i32p]),
     "bb_run_vanilla": (i32, [vp, i32, i32, vp, i32p]),
+    "bb_prefill_part": (i32, [vp, i32, vp]),
+    "bb_block_step_part": (i32, [vp, i32, vp]),
+    "bb_kv_gather": (i32, [vp, i32, i32, vp, vp]),
+    "bb_fresh_kv": (i32, [vp, i32, i32, vp, vp]),
+    "bb_sqdiff_norm": (i32, [vp, vp, i64, vp, vp]),
     "bb_commit_probs": (i32, [vp, i32, i32, vp, vp, f32, vp, vp, vp]),
     "bb_merge_sync_maps": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, f32, f32, i32, i32, vp, i32, vp, vp, vp,
                                  vp]),

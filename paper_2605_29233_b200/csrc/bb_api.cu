@@ -73,6 +73,7 @@ struct Session {
   // [l+1] = O(l) .. down(l) + QKV(l+1); empty = per-GEMM kernels
   std::vector<LskParams> lsk;
   unsigned int* lsk_bar = nullptr;  // [(layers+1)][16] grid-barrier counters
+  int* fresh_save = nullptr;         // [n_lp] page-table row saved by bb_fresh_kv
   unsigned long long* lsk_prof = nullptr;  // [64] CTA-0 phase profile (BB_KLOG)
   int lsk_grid = 0;
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
@@ -254,6 +255,7 @@ static void plan(Session* s, char* base, bool dry) {
   s->full.atstat = s->tstat + 13 * 8; // slots 13/14: full-pass attention
   s->tile_cnt = c.take<int>(8192);
   s->lsk_bar = c.take<unsigned int>((size_t)(D.layers + 1) * 16);
+  s->fresh_save = c.take<int>(S.n_lp);
   s->lsk_prof = c.take<unsigned long long>(64);
   s->ns_cap = 64 * 1024;
   s->ns_tabs = c.take<unsigned char>(s->ns_cap);
@@ -615,35 +617,59 @@ static cudaError_t head(Session* s, cudaStream_t st) {
   return launch_head_reduce(D, s->S, s->blk, s->H, s->st, st);
 }
 
-static int enqueue_prefill(Session* s, cudaStream_t st) {
+// prefill in two parts (the diagnostics mode reads the caches in between):
+// 0 = init + full forward + head, 1 = first commits, merge/sync, copies
+static int enqueue_prefill_part(Session* s, int part, cudaStream_t st) {
   const Dims& D = s->D;
   const Sess& S = s->S;
-  CK(launch_prefill_init(D, S, s->st, s->full, s->blk, s->H, st));
-  CK(launch_attn_keys(D, S, s->full, s->st, st));
-  CK(forward(s, s->full, s->gf, st));
-  CK(launch_gather_head(D, S, s->full, s->blk, s->H, -1, st));
-  CK(head(s, st));
-  CK(launch_prefill_post(D, S, s->st, s->blk, s->H, st));
-  CK(launch_merge_prep(D, S, s->st, s->M->W, st));
-  CK(launch_merge_sync(D, S, s->st, 1, st));
-  CK(launch_copy_pages(D, S, s->st, 1, st));
+  if (part == 0) {
+    CK(launch_prefill_init(D, S, s->st, s->full, s->blk, s->H, st));
+    CK(launch_attn_keys(D, S, s->full, s->st, st));
+    CK(forward(s, s->full, s->gf, st));
+    CK(launch_gather_head(D, S, s->full, s->blk, s->H, -1, st));
+    CK(head(s, st));
+  } else {
+    CK(launch_prefill_post(D, S, s->st, s->blk, s->H, st));
+    CK(launch_merge_prep(D, S, s->st, s->M->W, st));
+    CK(launch_merge_sync(D, S, s->st, 1, st));
+    CK(launch_copy_pages(D, S, s->st, 1, st));
+  }
+  return BB_OK;
+}
+
+static int enqueue_prefill(Session* s, cudaStream_t st) {
+  const int rc = enqueue_prefill_part(s, 0, st);
+  return rc != BB_OK ? rc : enqueue_prefill_part(s, 1, st);
+}
+
+// block step in three parts: 0 = pack + copy-on-write copies (ctrl then holds
+// the active set), 1 = forward + head, 2 = commit, EOS, merge/sync, copies
+static int enqueue_block_step_part(Session* s, int part, cudaStream_t st) {
+  const Dims& D = s->D;
+  const Sess& S = s->S;
+  if (part == 0) {
+    CK(cudaMemsetAsync(s->blk.skip, 1, sizeof(int), st));
+    CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
+    CK(launch_block_pack(D, S, s->st, s->blk, s->H, st));
+    CK(launch_copy_pages(D, S, s->st, 0, st));
+  } else if (part == 1) {
+    CK(launch_attn_keys(D, S, s->blk, s->st, st));
+    CK(forward(s, s->blk, s->gb, st));
+    CK(head(s, st));
+  } else {
+    CK(launch_step_commit(D, S, s->st, s->blk, s->H, st));
+    CK(launch_merge_prep(D, S, s->st, s->M->W, st));
+    CK(launch_merge_sync(D, S, s->st, 0, st));
+    CK(launch_copy_pages(D, S, s->st, 1, st));
+  }
   return BB_OK;
 }
 
 static int enqueue_block_step(Session* s, cudaStream_t st) {
-  const Dims& D = s->D;
-  const Sess& S = s->S;
-  CK(cudaMemsetAsync(s->blk.skip, 1, sizeof(int), st));
-  CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
-  CK(launch_block_pack(D, S, s->st, s->blk, s->H, st));
-  CK(launch_copy_pages(D, S, s->st, 0, st));
-  CK(launch_attn_keys(D, S, s->blk, s->st, st));
-  CK(forward(s, s->blk, s->gb, st));
-  CK(head(s, st));
-  CK(launch_step_commit(D, S, s->st, s->blk, s->H, st));
-  CK(launch_merge_prep(D, S, s->st, s->M->W, st));
-  CK(launch_merge_sync(D, S, s->st, 0, st));
-  CK(launch_copy_pages(D, S, s->st, 1, st));
+  for (int part = 0; part < 3; ++part) {
+    const int rc = enqueue_block_step_part(s, part, st);
+    if (rc != BB_OK) return rc;
+  }
   return BB_OK;
 }
 
@@ -802,7 +828,8 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.n_pp = (S.P + S.ps - 1) / S.ps;
   S.n_gp = (S.G + S.ps - 1) / S.ps;
   S.n_lp = S.n_pp + S.n_gp;
-  S.pool = S.B * S.n_lp;
+  S.diag = d->diagnostics ? 1 : 0;
+  S.pool = S.B * S.n_lp + (S.diag ? S.n_lp : 0);
   S.ch_block = d->pages_per_item > 0 ? d->pages_per_item : 4;
   S.max_items = S.B * ((S.n_lp + S.ch_block - 1) / S.ch_block) + 2 * S.B + 4;
   S.ev_cap = d->event_capacity > 0 ? d->event_capacity : 32768;
@@ -1018,6 +1045,49 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
   }
   CK(cudaStreamSynchronize(st));
   if (iterations_out) *iterations_out = it;
+  return BB_OK;
+}
+
+BB_API int bb_prefill_part(void* sess, int part, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || part < 0 || part > 1) return BB_ERR_CONTRACT;
+  return enqueue_prefill_part(s, part, (cudaStream_t)stream);
+}
+
+BB_API int bb_block_step_part(void* sess, int part, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || part < 0 || part > 2) return BB_ERR_CONTRACT;
+  return enqueue_block_step_part(s, part, (cudaStream_t)stream);
+}
+
+BB_API int bb_kv_gather(void* sess, int r, int k, float* dst, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !dst || r < 0 || r >= s->S.R || k < 0 || k >= s->S.B) return BB_ERR_CONTRACT;
+  CK(launch_kv_gather(s->D, s->S, s->st, r, k, dst, (cudaStream_t)stream));
+  return BB_OK;
+}
+
+// full_forward (model.py:322-328) of branch k's current row into the scratch
+// pages, vectorized into dst; the branch's page table is restored afterwards
+BB_API int bb_fresh_kv(void* sess, int r, int k, float* dst, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !dst || r < 0 || r >= s->S.R || k < 0 || k >= s->S.B) return BB_ERR_CONTRACT;
+  if (!s->S.diag) return fail(BB_ERR_CONFIG, "bb_fresh_kv needs a diagnostics session");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(s->full.skip, 1, sizeof(int), st));
+  CK(launch_fresh_pack(s->D, s->S, s->st, s->full, r, k, s->fresh_save, st));
+  CK(launch_attn_keys(s->D, s->S, s->full, s->st, st));
+  CK(forward(s, s->full, s->gf, st));
+  CK(launch_kv_gather(s->D, s->S, s->st, r, k, dst, st));
+  CK(launch_fresh_restore(s->S, s->st, r, k, s->fresh_save, st));
+  return BB_OK;
+}
+
+BB_API int bb_sqdiff_norm(const float* a, const float* b, long long n, double* out, void* stream) {
+  if (!a || !out || n < 0) return BB_ERR_CONTRACT;
+  static double* part = nullptr;
+  if (part == nullptr && cudaMalloc(&part, kNumSMs * sizeof(double)) != cudaSuccess) return BB_ERR_CUDA;
+  CK(launch_sqdiff_norm(a, b, n, part, kNumSMs, out, (cudaStream_t)stream));
   return BB_OK;
 }
 

@@ -347,14 +347,16 @@ __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk,
     }
   }
   for (int i = threadIdx.x; i < S.B * S.L; i += blockDim.x) st.covered[(long long)r * S.B * S.L + i] = 0;
-  // page pool: free stack pops 0,1,2...
+  // page pool: free stack pops 0,1,2...; a diagnostics session keeps the last
+  // n_lp pages out of it (scratch for bb_fresh_kv)
+  const int n_free = S.pool - (S.diag ? S.n_lp : 0);
   for (int i = threadIdx.x; i < S.pool; i += blockDim.x) {
-    st.freel[(long long)r * S.pool + i] = S.pool - 1 - i;
+    st.freel[(long long)r * S.pool + i] = n_free - 1 - i;
     st.refc[(long long)r * S.pool + i] = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    st.free_top[r] = S.pool;
+    st.free_top[r] = n_free;
     int* t0 = c.pt(0);
     for (int lp = 0; lp < S.n_lp; ++lp) t0[lp] = c.pg_alloc();
     for (int k = 1; k < S.B; ++k) {
@@ -1170,6 +1172,99 @@ __global__ void k_vanilla_commit(Dims D, Sess S, DevState st, Pass blk, Head H) 
   store_request(c);
 }
 
+// ------------------------------------------------------------------ KV-space diagnostics
+// kv_vectorize (model.py:346-352) of (request r, branch k): fp32
+// [layers][L][2][kv_dim], keys before values; CTA per (position, layer).
+template <typename T>
+__global__ void __launch_bounds__(256) k_kv_gather(Dims D, Sess S, DevState st, int r, int k, float* dst) {
+  pdl_enter();
+  const int pos = blockIdx.x, l = blockIdx.y;
+  const int kv_dim = D.nkv * D.hd;
+  const int lp = lp_of(S, pos);
+  const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + k) * S.n_lp + lp];
+  const long long lay = (long long)l * S.R * S.pool * D.nkv * S.ps * D.hd;
+  const int row = pos - lp_start(S, lp);
+  float* o = dst + ((long long)l * S.L + pos) * 2 * kv_dim;
+  for (int e = threadIdx.x; e < kv_dim; e += blockDim.x) {
+    const int kvh = e / D.hd, i = e - kvh * D.hd;
+    const long long src = lay + ((gpage * D.nkv + kvh) * S.ps + row) * D.hd + i;
+    o[e] = ldf(reinterpret_cast<const T*>(st.kv_k) + src);
+    o[kv_dim + e] = ldf(reinterpret_cast<const T*>(st.kv_v) + src);
+  }
+}
+
+// Point branch k of request r at the reserved scratch pages (saving its page
+// table) and set the full pass up for that one row (the other requests' rows
+// are padding).  CTA per request.
+__global__ void k_fresh_pack(Dims D, Sess S, DevState st, Pass full, int r, int k, int* save) {
+  pdl_enter();
+  const int rr = blockIdx.x;
+  const bool live = rr == r;
+  int* pt = st.pt + ((long long)rr * S.B + k) * S.n_lp;
+  if (live)
+    for (int lp = threadIdx.x; lp < S.n_lp; lp += blockDim.x) {
+      save[lp] = pt[lp];
+      pt[lp] = S.pool - S.n_lp + lp;
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int kk = 0; kk < MAXB; ++kk) {
+      full.rng_off[rr * MAXB + kk] = rr * S.L;
+      full.rng_cnt[rr * MAXB + kk] = (live && kk == k) ? S.L : 0;
+    }
+    full.n_items[rr] = live ? 1 : 0;
+    if (live) {
+      int* it = full.items + (long long)rr * ITW;
+      it[0] = 1 << k;
+      it[1] = 0;
+      it[2] = S.n_lp;
+      it[3] = k;
+      *full.skip = 0;
+    }
+  }
+  const int* rw = st.tokens + ((long long)rr * S.B + k) * S.L;
+  for (int p = threadIdx.x; p < S.L; p += blockDim.x) {
+    const int row = rr * S.L + p;
+    full.slot_pos[row] = live ? p : -1;
+    full.slot_req[row] = rr;
+    full.slot_br[row] = k;
+    full.slot_tok[row] = rw[p];
+    full.slot_kvoff[row] = live ? kv_row_off(D, S, st, rr, k, p) : 0;
+  }
+}
+
+__global__ void k_fresh_restore(Sess S, DevState st, int r, int k, const int* save) {
+  pdl_enter();
+  int* pt = st.pt + ((long long)r * S.B + k) * S.n_lp;
+  for (int lp = threadIdx.x; lp < S.n_lp; lp += blockDim.x) pt[lp] = save[lp];
+}
+
+// ||a - b||_2 in fp64: per-CTA strided partial sums, then one ordered sum
+__global__ void __launch_bounds__(256) k_sqdiff_partial(const float* a, const float* b, long long n, double* part) {
+  pdl_enter();
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double d = (double)a[i] - (b != nullptr ? (double)b[i] : 0.0);
+    acc += d * d;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x >> 1; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void k_sqdiff_final(const double* part, int n, double* out) {
+  pdl_enter();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    out[0] = sqrt(s);
+  }
+}
+
 // ------------------------------------------------------------------ copies
 // 16-byte vector copies; block-strided over (request, job, layer) units.
 template <typename T>
@@ -1414,6 +1509,28 @@ cudaError_t launch_vanilla_commit(const Dims& D, const Sess& S, const DevState& 
     a = true;
   }
   launch_k(k_vanilla_commit, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_gather(const Dims& D, const Sess& S, const DevState& st, int r, int k, float* dst,
+                             cudaStream_t s) {
+  if (D.dtype == 1) launch_k(k_kv_gather<__nv_bfloat16>, dim3(S.L, D.layers), dim3(256), (size_t)0, s, D, S, st, r, k, dst);
+  else launch_k(k_kv_gather<float>, dim3(S.L, D.layers), dim3(256), (size_t)0, s, D, S, st, r, k, dst);
+  return cudaGetLastError();
+}
+cudaError_t launch_fresh_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, int r, int k,
+                              int* save, cudaStream_t s) {
+  launch_k(k_fresh_pack, dim3(S.R), dim3(256), (size_t)0, s, D, S, st, full, r, k, save);
+  return cudaGetLastError();
+}
+cudaError_t launch_fresh_restore(const Sess& S, const DevState& st, int r, int k, const int* save, cudaStream_t s) {
+  launch_k(k_fresh_restore, dim3(1), dim3(256), (size_t)0, s, S, st, r, k, save);
+  return cudaGetLastError();
+}
+cudaError_t launch_sqdiff_norm(const float* a, const float* b, long long n, double* part, int n_part, double* out,
+                               cudaStream_t s) {
+  launch_k(k_sqdiff_partial, dim3(n_part), dim3(256), (size_t)0, s, a, b, n, part);
+  launch_k(k_sqdiff_final, dim3(1), dim3(32), (size_t)0, s, (const double*)part, n_part, out);
   return cudaGetLastError();
 }
 

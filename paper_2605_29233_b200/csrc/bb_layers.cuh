@@ -67,6 +67,14 @@ cudaError_t launch_refresh_begin(const Dims& D, const Sess& S, const DevState& s
 cudaError_t launch_refresh_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
                                 const Head& H, int branch, cudaStream_t s);
 cudaError_t launch_refresh_end(const Dims& D, const Sess& S, const DevState& st, cudaStream_t s);
+// KV-space diagnostics (log_kv / log_consistency)
+cudaError_t launch_kv_gather(const Dims& D, const Sess& S, const DevState& st, int r, int k, float* dst,
+                             cudaStream_t s);
+cudaError_t launch_fresh_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, int r, int k,
+                              int* save, cudaStream_t s);
+cudaError_t launch_fresh_restore(const Sess& S, const DevState& st, int r, int k, const int* save, cudaStream_t s);
+cudaError_t launch_sqdiff_norm(const float* a, const float* b, long long n, double* part, int n_part, double* out,
+                               cudaStream_t s);
 // vanilla_decode (decoding.py:279-321): round = pack -> full pass -> head -> commit
 cudaError_t launch_vanilla_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
                                 const Head& H, cudaStream_t s);

@@ -64,6 +64,7 @@ struct Sess {
   int ch_block;       // logical pages per attention item in block passes
   int max_items;      // attention items per request per pass
   int ev_cap, trace, hard_cap, max_copies;
+  int diag;           // diagnostics session: the last n_lp pages of each request's pool are scratch
 };
 
 struct DevState {

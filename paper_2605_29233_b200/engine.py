@@ -26,7 +26,8 @@ def _torch():
 
 class Session:
     def __init__(self, params, cfg, prompt_len: int, n_requests: int = 1, trace: bool = True,
-                 page_size: int = 16, pages_per_item: int = 4, event_capacity: int | None = None):
+                 page_size: int = 16, pages_per_item: int = 4, event_capacity: int | None = None,
+                 diagnostics: bool = False):
         torch = _torch()
         self.params = params
         self.cfg = cfg
@@ -43,7 +44,7 @@ class Session:
             tau_conf=cfg.tau_conf, tau_merge=cfg.tau_merge, tau_sync=float(cfg.tau_sync),
             refresh_interval=cfg.refresh_interval, merge_enabled=int(cfg.merge_enabled),
             sync_enabled=int(cfg.sync_enabled), page_size=page_size, pages_per_item=pages_per_item,
-            trace=int(trace), event_capacity=event_capacity)
+            trace=int(trace), event_capacity=event_capacity, diagnostics=int(diagnostics))
         nbytes = C.c_size_t(0)
         model = params.handle()
         _lib.check(L.bb_session_workspace_bytes(model, C.byref(self.desc), C.byref(nbytes)),
@@ -119,6 +120,43 @@ class Session:
         _lib.check(_lib.lib().bb_run_vanilla(self.h, self.max_iterations(), int(use_graph),
                                              C.c_void_p(self.stream.cuda_stream), C.byref(it)), "bb_run_vanilla")
         return it.value
+
+    # ---------------------------------------------------------------- diagnostics
+    # (log_kv / log_consistency: the step in parts, KV gathers, fresh forwards)
+    def prefill_part(self, part: int):
+        _lib.check(_lib.lib().bb_prefill_part(self.h, part, C.c_void_p(self.stream.cuda_stream)), "bb_prefill_part")
+
+    def block_step_part(self, part: int):
+        _lib.check(_lib.lib().bb_block_step_part(self.h, part, C.c_void_p(self.stream.cuda_stream)),
+                   "bb_block_step_part")
+
+    def refresh(self):
+        _lib.check(_lib.lib().bb_refresh(self.h, C.c_void_p(self.stream.cuda_stream)), "bb_refresh")
+
+    def kv_numel(self) -> int:
+        d = self.params.dims
+        return d.layers * self.Lseq * 2 * d.n_kv_heads * d.hd
+
+    def kv_gather(self, r: int, k: int, dst):
+        _lib.check(_lib.lib().bb_kv_gather(self.h, r, k, C.c_void_p(dst.data_ptr()),
+                                           C.c_void_p(self.stream.cuda_stream)), "bb_kv_gather")
+
+    def fresh_kv(self, r: int, k: int, dst):
+        _lib.check(_lib.lib().bb_fresh_kv(self.h, r, k, C.c_void_p(dst.data_ptr()),
+                                          C.c_void_p(self.stream.cuda_stream)), "bb_fresh_kv")
+
+    def sqdiff_norm(self, a, b=None) -> float:
+        torch = _torch()
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().bb_sqdiff_norm(C.c_void_p(a.data_ptr()), None if b is None else C.c_void_p(b.data_ptr()),
+                                             a.numel(), C.c_void_p(out.data_ptr()),
+                                             C.c_void_p(self.stream.cuda_stream)), "bb_sqdiff_norm")
+        self.stream.synchronize()
+        return float(out.item())
+
+    def ctrl_now(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.v_ctrl.cpu().numpy()
 
     def prefill(self):
         _lib.check(_lib.lib().bb_prefill(self.h, C.c_void_p(self.stream.cuda_stream)), "bb_prefill")

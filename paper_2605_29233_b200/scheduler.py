@@ -31,9 +31,9 @@ HARD_CAP_FACTOR = 4
 
 @dataclass
 class SchedulerConfig:
-    """scheduler.py:32-63.  ``log_kv`` / ``log_consistency`` are KV-space
-    diagnostics (out of scope of the device path): only their defaults are
-    accepted by ``run_blockbatch``."""
+    """scheduler.py:32-63.  ``log_kv`` ("norms" | "full") / ``log_consistency``
+    switch ``run_blockbatch`` to the diagnostics mode (the step in parts with
+    device KV gathers and side-effect-free fresh forwards between them)."""
 
     block_sizes: tuple = DEFAULT_BLOCK_SIZES
     tau_conf: float = 0.9
@@ -129,10 +129,10 @@ def get_session(params: ModelParams, cfg: SchedulerConfig, prompt_len: int, n_re
     return s
 
 
-def _check_call(params, cfg, tasks):
+def _check_call(params, cfg, tasks, diagnostics: bool = False):
     cfg.validate()
-    if cfg.log_kv != "none" or cfg.log_consistency:
-        raise ConfigError("KV-space logging (log_kv / log_consistency) is a CPU diagnostic, not on the device path")
+    if (cfg.log_kv != "none" or cfg.log_consistency) and not diagnostics:
+        raise ConfigError("KV-space logging (log_kv / log_consistency) is per request: use run_blockbatch")
     P = tasks[0].prompt_len
     for t in tasks:
         if t.gen_len != cfg.gen_len:
@@ -155,7 +155,139 @@ def run_blockbatch(params: ModelParams, task: Task, cfg: SchedulerConfig, forwar
     not supported on the device path."""
     if forward_observer is not None:
         raise NotImplementedError("forward_observer needs host KV snapshots; not supported on the device path")
+    cfg.validate()
+    if cfg.log_kv != "none" or cfg.log_consistency:
+        return _run_diagnostics(params, task, cfg, forward_hook)
     return run_batch(params, [task], cfg, forward_hook=forward_hook, _single=_single)[0]
+
+
+def _replay_hook(res, forward_hook):
+    for ev in res.trace:
+        if ev.kind == "init":
+            forward_hook("init")
+        elif ev.kind == "block_forward":
+            forward_hook("block")
+        elif ev.kind == "refresh":
+            forward_hook("refresh")
+
+
+def _run_diagnostics(params: ModelParams, task: Task, cfg: SchedulerConfig, forward_hook=None):
+    """run_blockbatch with the KV-space logging of scheduler.py:268-281,
+    288-294, 332-347 and 376-390: per block_forward / refresh event the
+    ``kv_delta`` norm of each touched branch's cache change (log_kv), its
+    vectorized cache ("full"), and ``E_before`` / ``E_after`` =
+    ||kv_vectorize(cache) - kv_vectorize(full_forward(row).cache)|| around the
+    forward (log_consistency); the init event carries each branch's cache norm.
+    The device runs the step in parts (bb_prefill_part / bb_block_step_part);
+    caches are gathered on the device (bb_kv_gather), fresh forwards run into
+    reserved scratch pages without changing the session (bb_fresh_kv), norms
+    are fp64 device reductions (bb_sqdiff_norm).  Decisions, tokens, NFE and
+    the rest of the trace are those of the plain run."""
+    import torch
+    P = _check_call(params, cfg, [task], diagnostics=True)
+    s = Session(params, cfg, P, 1, trace=True, diagnostics=True)
+    s.set_inputs(task.prompt[None], task.target[None])
+    B = len(cfg.block_sizes)
+    n = s.kv_numel()
+    snap = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(B)]
+    cur = torch.empty(n, dtype=torch.float32, device="cuda")
+    fresh = torch.empty(n, dtype=torch.float32, device="cuda")
+    norms, full = cfg.log_kv != "none", cfg.log_kv == "full"
+
+    def consistency(ks):
+        out = {}
+        for k in ks:
+            s.kv_gather(0, k, cur)
+            s.fresh_kv(0, k, fresh)
+            out[k] = s.sqdiff_norm(cur, fresh)
+        return out
+
+    def before(ks):
+        e = consistency(ks) if cfg.log_consistency else None
+        if norms:
+            for k in ks:
+                s.kv_gather(0, k, snap[k])
+        return e
+
+    def after(ks, e_before):
+        extra = {}
+        if norms:
+            d = {}
+            for k in ks:
+                s.kv_gather(0, k, cur)
+                d[k] = s.sqdiff_norm(cur, snap[k])
+            extra["kv_delta"] = d
+        if full:
+            kv = {}
+            for k in ks:
+                s.kv_gather(0, k, cur)
+                s.stream.synchronize()
+                kv[k] = cur.cpu().numpy().astype(np.float64).tolist()
+            extra["kv"] = kv
+        if cfg.log_consistency:
+            extra["E_before"] = e_before
+            extra["E_after"] = consistency(ks)
+        return _jsonify(extra)
+
+    def mask_list(m):
+        return [k for k in range(B) if (m >> k) & 1]
+
+    # prefill: the init event's kv_delta is each branch's cache norm (delta from empty)
+    s.prefill_part(0)
+    init_extra = {}
+    if norms:
+        init_extra["kv_delta"] = {}
+        for k in range(B):
+            s.kv_gather(0, k, cur)
+            init_extra["kv_delta"][k] = s.sqdiff_norm(cur)
+    if full:
+        s.stream.synchronize()
+        init_extra["kv"] = {}
+        for k in range(B):
+            s.kv_gather(0, k, cur)
+            s.stream.synchronize()
+            init_extra["kv"][k] = cur.cpu().numpy().astype(np.float64).tolist()
+    init_extra = _jsonify(init_extra)
+    s.prefill_part(1)
+    block_extras, refresh_extras = [], []
+    it = 0
+    while it < s.max_iterations():
+        c = s.ctrl_now()[0]
+        if c[_lib.C_STATUS] != 0:
+            break
+        it += 1
+        s.block_step_part(0)
+        c = s.ctrl_now()[0]
+        active = mask_list(int(c[_lib.C_ACTIVE_MASK])) if c[_lib.C_STATUS] == 0 else []
+        eb = before(active) if active else None
+        s.block_step_part(1)
+        if active:
+            block_extras.append(after(active, eb))
+        s.block_step_part(2)
+        if it % cfg.refresh_interval == 0:
+            c = s.ctrl_now()[0]
+            todo = mask_list(int(c[_lib.C_REFRESH_MASK])) if (c[_lib.C_STATUS] == 0 and c[_lib.C_REFRESH_DUE]) else []
+            eb = before(todo) if todo else None
+            s.refresh()
+            if todo:
+                refresh_extras.append(after(todo, eb))
+    s.stream.synchronize()
+    res = s.results([task], params.vocab)[0]
+    bi = ri = 0
+    for ev in res.trace:
+        if ev.kind == "init":
+            ev.extra.update(init_extra)
+        elif ev.kind == "block_forward":
+            ev.extra.update(block_extras[bi])
+            bi += 1
+        elif ev.kind == "refresh":
+            ev.extra.update(refresh_extras[ri])
+            ri += 1
+    if bi != len(block_extras) or ri != len(refresh_extras):
+        raise ContractError("diagnostics out of step with the device trace")
+    if forward_hook is not None:
+        _replay_hook(res, forward_hook)
+    return res
 
 
 def run_batch(params: ModelParams, tasks: list, cfg: SchedulerConfig, forward_hook=None, trace: bool = True,

@@ -3,7 +3,7 @@
 Run in the build container (needs /root/reference; it does not travel to the
 GPU box — the fixtures it writes do):
 
-    python tests/golden/make_golden.py [--vanilla-only]
+    python tests/golden/make_golden.py [--vanilla-only]   (vanilla + diag fixtures only)
 
 Outputs (all under tests/golden/):
   runs_ref.json     full-run results (tokens, NFE, winner, complete trace) of
@@ -17,6 +17,8 @@ Outputs (all under tests/golden/):
                     second architecture; fp32-weight and bf16-emulating runs.
   runs_vanilla.json the reference's vanilla_decode baseline (decoding.py:279-321)
                     on its own model (default dims, and C1 at head_scale 2).
+  runs_diag.json    reference run_blockbatch with log_kv="norms" and
+                    log_consistency (KV-space logging).
   kernels.json      reference confidence_transition / merge_sync outputs on
                     the fuzzed inputs of fuzz.py (inputs rebuilt from seeds).
   forward_c1.npz    reference full_forward / block_forward numerics (C1, seed 0).
@@ -114,6 +116,39 @@ def gen_ref_runs():
             rec.update(seed=s, block=b)
             sb.append(rec)
     out["single_branch_default"] = {"prompt_len": 16, "gen_len": 64, "runs": sb}
+    return out
+
+
+# ---- KV-space logging (row f(4)): run_blockbatch with log_kv / log_consistency --
+
+DIAG_CONFIGS = [
+    ("diag_default", dict(), 16, 64, range(4), dict(gen_len=64, log_kv="norms", log_consistency=True)),
+    ("diag_r4", dict(), 16, 64, range(3), dict(gen_len=64, refresh_interval=4, log_kv="norms",
+                                              log_consistency=True)),
+    ("diag_b8_32", dict(), 16, 64, range(3), dict(block_sizes=(8, 16, 32), gen_len=64, refresh_interval=8,
+                                                  log_kv="norms", log_consistency=True)),
+]
+
+
+def gen_diag_runs():
+    out = {}
+    for name, mk, P, G, seeds, sk in DIAG_CONFIGS:
+        t0 = time.time()
+        params, vocab = ref_params(mk)
+        cfg = bbs.SchedulerConfig(**sk)
+        runs = []
+        for s in seeds:
+            task = bbm.make_task(s, P, G, vocab)
+            runs.append(result_record(bbs.run_blockbatch(params, task, cfg)))
+        out[name] = {"model": {"vocab_size": vocab.size, "layers": params.dims.layers,
+                               "d_model": params.dims.d_model, "max_len": params.dims.max_len,
+                               "head_scale": params.head_scale, "gamma": params.gamma,
+                               "radius": params.radius, "spike_cut": params.spike_cut,
+                               "spike_gain": params.spike_gain, "seed": 0},
+                     "prompt_len": P, "gen_len": G, "seeds": list(seeds),
+                     "config": {k: (list(v) if isinstance(v, tuple) else v) for k, v in cfg.__dict__.items()},
+                     "runs": runs}
+        print(f"diag {name}: {time.time() - t0:.1f}s", flush=True)
     return out
 
 
@@ -284,6 +319,8 @@ def main():
     t0 = time.time()
     with open(os.path.join(HERE, "runs_vanilla.json"), "w") as fh:
         json.dump(gen_vanilla_runs(), fh, separators=(",", ":"))
+    with open(os.path.join(HERE, "runs_diag.json"), "w") as fh:
+        json.dump(gen_diag_runs(), fh, separators=(",", ":"))
     if "--vanilla-only" in sys.argv:
         print(f"done in {time.time() - t0:.1f}s")
         return

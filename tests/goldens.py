@@ -26,7 +26,7 @@ def _close(a, b, tol):
     return a == b
 
 
-def diff_trace(got: list, want: list, prob_tol=1e-9):
+def diff_trace(got: list, want: list, prob_tol=1e-9, kv_tol=1e-4):
     """First mismatch between two trace record lists, or None.  Discrete
     fields must be equal; merge-event probabilities within ``prob_tol``."""
     for i, (g, w) in enumerate(zip(got, want)):
@@ -40,6 +40,14 @@ def diff_trace(got: list, want: list, prob_tol=1e-9):
             if k == "prob":
                 if not _close(ge[k], we[k], prob_tol):
                     return f"event {i} prob: got {ge[k]} want {we[k]}"
+            elif k in ("kv_delta", "E_before", "E_after"):
+                # KV-space norms (scheduler.py:268-281): float64 reference vs the
+                # device's fp32 caches (fp64 reductions)
+                if set(ge[k]) != set(we[k]):
+                    return f"event {i} {k} branches: got {sorted(ge[k])} want {sorted(we[k])}"
+                for b in we[k]:
+                    if not math.isclose(float(ge[k][b]), float(we[k][b]), rel_tol=kv_tol, abs_tol=kv_tol):
+                        return f"event {i} {k}[{b}]: got {ge[k][b]} want {we[k][b]}"
             elif ge[k] != we[k]:
                 return f"event {i} extra {k}: got {ge[k]} want {we[k]}"
     if len(got) != len(want):
@@ -47,7 +55,7 @@ def diff_trace(got: list, want: list, prob_tol=1e-9):
     return None
 
 
-def compare_run(got: dict, want: dict, prob_tol=1e-9, trace=True):
+def compare_run(got: dict, want: dict, prob_tol=1e-9, trace=True, kv_tol=1e-4):
     for key in ("tokens", "nfe", "branch_index", "block_size", "tokens_decoded",
                 "eos_position", "correct"):
         g, w = got[key], want[key]
@@ -56,5 +64,5 @@ def compare_run(got: dict, want: dict, prob_tol=1e-9, trace=True):
         if g != w:
             return f"{key}: got {g} want {w}"
     if trace:
-        return diff_trace(got["trace"], want["trace"], prob_tol)
+        return diff_trace(got["trace"], want["trace"], prob_tol, kv_tol)
     return None

@@ -17,6 +17,7 @@ REF = goldens.load("runs_ref.json")
 LLADA = goldens.load("runs_llada.json")
 KER = goldens.load("kernels.json")
 VANILLA = goldens.load("runs_vanilla.json")
+DIAG = goldens.load("runs_diag.json")
 
 _MODELS = {}
 
@@ -339,4 +340,23 @@ def test_vanilla_decode_matches_reference_runs(name):
         task = bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab)
         got = record(bb.vanilla_decode(params, task, bb.DecodeConfig(block_size=g["gen_len"], gen_len=g["gen_len"])))
         err = goldens.compare_run(got, want)
+        assert err is None, f"{name} seed {seed}: {err}"
+
+
+@pytest.mark.parametrize("name", list(DIAG))
+def test_kv_logging_matches_reference_runs(name):
+    """run_blockbatch with log_kv="norms" and log_consistency (scheduler.py:
+    268-281, 288-294, 332-347, 376-390) in fp32 verification mode: decisions,
+    tokens, NFE and every trace record bit-exact; the per-branch kv_delta /
+    E_before / E_after norms (device fp32 caches, fp64 reductions) within 1e-4
+    relative of the reference's float64 values (E_after = 0 after a refresh)."""
+    g = DIAG[name]
+    params = ref_model(g["model"])
+    c = g["config"]
+    cfg = cfg_from(c)
+    cfg.log_kv, cfg.log_consistency = c["log_kv"], c["log_consistency"]
+    for seed, want in zip(g["seeds"], g["runs"]):
+        task = bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab)
+        got = record(bb.run_blockbatch(params, task, cfg))
+        err = goldens.compare_run(got, want, prob_tol=1e-4, kv_tol=1e-4)
         assert err is None, f"{name} seed {seed}: {err}"
