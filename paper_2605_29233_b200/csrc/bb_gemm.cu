@@ -187,6 +187,7 @@ __device__ __forceinline__ SplitK sk_of(const GemmTcParams& p, int G) {
   SplitK sk;
   sk.KB = p.KB;
   sk.n_chunks = p.n_chunks;
+  sk.n_ntiles = p.n_ntiles;
   sk.BN = p.rows_alloc / p.n_chunks;
   sk.G = G;
   sk.T = (long long)p.n_ntiles * p.n_chunks * p.KB;
@@ -239,14 +240,14 @@ __device__ void l2pf_issue(const L2Pf& f, int c, int g_cur, int lane) {
       for (long long y = y0 + lane; y < yend; y += 32) {
         const long long tile = y / f.KB;
         const int kb = (int)(y - tile * f.KB);
-        l2_prefetch_tile(f.tm, kb * 64, (int)(tile / f.n_chunks) * 128);
+        l2_prefetch_tile(f.tm, kb * 64, (int)(tile % f.n_ntiles) * 128);
       }
     } else {
       // tiles cn, cn + G, ... with KB k-blocks each, first nkb of that sequence
       for (int j = lane; j < f.nkb; j += 32) {
         const long long t = cn + (long long)(j / f.KB) * f.G;
         if (t >= f.T) break;
-        l2_prefetch_tile(f.tm, (j % f.KB) * 64, (int)(t / f.n_chunks) * 128);
+        l2_prefetch_tile(f.tm, (j % f.KB) * 64, (int)(t % f.n_ntiles) * 128);
       }
     }
   }
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(192)
     UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
     Unit u;
     while (pre < C::STAGES && it.next(u)) {
-      const int ntile = u.tile / p.n_chunks;
+      const int ntile = u.tile % p.n_ntiles;
       for (int kb = u.kb0; kb < u.kb1 && pre < C::STAGES; ++kb, ++pre) {
         mbar_expect_tx_only(&full[pre], C::A_BYTES);
         tma_load_2d(sA + pre * C::A_BYTES, &tmA, &full[pre], kb * 64, ntile * 128, pol_w);
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(192)
       UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
       Unit u;
       while (it.next(u)) {
-        const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
+        const int ntile = u.tile % p.n_ntiles, chunk = u.tile / p.n_ntiles;
         // (row chunks are never fully padding: rows_alloc = round_up(rows, BN))
         for (int kb = u.kb0; kb < u.kb1; ++kb, ++issued) {
           if (issued < pre) {
@@ -410,7 +411,7 @@ __global__ void __launch_bounds__(192)
     UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
     Unit u;
     while (it.next(u)) {
-      const int ntile = u.tile / p.n_chunks, chunk = u.tile % p.n_chunks;
+      const int ntile = u.tile % p.n_ntiles, chunk = u.tile / p.n_ntiles;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int n = ntile * 128 + q * 32 + lane;
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(192)
       const int et = threadIdx.x - 64, q = warp & 3;
       const int S = p.split, rank = (int)cluster.block_rank();
       const int tile = blockIdx.x / S;
-      const int ntile = tile / p.n_chunks, chunk = tile % p.n_chunks;
+      const int ntile = tile % p.n_ntiles, chunk = tile / p.n_ntiles;
       const int rows_per = BN / S;
       const int r0 = rank * rows_per;
       const int c = q * 32 + lane;
@@ -561,6 +562,7 @@ L2Pf tc_gemm_l2pf(const TcGemm& next, const CUtensorMap* tm_dev, long long bytes
   f.G = next.grid;
   f.KB = p.KB;
   f.n_chunks = p.n_chunks;
+  f.n_ntiles = p.n_ntiles;
   f.mode = p.mode;
   const long long n_tiles = (long long)p.n_ntiles * p.n_chunks;
   f.T = p.mode == 0 ? n_tiles * p.KB : n_tiles;
@@ -652,6 +654,7 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
   g.sk.KB = p.KB;
   g.sk.G = g.grid;
   g.sk.n_chunks = p.n_chunks;
+  g.sk.n_ntiles = p.n_ntiles;
   g.sk.BN = BN;
   g.sk.ns_tab = nullptr;
   g.max_slots = 1;

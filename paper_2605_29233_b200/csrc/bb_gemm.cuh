@@ -7,7 +7,10 @@
 // full M=128 MMAs and every weight byte is read from HBM exactly once.
 //
 // Work is split stream-K over (tile, k-block): CTA c owns k-blocks
-// [c*T/G, (c+1)*T/G) of the flattened (tile-major) space and writes one fp32
+// [c*T/G, (c+1)*T/G) of the flattened (tile-major) space, tiles ordered
+// chunk-outer (tile = chunk * n_ntiles + ntile) so that with several row
+// chunks (full passes, batched sessions) CTAs c and c + G/n_chunks stream the
+// same weight tiles at the same time: one HBM read, the other hits L2 and writes one fp32
 // partial "plane" per tile piece.  The consumer kernel (post-QKV / post-O /
 // ...) sums the pieces of a tile in slot order, so the reduction is
 // deterministic and no fp32 atomics are used.
@@ -23,6 +26,7 @@ struct SplitK {
   int KB;        // k-blocks per tile
   int G;         // CTAs
   int n_chunks;  // row chunks per weight tile
+  int n_ntiles;  // 128-row weight tiles; flattened tile = chunk * n_ntiles + ntile (chunk-outer)
   int BN;        // rows per chunk
   const unsigned char* ns_tab;  // optional [n_tiles] precomputed piece counts
 };
@@ -33,7 +37,7 @@ __host__ __device__ inline int sk_owner(long long y, long long T, int G) {
 }
 __host__ __device__ inline int sk_nslots(const SplitK& s, int row, int n) {
   if (s.T == 0) return 1;
-  const long long tile = (long long)(n >> 7) * s.n_chunks + row / s.BN;
+  const long long tile = (long long)(row / s.BN) * s.n_ntiles + (n >> 7);
 #ifdef __CUDA_ARCH__
   if (s.ns_tab != nullptr) return s.ns_tab[tile];
 #endif
@@ -93,7 +97,7 @@ struct EpiArgs {
 struct L2Pf {
   const CUtensorMap* tm;  // next GEMM's weight tensor map (copy in global memory), nullptr = off
   long long T;            // flattened k-blocks (stream-K) or tiles (mode 1)
-  int G, KB, n_chunks, mode, nkb;
+  int G, KB, n_chunks, n_ntiles, mode, nkb;
 };
 
 struct GemmTcParams {

@@ -165,7 +165,7 @@ struct ColMap {
 };
 // stream-K piece count of (row, column c) for BN = 64 row chunks
 __device__ __forceinline__ int lsk_ns(const LskGemm& g, int row, int c) {
-  return g.sk.ns_tab[(c >> 7) * g.n_chunks + (row >> 6)];
+  return g.sk.ns_tab[(row >> 6) * g.n_ntiles + (c >> 7)];
 }
 
 // Each thread processes its rows in batches of RB: every load of the batch is
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(224 + LSK_POST_THREADS, 1) k_lsk(const __grid_
         LskUnits it(g, blockIdx.x);
         int tile, kb0, kb1, slot;
         while (live && it.next(tile, kb0, kb1, slot)) {
-          const int ntile = tile / g.n_chunks;
+          const int ntile = tile % g.n_ntiles;
           for (int kb = kb0; kb < kb1; ++kb) {
             if (issued == pre) {
               pdl_wait();
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(224 + LSK_POST_THREADS, 1) k_lsk(const __grid_
           LskUnits it(g, blockIdx.x);
           int tile, kb0, kb1, slot;
           while (it.next(tile, kb0, kb1, slot)) {
-            const int chunk = tile % g.n_chunks;
+            const int chunk = tile / g.n_ntiles;
             for (int kb = kb0; kb < kb1; ++kb) {
               mbar_wait(&empty[stage], phase ^ 1);
               mbar_expect_tx(&full[stage], C::B_BYTES);
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(224 + LSK_POST_THREADS, 1) k_lsk(const __grid_
         LskUnits it(g, blockIdx.x);
         int tile, kb0, kb1, slot;
         while (it.next(tile, kb0, kb1, slot)) {
-          const int ntile = tile / g.n_chunks, chunk = tile % g.n_chunks;
+          const int ntile = tile % g.n_ntiles, chunk = tile / g.n_ntiles;
           mbar_wait(&tfull[acc], aphase);
           tc_fence_after();
           const int n = ntile * 128 + q * 32 + lane;
