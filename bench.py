@@ -140,6 +140,36 @@ def step_bytes_flops(params, cfgd, rows_block, kv_positions):
     return byts, flops, layer_w * e
 
 
+def nfe_weighted_roofline(params, cfgd, rows_block, nfe_split, hbm_gbs, tflops, ms_per_nfe):
+    """Roofline time per NFE weighted by NFE kind: a block step
+    streams the weights once for its window rows; the prefill is one full pass
+    of L rows (+ the LM head over the window rows); a refresh recomputes every
+    non-done branch over all L rows (charged as one NFE; the minimum streams the
+    weights once for B*L rows).  t = max(bytes / HBM, FLOPs / dense bf16 peak)."""
+    d = params.dims
+    e = 2
+    L = cfgd["P"] + cfgd["G"]
+    B = len(cfgd["bs"])
+    layer_w = (d.qkv_out * d.d_model + d.d_model * d.n_heads * d.hd + 2 * d.d_ff * d.d_model
+               + d.d_model * d.d_ff)
+    head_w = params.vocab.n_out * d.d_model
+    kv_pos = 2 * d.layers * d.n_kv_heads * d.hd * e  # bytes of K+V per position
+
+    def t(byts, flops):
+        return max(byts / (hbm_gbs * 1e6), flops / (tflops * 1e9))
+
+    w = e * (d.layers * layer_w + head_w)
+    t_block = t(w + kv_pos * L * B, 2 * rows_block * (d.layers * layer_w + head_w) + 4 * rows_block * L * d.n_heads * d.hd * d.layers)
+    t_init = t(w + kv_pos * L, 2 * L * d.layers * layer_w + 2 * rows_block * head_w + 4 * L * L * d.n_heads * d.hd * d.layers)
+    t_ref = t(w + kv_pos * L * B, 2 * B * L * d.layers * layer_w + 2 * rows_block * head_w
+              + 4 * B * L * L * d.n_heads * d.hd * d.layers)
+    n = [float(x) for x in nfe_split]
+    t_avg = (n[0] * t_init + n[1] * t_block + n[2] * t_ref) / max(sum(n), 1e-9)
+    return {"t_roof_ms": {"init": t_init, "block": t_block, "refresh": t_ref}, "nfe_split": n,
+            "t_roof_per_nfe_ms": t_avg, "ms_per_nfe": ms_per_nfe, "frac": t_avg / ms_per_nfe,
+            "peaks": {"hbm_gbs": hbm_gbs, "bf16_tflops": tflops}}
+
+
 # ---------------------------------------------------------------- CPU baseline (oracle port)
 def cpu_baseline(cfgd, nfe_split, tokens_per_req, budget_s=30.0):
     """Time the oracle (NumPy fp32, all host threads) on a bounded sample of the
@@ -365,6 +395,7 @@ def main():
         peaks = json.load(open(pk))
     hbm = peaks.get("hbm_gbs", 6650.0)
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    tflops = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1350.0))  # dense bf16, long steps
     d = params.dims
     rows = sum(cfgd["bs"])
     kinds = {0: (d.qkv_out, d.d_model), 1: (d.d_model, d.n_heads * d.hd), 2: (2 * d.d_ff, d.d_model),
@@ -392,7 +423,8 @@ def main():
             "launches_timed": launches, "per_kind": per_kind,
             "head_gemm_GBps": (2.0 * params.vocab.n_out * d.d_model * head_l / head_ns) if head_ns else None,
             "step": {"bytes": step_b, "flops": step_f, "t_roof_ms": step_b / (hbm * 1e6),
-                     "ms_per_nfe": ms_per_nfe, "frac": (step_b / (hbm * 1e6)) / ms_per_nfe}}
+                     "ms_per_nfe": ms_per_nfe, "frac": (step_b / (hbm * 1e6)) / ms_per_nfe},
+            "step_nfe_weighted": nfe_weighted_roofline(params, cfgd, rows, nfe_mean, hbm, tflops, ms_per_nfe)}
     trf = os.path.join(HERE, "profiles", "gemm_traffic.json")
     if os.path.exists(trf):
         try:
