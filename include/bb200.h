@@ -74,7 +74,7 @@ typedef struct {
   int prompt_len, gen_len;
   float tau_conf, tau_merge, tau_sync;
   int refresh_interval, merge_enabled, sync_enabled;
-  int page_size;       /* KV page positions (<= 32, default 16)          */
+  int page_size;       /* KV page positions (power of two <= 32, def. 16) */
   int pages_per_item;  /* attention split (pages per work item, def. 4)  */
   int trace;           /* record trace events (TraceEvent, decoding.py:61-75) */
   int event_capacity;  /* events per request                              */

@@ -824,7 +824,9 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.merge_en = d->merge_enabled;
   S.sync_en = d->sync_enabled;
   S.ps = d->page_size > 0 ? d->page_size : 16;
-  if (S.ps > 32) return BB_ERR_CONFIG;
+  if (S.ps > 32 || (S.ps & (S.ps - 1)) != 0) return BB_ERR_CONFIG;  // power of two <= 32
+  S.ps_shift = 0;
+  while ((1 << S.ps_shift) < S.ps) ++S.ps_shift;
   S.n_pp = (S.P + S.ps - 1) / S.ps;
   S.n_gp = (S.G + S.ps - 1) / S.ps;
   S.n_lp = S.n_pp + S.n_gp;

@@ -433,6 +433,10 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   const long long kvstride = (long long)S.ps * HD;
   // ci: chunk index relative to c_begin; part 0 = all keys, 1 = all but the
   // window keys (before the splice), 2 = only the window keys (after it)
+  // element offset of key (page pg, row) for this kv head: kbase + pg * pstride
+  // + row * HD (page size a power of two: shift/mask, no division per key)
+  const long long kbase = (lay * D.nkv + kvh) * kvstride, pstride = (long long)D.nkv * kvstride;
+  const int ps_sh = S.ps_shift, ps_mask = S.ps - 1;
   auto load_chunk = [&](int ci, int buf, int part) {
     bf* dK = sKb + buf * KC * LD;
     bf* dV = sVb + buf * KC * LD;
@@ -443,8 +447,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       const bool ok = j < nk;
       const bool win = ok && (e.y & KEY_WIN) != 0;
       if ((part == 1 && win) || (part == 2 && !win)) continue;
-      const int pg = e.x / S.ps;
-      const long long off = ((lay + pg) * D.nkv + kvh) * kvstride + (long long)(e.x - pg * S.ps) * HD + v * 8;
+      const long long off = kbase + (long long)(e.x >> ps_sh) * pstride + (e.x & ps_mask) * HD + v * 8;
       cp_async16(dK + j * LD + v * 8, Kg + (ok ? off : 0), ok);
       cp_async16(dV + j * LD + v * 8, Vg + (ok ? off : 0), ok);
     }

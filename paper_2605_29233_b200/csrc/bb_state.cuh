@@ -61,6 +61,7 @@ struct Sess {
   float tau_conf, tau_merge, tau_sync;
   int refresh_interval, merge_en, sync_en;
   int ps, n_pp, n_gp, n_lp, pool;
+  int ps_shift;       // log2(ps) (page sizes are powers of two)
   int ch_block;       // logical pages per attention item in block passes
   int max_items;      // attention items per request per pass
   int ev_cap, trace, hard_cap, max_copies;

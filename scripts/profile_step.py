@@ -9,9 +9,10 @@ from paper_2605_29233_b200.scheduler import get_session
 
 HS, GAMMA = float(os.environ.get("BB_HS", 0.4)), float(os.environ.get("BB_GAMMA", 8.0))
 N_PROF = int(os.environ.get("BB_PROF_ITERS", 2))
-P, G = 64, 256
+_CFG = {"c2": (64, 256, (8, 16, 32)), "c5": (2048, 1024, (8, 16, 32, 64))}[os.environ.get("BB_TL_CFG", "c2")]
+P, G = _CFG[0], _CFG[1]
 vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
-cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=G)
+cfg = bb.SchedulerConfig(block_sizes=_CFG[2], gen_len=G)
 params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=HS, gamma=GAMMA, dtype="bf16", init="hash")
 task = bb.make_task(2, P, G, vocab)
 s = get_session(params, cfg, P, 1)
