@@ -238,17 +238,6 @@ __device__ __forceinline__ void lsk_norm(const LskCore& p, const LskGemm& g, int
   const int* slot_pos = P.slot_pos;
   bf16* xn = reinterpret_cast<bf16*>(P.xn) + c;
   const float inv_d = 1.0f / (float)d, eps = D.eps;
-  if (p.prof != nullptr && blockIdx.x == 0 && et == 0) {  // (diagnostic) in-situ load latency, cycles
-    long long c0, c1, c2;
-    float v, w;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0)::"memory");
-    asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(P.x + c + 3 * d) : "memory");
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1) : "f"(v) : "memory");
-    asm volatile("ld.global.f32 %0, [%1];" : "=f"(w) : "l"(p.part + c + 7 * d) : "memory");
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c2) : "f"(w) : "memory");
-    atomicAdd(&p.prof[40], (unsigned long long)(c1 - c0));
-    atomicAdd(&p.prof[41], (unsigned long long)(c2 - c1));
-  }
   for (int r0 = m.rg; r0 < rows; r0 += m.nrg * RB) {
     float4 xv[RB];
     float sp[RB];

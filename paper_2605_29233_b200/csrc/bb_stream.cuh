@@ -45,7 +45,7 @@ struct LskGemm {
 struct LskCore {
   LskGemm g[LSK_MAXG];
   int n_gemm;
-  int flags;  // bit 0 (BB_LSK_NOAHEAD, diagnostic): weight producer waits at phase boundaries
+  int flags;  // BB_LSK_FLAGS bit 0 (diagnostic): the weight producer waits at phase boundaries
   int rows;  // rows the consumer ops visit (block pass: R * NRq; the rest are padding)
   Dims D;
   Sess S;

@@ -80,7 +80,3 @@ if pr[63]:
         vals = [pr[8 * gi + k] / n / 1e3 for k in range(8)]
         if any(vals):
             print(f"lsk gemm {gi}: " + ", ".join(f"{e} {v:.2f}" for e, v in zip(ev, vals)))
-    print(f"in-situ load latency (CTA0 norm, cycles): x {pr[40] / n:.0f}, part {pr[41] / n:.0f}")
-    for gi in (0, 2):
-        if pr[44 + gi]:
-            print(f"gemm {gi} norm: 1st call ends {pr[44 + gi] / n / 1e3:.2f}, 2nd call ends {pr[48 + gi] / n / 1e3:.2f}, 2nd call thread-0 cycles {pr[52 + gi] / n:.0f}")
