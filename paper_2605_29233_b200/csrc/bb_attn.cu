@@ -407,17 +407,19 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   constexpr int VPR = HD / 8;
   const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
   const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
-  const int n_all = (n_keys + KC - 1) / KC;
-  const int c_begin = (int)((long long)n_all * crank / ATT_CS), c_end = (int)((long long)n_all * (crank + 1) / ATT_CS);
-  const int n_chunks = c_end - c_begin;
+  // keys split evenly over the cluster's CTAs (not in whole chunks: a rank with
+  // one more chunk than the others would hold up the cluster merge); a partial
+  // last chunk only runs the MMA tiles that hold keys
+  const int k_begin = (int)((long long)n_keys * crank / ATT_CS);
+  const int nk_cta = (int)((long long)n_keys * (crank + 1) / ATT_CS) - k_begin;
+  const int n_chunks = (nk_cta + KC - 1) / KC;
   // this CTA's keys -> registers now, smem after the phase-A loads are out
   // (keeps the two L2 round trips overlapped)
   constexpr int KREG = 4;
   int2 kr[KREG];
   const int nkc = n_chunks * KC;
   {
-    const int2* src = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + (long long)c_begin * KC;
-    const int nk_cta = min(nkc, n_keys - c_begin * KC);
+    const int2* src = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + k_begin;
 #pragma unroll
     for (int u = 0; u < KREG; ++u) {
       const int i = threadIdx.x + u * 128;
@@ -431,7 +433,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       if (threadIdx.x + u * 128 < nkc) sKeys[threadIdx.x + u * 128] = kr[u];
   };
   const long long kvstride = (long long)S.ps * HD;
-  // ci: chunk index relative to c_begin; part 0 = all keys, 1 = all but the
+  // ci: chunk index from this CTA's first key; part 0 = all keys, 1 = all but the
   // window keys (before the splice), 2 = only the window keys (after it)
   // element offset of key (page pg, row) for this kv head: kbase + pg * pstride
   // + row * HD (page size a power of two: shift/mask, no division per key)
@@ -440,7 +442,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   auto load_chunk = [&](int ci, int buf, int part) {
     bf* dK = sKb + buf * KC * LD;
     bf* dV = sVb + buf * KC * LD;
-    const int nk = min(KC, n_keys - (c_begin + ci) * KC);
+    const int nk = min(KC, nk_cta - ci * KC);
     for (int i = threadIdx.x; i < KC * VPR; i += blockDim.x) {
       const int j = i / VPR, v = i % VPR;
       const int2 e = sKeys[ci * KC + j];
@@ -617,7 +619,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
   const float sl2 = D.attn_scale * 1.4426950408889634f;
   for (int ci = 0; ci < n_chunks; ++ci) {
-    const int nk = min(KC, n_keys - (c_begin + ci) * KC);
+    const int nk = min(KC, nk_cta - ci * KC);
     if (ci + 1 < n_chunks) {
       load_chunk(ci + 1, (ci + 1) & 1, 0);
       cp_async_wait<1>();
@@ -634,6 +636,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
 #pragma unroll
       for (int nt = 0; nt < KC / 8; ++nt) {
         s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
+        if (8 * nt >= nk) continue;  // no keys in this tile (masked to -inf below)
         const bf* k0p = sK + (8 * nt + g) * LD + 2 * t;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
@@ -686,6 +689,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       }
 #pragma unroll
       for (int kk = 0; kk < KC / 16; ++kk) {
+        if (16 * kk >= nk) continue;  // P == 0 for the keys past the chunk's end
         // P = hi + lo (two bf16 parts): P.V to ~fp32 accuracy (the spike
         // epilogue amplifies attention error ~34x)
         uint32_t a[4], al[4];
