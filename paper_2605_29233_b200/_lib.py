@@ -11,7 +11,7 @@ import os
 from .errors import ConfigError, ContractError, RunawayError, StateError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbb200.so")
+LIB_PATH = os.environ.get("BB_LIB_PATH") or os.path.join(_HERE, "libbb200.so")  # (override: A/B builds)
 
 BB_OK = 0
 BB_ERR_CONFIG, BB_ERR_CONTRACT, BB_ERR_STATE, BB_ERR_RUNAWAY = -1, -2, -3, -4
