@@ -344,11 +344,20 @@ static int setup_gemms(Session* s) {
       const char* wd = D.dff ? (const char*)W.wd + (size_t)l * D.d * D.dff * e : nullptr;
       if (D.dtype == BB_DTYPE_BF16) {
         const int gm = s->fuse_epi ? 3 : 0;
-        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
-        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
+        // stream-K grid per GEMM kind (0 = all SMs); BB_GRID_{QKV,O,GU,DN} override for the block pass
+        auto grid_of = [&](const char* name) {
+          const char* e = which == 0 ? getenv(name) : nullptr;
+          return e != nullptr ? atoi(e) : 0;
+        };
+        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_QKV")))
+          return BB_ERR_CONFIG;
+        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_O")))
+          return BB_ERR_CONFIG;
         if (D.dff) {
-          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
-          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, gm, 0)) return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_GU")))
+            return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_DN")))
+            return BB_ERR_CONFIG;
         }
         TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
