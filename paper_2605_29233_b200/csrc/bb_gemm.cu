@@ -16,6 +16,10 @@
 
 #include "bb_gemm.cuh"
 
+#ifndef HEAD_T
+#define HEAD_T 1  // transposed LM-head epilogue (0: per-row shuffle reductions)
+#endif
+
 namespace bb {
 
 struct Unit {
@@ -79,7 +83,8 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGES = BN >= 192 ? 4 : (BN >= 128 ? 5 : 8);
   static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr size_t RED = (size_t)3 * 4 * BN * 4;                 // LM-head epilogue
+  // LM-head epilogue: per-warp (max, argmax, sum) rows + a 32x33 transpose tile per warp
+  static constexpr size_t RED = ((size_t)3 * 4 * BN + 4 * 32 * 33) * 4;
   static constexpr size_t STG = (size_t)(32 * 129 + 4 * 32 + 32 + 64 + 16) * 4;  // staging + row sums + row meta
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16 +
                                  (RED > STG ? RED : STG);
@@ -220,6 +225,47 @@ __device__ __forceinline__ void head_rows(const GemmTcParams& p, float (&v)[32],
       red[(2 * 4 + q) * BN + j0 + j] = s;
     }
   }
+}
+
+// Same statistics, transposed: the warp stages its 32 columns x 32 rows in
+// shared memory and lane r reduces row r over the 32 columns sequentially (no
+// per-row shuffle trees); ties keep the lowest column as in warp_argmax.  The
+// spike and the target boost are applied by the row's lane.
+template <int BN>
+__device__ __forceinline__ void head_rows_t(const GemmTcParams& p, const float (&v)[32], int n0w, int q, int lane,
+                                            int row0, int j0, float* red, float* st) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) st[j * 33 + lane] = v[j];
+  __syncwarp();
+  const int row = row0 + j0 + lane;
+  float m = -INFINITY, s = 0.0f;
+  int a = n0w;
+  if (row < p.rows_alloc) {
+    const float hs = p.head_scale, sc = p.spike_cut, sg = p.spike_gain;
+    const int tg = __ldg(&p.tgt[row]);
+    const float bo = __ldg(&p.boost[row]);
+    const int nc = min(32, p.n_out - n0w);
+    float l[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const float raw = st[lane * 33 + c] * hs;
+      float x = raw + sg * fmaxf(0.0f, raw - sc);
+      if (n0w + c == tg) x += bo;
+      l[c] = c < nc ? x : -INFINITY;
+      if (l[c] > m) {
+        m = l[c];
+        a = n0w + c;
+      }
+    }
+    if (m != -INFINITY) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) s += (l[c] == -INFINITY) ? 0.0f : expf(l[c] - m);
+    }
+  }
+  red[(0 * 4 + q) * BN + j0 + lane] = m;
+  red[(1 * 4 + q) * BN + j0 + lane] = __int_as_float(a);
+  red[(2 * 4 + q) * BN + j0 + lane] = s;
+  __syncwarp();
 }
 
 __device__ __forceinline__ void l2_prefetch_tile(const CUtensorMap* tm, int x, int y) {
@@ -446,7 +492,11 @@ __global__ void __launch_bounds__(192)
         for (int j0 = 0; j0 < BN; j0 += 32) {
           float v[32];
           tmem_ld32(taddr + j0, v);
+#if HEAD_T
+          head_rows_t<BN>(p, v, ntile * 128 + q * 32, q, lane, row0, j0, red, red + 12 * BN + q * 32 * 33);
+#else
           head_rows<BN>(p, v, n, q, lane, row0, j0, red);
+#endif
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
