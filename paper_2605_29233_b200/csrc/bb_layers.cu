@@ -13,6 +13,10 @@
 #include "bb_launch.cuh"
 #include "bb_layers.cuh"
 
+#ifndef POST_RES_BATCH
+#define POST_RES_BATCH 1  // residual: all plane loads of a thread issued before use
+#endif
+
 namespace bb {
 
 __device__ __forceinline__ float block_sum(float v, float* sh) {
@@ -153,6 +157,73 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
   float* x = P.x + (long long)row * D.d;
   T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
   float ss = 0.0f;
+#if POST_RES_BATCH
+  // d <= 4096: each thread owns <= 2 column groups; all their loads (x and up
+  // to 8 partial planes each) are issued before any is used
+  constexpr int NG = 2, NSU = 8;
+  if (D.d <= NG * 4 * (int)blockDim.x) {
+    float4 xv[NG], w[NG][NSU];
+    int ns[NG], cc[NG];
+#pragma unroll
+    for (int u = 0; u < NG; ++u) {
+      cc[u] = (threadIdx.x + u * blockDim.x) * 4;
+      ns[u] = 0;
+      if (cc[u] < D.d) {
+        ns[u] = sk_nslots(pr.sk, row, cc[u]);
+        const float* pp = pr.part + (long long)row * pr.ldp + cc[u];
+        xv[u] = *reinterpret_cast<const float4*>(x + cc[u]);
+#pragma unroll
+        for (int k = 0; k < NSU; ++k)
+          if (k < ns[u]) w[u][k] = *reinterpret_cast<const float4*>(pp + (long long)k * pr.plane);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NG; ++u) {
+      if (cc[u] >= D.d) continue;
+      float4 acc = w[u][0];
+#pragma unroll
+      for (int k = 1; k < NSU; ++k)
+        if (k < ns[u]) {
+          acc.x += w[u][k].x;
+          acc.y += w[u][k].y;
+          acc.z += w[u][k].z;
+          acc.w += w[u][k].w;
+        }
+      const float* pp = pr.part + (long long)row * pr.ldp + cc[u];
+      for (int k = NSU; k < ns[u]; ++k) {
+        const float4 t = *reinterpret_cast<const float4*>(pp + (long long)k * pr.plane);
+        acc.x += t.x;
+        acc.y += t.y;
+        acc.z += t.z;
+        acc.w += t.w;
+      }
+      float4 v = xv[u];
+      v.x += acc.x;
+      v.y += acc.y;
+      v.z += acc.z;
+      v.w += acc.w;
+      *reinterpret_cast<float4*>(x + cc[u]) = v;
+      xv[u] = v;
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    float inv = 1.0f;
+    if (ln != nullptr) inv = 1.0f / sqrtf(block_sum(ss, sh) / (float)D.d + D.eps);
+#pragma unroll
+    for (int u = 0; u < NG; ++u) {
+      if (cc[u] >= D.d) continue;
+      float4 v = xv[u];
+      if (ln != nullptr) {
+        const float4 g = *reinterpret_cast<const float4*>(ln + cc[u]);
+        v.x *= inv * g.x;
+        v.y *= inv * g.y;
+        v.z *= inv * g.z;
+        v.w *= inv * g.w;
+      }
+      Vec4<T>::st(xn + cc[u], v);
+    }
+    return;
+  }
+#endif
   for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
     float4 v = *reinterpret_cast<float4*>(x + c);
     const int ns = sk_nslots(pr.sk, row, c);
