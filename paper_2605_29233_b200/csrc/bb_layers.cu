@@ -118,8 +118,39 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
   const int pos = P.slot_pos[row];
   if (pos < 0) return;
   const int c0 = hh * D.hd + i, c1 = c0 + half;
-  float a = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c0);
-  float b = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c1);
+  float a, b;
+#if POST_RES_BATCH
+  if (D.hd <= 128) {
+    // both halves' partial planes loaded before the adds (slot order kept);
+    // c0 and c1 lie in one 128-column tile, so they share the piece count
+    constexpr int NSU = 4;
+    const int ns = sk_nslots(pr.sk, row, c0);
+    const float* pa = pr.part + (long long)row * pr.ldp + c0;
+    float wa[NSU], wb[NSU];
+#pragma unroll
+    for (int k = 0; k < NSU; ++k)
+      if (k < ns) {
+        wa[k] = pa[(long long)k * pr.plane];
+        wb[k] = pa[(long long)k * pr.plane + half];
+      }
+    a = wa[0];
+    b = wb[0];
+#pragma unroll
+    for (int k = 1; k < NSU; ++k)
+      if (k < ns) {
+        a += wa[k];
+        b += wb[k];
+      }
+    for (int k = NSU; k < ns; ++k) {
+      a += pa[(long long)k * pr.plane];
+      b += pa[(long long)k * pr.plane + half];
+    }
+  } else
+#endif
+  {
+    a = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c0);
+    b = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c1);
+  }
   if (bias != nullptr) {
     a += bias[c0];
     b += bias[c1];
@@ -305,8 +336,27 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
   const int cg = ((f >> 6) << 7) + (f & 63);  // 4 gate features in one 64-block; up at +64
   const int ns = sk_nslots(pr.sk, row, cg);
   const float* pp = pr.part + (long long)row * pr.ldp + cg;
+#if POST_RES_BATCH
+  constexpr int NSU = 4;
+  float4 wg[NSU], wu[NSU];
+#pragma unroll
+  for (int i = 0; i < NSU; ++i)
+    if (i < ns) {
+      wg[i] = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane);
+      wu[i] = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane + 64);
+    }
+  float4 g = wg[0], u = wu[0];
+#pragma unroll
+  for (int i = 1; i < NSU; ++i)
+    if (i < ns) {
+      g.x += wg[i].x; g.y += wg[i].y; g.z += wg[i].z; g.w += wg[i].w;
+      u.x += wu[i].x; u.y += wu[i].y; u.z += wu[i].z; u.w += wu[i].w;
+    }
+  for (int i = NSU; i < ns; ++i) {
+#else
   float4 g = *reinterpret_cast<const float4*>(pp), u = *reinterpret_cast<const float4*>(pp + 64);
   for (int i = 1; i < ns; ++i) {
+#endif
     const float4 g2 = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane);
     const float4 u2 = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane + 64);
     g.x += g2.x; g.y += g2.y; g.z += g2.z; g.w += g2.w;
