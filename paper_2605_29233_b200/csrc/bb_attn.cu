@@ -325,6 +325,15 @@ __device__ __forceinline__ void phase_mark(unsigned long long* ph, int i, unsign
   if (ph != nullptr && threadIdx.x == 0) atomicAdd(&ph[i], globaltimer_ns() - t0);
 }
 
+#ifndef ATT_MERGE_H
+#define ATT_MERGE_H 1  // fp16 o/l exchange in the cluster merge
+#endif
+#ifndef ATT_MERGE_PUSH
+#define ATT_MERGE_PUSH 1  // bulk-copy push merge (needs ATT_MERGE_H)
+#endif
+#if ATT_MERGE_PUSH && !ATT_MERGE_H
+#error ATT_MERGE_PUSH needs ATT_MERGE_H
+#endif
 #ifndef ATT_KC
 #define ATT_KC 64  // keys per chunk (32 measured slower: 21.6 vs 19.5 us per layer at C2)
 #endif
@@ -365,6 +374,14 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   __shared__ long long sKvo[QR];
   __shared__ int s_nk, s_gen0;
   __shared__ int sNS[FQ ? 3 * (QR / ATT_CS) : 1];  // FQ: partial planes per (q|k|v, row)
+#if ATT_MERGE_PUSH
+  __shared__ __align__(8) uint64_t s_mbar;  // merge: all ranks' blocks received
+  if (threadIdx.x == 0) {
+    mbar_init(&s_mbar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&s_mbar, (uint32_t)(QR * (HD + 8) * 2));
+  }
+#endif
 
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -712,12 +729,60 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       }
     }
     __syncthreads();
+#if ATT_MERGE_PUSH
+    // start barrier, arrive after the first chunk (wait before the push): every
+    // rank's mbarrier is initialised (fence.mbarrier_init released it) and its
+    // q fragments were consumed, so sQ can receive merge blocks.  Relaxed: a
+    // release here would wait for the next chunk's cp.async in flight
+    if (ci == 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#endif
   }
+#if ATT_MERGE_PUSH
+  if (n_chunks == 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#endif
   phase_mark(ph, 6, t0);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+#if ATT_MERGE_H
+  // partial state -> own smem (reuses the K buffers): o/l as fp16 [QR][HD+8]
+  // (the exchanged bytes halve; the attention output is rounded to bf16, 8x
+  // coarser than these fp16 partials) and (m, l) as float2 [QR]
+  constexpr int OLD = HD + 8;  // (m, l) ride in the row padding
+  __half* sO = reinterpret_cast<__half*>(sKb);
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int lr = warp * 16 + g + 8 * half;
+    const float lsum = half ? l1 : l0;
+    const float il = lsum > 0.0f ? 1.0f / lsum : 0.0f;
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt)
+      *reinterpret_cast<__half2*>(sO + lr * OLD + 8 * nt + 2 * t) =
+          __floats2half2_rn(o[nt][2 * half] * il, o[nt][2 * half + 1] * il);
+    if (t == 0) *reinterpret_cast<float2*>(sO + lr * OLD + HD) = make_float2(half ? m1 : m0, lsum);
+  }
+#if ATT_MERGE_PUSH
+  // push: rank q's rows [r*RPC, (r+1)*RPC) -> rank r's receive buffer (the dead
+  // sQ: q lives in registers since the start barrier) block q, one bulk DSMEM
+  // copy each, completion counted on rank r's mbarrier; no cluster barrier
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (threadIdx.x < ATT_CS) {
+    constexpr uint32_t BLK = (QR / ATT_CS) * OLD * 2;
+    const uint32_t dst = mapa_u32(smem_u32(sQ) + crank * BLK, threadIdx.x);
+    const uint32_t bar = mapa_u32(smem_u32(&s_mbar), threadIdx.x);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t"
+        "cp.async.bulk.commit_group;" ::"r"(dst),
+        "r"(smem_u32(sO) + threadIdx.x * BLK), "r"(BLK), "r"(bar)
+        : "memory");
+  }
+  if (!FQ) phase_mark(ph, 2, t0);  // (timeline) start barrier / copies issued
+  mbar_wait(&s_mbar, 0);
+#endif
+#else
   // partial state -> own smem (reuses the K buffers): o [QR][HD+4], m, l [QR]
   constexpr int OLD = HD + 4;
   float* sO = reinterpret_cast<float*>(sKb);
@@ -734,7 +799,11 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       sL[lr] = half ? l1 : l0;
     }
   }
+#endif
+#if !ATT_MERGE_PUSH
   cluster.sync();
+  if (!FQ) phase_mark(ph, 2, t0);  // (timeline) merge barrier passed
+#endif
   // merge: this CTA normalises rows [crank*QR/CS, (crank+1)*QR/CS) across the
   // cluster; every rank's (m, l, o) is gathered into registers first
   constexpr int RPC = QR / ATT_CS;
@@ -748,10 +817,29 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     const int lr = crank * RPC + (i < RPC * V4 ? i / V4 : 0), c4 = (i % V4) * 4;
 #pragma unroll
     for (int q = 0; q < ATT_CS; ++q) {
+#if ATT_MERGE_H
+#if ATT_MERGE_PUSH
+      const __half* row = reinterpret_cast<const __half*>(sQ) + (q * RPC + lr - crank * RPC) * OLD;  // block q
+#else
+      const __half* row = cluster.map_shared_rank(sO + lr * OLD, q);
+#endif
+      const float2 ml = *reinterpret_cast<const float2*>(row + HD);
+      mr[k][q] = ml.x;
+      lv[k][q] = ml.y;
+      const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+      ov[k][q] = make_float4(a.x, a.y, b.x, b.y);  // o / l of rank q
+#else
       mr[k][q] = *cluster.map_shared_rank(sM + lr, q);
       lv[k][q] = *cluster.map_shared_rank(sL + lr, q);
       ov[k][q] = *reinterpret_cast<const float4*>(cluster.map_shared_rank(sO + lr * OLD + c4, q));
+#endif
     }
+  }
+  if (!FQ && ph != nullptr) {  // (timeline) gather landed: consume one loaded value
+    if (mr[0][0] == 12345.0f) __trap();
+    phase_mark(ph, 3, t0);
   }
 #pragma unroll
   for (int k = 0; k < NMI; ++k) {
@@ -768,8 +856,13 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
 #pragma unroll
     for (int q = 0; q < ATT_CS; ++q) {
       if (mr[k][q] == -INFINITY) continue;
+#if ATT_MERGE_H
+      const float w = exp2f(mr[k][q] - M) * lv[k][q];  // ov holds o / l
+      Lsum += w;
+#else
       const float w = exp2f(mr[k][q] - M);
       Lsum += w * lv[k][q];
+#endif
       acc.x += w * ov[k][q].x;
       acc.y += w * ov[k][q].y;
       acc.z += w * ov[k][q].z;
@@ -783,7 +876,13 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     u.y = *reinterpret_cast<uint32_t*>(&p1);
     *reinterpret_cast<uint2*>(out) = u;
   }
+  if (!FQ) phase_mark(ph, 4, t0);  // (timeline) outputs stored
+#if ATT_MERGE_PUSH
+  // the outgoing copies must have read this CTA's staging before it exits
+  if (threadIdx.x < ATT_CS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#else
   cluster.sync();
+#endif
   phase_mark(ph, 7, t0);
   tstat_end(ats);
 }

@@ -65,8 +65,8 @@ from paper_2605_29233_b200 import _lib
 ph = (C.c_ulonglong * 8)()
 _lib.lib().bb_session_phase_stats(s.h, ph, 0, C.c_void_p(s.stream.cuda_stream))
 if ph[0]:
-    names_ph = ["rows+keys loaded", "phase-A loads issued", "splice stored", "cluster barrier",
-                "chunk0 landed", "chunk loop done", "end"]
+    names_ph = ["rows+keys loaded", "FQ: phase-A loads / merge copies issued", "FQ: splice / merge blocks received",
+                "FQ: cluster barrier / outputs stored", "chunk0 landed", "chunk loop done", "end"]
     print("attention phase offsets (avg us from PDL release): " +
           ", ".join(f"{n} {ph[i + 1] / ph[0] / 1e3:.2f}" for i, n in enumerate(names_ph)))
 
