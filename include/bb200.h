@@ -150,7 +150,11 @@ BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int r
 /* Timeline sessions (BB_KLOG=1): phase offsets of the fused-QKV block
  * attention, out[8] = (CTAs, then summed ns from the PDL release to: rows and
  * keys loaded, phase-A loads issued, splice stored, cluster barrier passed,
- * chunk 0 landed, chunk loop done, end).  Averages = out[i] / out[0]. */
+ * chunk 0 landed, chunk loop done, end).  Averages = out[i] / out[0].
+ * out[8..15]: one GEMM kind's phases (env BB_GPH_KIND = 8*full + kind, kind 0-3
+ * = QKV, O, gate/up, down; default 1): (CTAs, summed ns resident before the
+ * dependency wait, then from it to: first stage landed, last MMA issued, first
+ * tile stored, end).  out must hold 16 values. */
 BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset, void* stream);
 /* layer-stream kernel phase profile (BB_KLOG=1 sessions), out[64]: CTA 0's
    summed ns from release to each phase event, [63] = launches */

@@ -33,6 +33,13 @@ struct PassGemms {
   int BN = 64;
 };
 
+// per-launch GEMM timing (%globaltimer, bb_session_gemm_stats); BB_LIVE_STATS=0
+// at session creation leaves it out of the captured kernels
+static bool live_stats() {
+  const char* e = getenv("BB_LIVE_STATS");
+  return !(e && e[0] == '0');
+}
+
 struct Session {
   Model* M;
   bb_session_desc desc;
@@ -52,6 +59,8 @@ struct Session {
   long long nodes_iter = 0, nodes_iter_ref = 0, nodes_prefill = 0, nodes_vanilla = 0;
   long long kernel_launches = 0, graph_launches = 0;
   unsigned long long* tstat = nullptr;  // [16][8] per-GEMM-kind live timing
+  unsigned long long* tsite = nullptr;  // [which 2][kind 5][layer] {min start, max end} (GEMM launch sites)
+  bool tsite_on = false;
   int* tile_cnt = nullptr;              // fused-epilogue arrival counters (self-resetting)
   unsigned char* ns_tabs = nullptr;     // per-GEMM-shape stream-K piece counts
   size_t ns_used = 0, ns_cap = 0;
@@ -251,6 +260,8 @@ static void plan(Session* s, char* base, bool dry) {
   s->tmap_cap = 8LL * D.layers + 1;
   s->tmaps = c.take<CUtensorMap>((size_t)s->tmap_cap, 128);
   s->tstat = c.take<unsigned long long>(16 * 8);
+  s->tsite = c.take<unsigned long long>((size_t)2 * 10 * D.layers);
+  s->tsite_on = live_stats();
   s->blk.atstat = s->tstat + 5 * 8;   // slots 5/6: block-pass attention (duration, start spread)
   s->full.atstat = s->tstat + 13 * 8; // slots 13/14: full-pass attention
   s->tile_cnt = c.take<int>(8192);
@@ -395,9 +406,13 @@ static int setup_gemms(Session* s) {
           E.d = D.d;
           E.ss_part = which == 0 ? s->ss_blk : s->ss_full;
           E.ss_ld = s->ss_ld;
-          all[g]->p.tstat = s->tstat + (size_t)(which * 8 + g) * 8;
+          all[g]->p.tstat = s->tsite_on ? s->tsite + 2 * ((size_t)(which * 5 + g) * D.layers + l) : nullptr;
           all[g]->p.klog = s->D.klog;
           all[g]->p.klog_cap = s->D.klog_cap;
+          {
+            const char* e = getenv("BB_GPH_KIND");  // GEMM phase profile: which*8 + kind
+            all[g]->p.ph = (s->D.klog != nullptr && which * 8 + g == (e ? atoi(e) : 1)) ? s->tstat + 15 * 8 : nullptr;
+          }
           all[g]->p.klog_id = 100 + which * 8 + g;
           if (!s->fuse_epi && attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
           all[g]->p.part = s->part;
@@ -429,7 +444,7 @@ static int setup_gemms(Session* s) {
     p.spike_cut = D.spike_cut;
     p.spike_gain = D.spike_gain;
     p.skip = s->H.skip;
-    p.tstat = s->tstat + (size_t)4 * 8;
+    p.tstat = s->tsite_on ? s->tsite + 2 * ((size_t)4 * D.layers) : nullptr;
     p.klog = s->D.klog;
     p.klog_cap = s->D.klog_cap;
     p.klog_id = 104;
@@ -549,6 +564,29 @@ static PartRef pref_simt(const SimtGemm& g) {
 }
 
 // ------------------------------------------------------------------ forward pass
+// GEMM launch sites -> per-kind (sum of max end - min start, launches) in
+// tstat[kind] (block 0-3, full 8-11, head 4); sites reset for the next pass
+__global__ void k_tsite_fold(unsigned long long* site, int n_layers, unsigned long long* tstat) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 10 * n_layers) return;
+  unsigned long long* t = site + 2 * (size_t)i;
+  const unsigned long long t0 = t[0], t1 = t[1];
+  if (t0 == ~0ull || t1 == 0ull) return;
+  const int sk = i / n_layers, which = sk / 5, kind = sk % 5;
+  unsigned long long* dst = tstat + 8 * (kind == 4 ? 4 : which * 8 + kind);
+  atomicAdd(&dst[3], t1 > t0 ? t1 - t0 : 0ull);
+  atomicAdd(&dst[4], 1ull);
+  t[0] = ~0ull;
+  t[1] = 0ull;
+}
+
+static cudaError_t tsite_fold(Session* s, cudaStream_t st) {
+  if (!s->tsite_on) return cudaSuccess;
+  const int n = 10 * s->D.layers;
+  k_tsite_fold<<<(n + 127) / 128, 128, 0, st>>>(s->tsite, s->D.layers, s->tstat);
+  return cudaGetLastError();
+}
+
 static cudaError_t run_gemm(Session* s, const TcGemm& tg, const SimtGemm& sg, PartRef* pr, cudaStream_t st) {
   if (s->D.dtype == BB_DTYPE_BF16) {
     *pr = pref_tc(tg, s->part);
@@ -611,7 +649,7 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
       if ((e = launch_post_residual(D, P, pr, next_ln, st)) != cudaSuccess) return e;
     }
   }
-  return cudaSuccess;
+  return tsite_fold(s, st);
 }
 
 static cudaError_t head(Session* s, cudaStream_t st) {
@@ -619,6 +657,7 @@ static cudaError_t head(Session* s, cudaStream_t st) {
   cudaError_t e;
   if (D.dtype == BB_DTYPE_BF16) {
     if ((e = tc_gemm_launch(s->head_tc, st)) != cudaSuccess) return e;
+    if ((e = tsite_fold(s, st)) != cudaSuccess) return e;
   } else {
     if ((e = simt_gemm_launch(s->head_simt, st)) != cudaSuccess) return e;
     if ((e = launch_head_tiles_f32(D, s->blk, s->H, st)) != cudaSuccess) return e;
@@ -925,6 +964,9 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
     std::vector<unsigned long long> ts(16 * 8, 0ull);
     for (int k = 0; k < 16; ++k) ts[k * 8] = ~0ull;
     cudaMemcpy(s->tstat, ts.data(), ts.size() * 8, cudaMemcpyHostToDevice);
+    std::vector<unsigned long long> site((size_t)2 * 10 * s->D.layers, 0ull);
+    for (size_t i = 0; i < site.size(); i += 2) site[i] = ~0ull;
+    cudaMemcpy(s->tsite, site.data(), site.size() * 8, cudaMemcpyHostToDevice);
   }
   if (cudaMallocHost(&s->host_ctrl, 4 * (size_t)s->S.R * C_WORDS * 4) != cudaSuccess) {
     delete s;
@@ -1178,14 +1220,17 @@ BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int r
 // timeline sessions (BB_KLOG=1): fused-QKV block attention phase offsets,
 // out[8] = (CTAs, sum ns to: rows/keys loaded, phase-A loads issued, splice
 // stored, cluster barrier, q gathered + chunk 0 landed, chunk loop done, end)
+// out[8..15]: the BB_GPH_KIND GEMM's phase sums (GemmTcParams::ph)
 BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset, void* stream) {
   Session* s = (Session*)sess;
   if (!s || !out) return BB_ERR_CONTRACT;
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemcpyAsync(out, s->tstat + 7 * 8, 8 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out + 8, s->tstat + 15 * 8, 8 * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (reset) {
     CK(cudaMemsetAsync(s->tstat + 7 * 8, 0, 8 * 8, st));
+    CK(cudaMemsetAsync(s->tstat + 15 * 8, 0, 8 * 8, st));
     CK(cudaStreamSynchronize(st));
   }
   return BB_OK;

@@ -334,6 +334,9 @@ __device__ __forceinline__ void phase_mark(unsigned long long* ph, int i, unsign
 #if ATT_MERGE_PUSH && !ATT_MERGE_H
 #error ATT_MERGE_PUSH needs ATT_MERGE_H
 #endif
+#ifndef ATT_MMA_ILP
+#define ATT_MMA_ILP 1  // independent back-to-back MMAs in the chunk loop
+#endif
 #ifndef ATT_KC
 #define ATT_KC 64  // keys per chunk (32 measured slower: 21.6 vs 19.5 us per layer at C2)
 #endif
@@ -651,8 +654,23 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       const int2* kmask = sKeys + ci * KC;
       float s[KC / 8][4];
 #pragma unroll
+      for (int nt = 0; nt < KC / 8; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
+#if ATT_MMA_ILP
+      // kk outer: consecutive MMAs accumulate into different key tiles (no
+      // back-to-back dependency); per tile the kk order is unchanged
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+#pragma unroll
+        for (int nt = 0; nt < KC / 8; ++nt) {
+          if (8 * nt >= nk) continue;  // no keys in this tile (masked to -inf below)
+          const bf* k0p = sK + (8 * nt + g) * LD + 2 * t + 16 * kk;
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(k0p);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(k0p + 8);
+          mma16816(s[nt], qf[kk], b0, b1);
+        }
+#else
+#pragma unroll
       for (int nt = 0; nt < KC / 8; ++nt) {
-        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
         if (8 * nt >= nk) continue;  // no keys in this tile (masked to -inf below)
         const bf* k0p = sK + (8 * nt + g) * LD + 2 * t;
 #pragma unroll
@@ -662,6 +680,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
           mma16816(s[nt], qf[kk], b0, b1);
         }
       }
+#endif
       float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
       for (int nt = 0; nt < KC / 8; ++nt) {
@@ -716,6 +735,20 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
         split_bf2(s[2 * kk + 1][2], s[2 * kk + 1][3], a[3], al[3]);
         const int mi = lane >> 3, rr = lane & 7;
         const int key = 16 * kk + (mi & 1) * 8 + rr;
+#if ATT_MMA_ILP
+        // all hi products, then all lo products (V fragments re-read): no
+        // back-to-back MMAs on one accumulator; per accumulator hi-then-lo as before
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+          for (int nt2 = 0; nt2 < HD / 8; nt2 += 2) {
+            const int dim = 8 * nt2 + (mi >> 1) * 8;
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(b0, b1, b2, b3, sV_u + (uint32_t)((key * LD + dim) * 2));
+            mma16816(o[nt2], pass ? al : a, b0, b1);
+            mma16816(o[nt2 + 1], pass ? al : a, b2, b3);
+          }
+#else
 #pragma unroll
         for (int nt2 = 0; nt2 < HD / 8; nt2 += 2) {
           const int dim = 8 * nt2 + (mi >> 1) * 8;
@@ -726,6 +759,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
           mma16816(o[nt2], al, b0, b1);
           mma16816(o[nt2 + 1], al, b2, b3);
         }
+#endif
       }
     }
     __syncthreads();

@@ -194,6 +194,16 @@ __device__ __forceinline__ void tstat_end(unsigned long long* ts) {
   }
 }
 
+// Per-launch-site GEMM timing without a completion protocol: every CTA only
+// issues fire-and-forget reductions of its start / end into the site's
+// {min start, max end}; a fold kernel after each pass turns sites into sums.
+__device__ __forceinline__ void tsite_begin(unsigned long long* ts) {
+  if (ts != nullptr && threadIdx.x == 0) atomicMin(&ts[0], globaltimer_ns());
+}
+__device__ __forceinline__ void tsite_end(unsigned long long* ts) {
+  if (ts != nullptr && threadIdx.x == 0) atomicMax(&ts[1], globaltimer_ns());
+}
+
 // Kernel timeline: CTA 0 stamps (id, %globaltimer) right after its PDL wait,
 // i.e. when its predecessor completed; consecutive stamps give each kernel's
 // slot in the real (graph, PDL) timeline including launch gaps.

@@ -299,6 +299,9 @@ __device__ void l2pf_issue(const L2Pf& f, int c, int g_cur, int lane) {
   }
 }
 
+#ifndef BB_GEMM_PH
+#define BB_GEMM_PH 0  // 1: timeline-session phase marks (GemmTcParams::ph); costs ~1% when built in
+#endif
 template <int BN>
 __global__ void __launch_bounds__(192)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -320,7 +323,10 @@ __global__ void __launch_bounds__(192)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = p.n_ntiles * p.n_chunks;
-  __shared__ int s_pre;  // stages whose weight tile was issued before the dependency wait
+  __shared__ int s_pre;
+#if BB_GEMM_PH
+  const unsigned long long t_in = p.ph != nullptr ? globaltimer_ns() : 0ull;
+#endif  // stages whose weight tile was issued before the dependency wait
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -361,7 +367,15 @@ __global__ void __launch_bounds__(192)
   }
   pdl_wait();
   klog_mark(p.klog, p.klog_cap, p.klog_id);
-  tstat_begin(p.tstat);
+  tsite_begin(p.tstat);
+  auto gph = [&](int i) {  // (timeline) ns since this CTA's entry
+#if BB_GEMM_PH
+    if (p.ph != nullptr) atomicAdd(&p.ph[i], globaltimer_ns() - t_in);
+#endif
+  };
+  if (BB_GEMM_PH && p.ph != nullptr && threadIdx.x == 0) atomicAdd(&p.ph[0], 1ull);
+  if (threadIdx.x == 32) gph(1);  // MMA thread: dependency wait returned
+  if (threadIdx.x == 0) gph(7);   // producer (issued the weight prefetch first)
   const bool skipped = p.skip != nullptr && *p.skip != 0;
   const int rows_valid = skipped ? 0 : (p.rows_valid != nullptr ? *p.rows_valid : p.rows_alloc);
   if (skipped) {
@@ -379,7 +393,7 @@ __global__ void __launch_bounds__(192)
       tmem_dealloc(tbase, C::TCOLS);
     }
     if (p.mode == 2) cg::this_cluster().sync();
-    tstat_end(p.tstat);
+    tsite_end(p.tstat);
     return;
   }
 
@@ -401,6 +415,7 @@ __global__ void __launch_bounds__(192)
             // weight tile already in flight: add the activation tile
             mbar_expect_tx(&full[stage_i], C::B_BYTES);
             tma_load_2d(sB + stage_i * C::B_BYTES, &tmB, &full[stage_i], kb * 64, chunk * BN, pol_x);
+            if (issued == 0) gph(6);
           } else {
             mbar_wait(&empty[stage_i], phase ^ 1);
             mbar_expect_tx(&full[stage_i], C::A_BYTES + C::B_BYTES);
@@ -425,6 +440,7 @@ __global__ void __launch_bounds__(192)
       uint32_t aphase = 0;
       UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
       Unit u;
+      bool first = true;
       while (it.next(u)) {
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
@@ -432,6 +448,10 @@ __global__ void __launch_bounds__(192)
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           mbar_wait(&full[stage_i], phase);
           tc_fence_after();
+          if (first) {
+            gph(2);
+            first = false;
+          }
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage_i * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage_i * C::B_BYTES));
 #pragma unroll
@@ -448,6 +468,7 @@ __global__ void __launch_bounds__(192)
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
+      gph(3);
     }
   } else {
     const int q = warp & 3;  // TMEM lane quadrant owned by this warp
@@ -535,6 +556,7 @@ __global__ void __launch_bounds__(192)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (et == 0 && acc == 0 && aphase == 0) gph(4);  // first tile stored
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
@@ -574,7 +596,8 @@ __global__ void __launch_bounds__(192)
     tc_fence_after();
     tmem_dealloc(tbase, C::TCOLS);
   }
-  tstat_end(p.tstat);
+  if (threadIdx.x == 0) gph(5);
+  tsite_end(p.tstat);
 }
 
 // ------------------------------------------------------------------ host

@@ -121,8 +121,12 @@ struct GemmTcParams {
   const float* boost;
   const int* tgt;
   float head_scale, spike_cut, spike_gain;
-  // live per-launch timing (%globaltimer): [min start, max end, CTAs done, sum ns, launches]
+  // live per-launch timing (%globaltimer): this launch site's {min start, max end}
   unsigned long long* tstat;
+  // timeline sessions, one GEMM kind (BB_GPH_KIND): per-CTA phase sums [CTAs,
+  // resident before the wait, first stage landed, last MMA issued, first tile
+  // stored, end] (ns, from the dependency wait's return; [1] before it)
+  unsigned long long* ph;
   unsigned long long* klog;
   int klog_cap, klog_id;
   EpiArgs epi;

@@ -28,7 +28,7 @@ for seed in (1000, 1001):
 s.stream.synchronize()
 s.klog(reset=True); s.gemm_stats(reset=True)
 import ctypes as _C0; from paper_2605_29233_b200 import _lib as _L0; _L0.lib().bb_session_lsk_prof(s.h, (_C0.c_ulonglong * 64)(), 1, _C0.c_void_p(s.stream.cuda_stream))
-import ctypes as _C; from paper_2605_29233_b200 import _lib as _L; _L.lib().bb_session_phase_stats(s.h, (_C.c_ulonglong * 8)(), 1, _C.c_void_p(s.stream.cuda_stream))
+import ctypes as _C; from paper_2605_29233_b200 import _lib as _L; _L.lib().bb_session_phase_stats(s.h, (_C.c_ulonglong * 16)(), 1, _C.c_void_p(s.stream.cuda_stream))
 s.set_inputs(*inputs(100200))
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 ev0.record(s.stream); it = s.launch(); ev1.record(s.stream); ev1.synchronize()
@@ -62,13 +62,21 @@ for k, name in ((5, "attn block: duration after PDL wait"), (6, "attn block: CTA
         print(f"live {name:40s} {gs[k][3] / gs[k][4] / 1e3:8.2f} us avg over {gs[k][4]} launches")
 import ctypes as C
 from paper_2605_29233_b200 import _lib
-ph = (C.c_ulonglong * 8)()
+ph = (C.c_ulonglong * 16)()
 _lib.lib().bb_session_phase_stats(s.h, ph, 0, C.c_void_p(s.stream.cuda_stream))
 if ph[0]:
     names_ph = ["rows+keys loaded", "FQ: phase-A loads / merge copies issued", "FQ: splice / merge blocks received",
                 "FQ: cluster barrier / outputs stored", "chunk0 landed", "chunk loop done", "end"]
     print("attention phase offsets (avg us from PDL release): " +
           ", ".join(f"{n} {ph[i + 1] / ph[0] / 1e3:.2f}" for i, n in enumerate(names_ph)))
+
+ph = (C.c_ulonglong * 16)()
+_lib.lib().bb_session_phase_stats(s.h, ph, 0, C.c_void_p(s.stream.cuda_stream))
+if ph[8]:
+    nm = ["dep wait returned (MMA thr)", "first stage landed", "last MMA issued", "first tile stored", "end",
+          "first B issued", "dep wait returned (producer)"]
+    print(f"gemm kind {os.environ.get('BB_GPH_KIND', '1')} phases (avg us from CTA entry): " +
+          ", ".join(f"{n} {ph[9 + i] / ph[8] / 1e3:.2f}" for i, n in enumerate(nm)))
 
 pr = (C.c_ulonglong * 64)()
 _lib.lib().bb_session_lsk_prof(s.h, pr, 0, C.c_void_p(s.stream.cuda_stream))
