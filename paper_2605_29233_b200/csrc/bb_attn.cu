@@ -321,6 +321,14 @@ cudaError_t launch_attn_keys(const Dims& D, const Sess& S, const Pass& P, const 
 // publishes the splice.
 // timeline runs only: per-CTA phase offsets from the PDL release, summed into
 // ph[1..7] with ph[0] = CTAs (bb_session_phase_stats)
+// 2^x on the SFU without exp2f's subnormal-result fix-up (results below
+// 2^-126 flush to 0; the softmax weights they would be are negligible)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void phase_mark(unsigned long long* ph, int i, unsigned long long t0) {
   if (ph != nullptr && threadIdx.x == 0) atomicAdd(&ph[i], globaltimer_ns() - t0);
 }
@@ -700,17 +708,19 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
       const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
       // rows with no visible key in this chunk keep their state (mn == -inf)
-      const float c0 = (m0 == -INFINITY || mn0 == -INFINITY) ? (mn0 == -INFINITY ? 1.0f : 0.0f) : exp2f(m0 - mn0);
-      const float c1 = (m1 == -INFINITY || mn1 == -INFINITY) ? (mn1 == -INFINITY ? 1.0f : 0.0f) : exp2f(m1 - mn1);
+      const float c0 = (m0 == -INFINITY || mn0 == -INFINITY) ? (mn0 == -INFINITY ? 1.0f : 0.0f) : ex2_ftz(m0 - mn0);
+      const float c1 = (m1 == -INFINITY || mn1 == -INFINITY) ? (mn1 == -INFINITY ? 1.0f : 0.0f) : ex2_ftz(m1 - mn1);
+      // rows with no visible key yet: every score is -inf, ex2(-inf - 0) = 0
+      const float mb0 = mn0 == -INFINITY ? 0.0f : mn0, mb1 = mn1 == -INFINITY ? 0.0f : mn1;
       m0 = mn0;
       m1 = mn1;
       float ps0 = 0.0f, ps1 = 0.0f;
 #pragma unroll
       for (int nt = 0; nt < KC / 8; ++nt) {
-        s[nt][0] = mn0 == -INFINITY ? 0.0f : exp2f(s[nt][0] - mn0);
-        s[nt][1] = mn0 == -INFINITY ? 0.0f : exp2f(s[nt][1] - mn0);
-        s[nt][2] = mn1 == -INFINITY ? 0.0f : exp2f(s[nt][2] - mn1);
-        s[nt][3] = mn1 == -INFINITY ? 0.0f : exp2f(s[nt][3] - mn1);
+        s[nt][0] = ex2_ftz(s[nt][0] - mb0);
+        s[nt][1] = ex2_ftz(s[nt][1] - mb0);
+        s[nt][2] = ex2_ftz(s[nt][2] - mb1);
+        s[nt][3] = ex2_ftz(s[nt][3] - mb1);
         ps0 += s[nt][0] + s[nt][1];
         ps1 += s[nt][2] + s[nt][3];
       }
