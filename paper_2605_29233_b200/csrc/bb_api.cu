@@ -259,7 +259,7 @@ static void plan(Session* s, char* base, bool dry) {
   s->full_rows = c.take<int>(1);
   s->tmap_cap = 8LL * D.layers + 1;
   s->tmaps = c.take<CUtensorMap>((size_t)s->tmap_cap, 128);
-  s->tstat = c.take<unsigned long long>(16 * 8);
+  s->tstat = c.take<unsigned long long>(17 * 8);  // slot 16: GEMM phase marks (BB_GEMM_PH builds)
   s->tsite = c.take<unsigned long long>((size_t)2 * 10 * D.layers);
   s->tsite_on = live_stats();
   s->blk.atstat = s->tstat + 5 * 8;   // slots 5/6: block-pass attention (duration, start spread)
@@ -411,7 +411,7 @@ static int setup_gemms(Session* s) {
           all[g]->p.klog_cap = s->D.klog_cap;
           {
             const char* e = getenv("BB_GPH_KIND");  // GEMM phase profile: which*8 + kind
-            all[g]->p.ph = (s->D.klog != nullptr && which * 8 + g == (e ? atoi(e) : 1)) ? s->tstat + 15 * 8 : nullptr;
+            all[g]->p.ph = (s->D.klog != nullptr && which * 8 + g == (e ? atoi(e) : 1)) ? s->tstat + 16 * 8 : nullptr;
           }
           all[g]->p.klog_id = 100 + which * 8 + g;
           if (!s->fuse_epi && attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
@@ -961,7 +961,7 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   cudaMemcpy(s->H.masked, zero.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->full_rows, &s->S.NF, sizeof(int), cudaMemcpyHostToDevice);
   {
-    std::vector<unsigned long long> ts(16 * 8, 0ull);
+    std::vector<unsigned long long> ts(17 * 8, 0ull);
     for (int k = 0; k < 16; ++k) ts[k * 8] = ~0ull;
     cudaMemcpy(s->tstat, ts.data(), ts.size() * 8, cudaMemcpyHostToDevice);
     std::vector<unsigned long long> site((size_t)2 * 10 * s->D.layers, 0ull);
@@ -1226,11 +1226,11 @@ BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset
   if (!s || !out) return BB_ERR_CONTRACT;
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemcpyAsync(out, s->tstat + 7 * 8, 8 * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(out + 8, s->tstat + 15 * 8, 8 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out + 8, s->tstat + 16 * 8, 8 * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (reset) {
     CK(cudaMemsetAsync(s->tstat + 7 * 8, 0, 8 * 8, st));
-    CK(cudaMemsetAsync(s->tstat + 15 * 8, 0, 8 * 8, st));
+    CK(cudaMemsetAsync(s->tstat + 16 * 8, 0, 8 * 8, st));
     CK(cudaStreamSynchronize(st));
   }
   return BB_OK;

@@ -108,23 +108,30 @@ __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restri
 template <typename T>
 __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
                                                   const float* __restrict__ rope, int layer, PartRef pr) {
-  pdl_enter();
-  klog_mark(D.klog, D.klog_cap, 2);
-  if (*P.skip) return;
+  pdl_launch();  // the successor launches now; our own loads follow
   const int half = D.hd >> 1;
   const int row = blockIdx.x;
   const int hh = blockIdx.y * (blockDim.x / half) + threadIdx.x / half, i = threadIdx.x % half;
-  if (hh >= D.nh + 2 * D.nkv) return;
-  const int pos = P.slot_pos[row];
-  if (pos < 0) return;
+  const bool live_hh = hh < D.nh + 2 * D.nkv;
   const int c0 = hh * D.hd + i, c1 = c0 + half;
+  // session constants (piece count, bias) before the dependency wait
+  const int ns = live_hh ? sk_nslots(pr.sk, row, c0) : 0;
+  float ba = 0.0f, bb = 0.0f;
+  if (bias != nullptr && live_hh) {
+    ba = bias[c0];
+    bb = bias[c1];
+  }
+  pdl_wait();
+  klog_mark(D.klog, D.klog_cap, 2);
+  // skip flag, slot, KV offset and the partial planes in one round trip
+  const int skip = *P.skip, pos = P.slot_pos[row];
+  const long long kvo = hh >= D.nh && live_hh ? P.slot_kvoff[row] : 0;
   float a, b;
 #if POST_RES_BATCH
   if (D.hd <= 128) {
     // both halves' partial planes loaded before the adds (slot order kept);
     // c0 and c1 lie in one 128-column tile, so they share the piece count
     constexpr int NSU = 4;
-    const int ns = sk_nslots(pr.sk, row, c0);
     const float* pa = pr.part + (long long)row * pr.ldp + c0;
     float wa[NSU], wb[NSU];
 #pragma unroll
@@ -133,6 +140,7 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
         wa[k] = pa[(long long)k * pr.plane];
         wb[k] = pa[(long long)k * pr.plane + half];
       }
+    if (skip || pos < 0 || !live_hh) return;
     a = wa[0];
     b = wb[0];
 #pragma unroll
@@ -148,12 +156,13 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
   } else
 #endif
   {
+    if (skip || pos < 0 || !live_hh) return;
     a = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c0);
     b = part_sum(pr.part, pr.plane, pr.ldp, pr.sk, row, c1);
   }
   if (bias != nullptr) {
-    a += bias[c0];
-    b += bias[c1];
+    a += ba;
+    b += bb;
   }
   if (D.arch == 1 && hh < D.nh + D.nkv) {
     const float2 cs = *reinterpret_cast<const float2*>(rope + ((long long)pos * half + i) * 2);
@@ -170,7 +179,7 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
   const bool isk = hh < D.nh + D.nkv;
   const int kvh = isk ? hh - D.nh : hh - D.nh - D.nkv;
   const long long lay = (long long)layer * S.R * S.pool * D.nkv * S.ps * D.hd;
-  T* dst = reinterpret_cast<T*>(isk ? st.kv_k : st.kv_v) + lay + P.slot_kvoff[row] + (long long)kvh * S.ps * D.hd;
+  T* dst = reinterpret_cast<T*>(isk ? st.kv_k : st.kv_v) + lay + kvo + (long long)kvh * S.ps * D.hd;
   stf(dst + i, a);
   stf(dst + i + half, b);
 }
@@ -179,28 +188,33 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
 
 template <typename T>
 __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef pr, const float* __restrict__ ln) {
-  pdl_enter();
-  klog_mark(D.klog, D.klog_cap, 4);
-  if (*P.skip) return;
   __shared__ float sh[32];
+  pdl_launch();  // the successor launches now; our own loads follow
   const int row = blockIdx.x;
-  if (P.slot_pos[row] < 0) return;
   float* x = P.x + (long long)row * D.d;
   T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
   float ss = 0.0f;
 #if POST_RES_BATCH
-  // d <= 4096: each thread owns <= 2 column groups; all their loads (x and up
-  // to 8 partial planes each) are issued before any is used
+  // d <= 4096: each thread owns <= 2 column groups.  Session constants (piece
+  // counts, norm weights) are read before the dependency wait; after it the
+  // skip flag, the row's slot, x and every partial plane are issued together
+  // (one round trip; rows that turn out idle discard what they loaded)
   constexpr int NG = 2, NSU = 8;
   if (D.d <= NG * 4 * (int)blockDim.x) {
-    float4 xv[NG], w[NG][NSU];
+    float4 xv[NG], w[NG][NSU], gv[NG];
     int ns[NG], cc[NG];
 #pragma unroll
     for (int u = 0; u < NG; ++u) {
       cc[u] = (threadIdx.x + u * blockDim.x) * 4;
-      ns[u] = 0;
+      ns[u] = cc[u] < D.d ? sk_nslots(pr.sk, row, cc[u]) : 0;
+      if (ln != nullptr && cc[u] < D.d) gv[u] = *reinterpret_cast<const float4*>(ln + cc[u]);
+    }
+    pdl_wait();
+    klog_mark(D.klog, D.klog_cap, 4);
+    const int skip = *P.skip, pos = P.slot_pos[row];
+#pragma unroll
+    for (int u = 0; u < NG; ++u) {
       if (cc[u] < D.d) {
-        ns[u] = sk_nslots(pr.sk, row, cc[u]);
         const float* pp = pr.part + (long long)row * pr.ldp + cc[u];
         xv[u] = *reinterpret_cast<const float4*>(x + cc[u]);
 #pragma unroll
@@ -208,6 +222,7 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
           if (k < ns[u]) w[u][k] = *reinterpret_cast<const float4*>(pp + (long long)k * pr.plane);
       }
     }
+    if (skip || pos < 0) return;
 #pragma unroll
     for (int u = 0; u < NG; ++u) {
       if (cc[u] >= D.d) continue;
@@ -244,7 +259,7 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
       if (cc[u] >= D.d) continue;
       float4 v = xv[u];
       if (ln != nullptr) {
-        const float4 g = *reinterpret_cast<const float4*>(ln + cc[u]);
+        const float4 g = gv[u];
         v.x *= inv * g.x;
         v.y *= inv * g.y;
         v.z *= inv * g.z;
@@ -255,6 +270,10 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
     return;
   }
 #endif
+  pdl_wait();
+  klog_mark(D.klog, D.klog_cap, 4);
+  if (*P.skip) return;
+  if (P.slot_pos[row] < 0) return;
   for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
     float4 v = *reinterpret_cast<float4*>(x + c);
     const int ns = sk_nslots(pr.sk, row, c);
@@ -326,17 +345,18 @@ __global__ void __launch_bounds__(512) k_norm(Dims D, Pass P, const float* __res
 // ------------------------------------------------------------------ SwiGLU
 template <typename T>
 __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
-  pdl_enter();
-  klog_mark(D.klog, D.klog_cap, 5);
-  if (*P.skip) return;
+  pdl_launch();  // the successor launches now; our own loads follow
   const int row = blockIdx.y;
-  if (P.slot_pos[row] < 0) return;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (f >= D.dff) return;
   const int cg = ((f >> 6) << 7) + (f & 63);  // 4 gate features in one 64-block; up at +64
-  const int ns = sk_nslots(pr.sk, row, cg);
+  // piece count: a session constant, read before the dependency wait
+  const int ns = f < D.dff ? sk_nslots(pr.sk, row, cg) : 0;
+  pdl_wait();
+  klog_mark(D.klog, D.klog_cap, 5);
   const float* pp = pr.part + (long long)row * pr.ldp + cg;
 #if POST_RES_BATCH
+  // skip flag, slot and the partial planes in one round trip (idle rows discard them)
+  const int skip = *P.skip, pos = P.slot_pos[row];
   constexpr int NSU = 4;
   float4 wg[NSU], wu[NSU];
 #pragma unroll
@@ -345,6 +365,7 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
       wg[i] = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane);
       wu[i] = *reinterpret_cast<const float4*>(pp + (long long)i * pr.plane + 64);
     }
+  if (skip || pos < 0 || f >= D.dff) return;
   float4 g = wg[0], u = wu[0];
 #pragma unroll
   for (int i = 1; i < NSU; ++i)
@@ -354,6 +375,7 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
     }
   for (int i = NSU; i < ns; ++i) {
 #else
+  if (*P.skip || P.slot_pos[row] < 0 || f >= D.dff) return;
   float4 g = *reinterpret_cast<const float4*>(pp), u = *reinterpret_cast<const float4*>(pp + 64);
   for (int i = 1; i < ns; ++i) {
 #endif
