@@ -323,10 +323,10 @@ __global__ void __launch_bounds__(192)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = p.n_ntiles * p.n_chunks;
-  __shared__ int s_pre;
+  __shared__ int s_pre;  // stages whose weight tile was issued before the dependency wait
 #if BB_GEMM_PH
   const unsigned long long t_in = p.ph != nullptr ? globaltimer_ns() : 0ull;
-#endif  // stages whose weight tile was issued before the dependency wait
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
