@@ -956,7 +956,7 @@ static cudaError_t attn_seg_launch(const Dims& D, const Sess& S, const Pass& P, 
 // with several requests per session, fewer CTAs per cluster (more keys each)
 // avoid running the grid in waves.  BB_ATT_CS forces.
 static int att_cs(const Dims& D, const Sess& S, const Pass& P, bool fq) {
-  static const int forced = getenv("BB_ATT_CS") != nullptr ? atoi(getenv("BB_ATT_CS")) : 0;
+  const int forced = getenv("BB_ATT_CS") != nullptr ? atoi(getenv("BB_ATT_CS")) : 0;
   if (forced == 8 || forced == 4 || (!fq && (forced == 2 || forced == 1))) return forced;
   if (P.full) return 8;  // full passes: 1-CTA clusters measured 1.3% slower per C2 request
   const int rows = S.NRq;
@@ -967,9 +967,406 @@ static int att_cs(const Dims& D, const Sess& S, const Pass& P, bool fq) {
   return per * 2 <= wave ? 2 : 1;
 }
 
+// ------------------------------------------------------------------ tcgen05 block attention
+// The same work split as k_attn_seg (cluster of CS CTAs per (request, head,
+// 64-row key tile), keys split evenly over the ranks, (m, l, o/l) merged
+// through DSMEM), with the chunk math on the 5th-gen tensor cores:
+//   S[64 x 64]  = Q[64 x 128] . K_chunk^T      tcgen05.mma M=64 N=64, S in TMEM
+//   O[64 x 128] += P_hi . V + P_lo . V         tcgen05.mma M=64 N=128 (V MN-major), O in TMEM
+// Q, K, V and P live in shared memory in the 128-byte-swizzled UMMA layouts
+// (K/V gathered per key by cp.async straight into that layout).  M=64 TMEM
+// layout (measured, scripts/tc_probe.cu): rows 16w..16w+15 in lanes 0-15 of
+// warp quadrant w, every column in the row's lane; so lanes 0-15 of each warp
+// own one query row each (all its keys and dims), lanes 16-31 only join the
+// warp-collective TMEM loads.  O is rescaled lazily (only when the row max
+// grows by more than 2^8, so P stays <= 256 and its bf16 hi/lo split keeps
+// ~2^-16 accuracy).
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// MN-major operand, 128B swizzle: 64-element MN atoms LBO bytes apart, 8-row
+// (K) groups SBO bytes apart
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// byte offset of 16-byte chunk c of row r in a [rows][64 bf16] SW128 tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+constexpr int ATC_QR = 64, ATC_KC = 64, ATC_HD = 128;
+constexpr uint32_t ATC_SUB = 64 * 128;  // one [64 rows][64 bf16] SW128 sub-tile (bytes)
+
+template <int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
+    k_attn_tc(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
+  klog_mark(D.klog, D.klog_cap, 24);
+  if (P.pf_base != nullptr && threadIdx.x == 0) {
+    // this CTA's slice of the O projection's weights -> L2 (see k_attn_seg)
+    const long long n_cta = (long long)gridDim.x * gridDim.y * gridDim.z;
+    const long long cta = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+    const long long per = ((P.pf_layer_bytes + n_cta - 1) / n_cta + 127) & ~127LL;
+    const char* base = P.pf_base + (long long)layer * P.pf_layer_bytes;
+    for (long long o = cta * per; o < min((cta + 1) * per, P.pf_layer_bytes); o += 65536) {
+      const long long n = min(65536LL, min((cta + 1) * per, P.pf_layer_bytes) - o);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"((uint32_t)n) : "memory");
+    }
+  }
+  using bf = __nv_bfloat16;
+  constexpr int HD = ATC_HD, QR = ATC_QR, KC = ATC_KC;
+  extern __shared__ __align__(1024) uint8_t smraw_tc[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw_tc) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                        // 2 sub-tiles (dims 0-63, 64-127)
+  uint8_t* sK = sQ + 2 * ATC_SUB;          // [2 buf][2 sub]
+  uint8_t* sV = sK + 4 * ATC_SUB;          // [2 buf][2 sub] (MN-major operand: row = key)
+  uint8_t* sPh = sV + 4 * ATC_SUB;         // [64 rows][64 keys] K-major
+  uint8_t* sPl = sPh + ATC_SUB;
+  int2* sKeys = reinterpret_cast<int2*>(sPl + ATC_SUB);
+  __shared__ int sRow[QR], sBr[QR];
+  __shared__ uint32_t sVis[2][32][2];  // [buf][branch][key word]: key visible to the branch
+  __shared__ int s_nk;
+  __shared__ __align__(8) uint64_t mbS, mbP;
+  __shared__ uint32_t s_tmem;
+
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int r = blockIdx.x / CS, h = blockIdx.y;
+  const int row0 = blockIdx.z * QR;
+  const int kvh = h / (D.nh / D.nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool act = lane < 16;
+  const int rl = 16 * warp + (lane & 15);  // my row (lanes 16-31 mirror lanes 0-15's rows, inactive)
+  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : blockIdx.z);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&mbS, 1);
+    mbar_init(&mbP, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&s_tmem, 256);  // S: 64 columns, O: 128 columns
+  pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 3);
+  unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;
+  tstat_begin(ats);
+  unsigned long long* const ph = ats != nullptr ? ats + 16 : nullptr;  // timeline phase marks
+  const unsigned long long t0 = ph != nullptr ? globaltimer_ns() : 0ull;
+  if (ph != nullptr && threadIdx.x == 0) atomicAdd(&ph[0], 1ull);
+  if (threadIdx.x < QR) {
+    const int lr = row0 + threadIdx.x;
+    int slot = -1, br = 0;
+    if (lr < rows_per_req) {
+      const int sl = slot_base + lr;
+      br = P.slot_br[sl];
+      if (P.slot_pos[sl] >= 0 && !*P.skip) slot = sl;
+    }
+    sRow[threadIdx.x] = slot;
+    sBr[threadIdx.x] = br;
+  } else if (threadIdx.x == QR) {
+    s_nk = P.akey_n[2 * kb];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tS = s_tmem, tO = s_tmem + 64;
+  const int n_keys = s_nk;
+  const int k_begin = (int)((long long)n_keys * crank / CS);
+  const int nk_cta = (int)((long long)n_keys * (crank + 1) / CS) - k_begin;
+  const int n_chunks = (nk_cta + KC - 1) / KC;
+  const int nkc = n_chunks * KC;
+  {
+    const int2* src = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + k_begin;
+    for (int i = threadIdx.x; i < nkc; i += blockDim.x) sKeys[i] = i < nk_cta ? src[i] : make_int2(0, 0);
+  }
+  const long long lay = (long long)layer * S.R * S.pool;
+  const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
+  const bf* Vg = reinterpret_cast<const bf*>(st.kv_v);
+  const long long kvstride = (long long)S.ps * HD;
+  const long long kbase = (lay * D.nkv + kvh) * kvstride, pstride = (long long)D.nkv * kvstride;
+  const int ps_sh = S.ps_shift, ps_mask = S.ps - 1;
+  // q rows -> SW128 sub-tiles (16-byte vector v of row rr: sub v/8, chunk v%8)
+  {
+    const bf* Qg = reinterpret_cast<const bf*>(P.q);
+    for (int i = threadIdx.x; i < QR * 16; i += blockDim.x) {
+      const int rr = i >> 4, v = i & 15;
+      const int slot = sRow[rr];
+      cp_async16(sQ + (v >> 3) * ATC_SUB + sw128_off(rr, v & 7),
+                 Qg + (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8, slot >= 0);
+    }
+    cp_async_commit();
+  }
+  __syncthreads();  // sKeys
+  phase_mark(ph, 1, t0);
+  auto load_chunk = [&](int ci, int buf) {
+    const int nk = min(KC, nk_cta - ci * KC);
+    uint8_t* dK = sK + buf * 2 * ATC_SUB;
+    uint8_t* dV = sV + buf * 2 * ATC_SUB;
+    for (int i = threadIdx.x; i < KC * 16; i += blockDim.x) {
+      const int j = i >> 4, v = i & 15;
+      const int2 e = sKeys[ci * KC + j];
+      const bool ok = j < nk;
+      const long long off = kbase + (long long)(e.x >> ps_sh) * pstride + (e.x & ps_mask) * HD + v * 8;
+      const uint32_t so = (v >> 3) * ATC_SUB + sw128_off(j, v & 7);
+      cp_async16(dK + so, Kg + (ok ? off : 0), ok);
+      cp_async16(dV + so, Vg + (ok ? off : 0), ok);
+    }
+    cp_async_commit();
+    // per-branch visibility bits of the chunk's keys (warp 0: keys 0-31, warp 1: 32-63)
+    if (warp < 2) {
+      const int j = 32 * warp + lane;
+      const int m = j < nk ? sKeys[ci * KC + j].y : 0;
+      for (int b = 0; b < MAXB; ++b) {
+        const uint32_t w = __ballot_sync(0xffffffffu, (m >> b) & 1);
+        if (lane == 0) sVis[buf][b][warp] = w;
+      }
+      if (lane == 0) sVis[buf][31][warp] = 0u;  // rows without a slot
+    }
+  };
+  if (n_chunks > 0) load_chunk(0, 0);
+  const int br_row = act && sRow[rl] >= 0 ? sBr[rl] : 31;  // bit 31 is never set: no visible key
+  const float sl2 = D.attn_scale * 1.4426950408889634f;
+  float m_ref = -INFINITY, l_part = 0.0f;
+  constexpr uint32_t IDS = idesc_bf16_f32(64, 64);
+  constexpr uint32_t IDO = idesc_bf16_f32(64, 128) | (1u << 16);  // B (V) MN-major
+  const uint32_t tl = (uint32_t)(32 * warp) << 16;                 // my TMEM lane quadrant
+  for (int ci = 0; ci < n_chunks; ++ci) {
+    const int buf = ci & 1;
+    const int nk = min(KC, nk_cta - ci * KC);
+    // loaders: this chunk (and q) landed -> visible to the tensor core, then
+    // the next chunk's gather (its buffer was last read by S and P.V of ci-1)
+    cp_async_wait<0>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (ci + 1 < n_chunks) {
+      if (ci > 0) mbar_wait(&mbP, (ci - 1) & 1);
+      load_chunk(ci + 1, buf ^ 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + buf * 2 * ATC_SUB);
+#pragma unroll
+      for (int ks = 0; ks < HD / 16; ++ks) {
+        const uint32_t sub = (ks >> 2) * ATC_SUB, ko = (ks & 3) * 32;
+        tc_mma_bf16(tS, sdesc_sw128(q0 + sub + ko), sdesc_sw128(k0 + sub + ko), IDS, ks > 0 ? 1u : 0u);
+      }
+      tc_commit(&mbS);
+    }
+    if (ci == 0) phase_mark(ph, 5, t0);  // (timeline) chunk 0 landed
+    mbar_wait(&mbS, ci & 1);  // S(ci) done, and with it P.V of chunk ci-1
+    tc_fence_after();
+    if (ci == 0) phase_mark(ph, 2, t0);  // (timeline) first S done
+    float s[64];
+    {
+      float t32[32];
+      tmem_ld32(tS + tl, t32);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) s[c] = t32[c];
+      tmem_ld32(tS + tl + 32, t32);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) s[32 + c] = t32[c];
+    }
+    const uint32_t v0w = sVis[buf][br_row][0], v1w = sVis[buf][br_row][1];
+    float mx4[4] = {m_ref, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int c = 0; c < 64; ++c) {
+      const uint32_t w = c < 32 ? v0w : v1w;
+      s[c] = ((w >> (c & 31)) & 1u) ? s[c] * sl2 : -INFINITY;
+      mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+    }
+    const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+    const bool grow = act && m_new > m_ref + 8.0f;  // (also the first visible key: m_ref = -inf)
+    const float f = !grow ? 1.0f : (m_ref == -INFINITY ? 0.0f : ex2_ftz(m_ref - m_new));
+    // O rows that held visible keys are rescaled in TMEM; tcgen05.ld/st are
+    // warp-collective, so the whole warp takes the branch (f = 1 elsewhere)
+    if (ci > 0 && __any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+      float o[32];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        tmem_ld32(tO + tl + 32 * q, o);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] *= f;
+        tmem_st32(tO + tl + 32 * q, o);
+      }
+    }
+    if (grow) {
+      l_part *= f;
+      m_ref = m_new;
+    }
+    const float mb = m_ref == -INFINITY ? 0.0f : m_ref;
+    // P = 2^(s - m_ref) as bf16 hi + lo, the 64 keys of row rl: 8 x 16-byte chunks
+    if (act) {
+      float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = ex2_ftz(s[8 * c8 + 2 * e] - mb), p1 = ex2_ftz(s[8 * c8 + 2 * e + 1] - mb);
+          ls[e] += p0 + p1;
+          split_bf2(p0, p1, hi[e], lo[e]);
+        }
+        const uint32_t off = sw128_off(rl, c8);
+        *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const uint32_t v0 = smem_u32(sV + buf * 2 * ATC_SUB), pa = smem_u32(sPh), pl = smem_u32(sPl);
+#pragma unroll
+      for (int kk = 0; kk < KC / 16; ++kk) {
+        const uint64_t bd = sdesc_sw128_mn(v0 + kk * 2048, ATC_SUB, 1024);
+        tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), bd, IDO, (ci > 0 || kk > 0) ? 1u : 0u);
+        tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+      }
+      tc_commit(&mbP);
+    }
+  }
+  // partial state (m_ref, l, o / l) of my row half -> fp16 staging in the
+  // (now idle) K buffers: [QR][HD + 8] halves, (m, l) in the row padding
+  constexpr int OLD = HD + 8;
+  __half* sO = reinterpret_cast<__half*>(sK);
+  phase_mark(ph, 6, t0);
+  if (n_chunks > 0) mbar_wait(&mbP, (n_chunks - 1) & 1);
+  tc_fence_after();
+  __syncthreads();
+  phase_mark(ph, 3, t0);  // (timeline) last P.V done
+
+  {
+    const float il = l_part > 0.0f ? 1.0f / l_part : 0.0f;
+    float o[32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (n_chunks > 0) {
+        tmem_ld32(tO + tl + 32 * q, o);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] = 0.0f;
+      }
+      if (act) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 2)
+          *reinterpret_cast<__half2*>(sO + rl * OLD + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+      }
+    }
+    if (act) *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, l_part);
+  }
+  tc_fence_before();
+  cluster.sync();
+  // merge rows [crank*RPC, (crank+1)*RPC) over the cluster (pull; fixed rank order)
+  constexpr int RPC = QR / CS, V4 = HD / 4, NMI = (RPC * V4 + 127) / 128;
+#pragma unroll
+  for (int k = 0; k < NMI; ++k) {
+    const int i = threadIdx.x + k * 128;
+    if (i >= RPC * V4) continue;
+    const int lr = crank * RPC + i / V4, c4 = (i % V4) * 4;
+    const int slot = sRow[lr];
+    float mr[CS], lv[CS];
+    float4 ov[CS];
+#pragma unroll
+    for (int q = 0; q < CS; ++q) {
+      const __half* row = cluster.map_shared_rank(sO + lr * OLD, q);
+      const float2 ml = *reinterpret_cast<const float2*>(row + HD);
+      mr[q] = ml.x;
+      lv[q] = ml.y;
+      const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+      ov[q] = make_float4(a.x, a.y, b.x, b.y);
+    }
+    if (slot < 0) continue;
+    float M = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < CS; ++q) M = fmaxf(M, mr[q]);
+    float Lsum = 0.0f;
+    float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+    for (int q = 0; q < CS; ++q) {
+      if (mr[q] == -INFINITY || lv[q] <= 0.0f) continue;
+      const float w = ex2_ftz(mr[q] - M) * lv[q];
+      Lsum += w;
+      acc.x += w * ov[q].x;
+      acc.y += w * ov[q].y;
+      acc.z += w * ov[q].z;
+      acc.w += w * ov[q].w;
+    }
+    const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
+    bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), p1 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&p0);
+    u.y = *reinterpret_cast<uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(out) = u;
+  }
+  phase_mark(ph, 4, t0);  // (timeline) merged outputs stored
+  cluster.sync();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(s_tmem, 256);
+  }
+  phase_mark(ph, 7, t0);
+  tstat_end(ats);
+}
+
+template <int CS>
+static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
+                                  cudaStream_t s) {
+  const int rows = P.full ? S.L : S.NRq;
+  const int max_ck = (P.akey_cap + ATC_KC * CS - 1) / (ATC_KC * CS);
+  const size_t smem = 1024 + (size_t)12 * ATC_SUB + (size_t)max_ck * ATC_KC * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_tc<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  dim3 grid(S.R * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
+  launch_k(k_attn_tc<CS>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
+  return cudaGetLastError();
+}
+
+// BB_ATT_TC=1: tcgen05 attention for hd = 128 (non-fused-QKV passes); read
+// per launch (launches are captured once into graphs).  Opt-in: correct
+// (tests/test_gpu_parity.py hd128 cases) but measured at parity with the
+// mma.sync kernel (C5 block attention 261 vs 263 us, C2 slower per NFE): the
+// chunk is bound by the 64-thread softmax / P staging (0.9 us) and the MMA
+// issue + commit round trip (~1 us), not by the tensor math.
+static bool att_tc_on() {
+  const char* e = getenv("BB_ATT_TC");
+  return e != nullptr && atoi(e) != 0;
+}
+
 template <int HD, bool FQ>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
+  if constexpr (HD == 128 && !FQ) {
+    if (att_tc_on()) {
+      switch (att_cs(D, S, P, FQ)) {
+        case 8: return attn_tc_launch<8>(D, S, P, st, layer, s);
+        case 4: return attn_tc_launch<4>(D, S, P, st, layer, s);
+        case 2: return attn_tc_launch<2>(D, S, P, st, layer, s);
+        default: return attn_tc_launch<1>(D, S, P, st, layer, s);
+      }
+    }
+  }
   switch (att_cs(D, S, P, FQ)) {
     case 8: return attn_seg_launch<HD, FQ, 8>(D, S, P, st, layer, pr, bias, rope, s);
     case 4: return attn_seg_launch<HD, FQ, 4>(D, S, P, st, layer, pr, bias, rope, s);

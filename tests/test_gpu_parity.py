@@ -260,9 +260,29 @@ def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol, lsk
     test.  lsk=1: the block pass runs the layer-stream kernels (BB_LSK=1,
     bf16 only; fp32 mode has no tensor-core path and ignores it)."""
     monkeypatch.setenv("BB_LSK", lsk)
+    _block_step_vs_oracle(LLADA[name], None, dtype, spike_gain, tol, name)
+
+
+@pytest.mark.parametrize("tc,cs", [("0", ""), ("1", ""), ("1", "1"), ("0", "1")])
+def test_block_step_hd128_attention_matches_oracle(tc, cs, monkeypatch):
+    """The block step at head_dim 128 (the LLaDA-8B head size; the tiny
+    fixtures use 64), with the tcgen05 attention (BB_ATT_TC=1: S and O in
+    TMEM) and with the mma.sync attention, against the oracle at the bf16
+    tolerance of the block-step test.  cs=1: one CTA per (head, row tile)
+    takes every key (several chunks: the online-softmax rescale path)."""
+    monkeypatch.setenv("BB_ATT_TC", tc)
+    if cs:
+        monkeypatch.setenv("BB_ATT_CS", cs)
+    g = LLADA["llada_tiny_bf16"]
+    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=2, head_dim=128), "bf16", 0.0, 2e-2,
+                          f"hd128 tc={tc} cs={cs or 'auto'}")
+
+
+def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name):
     from oracle import bb_oracle as O
     from paper_2605_29233_b200.engine import Session
-    g = LLADA[name]
+    if arch_override:
+        g = dict(g, arch=dict(g["arch"], **arch_override))
     a, params = _llada_params(g, dtype, spike_gain)
     cfg = cfg_from(g["config"])
     arch = O.OArch(**a)
