@@ -976,9 +976,9 @@ static int att_cs(const Dims& D, const Sess& S, const Pass& P, bool fq) {
 // Q, K, V and P live in shared memory in the 128-byte-swizzled UMMA layouts
 // (K/V gathered per key by cp.async straight into that layout).  M=64 TMEM
 // layout (measured, scripts/tc_probe.cu): rows 16w..16w+15 in lanes 0-15 of
-// warp quadrant w, every column in the row's lane; so lanes 0-15 of each warp
-// own one query row each (all its keys and dims), lanes 16-31 only join the
-// warp-collective TMEM loads.  O is rescaled lazily (only when the row max
+// warp quadrant w, every column in the row's lane.  The 16x32bx2 TMEM loads
+// hand lanes t and t+16 of warp w the two column halves of row 16w + t, so
+// each row is split over two lanes of one warp (max / sum by one shuffle).  O is rescaled lazily (only when the row max
 // grows by more than 2^8, so P stays <= 256 and its bf16 hi/lo split keeps
 // ~2^-16 accuracy).
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
@@ -990,6 +990,37 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
       "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
       "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// M=64 accumulators (16 lanes per warp quadrant): threads 0-15 get columns
+// [c, c+32) of lanes 0-15, threads 16-31 columns [c+OFF, c+OFF+32)
+template <int OFF>
+__device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], %33;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr), "n"(OFF));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st16x2(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x32.b32 [%0], %33, "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31]), "n"(OFF)
       : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -1048,8 +1079,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   const int row0 = blockIdx.z * QR;
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool act = lane < 16;
-  const int rl = 16 * warp + (lane & 15);  // my row (lanes 16-31 mirror lanes 0-15's rows, inactive)
+  const int rl = 16 * warp + (lane & 15), hh = lane >> 4;  // my row, my key half (S) / dim half (O)
   const int slot_base = P.full ? r * S.L : r * S.NRq;
   const long long kb = (long long)r * P.n_kz + (P.full ? 0 : blockIdx.z);
 
@@ -1137,7 +1167,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     }
   };
   if (n_chunks > 0) load_chunk(0, 0);
-  const int br_row = act && sRow[rl] >= 0 ? sBr[rl] : 31;  // bit 31 is never set: no visible key
+  const int br_row = sRow[rl] >= 0 ? sBr[rl] : 31;  // bit 31 is never set: no visible key
   const float sl2 = D.attn_scale * 1.4426950408889634f;
   float m_ref = -INFINITY, l_part = 0.0f;
   constexpr uint32_t IDS = idesc_bf16_f32(64, 64);
@@ -1169,37 +1199,29 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     mbar_wait(&mbS, ci & 1);  // S(ci) done, and with it P.V of chunk ci-1
     tc_fence_after();
     if (ci == 0) phase_mark(ph, 2, t0);  // (timeline) first S done
-    float s[64];
-    {
-      float t32[32];
-      tmem_ld32(tS + tl, t32);
-#pragma unroll
-      for (int c = 0; c < 32; ++c) s[c] = t32[c];
-      tmem_ld32(tS + tl + 32, t32);
-#pragma unroll
-      for (int c = 0; c < 32; ++c) s[32 + c] = t32[c];
-    }
-    const uint32_t v0w = sVis[buf][br_row][0], v1w = sVis[buf][br_row][1];
+    float s[32];
+    tmem_ld16x2<32>(tS + tl, s);  // row rl, keys 32*hh + [0, 32)
+    const uint32_t vw = sVis[buf][br_row][hh];
     float mx4[4] = {m_ref, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-    for (int c = 0; c < 64; ++c) {
-      const uint32_t w = c < 32 ? v0w : v1w;
-      s[c] = ((w >> (c & 31)) & 1u) ? s[c] * sl2 : -INFINITY;
+    for (int c = 0; c < 32; ++c) {
+      s[c] = ((vw >> c) & 1u) ? s[c] * sl2 : -INFINITY;
       mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
     }
-    const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-    const bool grow = act && m_new > m_ref + 8.0f;  // (also the first visible key: m_ref = -inf)
+    float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+    m_new = fmaxf(m_new, __shfl_xor_sync(0xffffffffu, m_new, 16));
+    const bool grow = m_new > m_ref + 8.0f;  // (also the first visible key: m_ref = -inf)
     const float f = !grow ? 1.0f : (m_ref == -INFINITY ? 0.0f : ex2_ftz(m_ref - m_new));
     // O rows that held visible keys are rescaled in TMEM; tcgen05.ld/st are
     // warp-collective, so the whole warp takes the branch (f = 1 elsewhere)
     if (ci > 0 && __any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
       float o[32];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        tmem_ld32(tO + tl + 32 * q, o);
+      for (int q = 0; q < 2; ++q) {
+        tmem_ld16x2<64>(tO + tl + 32 * q, o);
 #pragma unroll
         for (int c = 0; c < 32; ++c) o[c] *= f;
-        tmem_st32(tO + tl + 32 * q, o);
+        tmem_st16x2<64>(tO + tl + 32 * q, o);
       }
     }
     if (grow) {
@@ -1207,11 +1229,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
       m_ref = m_new;
     }
     const float mb = m_ref == -INFINITY ? 0.0f : m_ref;
-    // P = 2^(s - m_ref) as bf16 hi + lo, the 64 keys of row rl: 8 x 16-byte chunks
-    if (act) {
+    // P = 2^(s - m_ref) as bf16 hi + lo, my 32 keys of row rl: 4 x 16-byte chunks
+    {
       float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
+      for (int c8 = 0; c8 < 4; ++c8) {
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -1219,7 +1241,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
           ls[e] += p0 + p1;
           split_bf2(p0, p1, hi[e], lo[e]);
         }
-        const uint32_t off = sw128_off(rl, c8);
+        const uint32_t off = sw128_off(rl, 4 * hh + c8);
         *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
@@ -1251,23 +1273,22 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   phase_mark(ph, 3, t0);  // (timeline) last P.V done
 
   {
-    const float il = l_part > 0.0f ? 1.0f / l_part : 0.0f;
+    const float lsum = l_part + __shfl_xor_sync(0xffffffffu, l_part, 16);
+    const float il = lsum > 0.0f ? 1.0f / lsum : 0.0f;
     float o[32];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 2; ++q) {
       if (n_chunks > 0) {
-        tmem_ld32(tO + tl + 32 * q, o);
+        tmem_ld16x2<64>(tO + tl + 32 * q, o);  // dims 64*hh + 32*q + [0, 32)
       } else {
 #pragma unroll
         for (int c = 0; c < 32; ++c) o[c] = 0.0f;
       }
-      if (act) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 2)
-          *reinterpret_cast<__half2*>(sO + rl * OLD + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
-      }
+      for (int c = 0; c < 32; c += 2)
+        *reinterpret_cast<__half2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
     }
-    if (act) *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, l_part);
+    if (hh == 0) *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, lsum);
   }
   tc_fence_before();
   cluster.sync();
@@ -1343,22 +1364,27 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
   return cudaGetLastError();
 }
 
-// BB_ATT_TC=1: tcgen05 attention for hd = 128 (non-fused-QKV passes); read
-// per launch (launches are captured once into graphs).  Opt-in: correct
-// (tests/test_gpu_parity.py hd128 cases) but measured at parity with the
-// mma.sync kernel (C5 block attention 261 vs 263 us, C2 slower per NFE): the
-// chunk is bound by the 64-thread softmax / P staging (0.9 us) and the MMA
-// issue + commit round trip (~1 us), not by the tensor math.
-static bool att_tc_on() {
+// tcgen05 attention for hd = 128 (non-fused-QKV passes), the default;
+// BB_ATT_TC=0 selects the mma.sync kernel.  Read per launch (launches are
+// captured once into graphs).  Measured (C5 block attention 222 vs 262 us per
+// launch, C5 16.7 vs 17.9 ms/NFE; C2 attention slot 16.8 vs 19.4 us).
+// Full passes (prefill / refresh) take it at long context only (S.L >= 1024:
+// C5 16.7 vs 17.5 ms/NFE); at L = 320-640 each CTA holds about one chunk and
+// the mma.sync kernel's smaller setup wins (C3 15.53 vs 15.68).
+// BB_ATT_TC_FULL=0/1 forces.
+static bool att_tc_on(const Sess& S, const Pass& P) {
   const char* e = getenv("BB_ATT_TC");
-  return e != nullptr && atoi(e) != 0;
+  if (e != nullptr && atoi(e) == 0) return false;
+  if (!P.full) return true;
+  const char* f = getenv("BB_ATT_TC_FULL");
+  return f != nullptr ? atoi(f) != 0 : S.L >= 1024;
 }
 
 template <int HD, bool FQ>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
   if constexpr (HD == 128 && !FQ) {
-    if (att_tc_on()) {
+    if (att_tc_on(S, P)) {
       switch (att_cs(D, S, P, FQ)) {
         case 8: return attn_tc_launch<8>(D, S, P, st, layer, s);
         case 4: return attn_tc_launch<4>(D, S, P, st, layer, s);

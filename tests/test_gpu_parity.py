@@ -266,8 +266,8 @@ def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol, lsk
 @pytest.mark.parametrize("tc,cs", [("0", ""), ("1", ""), ("1", "1"), ("0", "1")])
 def test_block_step_hd128_attention_matches_oracle(tc, cs, monkeypatch):
     """The block step at head_dim 128 (the LLaDA-8B head size; the tiny
-    fixtures use 64), with the tcgen05 attention (BB_ATT_TC=1: S and O in
-    TMEM) and with the mma.sync attention, against the oracle at the bf16
+    fixtures use 64), with the tcgen05 attention (the default, S and O in
+    TMEM) and with the mma.sync attention (BB_ATT_TC=0), against the oracle at the bf16
     tolerance of the block-step test.  cs=1: one CTA per (head, row tile)
     takes every key (several chunks: the online-softmax rescale path)."""
     monkeypatch.setenv("BB_ATT_TC", tc)
