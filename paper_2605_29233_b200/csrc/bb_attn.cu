@@ -1065,9 +1065,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   uint8_t* sV = sK + 4 * ATC_SUB;          // [2 buf][2 sub] (MN-major operand: row = key)
   uint8_t* sPh = sV + 4 * ATC_SUB;         // [64 rows][64 keys] K-major
   uint8_t* sPl = sPh + ATC_SUB;
-  int2* sKeys = reinterpret_cast<int2*>(sPl + ATC_SUB);
   __shared__ int sRow[QR], sBr[QR];
   __shared__ uint32_t sVis[2][32][2];  // [buf][branch][key word]: key visible to the branch
+  __shared__ int2 sKr[2][ATC_KC];      // key-list ring: chunk c's keys in slot c & 1
   __shared__ int s_nk;
   __shared__ __align__(8) uint64_t mbS, mbP;
   __shared__ uint32_t s_tmem;
@@ -1117,10 +1117,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   const int k_begin = (int)((long long)n_keys * crank / CS);
   const int nk_cta = (int)((long long)n_keys * (crank + 1) / CS) - k_begin;
   const int n_chunks = (nk_cta + KC - 1) / KC;
-  const int nkc = n_chunks * KC;
-  {
-    const int2* src = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + k_begin;
-    for (int i = threadIdx.x; i < nkc; i += blockDim.x) sKeys[i] = i < nk_cta ? src[i] : make_int2(0, 0);
+  // the key list streams through a 2-slot ring one chunk ahead of its use
+  // (shared memory stays independent of the context length: 2 CTAs/SM)
+  const int2* ksrc = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + k_begin;
+  auto key_of = [&](int c) {
+    const int i = c * KC + (int)threadIdx.x;
+    return i < nk_cta ? ksrc[i] : make_int2(0, 0);
+  };
+  int2 kreg = make_int2(0, 0);
+  if (threadIdx.x < KC) {
+    sKr[0][threadIdx.x] = key_of(0);
+    sKr[1][threadIdx.x] = key_of(1);
+    kreg = key_of(2);
   }
   const long long lay = (long long)layer * S.R * S.pool;
   const bf* Kg = reinterpret_cast<const bf*>(st.kv_k);
@@ -1139,7 +1147,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     }
     cp_async_commit();
   }
-  __syncthreads();  // sKeys
+  __syncthreads();  // key ring
   phase_mark(ph, 1, t0);
   auto load_chunk = [&](int ci, int buf) {
     const int nk = min(KC, nk_cta - ci * KC);
@@ -1147,7 +1155,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     uint8_t* dV = sV + buf * 2 * ATC_SUB;
     for (int i = threadIdx.x; i < KC * 16; i += blockDim.x) {
       const int j = i >> 4, v = i & 15;
-      const int2 e = sKeys[ci * KC + j];
+      const int2 e = sKr[ci & 1][j];
       const bool ok = j < nk;
       const long long off = kbase + (long long)(e.x >> ps_sh) * pstride + (e.x & ps_mask) * HD + v * 8;
       const uint32_t so = (v >> 3) * ATC_SUB + sw128_off(j, v & 7);
@@ -1158,7 +1166,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     // per-branch visibility bits of the chunk's keys (warp 0: keys 0-31, warp 1: 32-63)
     if (warp < 2) {
       const int j = 32 * warp + lane;
-      const int m = j < nk ? sKeys[ci * KC + j].y : 0;
+      const int m = j < nk ? sKr[ci & 1][j].y : 0;
       for (int b = 0; b < MAXB; ++b) {
         const uint32_t w = __ballot_sync(0xffffffffu, (m >> b) & 1);
         if (lane == 0) sVis[buf][b][warp] = w;
@@ -1247,6 +1255,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
       }
       l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    // keys of chunk ci+2 into the slot chunk ci's keys held (read by
+    // load_chunk(ci), done); visible after this barrier, used at ci+1's top
+    if (threadIdx.x < KC) {
+      sKr[ci & 1][threadIdx.x] = kreg;
+      kreg = key_of(ci + 3);
     }
     tc_fence_before();
     __syncthreads();
@@ -1351,8 +1365,7 @@ template <int CS>
 static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                   cudaStream_t s) {
   const int rows = P.full ? S.L : S.NRq;
-  const int max_ck = (P.akey_cap + ATC_KC * CS - 1) / (ATC_KC * CS);
-  const size_t smem = 1024 + (size_t)12 * ATC_SUB + (size_t)max_ck * ATC_KC * 8;
+  const size_t smem = 1024 + (size_t)12 * ATC_SUB;  // keys stream through a static ring
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attn_tc<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
