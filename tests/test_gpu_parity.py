@@ -381,3 +381,31 @@ def test_kv_logging_matches_reference_runs(name):
         got = record(bb.run_blockbatch(params, task, cfg))
         err = goldens.compare_run(got, want, prob_tol=1e-4, kv_tol=1e-4)
         assert err is None, f"{name} seed {seed}: {err}"
+
+
+def test_live_gemm_stats_count_every_launch():
+    """The live per-launch GEMM timing the bench roofline reads (per-site
+    red.min / red.max of %globaltimer, folded once per pass by k_tsite_fold):
+    after a prefill and one block step every GEMM launch is counted once per
+    layer and kind, with a positive duration, and a reset clears the sums."""
+    from paper_2605_29233_b200.engine import Session
+    g = LLADA["llada_tiny_bf16"]
+    params = llada_model(g, "bf16")
+    cfg = cfg_from(g["config"])
+    layers = g["arch"]["layers"]
+    task = bb.make_task(g["seeds"][0], g["prompt_len"], g["gen_len"], params.vocab)
+    s = Session(params, cfg, g["prompt_len"], 1)
+    s.set_inputs(task.prompt[None], task.target[None])
+    s.gemm_stats(reset=True)
+    s.prefill()
+    st = s.fetch(trace=False)
+    assert st["ctrl"][0, 0] == 0
+    s.iteration(with_refresh=False, use_graph=False)
+    s.stream.synchronize()
+    gs = s.gemm_stats(reset=True)
+    for kind in range(4):  # block pass QKV, O, gate/up, down
+        assert gs[kind][4] == layers and gs[kind][3] > 0, (kind, gs[kind])
+        assert gs[8 + kind][4] == layers and gs[8 + kind][3] > 0, (8 + kind, gs[8 + kind])
+    assert gs[4][4] == 2 and gs[4][3] > 0  # LM head: prefill + block step
+    gs = s.gemm_stats(reset=False)
+    assert all(gs[k][4] == 0 for k in (0, 1, 2, 3, 4, 8, 9, 10, 11))
