@@ -1038,6 +1038,9 @@ __device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr, uint32_t lbo,
 // byte offset of 16-byte chunk c of row r in a [rows][64 bf16] SW128 tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+#ifndef ATT_TC_PLO
+#define ATT_TC_PLO 1  // P.V with the bf16 lo part of P (0: hi only; measurement builds)
+#endif
 constexpr int ATC_QR = 64, ATC_KC = 64, ATC_HD = 128;
 constexpr uint32_t ATC_SUB = 64 * 128;  // one [64 rows][64 bf16] SW128 sub-tile (bytes)
 
@@ -1251,7 +1254,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
         }
         const uint32_t off = sw128_off(rl, 4 * hh + c8);
         *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        if (ATT_TC_PLO) *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
       l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1271,7 +1274,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
       for (int kk = 0; kk < KC / 16; ++kk) {
         const uint64_t bd = sdesc_sw128_mn(v0 + kk * 2048, ATC_SUB, 1024);
         tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), bd, IDO, (ci > 0 || kk > 0) ? 1u : 0u);
-        tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+        if (ATT_TC_PLO) tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
       }
       tc_commit(&mbP);
     }

@@ -263,19 +263,22 @@ def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol, lsk
     _block_step_vs_oracle(LLADA[name], None, dtype, spike_gain, tol, name)
 
 
-@pytest.mark.parametrize("tc,cs,kvh", [("0", "", 2), ("1", "", 2), ("1", "1", 2), ("0", "1", 2), ("1", "", 1)])
-def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, monkeypatch):
+@pytest.mark.parametrize("tc,cs,kvh,gain,tol", [("0", "", 2, 0.0, 2e-2), ("1", "", 2, 0.0, 2e-2), ("1", "1", 2, 0.0, 2e-2),
+                                                ("0", "1", 2, 0.0, 2e-2), ("1", "", 1, 0.0, 2e-2),
+                                                ("1", "", 2, 33.0, 1e-1), ("0", "", 2, 33.0, 1e-1)])
+def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol, monkeypatch):
     """The block step at head_dim 128 (the LLaDA-8B head size; the tiny
     fixtures use 64), with the tcgen05 attention (the default, S and O in
     TMEM) and with the mma.sync attention (BB_ATT_TC=0), against the oracle at the bf16
     tolerance of the block-step test.  cs=1: one CTA per (head, row tile)
     takes every key (several chunks: the online-softmax rescale path).
-    kvh=1: grouped-query attention (2 query heads share one KV head)."""
+    kvh=1: grouped-query attention (2 query heads share one KV head).  gain 33:
+    the spike epilogue (x34 on raw-logit error) at the prefill test's tolerance."""
     monkeypatch.setenv("BB_ATT_TC", tc)
     if cs:
         monkeypatch.setenv("BB_ATT_CS", cs)
     g = LLADA["llada_tiny_bf16"]
-    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128), "bf16", 0.0, 2e-2,
+    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128), "bf16", gain, tol,
                           f"hd128 tc={tc} cs={cs or 'auto'} kvh={kvh}")
 
 
