@@ -1388,6 +1388,22 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
 // C5 16.7 vs 17.5 ms/NFE); at L = 320-640 each CTA holds about one chunk and
 // the mma.sync kernel's smaller setup wins (C3 15.53 vs 15.68).
 // BB_ATT_TC_FULL=0/1 forces.
+// Cluster size for k_attn_tc (2 CTAs/SM): the largest of 8 / 4 / 2 / 1 whose
+// grid fits one wave, else 1 (splitting keys over a cluster only pays while
+// the (request, head, row tile) units alone cannot fill the GPU).  C5 full
+// passes (1536 units): CS 8 / 4 / 2 = 1020 / 829 / 731 us per launch.
+static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P) {
+  const char* f = getenv("BB_ATT_CS");
+  const int forced = f != nullptr ? atoi(f) : 0;
+  if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
+  const int rows = P.full ? S.L : S.NRq;
+  const long long per = (long long)S.R * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
+  const long long wave = 2LL * kNumSMs;
+  for (int cs = 8; cs > 1; cs >>= 1)
+    if (per * cs <= wave) return cs;
+  return 1;
+}
+
 static bool att_tc_on(const Sess& S, const Pass& P) {
   const char* e = getenv("BB_ATT_TC");
   if (e != nullptr && atoi(e) == 0) return false;
@@ -1401,7 +1417,7 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
                                const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
   if constexpr (HD == 128 && !FQ) {
     if (att_tc_on(S, P)) {
-      switch (att_cs(D, S, P, FQ)) {
+      switch (att_cs_tc(D, S, P)) {
         case 8: return attn_tc_launch<8>(D, S, P, st, layer, s);
         case 4: return attn_tc_launch<4>(D, S, P, st, layer, s);
         case 2: return attn_tc_launch<2>(D, S, P, st, layer, s);

@@ -57,6 +57,7 @@ json.dump({"kernels": {k: {"n": n, "ns": ns} for k, (n, ns) in rows}, "nfe": nfe
           open("gpurun_out/timeline_c2.json", "w"))
 gs = s.gemm_stats()
 for k, name in ((5, "attn block: duration after PDL wait"), (6, "attn block: CTA start spread"),
+                (13, "attn full: duration after PDL wait"),
                 (0, "gemm qkv"), (1, "gemm o"), (2, "gemm gate_up"), (3, "gemm down"), (12, "layer_stream kernel")):
     if gs[k][4]:
         print(f"live {name:40s} {gs[k][3] / gs[k][4] / 1e3:8.2f} us avg over {gs[k][4]} launches")
