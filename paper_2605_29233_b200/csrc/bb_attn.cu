@@ -1384,10 +1384,6 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
 // BB_ATT_TC=0 selects the mma.sync kernel.  Read per launch (launches are
 // captured once into graphs).  Measured (C5 block attention 222 vs 262 us per
 // launch, C5 16.7 vs 17.9 ms/NFE; C2 attention slot 16.8 vs 19.4 us).
-// Full passes (prefill / refresh) take it at long context only (S.L >= 1024:
-// C5 16.7 vs 17.5 ms/NFE); at L = 320-640 each CTA holds about one chunk and
-// the mma.sync kernel's smaller setup wins (C3 15.53 vs 15.68).
-// BB_ATT_TC_FULL=0/1 forces.
 // Cluster size for k_attn_tc (2 CTAs/SM): the largest of 8 / 4 / 2 / 1 whose
 // grid fits one wave, else 1 (splitting keys over a cluster only pays while
 // the (request, head, row tile) units alone cannot fill the GPU).  C5 full
@@ -1404,12 +1400,16 @@ static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P) {
   return 1;
 }
 
+// Full passes (prefill / refresh) too: with the one-wave cluster rule the C2
+// full-pass attention takes 18.1 us per launch (mma.sync, 8-CTA clusters:
+// 50.6); C3 15.1 -> 14.1 ms/NFE.  BB_ATT_TC_FULL=0 keeps mma.sync there.
 static bool att_tc_on(const Sess& S, const Pass& P) {
+  (void)S;
   const char* e = getenv("BB_ATT_TC");
   if (e != nullptr && atoi(e) == 0) return false;
   if (!P.full) return true;
   const char* f = getenv("BB_ATT_TC_FULL");
-  return f != nullptr ? atoi(f) != 0 : S.L >= 1024;
+  return f == nullptr || atoi(f) != 0;
 }
 
 template <int HD, bool FQ>
