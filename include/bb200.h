@@ -79,6 +79,8 @@ typedef struct {
   int trace;           /* record trace events (TraceEvent, decoding.py:61-75) */
   int event_capacity;  /* events per request                              */
   int diagnostics;     /* 1: reserve scratch KV pages for bb_fresh_kv (log_consistency) */
+  int test_flags;      /* tests only (0 on the product path): bit 0 = mma.sync attention at
+                          head_dim 128; bits 4-7 = forced attention cluster size */
 } bb_session_desc;
 
 #define BB_VIEW_TOKENS 0   /* int32 [R][B][L]      branch rows              */
@@ -142,8 +144,9 @@ BB_API int bb_kv_gather(void* sess, int r, int k, float* dst, void* stream);
    session state (the pass writes into reserved scratch pages; needs
    diagnostics = 1 in the session desc) */
 BB_API int bb_fresh_kv(void* sess, int r, int k, float* dst, void* stream);
-/* out[0] = ||a - b||_2 (b may be NULL), fp64 accumulation in a fixed order */
-BB_API int bb_sqdiff_norm(const float* a, const float* b, long long n, double* out, void* stream);
+/* out[0] = ||a - b||_2 (b may be NULL), fp64 accumulation in a fixed order
+   (partial sums in the session's workspace) */
+BB_API int bb_sqdiff_norm(void* sess, const float* a, const float* b, long long n, double* out, void* stream);
 BB_API int bb_version(void);
 /* instrumentation: live per-launch GEMM timing and kernel-launch counters */
 BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int reset, void* stream);
@@ -156,9 +159,6 @@ BB_API int bb_session_gemm_stats(void* sess, unsigned long long* host_out, int r
  * dependency wait, then from it to: first stage landed, last MMA issued, first
  * tile stored, end).  out must hold 16 values. */
 BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset, void* stream);
-/* layer-stream kernel phase profile (BB_KLOG=1 sessions), out[64]: CTA 0's
-   summed ns from release to each phase event, [63] = launches */
-BB_API int bb_session_lsk_prof(void* sess, unsigned long long* out, int reset, void* stream);
 BB_API int bb_session_counters(void* sess, long long* out);
 BB_API int bb_session_klog(void* sess, unsigned long long* host_out, int cap, int reset, long long* n, void* stream);
 
@@ -166,10 +166,6 @@ BB_API int bb_session_klog(void* sess, unsigned long long* host_out, int cap, in
 BB_API int bb_debug_gemm_tc(const void* W, const void* X, void* out, int n_out, int K, int rows, int BN, int mode,
                             int max_grid, float* work, long long* work_floats, const int* tgt, const float* boost,
                             float head_scale, float spike_cut, float spike_gain, void* stream);
-/* Debug: prefetch a whole [n_out][K] bf16 weight matrix into L2 (kind 0 =
- * the GEMM's tensor-tile prefetch over all stream-K ranges, 1 = contiguous
- * 64 KB bulk prefetches).  Measurement hook for the next-GEMM prefetch. */
-BB_API int bb_debug_l2_prefetch(const void* W, int n_out, int K, int kind, void* stream);
 BB_API int bb_debug_gemm_simt(const float* W, const float* X, float* out, int n_out, int K, int rows,
                               void* stream);
 

@@ -45,7 +45,7 @@ class SessionDesc(C.Structure):
                 ("tau_merge", C.c_float), ("tau_sync", C.c_float), ("refresh_interval", C.c_int),
                 ("merge_enabled", C.c_int), ("sync_enabled", C.c_int), ("page_size", C.c_int),
                 ("pages_per_item", C.c_int), ("trace", C.c_int), ("event_capacity", C.c_int),
-                ("diagnostics", C.c_int)]
+                ("diagnostics", C.c_int), ("test_flags", C.c_int)]
 
 
 ARCH_REF, ARCH_LLADA = 0, 1
@@ -78,7 +78,6 @@ SIGNATURES = {
     "bb_session_ctrl": (i32, [vp, i32p, vp]),
     "bb_session_gemm_stats": (i32, [vp, C.POINTER(C.c_ulonglong), i32, vp]),
     "bb_session_phase_stats": (i32, [vp, vp, i32, vp]),
-    "bb_session_lsk_prof": (i32, [vp, vp, i32, vp]),
     "bb_session_counters": (i32, [vp, i64p]),
     "bb_session_klog": (i32, [vp, C.POINTER(C.c_ulonglong), i32, i32, i64p, vp]),
     "bb_prefill": (i32, [vp, vp]),
@@ -91,14 +90,13 @@ SIGNATURES = {
     "bb_block_step_part": (i32, [vp, i32, vp]),
     "bb_kv_gather": (i32, [vp, i32, i32, vp, vp]),
     "bb_fresh_kv": (i32, [vp, i32, i32, vp, vp]),
-    "bb_sqdiff_norm": (i32, [vp, vp, i64, vp, vp]),
+    "bb_sqdiff_norm": (i32, [vp, vp, vp, i64, vp, vp]),
     "bb_commit_probs": (i32, [vp, i32, i32, vp, vp, f32, vp, vp, vp]),
     "bb_merge_sync_maps": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, f32, f32, i32, i32, vp, i32, vp, vp, vp,
                                  vp]),
     "bb_fill_hash_uniform": (i32, [vp, i32, i64, C.c_ulonglong, i32, f32, i64, i32, i32, vp]),
     "bb_debug_gemm_tc": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp, i64p, vp, vp, f32, f32, f32, vp]),
     "bb_debug_gemm_simt": (i32, [vp, vp, vp, i32, i32, i32, vp]),
-    "bb_debug_l2_prefetch": (i32, [vp, i32, i32, i32, vp]),
 }
 
 

@@ -12,7 +12,6 @@
 #include "bb_common.cuh"
 #include "bb_gemm.cuh"
 #include "bb_layers.cuh"
-#include "bb_stream.cuh"
 
 namespace bb {
 
@@ -72,19 +71,11 @@ struct Session {
   float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
   float* ss_full = nullptr;
   int ss_ld = 1;
-  bool fuse_epi = false;     // BB_FUSE_EPI=1: fused GEMM epilogues (experimental; default stream-K + post kernels)
-  bool no_fq = true;         // BB_FQ=1: block-pass attention finalizes QKV in its prologue (opt-in; slower today)
-  long long l2pf_bytes = 0;  // BB_L2PF_MB: next-GEMM weight prefetch budget per GEMM (0 = off)
-  CUtensorMap* tmaps = nullptr;  // device copies of the GEMM weight tensor maps (prefetch operands)
-  long long tmap_cap = 0;
   unsigned long long* klog = nullptr;  // BB_KLOG=1: kernel timeline (cudaMalloc'd)
-  // layer-stream kernels of the block pass (bf16, BN 64): [0] = QKV(0),
-  // [l+1] = O(l) .. down(l) + QKV(l+1); empty = per-GEMM kernels
-  std::vector<LskParams> lsk;
-  unsigned int* lsk_bar = nullptr;  // [(layers+1)][16] grid-barrier counters
-  int* fresh_save = nullptr;         // [n_lp] page-table row saved by bb_fresh_kv
-  unsigned long long* lsk_prof = nullptr;  // [64] CTA-0 phase profile (BB_KLOG)
-  int lsk_grid = 0;
+  int* fresh_save = nullptr;           // [n_lp] page-table row saved by bb_fresh_kv
+  double* sq_part = nullptr;           // [n_sms] bb_sqdiff_norm partial sums
+  int n_sms = 148;                     // queried at session creation
+  int tflags = 0;                      // bb_session_desc.test_flags (tests only)
   int32_t* host_ctrl = nullptr;  // pinned [4][R][C_WORDS]
   cudaEvent_t ev[4] = {};
   long long layout[BB_VIEW_COUNT][2];
@@ -257,17 +248,14 @@ static void plan(Session* s, char* base, bool dry) {
   view(BB_VIEW_SLOT_BR, s->blk.slot_br, (size_t)rb * 4);
   H.skip = c.take<int>(1);
   s->full_rows = c.take<int>(1);
-  s->tmap_cap = 8LL * D.layers + 1;
-  s->tmaps = c.take<CUtensorMap>((size_t)s->tmap_cap, 128);
   s->tstat = c.take<unsigned long long>(17 * 8);  // slot 16: GEMM phase marks (BB_GEMM_PH builds)
   s->tsite = c.take<unsigned long long>((size_t)2 * 10 * D.layers);
   s->tsite_on = live_stats();
   s->blk.atstat = s->tstat + 5 * 8;   // slots 5/6: block-pass attention (duration, start spread)
   s->full.atstat = s->tstat + 13 * 8; // slots 13/14: full-pass attention
   s->tile_cnt = c.take<int>(8192);
-  s->lsk_bar = c.take<unsigned int>((size_t)(D.layers + 1) * 16);
   s->fresh_save = c.take<int>(S.n_lp);
-  s->lsk_prof = c.take<unsigned long long>(64);
+  s->sq_part = c.take<double>(1024);
   s->ns_cap = 64 * 1024;
   s->ns_tabs = c.take<unsigned char>(s->ns_cap);
   s->ss_ld = (D.d + 127) / 128;
@@ -285,7 +273,7 @@ static void plan(Session* s, char* base, bool dry) {
         if (outs[g] == 0) continue;
         const int ntiles = (outs[g] + 127) / 128, nch = rows / BN, KB = (ks[g] + 63) / 64;
         const long long T = (long long)ntiles * nch * KB;
-        const int G = (int)(T < kNumSMs ? T : kNumSMs);
+        const int G = (int)(T < s->n_sms ? T : s->n_sms);
         int ms = 1;
         for (long long t = 0; t < (long long)ntiles * nch; ++t) {
           const int ns = sk_owner(t * KB + KB - 1, T, G) - sk_owner(t * KB, T, G) + 1;
@@ -335,11 +323,11 @@ static int setup_gemms(Session* s) {
   const Dims& D = s->D;
   const Weights& W = s->M->W;
   const size_t e = esz(D);
-  // block pass: the attention prefetches the O projection's weights into L2
-  // (BB_ATT_L2PF=0 disables)
+  // block pass: the attention CTAs prefetch the O projection's weights into
+  // L2 while they run (HBM is otherwise idle during the attention)
   s->blk.pf_base = nullptr;
   s->full.pf_base = nullptr;
-  if (D.dtype == BB_DTYPE_BF16 && !(getenv("BB_ATT_L2PF") != nullptr && atoi(getenv("BB_ATT_L2PF")) == 0)) {
+  if (D.dtype == BB_DTYPE_BF16) {
     s->blk.pf_base = (const char*)W.wo;
     s->blk.pf_layer_bytes = (long long)D.d * D.attn_dim * (long long)e;
   }
@@ -354,70 +342,23 @@ static int setup_gemms(Session* s) {
       const char* wgu = D.dff ? (const char*)W.wgu + (size_t)l * 2 * D.dff * D.d * e : nullptr;
       const char* wd = D.dff ? (const char*)W.wd + (size_t)l * D.d * D.dff * e : nullptr;
       if (D.dtype == BB_DTYPE_BF16) {
-        const int gm = s->fuse_epi ? 3 : 0;
-        // stream-K grid per GEMM kind (0 = all SMs); BB_GRID_{QKV,O,GU,DN} override for the block pass
-        auto grid_of = [&](const char* name) {
-          const char* e = which == 0 ? getenv(name) : nullptr;
-          return e != nullptr ? atoi(e) : 0;
-        };
-        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_QKV")))
-          return BB_ERR_CONFIG;
-        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_O")))
-          return BB_ERR_CONFIG;
+        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
+        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
         if (D.dff) {
-          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_GU")))
-            return BB_ERR_CONFIG;
-          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, gm, grid_of("BB_GRID_DN")))
-            return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
         }
         TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
-          EpiArgs& E = all[g]->p.epi;
-          memset(&E, 0, sizeof(E));
-          E.kind = !s->fuse_epi ? 0 : (g == 0 ? 2 : (g == 2 ? 3 : 4));
-          E.tile_cnt = s->tile_cnt;
-          E.slot_kvoff = P.slot_kvoff;
-          E.kv_layer_elems = (long long)s->S.R * s->S.pool * D.nkv * s->S.ps * D.hd;
-          E.slot_pos = P.slot_pos;
-          E.slot_req = P.slot_req;
-          E.slot_br = P.slot_br;
-          E.nh = D.nh;
-          E.nkv = D.nkv;
-          E.hd = D.hd;
-          E.rope = D.arch == BB_ARCH_LLADA;
-          E.bias = W.bqkv != nullptr ? W.bqkv + (size_t)l * D.qkv_out : nullptr;
-          E.rope_tab = W.rope;
-          E.q = (__nv_bfloat16*)P.q;
-          E.attn_dim = D.attn_dim;
-          E.kv_k = (__nv_bfloat16*)s->st.kv_k;
-          E.kv_v = (__nv_bfloat16*)s->st.kv_v;
-          E.kv_layer_off = l;
-          E.pt = s->st.pt;
-          E.ps = s->S.ps;
-          E.P = s->S.P;
-          E.n_pp = s->S.n_pp;
-          E.L = s->S.L;
-          E.pool = s->S.pool;
-          E.B = s->S.B;
-          E.n_lp = s->S.n_lp;
-          E.act = (__nv_bfloat16*)P.act;
-          E.dff = D.dff;
-          E.x = P.x;
-          E.d = D.d;
-          E.ss_part = which == 0 ? s->ss_blk : s->ss_full;
-          E.ss_ld = s->ss_ld;
-          all[g]->p.tstat = s->tsite_on ? s->tsite + 2 * ((size_t)(which * 5 + g) * D.layers + l) : nullptr;
-          all[g]->p.klog = s->D.klog;
-          all[g]->p.klog_cap = s->D.klog_cap;
-          {
-            const char* e = getenv("BB_GPH_KIND");  // GEMM phase profile: which*8 + kind
-            all[g]->p.ph = (s->D.klog != nullptr && which * 8 + g == (e ? atoi(e) : 1)) ? s->tstat + 16 * 8 : nullptr;
-          }
-          all[g]->p.klog_id = 100 + which * 8 + g;
-          if (!s->fuse_epi && attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
-          all[g]->p.part = s->part;
-          all[g]->p.skip = P.skip;
-          all[g]->p.rows_valid = which == 1 ? s->full_rows : nullptr;
+          GemmTcParams& p = all[g]->p;
+          p.tstat = s->tsite_on ? s->tsite + 2 * ((size_t)(which * 5 + g) * D.layers + l) : nullptr;
+          p.klog = s->D.klog;
+          p.klog_cap = s->D.klog_cap;
+          p.klog_id = 100 + which * 8 + g;
+          if (attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
+          p.part = s->part;
+          p.skip = P.skip;
+          p.rows_valid = which == 1 ? s->full_rows : nullptr;
         }
       } else {
         lg.sqkv = SimtGemm{(const float*)wqkv, (const float*)P.xn, D.qkv_out, D.d, P.rows_alloc,
@@ -434,7 +375,7 @@ static int setup_gemms(Session* s) {
     }
   }
   if (D.dtype == BB_DTYPE_BF16) {
-    if (!tc_gemm_setup(s->head_tc, W.head, D.n_out, D.d, s->blk.xn, s->blk.rows_alloc, s->gb.BN, 1, 0))
+    if (!tc_gemm_setup(s->head_tc, W.head, D.n_out, D.d, s->blk.xn, s->blk.rows_alloc, s->gb.BN, 1, s->n_sms))
       return BB_ERR_CONFIG;
     GemmTcParams& p = s->head_tc.p;
     p.head_part = s->H.hpart;
@@ -452,109 +393,6 @@ static int setup_gemms(Session* s) {
     s->head_simt = SimtGemm{(const float*)W.head, (const float*)s->blk.xn, D.n_out, D.d, s->blk.rows_alloc,
                             nullptr, s->H.skip, s->H.logits, D.n_out};
   }
-  // L2 prefetch chain: each GEMM's producer warp, after its last TMA load,
-  // prefetches the first part of the next GEMM's per-CTA weight ranges
-  // (qkv -> o -> gate/up -> down -> next layer's qkv; last block-pass down ->
-  // LM head), so HBM streams through the attention / post kernels between.
-  if (D.dtype == BB_DTYPE_BF16 && !s->fuse_epi && s->l2pf_bytes > 0) {
-    // device copies of every GEMM's weight tensor map (the prefetch operand)
-    std::vector<const TcGemm*> gl;
-    for (int which = 0; which < 2; ++which)
-      for (auto& lg : (which == 0 ? s->gb : s->gf).layers) {
-        gl.push_back(&lg.qkv);
-        gl.push_back(&lg.o);
-        if (D.dff) {
-          gl.push_back(&lg.gu);
-          gl.push_back(&lg.dn);
-        }
-      }
-    gl.push_back(&s->head_tc);
-    if ((long long)gl.size() > s->tmap_cap) return BB_ERR_NOMEM;
-    std::vector<CUtensorMap> maps(gl.size());
-    for (size_t i = 0; i < gl.size(); ++i) maps[i] = gl[i]->tmA;
-    if (cudaMemcpy(s->tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess)
-      return BB_ERR_CUDA;
-    auto dev_map = [&](const TcGemm* g) -> const CUtensorMap* {
-      for (size_t i = 0; i < gl.size(); ++i)
-        if (gl[i] == g) return s->tmaps + i;
-      return nullptr;
-    };
-    for (int which = 0; which < 2; ++which) {
-      PassGemms& G = which == 0 ? s->gb : s->gf;
-      for (int l = 0; l < D.layers; ++l) {
-        LayerGemms& lg = G.layers[l];
-        std::vector<TcGemm*> chain = {&lg.qkv, &lg.o};
-        if (D.dff) {
-          chain.push_back(&lg.gu);
-          chain.push_back(&lg.dn);
-        }
-        for (size_t i = 0; i < chain.size(); ++i) {
-          const TcGemm* next = i + 1 < chain.size() ? chain[i + 1]
-                               : (l + 1 < D.layers ? &G.layers[l + 1].qkv : (which == 0 ? &s->head_tc : nullptr));
-          if (next != nullptr) chain[i]->p.pf = tc_gemm_l2pf(*next, dev_map(next), s->l2pf_bytes);
-        }
-      }
-    }
-  }
-  return BB_OK;
-}
-
-// Layer-stream kernels for the block pass (opt-in, BB_LSK=1; default: one
-// kernel per GEMM and per consumer op)
-static int setup_lsk(Session* s) {
-  const Dims& D = s->D;
-  const Weights& W = s->M->W;
-  s->lsk.clear();
-  const char* env = getenv("BB_LSK");  // opt-in (BB_LSK=1): slower than the per-GEMM kernels today
-  if (env == nullptr || atoi(env) == 0) return BB_OK;
-  if (D.dtype != BB_DTYPE_BF16 || s->fuse_epi || s->gb.BN != 64 || D.d % 128 != 0 || D.hd % 8 != 0) return BB_OK;
-  int dev = 0, sms = 0;
-  CK(cudaGetDevice(&dev));
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  s->lsk_grid = sms;
-  PassGemms& G = s->gb;
-  auto base = [&](int idx) {
-    LskParams p;
-    memset(&p, 0, sizeof(p));
-    p.c.D = D;
-    p.c.S = s->S;
-    p.c.P = s->blk;
-    p.c.st = s->st;
-    p.c.part = s->part;
-    p.c.rows = s->S.NR;
-    p.c.flags = getenv("BB_LSK_FLAGS") != nullptr ? atoi(getenv("BB_LSK_FLAGS")) : 0;
-    p.c.ss = s->ss_blk;
-    p.c.rope = W.rope;
-    p.c.bar = s->lsk_bar + (size_t)idx * 16;
-    p.c.tstat = s->tstat + 12 * 8;
-    p.c.prof = D.klog != nullptr ? s->lsk_prof : nullptr;
-    return p;
-  };
-  auto bias = [&](int l) -> const float* { return W.bqkv != nullptr ? W.bqkv + (size_t)l * D.qkv_out : nullptr; };
-  LskParams p0 = base(0);
-  if (!lsk_add_gemm(p0, G.layers[0].qkv, LSK_POST_QKV, nullptr, bias(0), 0, s->tstat + 0 * 8)) return BB_OK;
-  std::vector<LskParams> all = {p0};
-  for (int l = 0; l < D.layers; ++l) {
-    LayerGemms& lg = G.layers[l];
-    const float* next_ln = l + 1 < D.layers ? (D.arch == BB_ARCH_LLADA ? W.ln1 + (size_t)(l + 1) * D.d : nullptr)
-                                            : (D.arch == BB_ARCH_LLADA ? W.lnf : nullptr);
-    LskParams p = base(l + 1);
-    bool ok = true;
-    if (D.dff) {
-      ok &= lsk_add_gemm(p, lg.o, LSK_POST_RESIDUAL, W.ln2 + (size_t)l * D.d, nullptr, l, s->tstat + 1 * 8);
-      ok &= lsk_add_gemm(p, lg.gu, LSK_POST_SWIGLU, nullptr, nullptr, l, s->tstat + 2 * 8);
-      ok &= lsk_add_gemm(p, lg.dn, LSK_POST_RESIDUAL, next_ln, nullptr, l, s->tstat + 3 * 8);
-    } else {
-      ok &= lsk_add_gemm(p, lg.o, LSK_POST_RESIDUAL, next_ln, nullptr, l, s->tstat + 1 * 8);
-    }
-    if (l + 1 < D.layers)
-      ok &= lsk_add_gemm(p, G.layers[l + 1].qkv, LSK_POST_QKV, nullptr, bias(l + 1), l + 1, s->tstat + 0 * 8);
-    if (!ok) return BB_OK;  // shape not supported: per-GEMM kernels
-    all.push_back(p);
-  }
-  CK(cudaMemset(s->lsk_bar, 0, (size_t)(D.layers + 1) * 16 * sizeof(unsigned int)));
-  CK(cudaMemset(s->lsk_prof, 0, 64 * sizeof(unsigned long long)));
-  s->lsk = all;
   return BB_OK;
 }
 
@@ -601,43 +439,14 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
   const Weights& W = s->M->W;
   cudaError_t e;
   if ((e = launch_embed(D, s->S, P, W, st)) != cudaSuccess) return e;
-  if (&P == &s->blk && !s->lsk.empty()) {
-    // attention(l) -> layer-stream kernel (O .. down of layer l, QKV of l+1)
-    if ((e = lsk_launch(s->lsk[0], s->lsk_grid, st)) != cudaSuccess) return e;
-    for (int l = 0; l < D.layers; ++l) {
-      if ((e = launch_attn(D, s->S, P, s->st, l, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
-      if ((e = lsk_launch(s->lsk[l + 1], s->lsk_grid, st)) != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-  }
-  const bool fused = D.dtype == BB_DTYPE_BF16 && s->fuse_epi;
-  float* ss = &P == &s->full ? s->ss_full : s->ss_blk;
   for (int l = 0; l < D.layers; ++l) {
     LayerGemms& lg = G.layers[l];
     const float* next_ln = l + 1 < D.layers ? (D.arch == BB_ARCH_LLADA ? W.ln1 + (size_t)(l + 1) * D.d : nullptr)
                                             : (D.arch == BB_ARCH_LLADA ? W.lnf : nullptr);
-    if (fused) {
-      // QKV (+bias, RoPE, KV splice) -> attention -> O (+residual) -> norm -> GU (+SwiGLU) -> down (+residual) -> norm
-      if ((e = tc_gemm_launch(lg.qkv, st)) != cudaSuccess) return e;
-      if ((e = launch_attn(D, s->S, P, s->st, l, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
-      if ((e = tc_gemm_launch(lg.o, st)) != cudaSuccess) return e;
-      if (D.dff) {
-        if ((e = launch_norm(D, P, ss, s->ss_ld, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
-        if ((e = tc_gemm_launch(lg.gu, st)) != cudaSuccess) return e;
-        if ((e = tc_gemm_launch(lg.dn, st)) != cudaSuccess) return e;
-      }
-      if ((e = launch_norm(D, P, ss, s->ss_ld, next_ln, st)) != cudaSuccess) return e;
-      continue;
-    }
     PartRef pr;
     if ((e = run_gemm(s, lg.qkv, lg.sqkv, &pr, st)) != cudaSuccess) return e;
-    if (D.dtype == BB_DTYPE_BF16 && attn_fuses_qkv(D, s->S, P) && !s->no_fq) {
-      const float* bias = W.bqkv != nullptr ? W.bqkv + (size_t)l * D.qkv_out : nullptr;
-      if ((e = launch_attn(D, s->S, P, s->st, l, &pr, bias, W.rope, st)) != cudaSuccess) return e;
-    } else {
-      if ((e = launch_post_qkv(D, s->S, P, s->st, W, l, pr, st)) != cudaSuccess) return e;
-      if ((e = launch_attn(D, s->S, P, s->st, l, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
-    }
+    if ((e = launch_post_qkv(D, s->S, P, s->st, W, l, pr, st)) != cudaSuccess) return e;
+    if ((e = launch_attn(D, s->S, P, s->st, l, s->tflags, st)) != cudaSuccess) return e;
     if ((e = run_gemm(s, lg.o, lg.so, &pr, st)) != cudaSuccess) return e;
     if (D.dff) {
       if ((e = launch_post_residual(D, P, pr, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
@@ -840,6 +649,13 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   s->M = M;
   s->desc = *d;
   s->D = M->D;
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+        sms > 0)
+      s->n_sms = sms > 1024 ? 1024 : sms;
+    s->tflags = d->test_flags;
+  }
   Sess& S = s->S;
   memset(&S, 0, sizeof(S));
   if (d->n_requests < 1 || d->n_branches < 1 || d->n_branches > MAXB) return BB_ERR_CONFIG;
@@ -879,6 +695,7 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.n_gp = (S.G + S.ps - 1) / S.ps;
   S.n_lp = S.n_pp + S.n_gp;
   S.diag = d->diagnostics ? 1 : 0;
+  S.n_sms = s->n_sms;
   S.pool = S.B * S.n_lp + (S.diag ? S.n_lp : 0);
   S.ch_block = d->pages_per_item > 0 ? d->pages_per_item : 4;
   S.max_items = S.B * ((S.n_lp + S.ch_block - 1) / S.ch_block) + 2 * S.B + 4;
@@ -936,9 +753,6 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   s->ws = (char*)workspace;
   for (int i = 0; i < BB_VIEW_COUNT; ++i)
     if (s->layout[i][1]) s->layout[i][0] += (long long)(base - (char*)workspace);
-  s->fuse_epi = s->D.dtype == BB_DTYPE_BF16 && getenv("BB_FUSE_EPI") != nullptr && atoi(getenv("BB_FUSE_EPI")) != 0;
-  s->no_fq = !(getenv("BB_FQ") != nullptr && atoi(getenv("BB_FQ")) != 0);
-  s->l2pf_bytes = (long long)(getenv("BB_L2PF_MB") != nullptr ? atof(getenv("BB_L2PF_MB")) : 0.0) * (1 << 20);
   if (getenv("BB_KLOG") != nullptr && atoi(getenv("BB_KLOG")) != 0) {
     const int cap = 1 << 20;
     if (cudaMalloc(&s->klog, (1 + 2 * (size_t)cap) * 8) == cudaSuccess) {
@@ -948,7 +762,6 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
     }
   }
   rc = setup_gemms(s);
-  if (rc == BB_OK) rc = setup_lsk(s);
   if (rc != BB_OK) {
     delete s;
     return rc;
@@ -1136,11 +949,10 @@ BB_API int bb_fresh_kv(void* sess, int r, int k, float* dst, void* stream) {
   return BB_OK;
 }
 
-BB_API int bb_sqdiff_norm(const float* a, const float* b, long long n, double* out, void* stream) {
-  if (!a || !out || n < 0) return BB_ERR_CONTRACT;
-  static double* part = nullptr;
-  if (part == nullptr && cudaMalloc(&part, kNumSMs * sizeof(double)) != cudaSuccess) return BB_ERR_CUDA;
-  CK(launch_sqdiff_norm(a, b, n, part, kNumSMs, out, (cudaStream_t)stream));
+BB_API int bb_sqdiff_norm(void* sess, const float* a, const float* b, long long n, double* out, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !a || !out || n < 0) return BB_ERR_CONTRACT;
+  CK(launch_sqdiff_norm(a, b, n, s->sq_part, s->n_sms, out, (cudaStream_t)stream));
   return BB_OK;
 }
 
@@ -1231,23 +1043,6 @@ BB_API int bb_session_phase_stats(void* sess, unsigned long long* out, int reset
   if (reset) {
     CK(cudaMemsetAsync(s->tstat + 7 * 8, 0, 8 * 8, st));
     CK(cudaMemsetAsync(s->tstat + 16 * 8, 0, 8 * 8, st));
-    CK(cudaStreamSynchronize(st));
-  }
-  return BB_OK;
-}
-
-// layer-stream kernel phase profile of CTA 0 (BB_KLOG=1 sessions): out[64],
-// [8i + k] summed ns from the epilogue's release to: k=0 GEMM i planes written,
-// 1 step-1 barrier passed, 2 step 1 done, 3 step-2 barrier passed, 4 step 2
-// done, 5 (activation producer) GEMM i inputs released; [63] launches
-BB_API int bb_session_lsk_prof(void* sess, unsigned long long* out, int reset, void* stream) {
-  Session* s = (Session*)sess;
-  if (!s || !out) return BB_ERR_CONTRACT;
-  cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(out, s->lsk_prof, 64 * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (reset) {
-    CK(cudaMemsetAsync(s->lsk_prof, 0, 64 * 8, st));
     CK(cudaStreamSynchronize(st));
   }
   return BB_OK;

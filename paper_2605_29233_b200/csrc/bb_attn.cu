@@ -310,15 +310,6 @@ cudaError_t launch_attn_keys(const Dims& D, const Sess& S, const Pass& P, const 
 // branch.  Online softmax per row, one pass, normalised output written
 // directly (no split-K partials, no combine kernel).
 //
-// FQ (block pass, all rows of a request in one tile): the QKV finalize
-// (model.py:283-293: + bias, RoPE, splice of the window's fresh K/V into the
-// branch's pages) runs in the prologue instead of a separate post kernel.
-// CTA c of the cluster sums the stream-K partial planes for rows
-// [8c, 8c+8) of its head's q and its kv-head's k/v, writes k/v into the
-// pages, and the q rows are exchanged through distributed shared memory.
-// Chunks made only of prompt keys are prefetched before the splice; chunks
-// that may hold window keys are loaded after the cluster barrier that
-// publishes the splice.
 // timeline runs only: per-CTA phase offsets from the PDL release, summed into
 // ph[1..7] with ph[0] = CTAs (bb_session_phase_stats)
 // 2^x on the SFU without exp2f's subnormal-result fix-up (results below
@@ -348,10 +339,9 @@ __device__ __forceinline__ void phase_mark(unsigned long long* ph, int i, unsign
 #ifndef ATT_KC
 #define ATT_KC 64  // keys per chunk (32 measured slower: 21.6 vs 19.5 us per layer at C2)
 #endif
-template <int HD, bool FQ, int ATT_CS>
+template <int HD, int ATT_CS>
 __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
-    k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req, PartRef pr,
-               const float* __restrict__ bias, const float* __restrict__ rope) {
+    k_attn_seg(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
   klog_mark(D.klog, D.klog_cap, 24);  // (timeline) CTA 0 resident, before the dependency wait
   if (P.pf_base != nullptr && threadIdx.x == 0) {
     // this CTA's slice of the O projection's weights -> L2 (constant data: no
@@ -382,9 +372,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   bf* sVb = sKb + 2 * KC * LD;  // [2][KC][LD]
   int2* sKeys = reinterpret_cast<int2*>(sVb + 2 * KC * LD);  // this CTA's keys
   __shared__ int sRow[QR], sBr[QR], sPos[QR];
-  __shared__ long long sKvo[QR];
   __shared__ int s_nk, s_gen0;
-  __shared__ int sNS[FQ ? 3 * (QR / ATT_CS) : 1];  // FQ: partial planes per (q|k|v, row)
 #if ATT_MERGE_PUSH
   __shared__ __align__(8) uint64_t s_mbar;  // merge: all ranks' blocks received
   if (threadIdx.x == 0) {
@@ -406,27 +394,18 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   if (threadIdx.x < QR) {
     const int lr = row0 + threadIdx.x;
     int slot = -1, br = 0, pos = -1;
-    long long kvo = 0;
     if (lr < rows_per_req) {
       const int sl = slot_base + lr;
       pos = P.slot_pos[sl];
       br = P.slot_br[sl];
-      if (FQ) kvo = P.slot_kvoff[sl];
       if (pos >= 0 && !*P.skip) slot = sl;
     }
     sRow[threadIdx.x] = slot;
     sBr[threadIdx.x] = br;
     sPos[threadIdx.x] = pos;
-    sKvo[threadIdx.x] = kvo;
   } else if (threadIdx.x == QR) {
     s_nk = P.akey_n[2 * kb];
     s_gen0 = P.akey_n[2 * kb + 1];
-  } else if (FQ && threadIdx.x > QR && threadIdx.x <= QR + 3 * (QR / ATT_CS)) {
-    // stream-K piece count of the (q|k|v column tile, row) pairs this CTA finalizes
-    const int e = threadIdx.x - QR - 1, which = e / (QR / ATT_CS), rr = e % (QR / ATT_CS);
-    const int hh = which == 0 ? h : (which == 1 ? D.nh + kvh : D.nh + D.nkv + kvh);
-    const int row = slot_base + row0 + crank * (QR / ATT_CS) + rr;
-    sNS[e] = row < P.rows_alloc ? sk_nslots(pr.sk, row, hh * HD) : 1;
   }
   __syncthreads();
   const int n_keys = s_nk;
@@ -483,132 +462,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     }
     cp_async_commit();
   };
-  if (FQ) {
-    // QKV finalize for rows [8*crank, 8*crank+8) of this tile.  Items are
-    // (row, q|k|v, 4 consecutive pair indices); the plane loop is outside
-    // the item loop so every item's plane-q loads are independent (one L2
-    // round trip per plane level, no stores in between), then math + stores.
-    constexpr int RPC = QR / ATT_CS, HALF = HD / 2, I4 = HALF / 4;
-    constexpr int TOT = RPC * 3 * I4, NIT = (TOT + 127) / 128;
-    const long long lay_el = (long long)layer * S.R * S.pool * D.nkv * kvstride;
-    float4 va[NIT], vb[NIT], ba[NIT], bb4[NIT], c01[NIT], c23[NIT];
-    const float* pk[NIT];
-    int nsk[NIT];
-#pragma unroll
-    for (int k = 0; k < NIT; ++k) {
-      const int it = threadIdx.x + k * 128;
-      const int rr = it / (3 * I4), rem = it - rr * 3 * I4;
-      const int which = rem / I4, i = (rem - which * I4) * 4;
-      const int lr = crank * RPC + rr;
-      const int slot = it < TOT ? sRow[lr] : -1;
-      const int hh = which == 0 ? h : (which == 1 ? D.nh + kvh : D.nh + D.nkv + kvh);
-      const int c0 = hh * HD + i;
-      nsk[k] = slot >= 0 ? sNS[which * RPC + rr] : 0;
-      pk[k] = pr.part + (long long)(slot >= 0 ? slot : 0) * pr.ldp + c0;
-      va[k] = vb[k] = ba[k] = bb4[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      c01[k] = c23[k] = make_float4(1.0f, 0.0f, 1.0f, 0.0f);
-      if (slot >= 0 && bias != nullptr) {
-        ba[k] = __ldg(reinterpret_cast<const float4*>(bias + c0));
-        bb4[k] = __ldg(reinterpret_cast<const float4*>(bias + c0 + HALF));
-      }
-      if (slot >= 0 && D.arch == 1 && which < 2) {
-        const float4* cp = reinterpret_cast<const float4*>(rope + ((long long)sPos[lr] * HALF + i) * 2);
-        c01[k] = __ldg(cp);
-        c23[k] = __ldg(cp + 1);
-      }
-    }
-    auto add4 = [](float4& acc, const float4 v) {
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
-    };
-    // all plane levels in one batch (one L2 round trip), then the keys to
-    // smem and the splice-independent part of the first chunk
-    float4 ta[4][NIT], tb[4][NIT];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int k = 0; k < NIT; ++k) {
-        ta[q][k] = tb[q][k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        if (q < nsk[k]) {
-          ta[q][k] = __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane));
-          tb[q][k] = __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane + HALF));
-        }
-      }
-    store_keys();
-    __syncthreads();  // sKeys
-    if (n_chunks > 0) load_chunk(0, 0, 1);
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int k = 0; k < NIT; ++k) {
-        add4(va[k], ta[q][k]);
-        add4(vb[k], tb[q][k]);
-      }
-#pragma unroll
-    for (int k = 0; k < NIT; ++k)
-      for (int q = 4; q < nsk[k]; ++q) {
-        add4(va[k], __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane)));
-        add4(vb[k], __ldg(reinterpret_cast<const float4*>(pk[k] + q * pr.plane + HALF)));
-      }
-    phase_mark(ph, 2, t0);  // (issue order only: the adds below wait for the loads)
-#pragma unroll
-    for (int k = 0; k < NIT; ++k) {  // bias after the planes: part_sum's rounding order
-      add4(va[k], ba[k]);
-      add4(vb[k], bb4[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < NIT; ++k) {
-      const int it = threadIdx.x + k * 128;
-      if (it >= TOT) continue;
-      const int rr = it / (3 * I4), rem = it - rr * 3 * I4;
-      const int which = rem / I4, i = (rem - which * I4) * 4;
-      const int lr = crank * RPC + rr;
-      const float ax[4] = {va[k].x, va[k].y, va[k].z, va[k].w}, bx[4] = {vb[k].x, vb[k].y, vb[k].z, vb[k].w};
-      const float cx[4] = {c01[k].x, c01[k].z, c23[k].x, c23[k].z}, sx[4] = {c01[k].y, c01[k].w, c23[k].y, c23[k].w};
-      __align__(8) bf oa[4], ob[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        oa[e] = __float2bfloat16(ax[e] * cx[e] - bx[e] * sx[e]);
-        ob[e] = __float2bfloat16(bx[e] * cx[e] + ax[e] * sx[e]);
-      }
-      bf* dst;
-      if (which == 0) {
-        dst = sQ + lr * LD;
-      } else {
-        if (sRow[lr] < 0) continue;
-        dst = reinterpret_cast<bf*>(which == 1 ? st.kv_k : st.kv_v) + lay_el + sKvo[lr] + (long long)kvh * kvstride;
-      }
-      *reinterpret_cast<uint2*>(dst + i) = *reinterpret_cast<const uint2*>(oa);
-      *reinterpret_cast<uint2*>(dst + i + HALF) = *reinterpret_cast<const uint2*>(ob);
-    }
-    phase_mark(ph, 3, t0);
-    cluster.sync();  // publishes the K/V splice and every CTA's q rows
-    phase_mark(ph, 4, t0);
-    constexpr int QV = HD / 8;  // 16-byte vectors per q row
-    constexpr int NG = QR * QV / 128;
-    uint4 qv[NG];
-#pragma unroll
-    for (int k = 0; k < NG; ++k) {
-      const int idx = threadIdx.x + k * 128;
-      const int lr = idx / QV, v = idx - lr * QV;
-      const int owner = lr / RPC;
-      const bf* src = owner == crank ? sQ + lr * LD : cluster.map_shared_rank(sQ + lr * LD, owner);
-      qv[k] = reinterpret_cast<const uint4*>(src)[v];
-    }
-#pragma unroll
-    for (int k = 0; k < NG; ++k) {
-      const int idx = threadIdx.x + k * 128;
-      const int lr = idx / QV, v = idx - lr * QV;
-      if (lr / RPC != crank) reinterpret_cast<uint4*>(sQ + lr * LD)[v] = qv[k];
-    }
-    if (n_chunks > 0) {
-      load_chunk(0, 0, 2);  // the window keys just spliced
-      cp_async_wait<0>();
-    }
-    phase_mark(ph, 5, t0);
-  } else {
+  {
     const bf* Qg = reinterpret_cast<const bf*>(P.q);
     for (int i = threadIdx.x; i < QR * VPR; i += blockDim.x) {
       const int rr = i / VPR, v = i % VPR;
@@ -823,7 +677,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
         "r"(smem_u32(sO) + threadIdx.x * BLK), "r"(BLK), "r"(bar)
         : "memory");
   }
-  if (!FQ) phase_mark(ph, 2, t0);  // (timeline) start barrier / copies issued
+  phase_mark(ph, 2, t0);  // (timeline) start barrier / copies issued
   mbar_wait(&s_mbar, 0);
 #endif
 #else
@@ -846,7 +700,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
 #endif
 #if !ATT_MERGE_PUSH
   cluster.sync();
-  if (!FQ) phase_mark(ph, 2, t0);  // (timeline) merge barrier passed
+  phase_mark(ph, 2, t0);  // (timeline) merge barrier passed
 #endif
   // merge: this CTA normalises rows [crank*QR/CS, (crank+1)*QR/CS) across the
   // cluster; every rank's (m, l, o) is gathered into registers first
@@ -881,7 +735,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
 #endif
     }
   }
-  if (!FQ && ph != nullptr) {  // (timeline) gather landed: consume one loaded value
+  if (ph != nullptr) {  // (timeline) gather landed: consume one loaded value
     if (mr[0][0] == 12345.0f) __trap();
     phase_mark(ph, 3, t0);
   }
@@ -920,7 +774,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
     u.y = *reinterpret_cast<uint32_t*>(&p1);
     *reinterpret_cast<uint2*>(out) = u;
   }
-  if (!FQ) phase_mark(ph, 4, t0);  // (timeline) outputs stored
+  phase_mark(ph, 4, t0);  // (timeline) outputs stored
 #if ATT_MERGE_PUSH
   // the outgoing copies must have read this CTA's staging before it exits
   if (threadIdx.x < ATT_CS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -931,9 +785,9 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   tstat_end(ats);
 }
 
-template <int HD, bool FQ, int CS>
+template <int HD, int CS>
 static cudaError_t attn_seg_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
-                                   const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
+                                   cudaStream_t s) {
   const int rows = P.full ? S.L : S.NRq;
   const int max_ck = (P.akey_cap + ATT_KC * CS - 1) / (ATT_KC * CS);  // chunks per CTA, upper bound
   // q + double-buffered K/V chunks (>= the merge scratch that reuses them) + keys
@@ -941,12 +795,12 @@ static cudaError_t attn_seg_launch(const Dims& D, const Sess& S, const Pass& P, 
   const size_t smem = (size_t)64 * (HD + 8) * 2 + (kv > merge ? kv : merge) + (size_t)max_ck * ATT_KC * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_seg<HD, FQ, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_attn_seg<HD, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
   dim3 grid(S.R * CS, D.nh, (rows + 63) / 64);
-  launch_k(k_attn_seg<HD, FQ, CS>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows, pr, bias, rope);
+  launch_k(k_attn_seg<HD, CS>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
   return cudaGetLastError();
 }
 
@@ -954,16 +808,16 @@ static cudaError_t attn_seg_launch(const Dims& D, const Sess& S, const Pass& P, 
 // tile) whose grid still fits one wave (2 CTAs of 89 KB / 238 registers per
 // SM): at one request (C2 block pass, 32 heads) 8-CTA clusters split the keys;
 // with several requests per session, fewer CTAs per cluster (more keys each)
-// avoid running the grid in waves.  BB_ATT_CS forces.
-static int att_cs(const Dims& D, const Sess& S, const Pass& P, bool fq) {
-  const int forced = getenv("BB_ATT_CS") != nullptr ? atoi(getenv("BB_ATT_CS")) : 0;
-  if (forced == 8 || forced == 4 || (!fq && (forced == 2 || forced == 1))) return forced;
+// avoid running the grid in waves.  Test flags (bits 4-7) force a size.
+static int att_cs(const Dims& D, const Sess& S, const Pass& P, int tflags) {
+  const int forced = (tflags >> 4) & 15;
+  if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   if (P.full) return 8;  // full passes: 1-CTA clusters measured 1.3% slower per C2 request
   const int rows = S.NRq;
   const long long per = (long long)S.R * D.nh * ((rows + 63) / 64);
-  const long long wave = 2LL * kNumSMs;
+  const long long wave = 2LL * S.n_sms;
   if (per * 8 <= wave) return 8;
-  if (fq || per * 4 <= wave) return 4;
+  if (per * 4 <= wave) return 4;
   return per * 2 <= wave ? 2 : 1;
 }
 
@@ -1380,44 +1234,32 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
   return cudaGetLastError();
 }
 
-// tcgen05 attention for hd = 128 (non-fused-QKV passes), the default;
-// BB_ATT_TC=0 selects the mma.sync kernel.  Read per launch (launches are
-// captured once into graphs).  Measured (C5 block attention 222 vs 262 us per
-// launch, C5 16.7 vs 17.9 ms/NFE; C2 attention slot 16.8 vs 19.4 us).
+// tcgen05 attention for hd = 128 in every pass (block, prefill, refresh).
+// Measured (C5 block attention 222 vs 262 us per launch for the mma.sync
+// kernel, C5 16.7 vs 17.9 ms/NFE; C2 attention slot 16.8 vs 19.4 us).
 // Cluster size for k_attn_tc (2 CTAs/SM): the largest of 8 / 4 / 2 / 1 whose
 // grid fits one wave, else 1 (splitting keys over a cluster only pays while
 // the (request, head, row tile) units alone cannot fill the GPU).  C5 full
 // passes (1536 units): CS 8 / 4 / 2 = 1020 / 829 / 731 us per launch.
-static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P) {
-  const char* f = getenv("BB_ATT_CS");
-  const int forced = f != nullptr ? atoi(f) : 0;
+static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P, int tflags) {
+  const int forced = (tflags >> 4) & 15;
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   const int rows = P.full ? S.L : S.NRq;
   const long long per = (long long)S.R * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
-  const long long wave = 2LL * kNumSMs;
+  const long long wave = 2LL * S.n_sms;
   for (int cs = 8; cs > 1; cs >>= 1)
     if (per * cs <= wave) return cs;
   return 1;
 }
 
-// Full passes (prefill / refresh) too: with the one-wave cluster rule the C2
-// full-pass attention takes 18.1 us per launch (mma.sync, 8-CTA clusters:
-// 50.6); C3 15.1 -> 14.1 ms/NFE.  BB_ATT_TC_FULL=0 keeps mma.sync there.
-static bool att_tc_on(const Sess& S, const Pass& P) {
-  (void)S;
-  const char* e = getenv("BB_ATT_TC");
-  if (e != nullptr && atoi(e) == 0) return false;
-  if (!P.full) return true;
-  const char* f = getenv("BB_ATT_TC_FULL");
-  return f == nullptr || atoi(f) != 0;
-}
-
-template <int HD, bool FQ>
+// test flag bit 0 (BB_TF_ATTN_MMA_SYNC): the mma.sync kernel at hd 128 (tests
+// compare the two tensor-core attentions; never set on the product path)
+template <int HD>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
-                               const PartRef& pr, const float* bias, const float* rope, cudaStream_t s) {
-  if constexpr (HD == 128 && !FQ) {
-    if (att_tc_on(S, P)) {
-      switch (att_cs_tc(D, S, P)) {
+                               int tflags, cudaStream_t s) {
+  if constexpr (HD == 128) {
+    if (!(tflags & 1)) {
+      switch (att_cs_tc(D, S, P, tflags)) {
         case 8: return attn_tc_launch<8>(D, S, P, st, layer, s);
         case 4: return attn_tc_launch<4>(D, S, P, st, layer, s);
         case 2: return attn_tc_launch<2>(D, S, P, st, layer, s);
@@ -1425,15 +1267,12 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
       }
     }
   }
-  switch (att_cs(D, S, P, FQ)) {
-    case 8: return attn_seg_launch<HD, FQ, 8>(D, S, P, st, layer, pr, bias, rope, s);
-    case 4: return attn_seg_launch<HD, FQ, 4>(D, S, P, st, layer, pr, bias, rope, s);
+  switch (att_cs(D, S, P, tflags)) {
+    case 8: return attn_seg_launch<HD, 8>(D, S, P, st, layer, s);
+    case 4: return attn_seg_launch<HD, 4>(D, S, P, st, layer, s);
+    case 2: return attn_seg_launch<HD, 2>(D, S, P, st, layer, s);
+    default: return attn_seg_launch<HD, 1>(D, S, P, st, layer, s);
   }
-  if constexpr (!FQ) {
-    if (att_cs(D, S, P, FQ) == 2) return attn_seg_launch<HD, false, 2>(D, S, P, st, layer, pr, bias, rope, s);
-    return attn_seg_launch<HD, false, 1>(D, S, P, st, layer, pr, bias, rope, s);
-  }
-  return cudaErrorInvalidValue;
 }
 
 // LSE-merge of the partials of the items covering (row, head).  CTA per
@@ -1521,27 +1360,14 @@ static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const De
   return cudaGetLastError();
 }
 
-bool attn_fuses_qkv(const Dims& D, const Sess& S, const Pass& P) {
-  return !uses_items(D) && !P.full && S.NRq <= 64;
-}
-
-cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
-                        const PartRef* qkv, const float* bias, const float* rope, cudaStream_t s) {
+cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, int tflags,
+                        cudaStream_t s) {
   const int max_items = P.full ? 1 : S.max_items;
   cudaError_t e = cudaErrorInvalidValue;
   dim3 cgrid(P.rows_alloc, D.nh);
   const int cthreads = D.hd < 256 ? D.hd : 256;
-  if (D.dtype == 1 && (D.hd == 64 || D.hd == 128)) {
-    PartRef none{};
-    if (qkv != nullptr) {
-      if (!attn_fuses_qkv(D, S, P)) return cudaErrorInvalidValue;
-      return D.hd == 64 ? attn_seg_hd<64, true>(D, S, P, st, layer, *qkv, bias, rope, s)
-                        : attn_seg_hd<128, true>(D, S, P, st, layer, *qkv, bias, rope, s);
-    }
-    return D.hd == 64 ? attn_seg_hd<64, false>(D, S, P, st, layer, none, nullptr, nullptr, s)
-                      : attn_seg_hd<128, false>(D, S, P, st, layer, none, nullptr, nullptr, s);
-  }
-  if (qkv != nullptr) return cudaErrorInvalidValue;
+  if (D.dtype == 1 && (D.hd == 64 || D.hd == 128))
+    return D.hd == 64 ? attn_seg_hd<64>(D, S, P, st, layer, tflags, s) : attn_seg_hd<128>(D, S, P, st, layer, tflags, s);
   if (D.dtype == 1) {
     using T = __nv_bfloat16;
     if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);

@@ -14,8 +14,6 @@
 
 namespace bb {
 
-constexpr int kNumSMs = 148;
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -1439,8 +1439,8 @@ cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, 
   return cudaGetLastError();
 }
 cudaError_t launch_copy_pages(const Dims& D, const Sess& S, const DevState& st, int with_pm, cudaStream_t s) {
-  if (D.dtype == 1) launch_k(k_copy_pages<__nv_bfloat16>, dim3(2 * kNumSMs), dim3(512), (size_t)(0), s, D, S, st, with_pm);
-  else launch_k(k_copy_pages<float>, dim3(2 * kNumSMs), dim3(512), (size_t)(0), s, D, S, st, with_pm);
+  if (D.dtype == 1) launch_k(k_copy_pages<__nv_bfloat16>, dim3(2 * S.n_sms), dim3(512), (size_t)(0), s, D, S, st, with_pm);
+  else launch_k(k_copy_pages<float>, dim3(2 * S.n_sms), dim3(512), (size_t)(0), s, D, S, st, with_pm);
   return cudaGetLastError();
 }
 cudaError_t launch_step_commit(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,

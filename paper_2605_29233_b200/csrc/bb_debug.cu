@@ -55,10 +55,6 @@ BB_API int bb_debug_gemm_tc(const void* W, const void* X, void* out, int n_out, 
   return cudaGetLastError() == cudaSuccess ? 0 : -10;
 }
 
-BB_API int bb_debug_l2_prefetch(const void* W, int n_out, int K, int kind, void* stream) {
-  return tc_debug_l2_prefetch(W, n_out, K, kind, (cudaStream_t)stream);
-}
-
 BB_API int bb_debug_gemm_simt(const float* W, const float* X, float* out, int n_out, int K, int rows, void* stream) {
   SimtGemm g{W, X, n_out, K, rows, nullptr, nullptr, out, n_out};
   return simt_gemm_launch(g, (cudaStream_t)stream) == cudaSuccess ? 0 : -10;

@@ -28,19 +28,16 @@ struct Unit {
 
 struct UnitIter {
   long long x, end, T;
-  int KB, G, c, mode, n_tiles, split;
-  __device__ UnitIter(int c_, int G_, int KB_, int n_tiles_, int mode_, int split_)
-      : c(c_), G(G_), KB(KB_), n_tiles(n_tiles_), mode(mode_), split(split_) {
+  int KB, G, c, mode, n_tiles;
+  __device__ UnitIter(int c_, int G_, int KB_, int n_tiles_, int mode_)
+      : c(c_), G(G_), KB(KB_), n_tiles(n_tiles_), mode(mode_) {
     T = (long long)n_tiles * KB;
     if (mode == 0) {
       x = (long long)c * T / G;
       end = (long long)(c + 1) * T / G;
-    } else if (mode == 1) {
+    } else {
       x = c;
       end = n_tiles;
-    } else {
-      x = c / split;  // one unit: (tile, k-slice = cluster rank)
-      end = x + 1;
     }
   }
   __device__ bool next(Unit& u) {
@@ -51,15 +48,6 @@ struct UnitIter {
       u.kb1 = KB;
       u.slot = 0;
       x += G;
-      return true;
-    }
-    if (mode == 2) {
-      const int ks = c % split;
-      u.tile = (int)x;
-      u.kb0 = (int)((long long)KB * ks / split);
-      u.kb1 = (int)((long long)KB * (ks + 1) / split);
-      u.slot = ks;
-      x = end;
       return true;
     }
     const int tile = (int)(x / KB);
@@ -88,8 +76,6 @@ struct TcCfg {
   static constexpr size_t STG = (size_t)(32 * 129 + 4 * 32 + 32 + 64 + 16) * 4;  // staging + row sums + row meta
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16 +
                                  (RED > STG ? RED : STG);
-  // cluster split-K staging of the full accumulator reuses the pipeline stages
-  static constexpr bool SPLIT_OK = (size_t)BN * 128 * 4 <= (size_t)STAGES * (A_BYTES + B_BYTES);
 };
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -268,37 +254,6 @@ __device__ __forceinline__ void head_rows_t(const GemmTcParams& p, const float (
   __syncwarp();
 }
 
-__device__ __forceinline__ void l2_prefetch_tile(const CUtensorMap* tm, int x, int y) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(tm)),
-               "r"(x), "r"(y)
-               : "memory");
-}
-
-// Issued by the 32 lanes of one warp of CTA `c` of a grid of `g_cur` CTAs:
-// one tensor prefetch per 128 x 64 weight k-block, covering the next GEMM's
-// CTA ranges c, c + g_cur, ...
-__device__ void l2pf_issue(const L2Pf& f, int c, int g_cur, int lane) {
-  if (f.tm == nullptr || f.nkb <= 0) return;
-  for (int cn = c; cn < f.G; cn += g_cur) {
-    if (f.mode == 0) {
-      const long long y0 = (long long)cn * f.T / f.G, hi = (long long)(cn + 1) * f.T / f.G;
-      const long long yend = y0 + f.nkb < hi ? y0 + f.nkb : hi;
-      for (long long y = y0 + lane; y < yend; y += 32) {
-        const long long tile = y / f.KB;
-        const int kb = (int)(y - tile * f.KB);
-        l2_prefetch_tile(f.tm, kb * 64, (int)(tile % f.n_ntiles) * 128);
-      }
-    } else {
-      // tiles cn, cn + G, ... with KB k-blocks each, first nkb of that sequence
-      for (int j = lane; j < f.nkb; j += 32) {
-        const long long t = cn + (long long)(j / f.KB) * f.G;
-        if (t >= f.T) break;
-        l2_prefetch_tile(f.tm, (j % f.KB) * 64, (int)(t % f.n_ntiles) * 128);
-      }
-    }
-  }
-}
-
 #ifndef BB_GEMM_PH
 #define BB_GEMM_PH 0  // 1: timeline-session phase marks (GemmTcParams::ph); costs ~1% when built in
 #endif
@@ -319,7 +274,6 @@ __global__ void __launch_bounds__(192)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* red = reinterpret_cast<float*>(tslot + 4);  // LM-head reduction / fused-epilogue staging
   float* stage = red;
-  float* acc_stage = reinterpret_cast<float*>(sA);   // mode 2: [BN][128] partial accumulator
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = p.n_ntiles * p.n_chunks;
@@ -354,7 +308,7 @@ __global__ void __launch_bounds__(192)
   if (warp == 0 && lane == 0) {
     const uint64_t pol_w = policy_evict_first();
     int pre = 0;
-    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
     Unit u;
     while (pre < C::STAGES && it.next(u)) {
       const int ntile = u.tile % p.n_ntiles;
@@ -386,13 +340,11 @@ __global__ void __launch_bounds__(192)
         mbar_arrive(&full[st]);
         mbar_wait(&full[st], 0);
       }
-    if (p.mode == 2) cg::this_cluster().sync();
     __syncthreads();
     if (warp == 1) {
       tc_fence_after();
       tmem_dealloc(tbase, C::TCOLS);
     }
-    if (p.mode == 2) cg::this_cluster().sync();
     tsite_end(p.tstat);
     return;
   }
@@ -405,7 +357,7 @@ __global__ void __launch_bounds__(192)
       uint32_t phase = 0;
       int issued = 0;  // global k-block counter (matches the prefetch order)
       const int pre = s_pre;
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
       Unit u;
       while (it.next(u)) {
         const int ntile = u.tile % p.n_ntiles, chunk = u.tile / p.n_ntiles;
@@ -429,8 +381,6 @@ __global__ void __launch_bounds__(192)
         }
       }
     }
-    __syncwarp();
-    l2pf_issue(p.pf, blockIdx.x, gridDim.x, lane);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
@@ -438,7 +388,7 @@ __global__ void __launch_bounds__(192)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
       Unit u;
       bool first = true;
       while (it.next(u)) {
@@ -475,7 +425,7 @@ __global__ void __launch_bounds__(192)
     const int et = threadIdx.x - 64;
     int acc = 0;
     uint32_t aphase = 0;
-    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode, p.split);
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
     Unit u;
     while (it.next(u)) {
       const int ntile = u.tile % p.n_ntiles, chunk = u.tile / p.n_ntiles;
@@ -498,15 +448,6 @@ __global__ void __launch_bounds__(192)
               if (row < rows_valid) dst[(long long)row * p.ldp] = v[j];
             }
           }
-        }
-      } else if (p.mode == 2) {
-        // cluster split-K: stage the partial accumulator; reduced after the loop
-#pragma unroll 1
-        for (int j0 = 0; j0 < BN; j0 += 32) {
-          float v[32];
-          tmem_ld32(taddr + j0, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc_stage[(j0 + j) * 128 + q * 32 + lane] = v[j];
         }
       } else if (p.epi.kind == 1) {
 #pragma unroll 1
@@ -561,35 +502,6 @@ __global__ void __launch_bounds__(192)
       if (acc == 0) aphase ^= 1;
     }
   }
-  if (p.mode == 2) {
-    // ---- cluster split-K reduction through DSMEM (rank order: deterministic)
-    cg::cluster_group cluster = cg::this_cluster();
-    __syncthreads();
-    cluster.sync();
-    if (warp >= 2) {
-      const int et = threadIdx.x - 64, q = warp & 3;
-      const int S = p.split, rank = (int)cluster.block_rank();
-      const int tile = blockIdx.x / S;
-      const int ntile = tile % p.n_ntiles, chunk = tile / p.n_ntiles;
-      const int rows_per = BN / S;
-      const int r0 = rank * rows_per;
-      const int c = q * 32 + lane;
-      for (int j0 = 0; j0 < rows_per; j0 += 32) {
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float a = 0.0f;
-          if (j0 + j < rows_per)
-            for (int qq = 0; qq < S; ++qq) a += *cluster.map_shared_rank(acc_stage + (r0 + j0 + j) * 128 + c, qq);
-          v[j] = a;
-        }
-        const int rbase = chunk * BN + r0 + j0;
-        const int rv = min(rows_valid, rbase + min(32, rows_per - j0));
-        epi_apply(p.epi, v, ntile * 128, c, et, rbase, rv, p.n_out, ntile, stage);
-      }
-    }
-    cluster.sync();
-  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -626,54 +538,6 @@ static bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t
   return r == CUDA_SUCCESS;
 }
 
-L2Pf tc_gemm_l2pf(const TcGemm& next, const CUtensorMap* tm_dev, long long bytes) {
-  L2Pf f;
-  memset(&f, 0, sizeof(f));
-  const GemmTcParams& p = next.p;
-  if (bytes <= 0 || tm_dev == nullptr || (p.mode != 0 && p.mode != 1) || next.grid <= 0) return f;
-  f.tm = tm_dev;
-  f.G = next.grid;
-  f.KB = p.KB;
-  f.n_chunks = p.n_chunks;
-  f.n_ntiles = p.n_ntiles;
-  f.mode = p.mode;
-  const long long n_tiles = (long long)p.n_ntiles * p.n_chunks;
-  f.T = p.mode == 0 ? n_tiles * p.KB : n_tiles;
-  const long long per_cta = p.mode == 0 ? (f.T + f.G - 1) / f.G : ((n_tiles + f.G - 1) / f.G) * p.KB;
-  long long nkb = bytes / ((long long)f.G * 128 * 128);
-  if (nkb > per_cta) nkb = per_cta;
-  f.nkb = (int)nkb;
-  if (f.nkb <= 0) f.tm = nullptr;
-  return f;
-}
-
-__global__ void k_l2pf_debug(L2Pf f, const char* w, long long bytes, int kind) {
-  if (kind == 0) {
-    if (threadIdx.x < 32) l2pf_issue(f, blockIdx.x, gridDim.x, threadIdx.x);
-  } else {
-    const long long chunk = 64 << 10;
-    for (long long o = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * chunk; o < bytes;
-         o += (long long)gridDim.x * blockDim.x * chunk) {
-      const long long n = bytes - o < chunk ? bytes - o : chunk;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w + o), "r"((uint32_t)n) : "memory");
-    }
-  }
-}
-
-// debug: prefetch a whole [n_out][K] bf16 weight into L2 -- kind 0 = the
-// GEMM's own tensor-tile prefetch over all its stream-K ranges, 1 = contiguous
-// 64 KB bulk prefetches
-int tc_debug_l2_prefetch(const void* W, int n_out, int K, int kind, cudaStream_t s) {
-  TcGemm g;
-  if (!tc_gemm_setup(g, W, n_out, K, W, 64, 64, 0, 0)) return -3;
-  static CUtensorMap* dmap = nullptr;
-  if (dmap == nullptr && cudaMalloc(&dmap, sizeof(CUtensorMap)) != cudaSuccess) return -10;
-  if (cudaMemcpy(dmap, &g.tmA, sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess) return -10;
-  L2Pf f = tc_gemm_l2pf(g, dmap, 1LL << 40);
-  k_l2pf_debug<<<g.grid, 128, 0, s>>>(f, (const char*)W, (long long)n_out * K * 2, kind);
-  return cudaGetLastError() == cudaSuccess ? 0 : -10;
-}
-
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN, int mode,
                    int max_grid) {
   if (BN != 64 && BN != 128 && BN != 160 && BN != 192 && BN != 256) return false;
@@ -695,33 +559,15 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
   p.plane = (long long)rows_alloc * n_out;
   const long long n_tiles = (long long)p.n_ntiles * p.n_chunks;
   const long long T = n_tiles * p.KB;
-  const int resident = kNumSMs;  // one CTA per SM (TcCfg smem budget)
-  p.split = 1;
+  const int resident = max_grid > 0 ? max_grid : 148;  // one CTA per SM (TcCfg smem budget)
   if (mode == 1) p.epi.kind = 1;  // LM-head epilogue
-  if (mode == 3) {
-    // fused epilogue: whole tiles when there are enough to keep ~100 SMs
-    // streaming (96 CTAs reach ~97% of the 148-CTA bandwidth), otherwise split
-    // K over a thread-block cluster of up to 4 CTAs (DSMEM reduction)
-    const bool split_ok = BN == 64 ? TcCfg<64>::SPLIT_OK : (BN == 128 ? TcCfg<128>::SPLIT_OK : false);
-    if (n_tiles >= 96 || !split_ok) {
-      mode = 1;
-    } else {
-      mode = 2;
-      int sp = (int)(resident / n_tiles);
-      p.split = sp >= 4 ? 4 : (sp >= 2 ? 2 : 1);
-      if (p.split == 1) mode = 1;
-    }
-    p.mode = mode;
-  }
   if (mode == 0) {
-    const int gmax = max_grid > 0 ? max_grid : kNumSMs;
+    const int gmax = resident;
     g.grid = (int)(T < gmax ? T : gmax);
-  } else if (mode == 1) {
+  } else {
     const int gmax = max_grid > 0 ? max_grid : resident;
     const long long rounds = (n_tiles + gmax - 1) / gmax;
     g.grid = (int)((n_tiles + rounds - 1) / rounds);
-  } else {
-    g.grid = (int)(n_tiles * p.split);
   }
   g.sk.T = mode == 0 ? T : 0;
   g.sk.KB = p.KB;
@@ -753,10 +599,7 @@ static cudaError_t launch_bn(const TcGemm& g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (g.p.mode == 2)
-    launch_kc(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.p.split, g.tmA, g.tmB, g.p);
-  else
-    launch_k(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.tmA, g.tmB, g.p);
+  launch_k(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.tmA, g.tmB, g.p);
   return cudaGetLastError();
 }
 

@@ -89,17 +89,6 @@ struct EpiArgs {
   int ss_ld;
 };
 
-// L2 prefetch of the NEXT GEMM's weights, issued by this GEMM's producer
-// warp once its own last TMA load is out: the first `nkb` k-blocks of every
-// range the next GEMM's CTAs will stream (stream-K ranges, mode 0; or the
-// round-robin tile sequence, mode 1), so HBM keeps streaming weights through
-// the non-GEMM kernels in between instead of idling.
-struct L2Pf {
-  const CUtensorMap* tm;  // next GEMM's weight tensor map (copy in global memory), nullptr = off
-  long long T;            // flattened k-blocks (stream-K) or tiles (mode 1)
-  int G, KB, n_chunks, n_ntiles, mode, nkb;
-};
-
 struct GemmTcParams {
   // mode 0: stream-K into fp32 partial planes (consumed by post kernels)
   // mode 1: whole tiles round-robin over a persistent grid, epilogue from TMEM
@@ -130,7 +119,6 @@ struct GemmTcParams {
   unsigned long long* klog;
   int klog_cap, klog_id;
   EpiArgs epi;
-  L2Pf pf;
 };
 
 struct TcGemm {
@@ -147,10 +135,6 @@ struct TcGemm {
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN,
                    int mode, int max_grid);
 cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s);
-// prefetch descriptor for `next` with a budget of ~`bytes` of its weights (0 = off);
-// `tm_dev` = a copy of next.tmA in device global memory (64-byte aligned)
-L2Pf tc_gemm_l2pf(const TcGemm& next, const CUtensorMap* tm_dev, long long bytes);
-int tc_debug_l2_prefetch(const void* W, int n_out, int K, int kind, cudaStream_t s);
 
 struct SimtGemm {
   const float* W;

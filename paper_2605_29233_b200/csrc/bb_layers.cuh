@@ -38,11 +38,9 @@ cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s);
 cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int ss_ld, const float* ln,
                         cudaStream_t s);
-// qkv != null: the attention prologue also finalizes the QKV GEMM's stream-K
-// partial planes (bias, RoPE, KV splice); only when attn_fuses_qkv()
-cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
-                        const PartRef* qkv, const float* bias, const float* rope, cudaStream_t s);
-bool attn_fuses_qkv(const Dims& D, const Sess& S, const Pass& P);
+// tflags: bb_session_desc.test_flags (tests only)
+cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, int tflags,
+                        cudaStream_t s);
 cudaError_t launch_attn_keys(const Dims& D, const Sess& S, const Pass& P, const DevState& st, cudaStream_t s);
 cudaError_t launch_gather_head(const Dims& D, const Sess& S, const Pass& full, const Pass& blk, const Head& H,
                                int branch_filter, cudaStream_t s);

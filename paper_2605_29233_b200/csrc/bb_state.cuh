@@ -66,6 +66,7 @@ struct Sess {
   int max_items;      // attention items per request per pass
   int ev_cap, trace, hard_cap, max_copies;
   int diag;           // diagnostics session: the last n_lp pages of each request's pool are scratch
+  int n_sms;          // SMs of the device (grid sizing)
 };
 
 struct DevState {

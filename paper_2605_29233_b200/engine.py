@@ -27,9 +27,12 @@ def _torch():
 class Session:
     def __init__(self, params, cfg, prompt_len: int, n_requests: int = 1, trace: bool = True,
                  page_size: int = 16, pages_per_item: int = 4, event_capacity: int | None = None,
-                 diagnostics: bool = False):
+                 diagnostics: bool = False, test_flags: int = 0):
         torch = _torch()
-        self.params = params
+        # no reference to `params` itself: the model's session cache
+        # (ModelParams._sessions) owns its sessions, so a session must not keep
+        # the model alive (the cache would never be collected)
+        self.dims, self.vocab = params.dims, params.vocab
         self.cfg = cfg
         self.P, self.G, self.R = prompt_len, cfg.gen_len, n_requests
         self.B = len(cfg.block_sizes)
@@ -44,7 +47,8 @@ class Session:
             tau_conf=cfg.tau_conf, tau_merge=cfg.tau_merge, tau_sync=float(cfg.tau_sync),
             refresh_interval=cfg.refresh_interval, merge_enabled=int(cfg.merge_enabled),
             sync_enabled=int(cfg.sync_enabled), page_size=page_size, pages_per_item=pages_per_item,
-            trace=int(trace), event_capacity=event_capacity, diagnostics=int(diagnostics))
+            trace=int(trace), event_capacity=event_capacity, diagnostics=int(diagnostics),
+            test_flags=int(test_flags))
         nbytes = C.c_size_t(0)
         model = params.handle()
         _lib.check(L.bb_session_workspace_bytes(model, C.byref(self.desc), C.byref(nbytes)),
@@ -91,12 +95,15 @@ class Session:
     # ---------------------------------------------------------------- inputs
     def set_inputs(self, prompts, targets):
         """prompts [R, P], targets [R, G]: host arrays (copied H2D on the session
-        stream) or CUDA tensors (copied D2D)."""
+        stream) or CUDA tensors (copied D2D after the producing stream's work)."""
         torch = _torch()
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             for dst, src in ((self.v_prompt, prompts), (self.v_target, targets)):
                 if isinstance(src, torch.Tensor) and src.is_cuda:
-                    dst.copy_(src.to(torch.int32), non_blocking=True)
+                    t = src if src.dtype == torch.int32 else src.to(torch.int32)
+                    dst.copy_(t, non_blocking=True)
+                    t.record_stream(self.stream)
                 else:
                     t = torch.from_numpy(np.ascontiguousarray(np.asarray(src), dtype=np.int32)).pin_memory()
                     dst.copy_(t, non_blocking=True)
@@ -134,7 +141,7 @@ class Session:
         _lib.check(_lib.lib().bb_refresh(self.h, C.c_void_p(self.stream.cuda_stream)), "bb_refresh")
 
     def kv_numel(self) -> int:
-        d = self.params.dims
+        d = self.dims
         return d.layers * self.Lseq * 2 * d.n_kv_heads * d.hd
 
     def kv_gather(self, r: int, k: int, dst):
@@ -148,7 +155,7 @@ class Session:
     def sqdiff_norm(self, a, b=None) -> float:
         torch = _torch()
         out = torch.zeros(1, dtype=torch.float64, device="cuda")
-        _lib.check(_lib.lib().bb_sqdiff_norm(C.c_void_p(a.data_ptr()), None if b is None else C.c_void_p(b.data_ptr()),
+        _lib.check(_lib.lib().bb_sqdiff_norm(self.h, C.c_void_p(a.data_ptr()), None if b is None else C.c_void_p(b.data_ptr()),
                                              a.numel(), C.c_void_p(out.data_ptr()),
                                              C.c_void_p(self.stream.cuda_stream)), "bb_sqdiff_norm")
         self.stream.synchronize()

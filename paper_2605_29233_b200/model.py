@@ -259,6 +259,11 @@ class ModelParams:
     wo: tuple = ()
     w_head: np.ndarray | None = None
     _handle: list = field(default_factory=lambda: [None], repr=False)
+    _sessions: dict = field(default_factory=dict, repr=False)  # device sessions (scheduler.get_session)
+
+    def clear_sessions(self) -> None:
+        """Drop this model's cached device sessions (their workspaces free with them)."""
+        self._sessions.clear()
 
     def desc(self) -> _lib.ModelDesc:
         d = self.dims
@@ -288,6 +293,7 @@ class ModelParams:
 
     def __del__(self):
         try:
+            self._sessions.clear()
             if self._handle[0] is not None and _lib._lib is not None:
                 _lib._lib.bb_model_destroy(self._handle[0])
         except Exception:

@@ -13,7 +13,6 @@ from __future__ import annotations
 
 import ctypes as C
 import json
-import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -106,9 +105,6 @@ def select_eos_winner(branches, rows, vocab: Vocab) -> BranchState:
 
 
 # -------------------------------------------------------------- sessions
-_SESSIONS: "weakref.WeakKeyDictionary[ModelParams, dict]" = weakref.WeakKeyDictionary()
-
-
 def _cfg_key(cfg: SchedulerConfig, P: int, R: int, trace: bool):
     return (tuple(cfg.block_sizes), float(cfg.tau_conf), float(cfg.tau_merge), float(cfg.tau_sync),
             int(cfg.refresh_interval), int(cfg.gen_len), bool(cfg.merge_enabled), bool(cfg.sync_enabled),
@@ -117,8 +113,9 @@ def _cfg_key(cfg: SchedulerConfig, P: int, R: int, trace: bool):
 
 def get_session(params: ModelParams, cfg: SchedulerConfig, prompt_len: int, n_requests: int = 1,
                 trace: bool = True) -> Session:
-    """Cached device session for (params, cfg, prompt_len, n_requests)."""
-    cache = _SESSIONS.setdefault(params, {})
+    """Cached device session for (params, cfg, prompt_len, n_requests); the
+    cache lives on the model (freed with it, or by params.clear_sessions())."""
+    cache = params._sessions
     key = _cfg_key(cfg, prompt_len, n_requests, trace)
     s = cache.get(key)
     if s is None:

@@ -27,7 +27,6 @@ for seed in (1000, 1001):
     s.set_inputs(*inputs(seed * 100)); s.launch()
 s.stream.synchronize()
 s.klog(reset=True); s.gemm_stats(reset=True)
-import ctypes as _C0; from paper_2605_29233_b200 import _lib as _L0; _L0.lib().bb_session_lsk_prof(s.h, (_C0.c_ulonglong * 64)(), 1, _C0.c_void_p(s.stream.cuda_stream))
 import ctypes as _C; from paper_2605_29233_b200 import _lib as _L; _L.lib().bb_session_phase_stats(s.h, (_C.c_ulonglong * 16)(), 1, _C.c_void_p(s.stream.cuda_stream))
 s.set_inputs(*inputs(100200))
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -58,7 +57,7 @@ json.dump({"kernels": {k: {"n": n, "ns": ns} for k, (n, ns) in rows}, "nfe": nfe
 gs = s.gemm_stats()
 for k, name in ((5, "attn block: duration after PDL wait"), (6, "attn block: CTA start spread"),
                 (13, "attn full: duration after PDL wait"),
-                (0, "gemm qkv"), (1, "gemm o"), (2, "gemm gate_up"), (3, "gemm down"), (12, "layer_stream kernel")):
+                (0, "gemm qkv"), (1, "gemm o"), (2, "gemm gate_up"), (3, "gemm down")):
     if gs[k][4]:
         print(f"live {name:40s} {gs[k][3] / gs[k][4] / 1e3:8.2f} us avg over {gs[k][4]} launches")
 import ctypes as C
@@ -66,26 +65,8 @@ from paper_2605_29233_b200 import _lib
 ph = (C.c_ulonglong * 16)()
 _lib.lib().bb_session_phase_stats(s.h, ph, 0, C.c_void_p(s.stream.cuda_stream))
 if ph[0]:
-    names_ph = ["rows+keys loaded", "FQ: phase-A loads / merge copies issued", "FQ: splice / merge blocks received",
-                "FQ: cluster barrier / outputs stored", "chunk0 landed", "chunk loop done", "end"]
+    names_ph = ["rows+keys loaded", "merge copies issued", "merge blocks received",
+                "outputs stored", "chunk0 landed", "chunk loop done", "end"]
     print("attention phase offsets (avg us from PDL release): " +
           ", ".join(f"{n} {ph[i + 1] / ph[0] / 1e3:.2f}" for i, n in enumerate(names_ph)))
 
-ph = (C.c_ulonglong * 16)()
-_lib.lib().bb_session_phase_stats(s.h, ph, 0, C.c_void_p(s.stream.cuda_stream))
-if ph[8]:
-    nm = ["dep wait returned (MMA thr)", "first stage landed", "last MMA issued", "first tile stored", "end",
-          "first B issued", "dep wait returned (producer)"]
-    print(f"gemm kind {os.environ.get('BB_GPH_KIND', '1')} phases (avg us from CTA entry): " +
-          ", ".join(f"{n} {ph[9 + i] / ph[8] / 1e3:.2f}" for i, n in enumerate(nm)))
-
-pr = (C.c_ulonglong * 64)()
-_lib.lib().bb_session_lsk_prof(s.h, pr, 0, C.c_void_p(s.stream.cuda_stream))
-if pr[63]:
-    n = pr[63]
-    ev = ["planes written", "step1 barrier", "step1 done", "step2 barrier", "step2 done", "inputs released",
-          "step1 op returned", "step1 fenced"]
-    for gi in range(4):
-        vals = [pr[8 * gi + k] / n / 1e3 for k in range(8)]
-        if any(vals):
-            print(f"lsk gemm {gi}: " + ", ".join(f"{e} {v:.2f}" for e, v in zip(ev, vals)))

@@ -251,38 +251,33 @@ def _llada_params(g, dtype, spike_gain):
     ("llada_tiny_bf16", "bf16", 0.0, 2e-2), ("dream_tiny_bf16", "bf16", 0.0, 2e-2),
     ("llada_tiny_bf16", "bf16", 33.0, 1e-1), ("dream_tiny_bf16", "bf16", 33.0, 1e-1),
     ("llada_tiny_f32", "f32", 33.0, 1e-4)])
-@pytest.mark.parametrize("lsk", ["0", "1"])
-def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol, lsk, monkeypatch):
+def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol):
     """One block step after prefill (the block pass: window KV splice into the
     branches' aliased prefill pages, segment-masked attention over shared
     pages, LM head) vs the oracle's block_forward of every active branch on
     the prefill cache (model.py:331-343).  Same tolerances as the prefill
-    test.  lsk=1: the block pass runs the layer-stream kernels (BB_LSK=1,
-    bf16 only; fp32 mode has no tensor-core path and ignores it)."""
-    monkeypatch.setenv("BB_LSK", lsk)
+    test."""
     _block_step_vs_oracle(LLADA[name], None, dtype, spike_gain, tol, name)
 
 
 @pytest.mark.parametrize("tc,cs,kvh,gain,tol", [("0", "", 2, 0.0, 2e-2), ("1", "", 2, 0.0, 2e-2), ("1", "1", 2, 0.0, 2e-2),
                                                 ("0", "1", 2, 0.0, 2e-2), ("1", "", 1, 0.0, 2e-2),
                                                 ("1", "", 2, 33.0, 1e-1), ("0", "", 2, 33.0, 1e-1)])
-def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol, monkeypatch):
+def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol):
     """The block step at head_dim 128 (the LLaDA-8B head size; the tiny
     fixtures use 64), with the tcgen05 attention (the default, S and O in
-    TMEM) and with the mma.sync attention (BB_ATT_TC=0), against the oracle at the bf16
+    TMEM) and with the mma.sync attention (test flag 1), against the oracle at the bf16
     tolerance of the block-step test.  cs=1: one CTA per (head, row tile)
     takes every key (several chunks: the online-softmax rescale path).
     kvh=1: grouped-query attention (2 query heads share one KV head).  gain 33:
     the spike epilogue (x34 on raw-logit error) at the prefill test's tolerance."""
-    monkeypatch.setenv("BB_ATT_TC", tc)
-    if cs:
-        monkeypatch.setenv("BB_ATT_CS", cs)
+    flags = (0 if tc == "1" else 1) | ((int(cs) if cs else 0) << 4)
     g = LLADA["llada_tiny_bf16"]
     _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128), "bf16", gain, tol,
-                          f"hd128 tc={tc} cs={cs or 'auto'} kvh={kvh}")
+                          f"hd128 tc={tc} cs={cs or 'auto'} kvh={kvh}", test_flags=flags)
 
 
-def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name):
+def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name, test_flags=0):
     from oracle import bb_oracle as O
     from paper_2605_29233_b200.engine import Session
     if arch_override:
@@ -296,7 +291,7 @@ def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name):
     worst_lp, worst_lse, agree, n = 0.0, 0.0, 0, 0
     for seed in g["seeds"][:3]:
         task = bb.make_task(seed, P, G, params.vocab)
-        s = Session(params, cfg, P, 1)
+        s = Session(params, cfg, P, 1, test_flags=test_flags)
         s.set_inputs(task.prompt[None], task.target[None])
         s.prefill()
         st = s.fetch(trace=False)
@@ -329,28 +324,6 @@ def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name):
     assert n > 0
     assert worst_lp <= tol and worst_lse <= tol
     assert agree >= n - max(1, n // 20)
-
-
-@pytest.mark.parametrize("name", ["llada_tiny_bf16", "dream_tiny_bf16"])
-def test_fused_qkv_attention_equals_separate_finalize(name, monkeypatch):
-    """The block-pass attention that finalizes the QKV partial planes in its
-    prologue (bias, RoPE, KV splice, q through DSMEM) is bit-identical to the
-    separate post_qkv kernel + attention (the default; BB_FQ=1 selects the
-    fused prologue): same rounding points, same key order."""
-    from paper_2605_29233_b200.engine import Session
-    g = LLADA[name]
-    params = llada_model(g, "bf16")
-    cfg = cfg_from(g["config"])
-    outs = []
-    for fq in ("1", "0"):
-        monkeypatch.setenv("BB_FQ", fq)
-        s = Session(params, cfg, g["prompt_len"], 2)
-        tasks = [bb.make_task(seed, g["prompt_len"], g["gen_len"], params.vocab) for seed in g["seeds"][:2]]
-        s.set_inputs(np.stack([t.prompt for t in tasks]), np.stack([t.target for t in tasks]))
-        s.launch()
-        outs.append(s.fetch())
-    for key in ("ctrl", "tokens", "branch", "events"):
-        assert np.array_equal(outs[0][key], outs[1][key]), key
 
 
 @pytest.mark.parametrize("name", list(VANILLA))
