@@ -81,6 +81,9 @@ typedef struct {
   int diagnostics;     /* 1: reserve scratch KV pages for bb_fresh_kv (log_consistency) */
   int test_flags;      /* tests only (0 on the product path): bit 0 = mma.sync attention at
                           head_dim 128; bits 4-7 = forced attention cluster size */
+  int logits;          /* 1: the LM head also keeps raw logits (bb_head_logits; forward observers) */
+  int seam;            /* 1: step-operator seam session (bb_seam_*): private pages per branch */
+  int hard_cap;        /* > 0: override the forward cap 4*G*B+16 (scheduler.py:310; tests) */
 } bb_session_desc;
 
 #define BB_VIEW_TOKENS 0   /* int32 [R][B][L]      branch rows              */
@@ -144,6 +147,25 @@ BB_API int bb_kv_gather(void* sess, int r, int k, float* dst, void* stream);
    session state (the pass writes into reserved scratch pages; needs
    diagnostics = 1 in the session desc) */
 BB_API int bb_fresh_kv(void* sess, int r, int k, float* dst, void* stream);
+/* ---- step-operator seams (model.py:322-343 full_forward / block_forward,
+   scheduler.py:80-89 init_full_forward, :116-131 batched_block_forward) on a
+   seam session (desc.seam = 1).  Rows, windows and targets are written through
+   the TOKENS / BRANCH / TARGET views; caches through bb_kv_scatter. */
+/* every branch of every request gets its own private pages (no aliasing) */
+BB_API int bb_seam_init(void* sess, void* stream);
+/* full = 0: block_forward of each branch in branch_mask over its window
+   [start, end) and its current pages (the window's K/V rewritten in place);
+   full = 1: full_forward of each branch in branch_mask (every position's K/V,
+   head over every masked position; slot j of the branch = position j).
+   use_target = 0: no agreement boost (target None, model.py:249-251). */
+BB_API int bb_seam_forward(void* sess, int full, int branch_mask, int use_target, void* stream);
+/* kv_vectorize inverse (model.py:346-352): fp32 [layers][L][2][kv_dim] (device)
+   into branch k's pages of request r, rounded to the model dtype */
+BB_API int bb_kv_scatter(void* sess, int r, int k, const float* src, void* stream);
+/* DenoiseOutput of the last head pass (model.py:160-170): logits / probs fp32
+   [head rows][n_out] (device; masked head slots written, others untouched).
+   Needs desc.logits = 1 or desc.seam = 1. */
+BB_API int bb_head_logits(void* sess, float* logits, float* probs, void* stream);
 /* out[0] = ||a - b||_2 (b may be NULL), fp64 accumulation in a fixed order
    (partial sums in the session's workspace) */
 BB_API int bb_sqdiff_norm(void* sess, const float* a, const float* b, long long n, double* out, void* stream);

@@ -12,8 +12,10 @@ from .decoding import (DecodeConfig, GenerationResult, NfeCounter, TraceEvent, B
                        confidence_transition, single_branch_decode, vanilla_decode)
 from .errors import ConfigError, ContractError, RunawayError, StateError
 from .model import (BlockWindow, DenoiseOutput, KvCache, ModelDims, ModelParams, SequenceRow, Task, Vocab,
-                    build_model, make_task, exact_match, serialize_params, LLADA_8B, LLADA_8B_VOCAB, DREAM_7B,
-                    DREAM_7B_VOCAB)
-from .scheduler import (SchedulerConfig, merge_sync, read_trace, run_blockbatch, run_batch, write_trace)
+                    block_forward, build_model, full_forward, kv_vectorize, make_task, exact_match, serialize_params,
+                    LLADA_8B, LLADA_8B_VOCAB, DREAM_7B, DREAM_7B_VOCAB)
+from .scheduler import (PackedQuery, SchedulerConfig, batched_block_forward, get_active_branches, init_full_forward,
+                        merge_sync, pack_active_blocks, read_trace, run_blockbatch, run_batch, select_eos_winner,
+                        write_trace)
 
 __version__ = "0.1.0"

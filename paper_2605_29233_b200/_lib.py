@@ -45,7 +45,8 @@ class SessionDesc(C.Structure):
                 ("tau_merge", C.c_float), ("tau_sync", C.c_float), ("refresh_interval", C.c_int),
                 ("merge_enabled", C.c_int), ("sync_enabled", C.c_int), ("page_size", C.c_int),
                 ("pages_per_item", C.c_int), ("trace", C.c_int), ("event_capacity", C.c_int),
-                ("diagnostics", C.c_int), ("test_flags", C.c_int)]
+                ("diagnostics", C.c_int), ("test_flags", C.c_int), ("logits", C.c_int), ("seam", C.c_int),
+                ("hard_cap", C.c_int)]
 
 
 ARCH_REF, ARCH_LLADA = 0, 1
@@ -90,6 +91,10 @@ SIGNATURES = {
     "bb_block_step_part": (i32, [vp, i32, vp]),
     "bb_kv_gather": (i32, [vp, i32, i32, vp, vp]),
     "bb_fresh_kv": (i32, [vp, i32, i32, vp, vp]),
+    "bb_seam_init": (i32, [vp, vp]),
+    "bb_seam_forward": (i32, [vp, i32, i32, i32, vp]),
+    "bb_kv_scatter": (i32, [vp, i32, i32, vp, vp]),
+    "bb_head_logits": (i32, [vp, vp, vp, vp]),
     "bb_sqdiff_norm": (i32, [vp, vp, vp, i64, vp, vp]),
     "bb_commit_probs": (i32, [vp, i32, i32, vp, vp, f32, vp, vp, vp]),
     "bb_merge_sync_maps": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, f32, f32, i32, i32, vp, i32, vp, vp, vp,

@@ -236,6 +236,7 @@ static void plan(Session* s, char* base, bool dry) {
   H.tgt = c.take<int>(rb);
   H.hpart = c.take<float4>((long long)rb * D.n_vtiles);
   H.logits = D.dtype == BB_DTYPE_F32 ? c.take<float>((long long)rb * D.n_out) : nullptr;
+  H.raw = (D.dtype == BB_DTYPE_BF16 && (s->desc.logits || s->desc.seam)) ? c.take<float>((long long)rb * D.n_out) : nullptr;
   H.res_conf = c.take<float>(rb);
   H.res_arg = c.take<int>(rb);
   H.res_m = c.take<float>(rb);
@@ -379,6 +380,7 @@ static int setup_gemms(Session* s) {
       return BB_ERR_CONFIG;
     GemmTcParams& p = s->head_tc.p;
     p.head_part = s->H.hpart;
+    p.raw_out = s->H.raw;
     p.boost = s->H.boost;
     p.tgt = s->H.tgt;
     p.head_scale = D.head_scale;
@@ -701,7 +703,7 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.max_items = S.B * ((S.n_lp + S.ch_block - 1) / S.ch_block) + 2 * S.B + 4;
   S.ev_cap = d->event_capacity > 0 ? d->event_capacity : 32768;
   S.trace = d->trace;
-  S.hard_cap = 4 * S.G * S.B + 16;  // scheduler.py:310
+  S.hard_cap = d->hard_cap > 0 ? d->hard_cap : 4 * S.G * S.B + 16;  // scheduler.py:310
   S.max_copies = S.B * (maxb / S.ps + 2);
   const int NR = S.NR;
   s->gb.BN = NR <= 64 ? 64 : (NR <= 128 ? 128 : 256);
@@ -946,6 +948,52 @@ BB_API int bb_fresh_kv(void* sess, int r, int k, float* dst, void* stream) {
   CK(forward(s, s->full, s->gf, st));
   CK(launch_kv_gather(s->D, s->S, s->st, r, k, dst, st));
   CK(launch_fresh_restore(s->S, s->st, r, k, s->fresh_save, st));
+  return BB_OK;
+}
+
+BB_API int bb_seam_init(void* sess, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !s->desc.seam) return BB_ERR_CONTRACT;
+  CK(launch_seam_init(s->D, s->S, s->st, (cudaStream_t)stream));
+  return BB_OK;
+}
+
+BB_API int bb_seam_forward(void* sess, int full, int branch_mask, int use_target, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !s->desc.seam || branch_mask <= 0 || branch_mask >= (1 << s->S.B)) return BB_ERR_CONTRACT;
+  const Dims& D = s->D;
+  const Sess& S = s->S;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!full) {
+    CK(launch_seam_block_pack(D, S, s->st, s->blk, s->H, branch_mask, use_target, st));
+    CK(launch_attn_keys(D, S, s->blk, s->st, st));
+    CK(forward(s, s->blk, s->gb, st));
+  } else {
+    CK(cudaMemsetAsync(s->H.masked, 0, (size_t)s->blk.rows_alloc * 4, st));
+    for (int k = 0; k < S.B; ++k) {
+      if (!((branch_mask >> k) & 1)) continue;
+      CK(launch_seam_full_pack(D, S, s->st, s->full, s->blk, s->H, k, use_target, st));
+      CK(launch_attn_keys(D, S, s->full, s->st, st));
+      CK(forward(s, s->full, s->gf, st));
+      CK(launch_gather_head(D, S, s->full, s->blk, s->H, k, st));
+    }
+  }
+  CK(head(s, st));
+  return BB_OK;
+}
+
+BB_API int bb_kv_scatter(void* sess, int r, int k, const float* src, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !src || r < 0 || r >= s->S.R || k < 0 || k >= s->S.B) return BB_ERR_CONTRACT;
+  CK(launch_kv_scatter(s->D, s->S, s->st, r, k, src, (cudaStream_t)stream));
+  return BB_OK;
+}
+
+BB_API int bb_head_logits(void* sess, float* logits, float* probs, void* stream) {
+  Session* s = (Session*)sess;
+  if (!s || !logits || !probs) return BB_ERR_CONTRACT;
+  if (s->D.dtype == BB_DTYPE_BF16 && s->H.raw == nullptr) return fail(BB_ERR_CONFIG, "bb_head_logits needs desc.logits");
+  CK(launch_head_logits(s->D, s->blk, s->H, logits, probs, (cudaStream_t)stream));
   return BB_OK;
 }
 

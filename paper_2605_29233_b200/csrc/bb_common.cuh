@@ -14,6 +14,16 @@
 
 namespace bb {
 
+// LM-head logit of one (position, vocab) pair before the target boost
+// (model.py:306-309): raw = (h . w_v) * head_scale, then the synthetic spike
+// raw + gain * max(0, raw - cut).  One definition for every kernel that
+// evaluates it (fused head epilogue, fp32 head, merge recomputation, logits
+// materialisation), so all of them round identically.
+__device__ __forceinline__ float head_logit(float dot, float hs, float sc, float sg) {
+  const float raw = dot * hs;
+  return raw + sg * fmaxf(0.0f, raw - sc);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -308,6 +308,11 @@ __device__ __forceinline__ long long kv_row_off(const Dims& D, const Sess& S, co
 __device__ void slot_boost(const Dims& D, const Sess& S, const int* rw, const int* target, int pos, float* boost,
                            int* tgt) {
   const int mask_id = D.V + 1;
+  if (pos < S.P || target == nullptr) {  // prompt position (seams) / no target: not predictable (model.py:310-317)
+    *boost = 0.0f;
+    *tgt = -1;
+    return;
+  }
   const int t = target[pos - S.P];
   const int lo = max(pos - D.radius, 0), hi = min(pos + D.radius + 1, S.L);
   int nc = 0, nm = 0;
@@ -515,6 +520,100 @@ __global__ void k_prefill_post(Dims D, Sess S, DevState st, Pass blk, Head H) {
 }
 
 // ------------------------------------------------------------------ block step
+// Block pass of the branches in `active` (all threads call; thread 0 does
+// the page work): copy-on-write of the window pages (model.py:289
+// copy-then-write), the SIMT attention items (active branches grouped by
+// physical page), the per-branch row ranges and the head slots (window
+// positions; masked ones report to the LM head).
+__device__ void pack_block_pass(RC& c, int active, const Pass& blk, const Head& H, const int* target) {
+  const Dims& D = *c.D;
+  const Sess& S = *c.S;
+  const int r = c.r;
+  if (threadIdx.x == 0) {
+    c.ctrl[C_NCOPY] = 0;
+    if (active) {
+      for (int k = 0; k < S.B; ++k) {
+        if (!((active >> k) & 1) || c.B_(k, B_START) >= c.B_(k, B_END)) continue;
+        const int lp0 = lp_of(S, c.B_(k, B_START)), lp1 = lp_of(S, c.B_(k, B_END) - 1);
+        for (int lp = lp0; lp <= lp1; ++lp) c.write_intent(k, lp, true);
+      }
+      // SIMT attention items: the logical pages split into fixed runs of
+      // ch_block pages; active branches whose run maps to the same physical
+      // pages share one item.  A row's key partition (and so its partials'
+      // combine order) is the same whatever pages its branch shares, so a
+      // branch's block forward is bitwise the same batched or alone
+      // (scheduler.py:116-131, test_scheduler.py:72-91).
+      int n_items = 0, shared_pages = 0;
+      const int n_runs = uses_items(D) ? (S.n_lp + S.ch_block - 1) / S.ch_block : 0;
+      for (int run = 0; run < n_runs; ++run) {
+        const int lp0 = run * S.ch_block, lp1 = min(lp0 + S.ch_block, S.n_lp);
+        int done_mask = 0;
+        for (int k = 0; k < S.B; ++k) {
+          if (!((active >> k) & 1) || ((done_mask >> k) & 1)) continue;
+          int m = 0;
+          for (int k2 = k; k2 < S.B; ++k2) {
+            if (!((active >> k2) & 1)) continue;
+            bool same = true;
+            for (int lp = lp0; lp < lp1 && same; ++lp) same = c.pt(k2)[lp] == c.pt(k)[lp];
+            if (same) m |= 1 << k2;
+          }
+          done_mask |= m;
+          if (__popc(m) > 1) shared_pages += lp1 - lp0;
+          if (n_items < S.max_items) {
+            int* ni = blk.items + ((long long)r * S.max_items + n_items) * ITW;
+            ni[0] = m;
+            ni[1] = lp0;
+            ni[2] = lp1;
+            ni[3] = k;
+            ++n_items;
+          } else {
+            c.ctrl[C_STATUS] = BB_ERR_STATE;
+          }
+        }
+      }
+      blk.n_items[r] = n_items;
+      c.ctrl[C_SHARED_PAGES] = shared_pages;
+      *blk.skip = 0;
+      *H.skip = 0;
+    } else {
+      blk.n_items[r] = 0;
+    }
+    int rows = 0;
+    for (int k = 0; k < MAXB; ++k) {
+      const bool a = k < S.B && ((active >> k) & 1);
+      blk.rng_off[r * MAXB + k] = r * S.NRq + (k < S.B ? S.off[k] : 0);
+      blk.rng_cnt[r * MAXB + k] = a ? c.B_(k, B_END) - c.B_(k, B_START) : 0;
+      rows += blk.rng_cnt[r * MAXB + k];
+    }
+    c.ctrl[C_BLOCK_ROWS] = rows;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S.NRq; i += blockDim.x) {
+    const int slot = r * S.NRq + i;
+    int k = -1;
+    for (int kk = 0; kk < S.B; ++kk)
+      if (i >= S.off[kk] && i < S.off[kk] + S.bs[kk]) k = kk;
+    int pos = -1;
+    if (k >= 0 && ((active >> k) & 1)) {
+      const int j = i - S.off[k];
+      if (c.B_(k, B_START) + j < c.B_(k, B_END)) pos = c.B_(k, B_START) + j;
+    }
+    blk.slot_req[slot] = r;
+    blk.slot_br[slot] = k < 0 ? 0 : k;
+    blk.slot_pos[slot] = pos;
+    const int tok = pos >= 0 ? c.rows[k * S.L + pos] : 0;
+    blk.slot_tok[slot] = tok;
+    blk.slot_kvoff[slot] = pos >= 0 ? kv_row_off(D, S, c.st, r, k, pos) : 0;
+    const int msk = pos >= 0 && tok == c.mask_id;
+    H.masked[slot] = msk;
+    if (msk) slot_boost(D, S, c.rows + k * S.L, target, pos, &H.boost[slot], &H.tgt[slot]);
+    else {
+      H.boost[slot] = 0.0f;
+      H.tgt[slot] = -1;
+    }
+  }
+}
+
 __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
   pdl_enter();
   klog_mark(D.klog, D.klog_cap, 12);
@@ -548,107 +647,97 @@ __global__ void k_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H) {
   const int active = s_active;
   if (threadIdx.x == 0) {
     c.ctrl[C_ACTIVE_MASK] = active;
-    c.ctrl[C_NCOPY] = 0;
     if (active) {
-      // copy-on-write of the pages the window rows will write (model.py:289 copy-then-write)
-      for (int k = 0; k < S.B; ++k) {
-        if (!((active >> k) & 1)) continue;
-        const int lp0 = lp_of(S, c.B_(k, B_START)), lp1 = lp_of(S, c.B_(k, B_END) - 1);
-        for (int lp = lp0; lp <= lp1; ++lp) c.write_intent(k, lp, true);
-      }
-      // attention items (SIMT path): group active branches by physical page, runs of <= ch_block pages
-      int n_items = 0;
-      const int n_lp_items = uses_items(D) ? S.n_lp : 0;
-      int open_mask[MAXB], open_idx[MAXB], n_open = 0;
-      int shared_pages = 0;
-      for (int lp = 0; lp < n_lp_items; ++lp) {
-        int done_mask = 0;
-        for (int k = 0; k < S.B; ++k) {
-          if (!((active >> k) & 1) || ((done_mask >> k) & 1)) continue;
-          const int p = c.pt(k)[lp];
-          int m = 0;
-          for (int k2 = k; k2 < S.B; ++k2)
-            if (((active >> k2) & 1) && c.pt(k2)[lp] == p) m |= 1 << k2;
-          done_mask |= m;
-          if (__popc(m) > 1) ++shared_pages;
-          int slot = -1;
-          for (int o = 0; o < n_open; ++o)
-            if (open_mask[o] == m) slot = o;
-          int* itp = slot >= 0 ? blk.items + ((long long)r * S.max_items + open_idx[slot]) * ITW : nullptr;
-          if (itp != nullptr && itp[2] == lp && itp[2] - itp[1] < S.ch_block) {
-            itp[2] = lp + 1;
-          } else if (n_items < S.max_items) {
-            int* ni = blk.items + ((long long)r * S.max_items + n_items) * ITW;
-            ni[0] = m;
-            ni[1] = lp;
-            ni[2] = lp + 1;
-            ni[3] = k;
-            if (slot >= 0) open_idx[slot] = n_items;
-            else if (n_open < MAXB) {
-              open_mask[n_open] = m;
-              open_idx[n_open++] = n_items;
-            } else {
-              // evict the oldest open run
-              for (int o = 1; o < n_open; ++o) {
-                open_mask[o - 1] = open_mask[o];
-                open_idx[o - 1] = open_idx[o];
-              }
-              open_mask[n_open - 1] = m;
-              open_idx[n_open - 1] = n_items;
-            }
-            ++n_items;
-          } else {
-            c.ctrl[C_STATUS] = BB_ERR_STATE;
-          }
-        }
-      }
-      blk.n_items[r] = n_items;
-      c.ctrl[C_SHARED_PAGES] = shared_pages;
       c.ctrl[C_NFE1] += 1;
       c.ctrl[C_SINCE_REFRESH] += 1;
       c.ctrl[C_LAST_ACTIVE] = active;
       c.emit(EV_BLOCK, -1, active);
-      *blk.skip = 0;
-      *H.skip = 0;
-    } else {
-      blk.n_items[r] = 0;
     }
-    int rows = 0;
-    for (int k = 0; k < MAXB; ++k) {
-      const bool a = k < S.B && ((active >> k) & 1);
-      blk.rng_off[r * MAXB + k] = r * S.NRq + (k < S.B ? S.off[k] : 0);
-      blk.rng_cnt[r * MAXB + k] = a ? c.B_(k, B_END) - c.B_(k, B_START) : 0;
-      rows += blk.rng_cnt[r * MAXB + k];
+  }
+  pack_block_pass(c, active, blk, H, st.target + (long long)r * S.G);
+  store_request(c);
+}
+
+// ------------------------------------------------------------------ step-operator seams
+// Seam sessions (model.py:322-343 full_forward / block_forward, scheduler.py:
+// 80-89 init_full_forward, 116-131 batched_block_forward): every branch owns
+// private pages [k*n_lp, (k+1)*n_lp) (the caller loads its cache into them);
+// no NFE accounting, no events.
+__global__ void k_seam_init(Dims D, Sess S, DevState st) {
+  pdl_enter();
+  const int r = blockIdx.x;
+  if (threadIdx.x < C_WORDS) st.ctrl[(long long)r * C_WORDS + threadIdx.x] = 0;
+  for (int i = threadIdx.x; i < S.pool; i += blockDim.x) {
+    const bool own = i < S.B * S.n_lp;
+    st.refc[(long long)r * S.pool + i] = own ? 1 : 0;
+    // free stack: the pages no branch owns (diagnostics scratch excluded)
+    const int n_free = S.pool - S.B * S.n_lp - (S.diag ? S.n_lp : 0);
+    if (i < n_free) st.freel[(long long)r * S.pool + i] = S.B * S.n_lp + i;
+  }
+  for (int i = threadIdx.x; i < S.B * S.n_lp; i += blockDim.x) st.pt[(long long)r * S.B * S.n_lp + i] = i;
+  if (threadIdx.x == 0) st.free_top[r] = S.pool - S.B * S.n_lp - (S.diag ? S.n_lp : 0);
+}
+
+// block_forward of the branches in `mask` over their windows [start, end)
+// (whether or not the window holds a mask: the reference recomputes the
+// window's K/V regardless, model.py:331-343)
+__global__ void k_seam_block_pack(Dims D, Sess S, DevState st, Pass blk, Head H, int mask, int use_target) {
+  pdl_enter();
+  RC_SETUP();
+  load_request(c);
+  pack_block_pass(c, mask, blk, H, use_target ? st.target + (long long)c.r * S.G : nullptr);
+  if (threadIdx.x == 0) {
+    *blk.skip = 0;
+    *H.skip = 0;
+  }
+  store_request(c);
+}
+
+// full_forward of branch k (all L positions from an empty cache); the head
+// slots of branch k report every masked position (slot j <-> position j)
+__global__ void k_seam_full_pack(Dims D, Sess S, DevState st, Pass full, Pass blk, Head H, int k, int use_target) {
+  pdl_enter();
+  RC_SETUP();
+  const int r = c.r;
+  load_request(c);
+  if (threadIdx.x == 0) {
+    for (int kk = 0; kk < MAXB; ++kk) {
+      full.rng_off[r * MAXB + kk] = r * S.L;
+      full.rng_cnt[r * MAXB + kk] = kk == k ? S.L : 0;
     }
-    c.ctrl[C_BLOCK_ROWS] = rows;
+    full.n_items[r] = 1;
+    int* it = full.items + (long long)r * ITW;
+    it[0] = 1 << k;
+    it[1] = 0;
+    it[2] = S.n_lp;
+    it[3] = k;
+    for (int lp = 0; lp < S.n_lp; ++lp) c.write_intent(k, lp, false);  // fully rewritten
+    *full.skip = 0;
+    *H.skip = 0;
   }
   __syncthreads();
-  const int* target = st.target + (long long)r * S.G;
-  for (int i = threadIdx.x; i < S.NRq; i += blockDim.x) {
-    const int slot = r * S.NRq + i;
-    int k = -1;
-    for (int kk = 0; kk < S.B; ++kk)
-      if (i >= S.off[kk] && i < S.off[kk] + S.bs[kk]) k = kk;
-    int pos = -1;
-    if (k >= 0 && ((active >> k) & 1)) {
-      const int j = i - S.off[k];
-      if (c.B_(k, B_START) + j < c.B_(k, B_END)) pos = c.B_(k, B_START) + j;
-    }
+  for (int p = threadIdx.x; p < S.L; p += blockDim.x) {
+    const int row = r * S.L + p;
+    full.slot_pos[row] = p;
+    full.slot_req[row] = r;
+    full.slot_br[row] = k;
+    full.slot_tok[row] = c.rows[k * S.L + p];
+    full.slot_kvoff[row] = kv_row_off(D, S, st, r, k, p);
+  }
+  const int* target = use_target ? st.target + (long long)r * S.G : nullptr;
+  for (int j = threadIdx.x; j < S.bs[k]; j += blockDim.x) {
+    const int slot = r * S.NRq + S.off[k] + j;
+    const bool in = j < S.L && c.rows[k * S.L + j] == c.mask_id;
     blk.slot_req[slot] = r;
-    blk.slot_br[slot] = k < 0 ? 0 : k;
-    blk.slot_pos[slot] = pos;
-    const int tok = pos >= 0 ? c.rows[k * S.L + pos] : 0;
-    blk.slot_tok[slot] = tok;
-    blk.slot_kvoff[slot] = pos >= 0 ? kv_row_off(D, S, st, r, k, pos) : 0;
-    const int msk = pos >= 0 && tok == c.mask_id;
-    H.masked[slot] = msk;
-    if (msk) slot_boost(D, S, c.rows + k * S.L, target, pos, &H.boost[slot], &H.tgt[slot]);
+    blk.slot_br[slot] = k;
+    blk.slot_pos[slot] = in ? j : -1;
+    H.masked[slot] = in ? 1 : 0;
+    if (in) slot_boost(D, S, c.rows + k * S.L, target, j, &H.boost[slot], &H.tgt[slot]);
     else {
       H.boost[slot] = 0.0f;
       H.tgt[slot] = -1;
     }
   }
-  store_request(c);
 }
 
 __global__ void k_step_commit(Dims D, Sess S, DevState st, Pass blk, Head H) {
@@ -758,8 +847,7 @@ __global__ void __launch_bounds__(256) k_merge_prep(Dims D, Sess S, DevState st,
       for (int e = 0; e < VE; ++e) a = fmaf(ldf(hp + e), ldf(wp + e), a);
     }
     a = warp_sum(a);
-    const float raw = a * D.head_scale;
-    float l = raw + D.spike_gain * fmaxf(0.0f, raw - D.spike_cut);
+    float l = head_logit(a, D.head_scale, D.spike_cut, D.spike_gain);
     if (v == tg && tg <= D.V) l += boost;
     if (lane == 0) st.ptab[pmi * S.B + s] = expf(l - m) / ssum;
   }
@@ -1193,6 +1281,26 @@ __global__ void __launch_bounds__(256) k_kv_gather(Dims D, Sess S, DevState st, 
   }
 }
 
+// inverse of k_kv_gather: a dense kv_vectorize-layout cache -> branch k's
+// pages (rounded to the model dtype); the seams' cache upload
+template <typename T>
+__global__ void __launch_bounds__(256) k_kv_scatter(Dims D, Sess S, DevState st, int r, int k, const float* src) {
+  pdl_enter();
+  const int pos = blockIdx.x, l = blockIdx.y;
+  const int kv_dim = D.nkv * D.hd;
+  const int lp = lp_of(S, pos);
+  const long long gpage = (long long)r * S.pool + st.pt[((long long)r * S.B + k) * S.n_lp + lp];
+  const long long lay = (long long)l * S.R * S.pool * D.nkv * S.ps * D.hd;
+  const int row = pos - lp_start(S, lp);
+  const float* o = src + ((long long)l * S.L + pos) * 2 * kv_dim;
+  for (int e = threadIdx.x; e < kv_dim; e += blockDim.x) {
+    const int kvh = e / D.hd, i = e - kvh * D.hd;
+    const long long dst = lay + ((gpage * D.nkv + kvh) * S.ps + row) * D.hd + i;
+    stf(reinterpret_cast<T*>(st.kv_k) + dst, o[e]);
+    stf(reinterpret_cast<T*>(st.kv_v) + dst, o[kv_dim + e]);
+  }
+}
+
 // Point branch k of request r at the reserved scratch pages (saving its page
 // table) and set the full pass up for that one row (the other requests' rows
 // are padding).  CTA per request.
@@ -1438,6 +1546,25 @@ cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, 
   launch_k(k_block_pack, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
   return cudaGetLastError();
 }
+cudaError_t launch_seam_init(const Dims& D, const Sess& S, const DevState& st, cudaStream_t s) {
+  launch_k(k_seam_init, dim3(S.R), dim3(256), (size_t)0, s, D, S, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seam_block_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                                   int mask, int use_target, cudaStream_t s) {
+  big_smem(k_seam_block_pack);
+  launch_k(k_seam_block_pack, dim3(S.R), dim3(256), rc_smem(S), s, D, S, st, blk, H, mask, use_target);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seam_full_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
+                                  const Head& H, int k, int use_target, cudaStream_t s) {
+  big_smem(k_seam_full_pack);
+  launch_k(k_seam_full_pack, dim3(S.R), dim3(256), rc_smem(S), s, D, S, st, full, blk, H, k, use_target);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy_pages(const Dims& D, const Sess& S, const DevState& st, int with_pm, cudaStream_t s) {
   if (D.dtype == 1) launch_k(k_copy_pages<__nv_bfloat16>, dim3(2 * S.n_sms), dim3(512), (size_t)(0), s, D, S, st, with_pm);
   else launch_k(k_copy_pages<float>, dim3(2 * S.n_sms), dim3(512), (size_t)(0), s, D, S, st, with_pm);
@@ -1509,6 +1636,13 @@ cudaError_t launch_vanilla_commit(const Dims& D, const Sess& S, const DevState& 
     a = true;
   }
   launch_k(k_vanilla_commit, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_scatter(const Dims& D, const Sess& S, const DevState& st, int r, int k, const float* src,
+                              cudaStream_t s) {
+  if (D.dtype == 1) launch_k(k_kv_scatter<__nv_bfloat16>, dim3(S.L, D.layers), dim3(256), (size_t)0, s, D, S, st, r, k, src);
+  else launch_k(k_kv_scatter<float>, dim3(S.L, D.layers), dim3(256), (size_t)0, s, D, S, st, r, k, src);
   return cudaGetLastError();
 }
 

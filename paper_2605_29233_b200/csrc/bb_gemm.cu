@@ -196,8 +196,7 @@ __device__ __forceinline__ void head_rows(const GemmTcParams& p, float (&v)[32],
     const int row = row0 + j0 + j;
     float l = -INFINITY;
     if (n < p.n_out && row < p.rows_alloc) {
-      const float raw = v[j] * hs;
-      l = raw + sg * fmaxf(0.0f, raw - sc);
+      l = head_logit(v[j], hs, sc, sg);
       if (n == __ldg(&p.tgt[row])) l += __ldg(&p.boost[row]);
     }
     float m = l;
@@ -234,8 +233,7 @@ __device__ __forceinline__ void head_rows_t(const GemmTcParams& p, const float (
     float l[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      const float raw = st[lane * 33 + c] * hs;
-      float x = raw + sg * fmaxf(0.0f, raw - sc);
+      float x = head_logit(st[lane * 33 + c], hs, sc, sg);
       if (n0w + c == tg) x += bo;
       l[c] = c < nc ? x : -INFINITY;
       if (l[c] > m) {
@@ -454,6 +452,11 @@ __global__ void __launch_bounds__(192)
         for (int j0 = 0; j0 < BN; j0 += 32) {
           float v[32];
           tmem_ld32(taddr + j0, v);
+          if (p.raw_out != nullptr && n < p.n_out) {  // seams / observers: raw h . w_v per (row, column)
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (row0 + j0 + j < rows_valid) p.raw_out[(long long)(row0 + j0 + j) * p.n_out + n] = v[j];
+          }
 #if HEAD_T
           head_rows_t<BN>(p, v, ntile * 128 + q * 32, q, lane, row0, j0, red, red + 12 * BN + q * 32 * 33);
 #else

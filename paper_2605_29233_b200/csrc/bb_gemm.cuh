@@ -110,6 +110,7 @@ struct GemmTcParams {
   const float* boost;
   const int* tgt;
   float head_scale, spike_cut, spike_gain;
+  float* raw_out;     // optional [rows_alloc][n_out]: raw dot products (materialised logits)
   // live per-launch timing (%globaltimer): this launch site's {min start, max end}
   unsigned long long* tstat;
   // timeline sessions, one GEMM kind (BB_GPH_KIND): per-CTA phase sums [CTAs,

@@ -418,8 +418,7 @@ __global__ void __launch_bounds__(128) k_head_tiles_f32(Dims D, Head H) {
   const int n = vt * 128 + threadIdx.x;
   float l = -INFINITY;
   if (n < D.n_out) {
-    const float raw = H.logits[(long long)row * D.n_out + n] * D.head_scale;
-    l = raw + D.spike_gain * fmaxf(0.0f, raw - D.spike_cut);
+    l = head_logit(H.logits[(long long)row * D.n_out + n], D.head_scale, D.spike_cut, D.spike_gain);
     if (n == H.tgt[row]) l += H.boost[row];
   }
   float m = l;
@@ -509,6 +508,24 @@ __global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, H
   for (int c = threadIdx.x; c < D.d; c += blockDim.x) dst[c] = src[c];
 }
 
+// Materialised logits / probabilities of the last head pass (the seams'
+// DenoiseOutput, model.py:160-170): per masked head slot, logit = spike(raw)
+// + boost at the target column, prob = exp(logit - m) / s with the (m, s) the
+// head reduction produced (so probs agree with the committed confidences).
+__global__ void __launch_bounds__(128) k_head_logits(Dims D, Head H, const float* __restrict__ raw, float* logits,
+                                                     float* probs) {
+  pdl_enter();
+  const int row = blockIdx.y;
+  if (*H.skip || !H.masked[row]) return;
+  const int n = blockIdx.x * 128 + threadIdx.x;
+  if (n >= D.n_out) return;
+  const long long i = (long long)row * D.n_out + n;
+  float l = head_logit(raw[i], D.head_scale, D.spike_cut, D.spike_gain);
+  if (n == H.tgt[row]) l += H.boost[row];
+  logits[i] = l;
+  probs[i] = expf(l - H.res_m[row]) / H.res_s[row];
+}
+
 // ------------------------------------------------------------------ launchers
 #define BB_DISPATCH(D, ...)                                  \
   do {                                                       \
@@ -553,6 +570,14 @@ cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int 
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s) {
   dim3 grid((D.dff / 4 + 255) / 256, P.rows_alloc);
   BB_DISPATCH(D, (launch_k(k_post_gu<T>, dim3(grid), dim3(256), (size_t)(0), s, D, P, pr)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_head_logits(const Dims& D, const Pass& blk, const Head& H, float* logits, float* probs,
+                               cudaStream_t s) {
+  const float* raw = D.dtype == 1 ? H.raw : H.logits;
+  if (raw == nullptr) return cudaErrorInvalidValue;
+  launch_k(k_head_logits, dim3(D.n_vtiles, blk.rows_alloc), dim3(128), (size_t)0, s, D, H, raw, logits, probs);
   return cudaGetLastError();
 }
 

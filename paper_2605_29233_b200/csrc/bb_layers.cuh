@@ -44,6 +44,8 @@ cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevSt
 cudaError_t launch_attn_keys(const Dims& D, const Sess& S, const Pass& P, const DevState& st, cudaStream_t s);
 cudaError_t launch_gather_head(const Dims& D, const Sess& S, const Pass& full, const Pass& blk, const Head& H,
                                int branch_filter, cudaStream_t s);
+cudaError_t launch_head_logits(const Dims& D, const Pass& blk, const Head& H, float* logits, float* probs,
+                               cudaStream_t s);
 cudaError_t launch_head_tiles_f32(const Dims& D, const Pass& blk, const Head& H, cudaStream_t s);
 cudaError_t launch_head_reduce(const Dims& D, const Sess& S, const Pass& blk, const Head& H, const DevState& st,
                                cudaStream_t s);
@@ -66,6 +68,13 @@ cudaError_t launch_refresh_pack(const Dims& D, const Sess& S, const DevState& st
                                 const Head& H, int branch, cudaStream_t s);
 cudaError_t launch_refresh_end(const Dims& D, const Sess& S, const DevState& st, cudaStream_t s);
 // KV-space diagnostics (log_kv / log_consistency)
+cudaError_t launch_kv_scatter(const Dims& D, const Sess& S, const DevState& st, int r, int k, const float* src,
+                              cudaStream_t s);
+cudaError_t launch_seam_init(const Dims& D, const Sess& S, const DevState& st, cudaStream_t s);
+cudaError_t launch_seam_block_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                                   int mask, int use_target, cudaStream_t s);
+cudaError_t launch_seam_full_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, const Pass& blk,
+                                  const Head& H, int k, int use_target, cudaStream_t s);
 cudaError_t launch_kv_gather(const Dims& D, const Sess& S, const DevState& st, int r, int k, float* dst,
                              cudaStream_t s);
 cudaError_t launch_fresh_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& full, int r, int k,

@@ -134,7 +134,8 @@ struct Head {
   float* boost;       // [rows]
   int* tgt;           // [rows]
   float4* hpart;      // [rows][n_vtiles]
-  float* logits;      // fp32 mode: [rows][n_out]
+  float* logits;      // fp32 mode: [rows][n_out] raw dot products
+  float* raw;         // bf16 mode, logits sessions: [rows][n_out] raw dot products (else null)
   float* res_conf;    // [rows]
   int* res_arg;
   float* res_m;

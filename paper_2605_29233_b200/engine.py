@@ -27,7 +27,8 @@ def _torch():
 class Session:
     def __init__(self, params, cfg, prompt_len: int, n_requests: int = 1, trace: bool = True,
                  page_size: int = 16, pages_per_item: int = 4, event_capacity: int | None = None,
-                 diagnostics: bool = False, test_flags: int = 0):
+                 diagnostics: bool = False, test_flags: int = 0, logits: bool = False, seam: bool = False,
+                 hard_cap: int = 0):
         torch = _torch()
         # no reference to `params` itself: the model's session cache
         # (ModelParams._sessions) owns its sessions, so a session must not keep
@@ -48,7 +49,7 @@ class Session:
             refresh_interval=cfg.refresh_interval, merge_enabled=int(cfg.merge_enabled),
             sync_enabled=int(cfg.sync_enabled), page_size=page_size, pages_per_item=pages_per_item,
             trace=int(trace), event_capacity=event_capacity, diagnostics=int(diagnostics),
-            test_flags=int(test_flags))
+            test_flags=int(test_flags), logits=int(logits), seam=int(seam), hard_cap=int(hard_cap))
         nbytes = C.c_size_t(0)
         model = params.handle()
         _lib.check(L.bb_session_workspace_bytes(model, C.byref(self.desc), C.byref(nbytes)),
@@ -160,6 +161,55 @@ class Session:
                                              C.c_void_p(self.stream.cuda_stream)), "bb_sqdiff_norm")
         self.stream.synchronize()
         return float(out.item())
+
+    # ---------------------------------------------------------------- seams
+    def seam_init(self):
+        _lib.check(_lib.lib().bb_seam_init(self.h, C.c_void_p(self.stream.cuda_stream)), "bb_seam_init")
+
+    def seam_forward(self, full: bool, mask: int, use_target: bool):
+        _lib.check(_lib.lib().bb_seam_forward(self.h, int(full), int(mask), int(use_target),
+                                              C.c_void_p(self.stream.cuda_stream)), "bb_seam_forward")
+
+    def kv_scatter(self, r: int, k: int, src):
+        _lib.check(_lib.lib().bb_kv_scatter(self.h, r, k, C.c_void_p(src.data_ptr()),
+                                            C.c_void_p(self.stream.cuda_stream)), "bb_kv_scatter")
+
+    def head_outputs(self, branches, r: int = 0) -> dict:
+        """DenoiseOutput per branch of the last head pass (masked head slots
+        of request r, in position order): materialised logits and probs."""
+        torch = _torch()
+        from .model import DenoiseOutput
+        rows = self.info[9]
+        n_out = self.vocab.n_out
+        if getattr(self, "_lbuf", None) is None:
+            self._lbuf = torch.empty(rows, n_out, dtype=torch.float32, device="cuda")
+            self._pbuf = torch.empty(rows, n_out, dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().bb_head_logits(self.h, C.c_void_p(self._lbuf.data_ptr()),
+                                             C.c_void_p(self._pbuf.data_ptr()),
+                                             C.c_void_p(self.stream.cuda_stream)), "bb_head_logits")
+        self.stream.synchronize()
+        masked = self.v_head["masked"].cpu().numpy()
+        pos = self.v_head["pos"].cpu().numpy()
+        br = self.v_head["branch"].cpu().numpy()
+        nrq = self.info[14]
+        out = {}
+        for k in branches:
+            sl = np.flatnonzero((masked != 0) & (br == k) & (pos >= 0))
+            sl = sl[(sl >= r * nrq) & (sl < (r + 1) * nrq)]
+            sl = sl[np.argsort(pos[sl], kind="stable")]
+            idx = torch.from_numpy(sl.astype(np.int64)).to("cuda")
+            lg = self._lbuf.index_select(0, idx).double().cpu().numpy()
+            pr = self._pbuf.index_select(0, idx).double().cpu().numpy()
+            out[k] = DenoiseOutput(pos[sl].astype(int), lg, pr)
+        return out
+
+    def kv_vec(self, r: int, k: int):
+        """Branch k's cache of request r as a new CUDA fp32 kv_vectorize vector."""
+        torch = _torch()
+        v = torch.empty(self.kv_numel(), dtype=torch.float32, device="cuda")
+        self.kv_gather(r, k, v)
+        self.stream.synchronize()
+        return v
 
     def ctrl_now(self) -> np.ndarray:
         self.stream.synchronize()

@@ -160,17 +160,108 @@ class DenoiseOutput:
 
 
 class KvCache:
-    """Handle to a branch's device KV (a row of the session page table).
+    """Per-layer, per-position keys/values plus validity flags (model.py:136-157).
 
-    The reference's KvCache (model.py:136-157) is a dense (layers, L, d) copy
-    per branch; on the device the cache is paged and copy-on-write, so
-    ``copy()`` only aliases (the seam ``merge_sync`` needs, scheduler.py:202)."""
+    ``keys`` / ``values`` are (layers, L, kv_dim) float64 arrays and ``valid``
+    an (L,) bool array, as in the reference (kv_dim = d_model for the
+    reference architecture).  Caches produced by the device seams
+    (``full_forward`` / ``block_forward`` / forward observers) live on the GPU
+    as one fp32 vector in ``kv_vectorize`` layout; the host arrays are
+    materialised on first access.  Once a caller has touched the host arrays
+    they are the source of truth (in-place edits are honoured)."""
 
-    def __init__(self, tag=None):
-        self.tag = tag
+    def __init__(self, keys=None, values=None, valid=None, *, vec=None, shape=None):
+        if vec is not None:
+            if shape is None or valid is None:
+                raise ContractError("a device KvCache needs its shape and validity flags")
+            self._vec, self._shape = vec, tuple(shape)
+            self._keys = self._values = None
+        else:
+            if keys is None or values is None or valid is None:
+                raise ContractError("KvCache needs keys, values and valid")
+            self._keys, self._values = np.asarray(keys), np.asarray(values)
+            self._vec, self._shape = None, tuple(self._keys.shape)
+        self.valid = np.asarray(valid, dtype=bool)
+
+    @classmethod
+    def empty(cls, layers: int, length: int, d_model: int) -> "KvCache":
+        return cls(np.zeros((layers, length, d_model)), np.zeros((layers, length, d_model)),
+                   np.zeros(length, dtype=bool))
+
+    def _host(self):
+        if self._keys is None:
+            layers, L, kvd = self._shape
+            a = self._vec.view(layers, L, 2, kvd).double().cpu().numpy()
+            self._keys, self._values = a[:, :, 0, :].copy(), a[:, :, 1, :].copy()
+            self._vec = None  # host arrays are authoritative from now on
+        return self._keys, self._values
+
+    @property
+    def keys(self) -> np.ndarray:
+        return self._host()[0]
+
+    @keys.setter
+    def keys(self, v):
+        self._host()
+        self._keys = np.asarray(v)
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._host()[1]
+
+    @values.setter
+    def values(self, v):
+        self._host()
+        self._values = np.asarray(v)
+
+    @property
+    def length(self) -> int:
+        return self._shape[1]
+
+    @property
+    def shape(self) -> tuple:
+        return self._shape
+
+    def device_vec(self):
+        """The cache as a CUDA fp32 vector in kv_vectorize layout (uploaded if host-resident)."""
+        if self._vec is None:
+            import torch
+            k, v = self._keys, self._values
+            self._shape = tuple(k.shape)
+            self._vec = torch.from_numpy(np.ascontiguousarray(np.stack([k, v], axis=2), dtype=np.float32)
+                                         .reshape(-1)).to("cuda")
+            return self._vec
+        return self._vec
 
     def copy(self) -> "KvCache":
-        return KvCache(self.tag)
+        if self._keys is not None:
+            return KvCache(self._keys.copy(), self._values.copy(), self.valid.copy())
+        return KvCache(vec=self._vec.clone(), shape=self._shape, valid=self.valid.copy())
+
+
+def kv_vectorize(cache: KvCache) -> np.ndarray:
+    """model.py:346-352: layer-major, position-minor, key before value."""
+    if not np.asarray(cache.valid).all():
+        raise StateError("cannot vectorize a cache with invalid positions")
+    if cache._keys is None:
+        return cache._vec.double().cpu().numpy()
+    layers, length, d = cache.keys.shape
+    return np.stack([cache.keys, cache.values], axis=2).reshape(layers * length * 2 * d).copy()
+
+
+def full_forward(params: "ModelParams", row: SequenceRow, target) -> tuple:
+    """model.py:322-328 on the device: the whole row from an empty cache;
+    DenoiseOutput over every masked position plus the new KvCache."""
+    from . import seams
+    return seams.full_forward(params, row, target)
+
+
+def block_forward(params: "ModelParams", row: SequenceRow, cache: KvCache, window: BlockWindow, target) -> tuple:
+    """model.py:331-343 on the device: recompute the window's K/V only, attend
+    to ``cache`` everywhere else; DenoiseOutput over the window's masked
+    positions plus the new KvCache (copy-then-write: ``cache`` is unchanged)."""
+    from . import seams
+    return seams.block_forward(params, row, cache, window, target)
 
 
 @dataclass(frozen=True)

@@ -96,6 +96,20 @@ def pack_active_blocks(rows, branches, active, mask_id) -> PackedQuery:
     return PackedQuery(tuple(active), np.concatenate(chunks), tuple(offsets))
 
 
+def init_full_forward(params: ModelParams, rows: list, target):
+    """scheduler.py:80-89 on the device (seams.init_full_forward)."""
+    from . import seams
+    return seams.init_full_forward(params, rows, target)
+
+
+def batched_block_forward(params: ModelParams, packed: PackedQuery, rows: list, caches: list, branches: list,
+                          target) -> dict:
+    """scheduler.py:116-131: one fused device pass over every packed branch's
+    window (seams.batched_block_forward); replaces ``caches[k]``."""
+    from . import seams
+    return seams.batched_block_forward(params, packed, rows, caches, branches, target)
+
+
 def select_eos_winner(branches, rows, vocab: Vocab) -> BranchState:
     """scheduler.py:216-222"""
     ready = [b for b in branches if check_eos(b, rows[b.index], vocab) == EOS_READY]
@@ -142,54 +156,69 @@ def _check_call(params, cfg, tasks, diagnostics: bool = False):
 
 
 def run_blockbatch(params: ModelParams, task: Task, cfg: SchedulerConfig, forward_hook=None,
-                   forward_observer=None, _single: bool = False) -> GenerationResult:
+                   forward_observer=None, _single: bool = False, _hard_cap: int = 0) -> GenerationResult:
     """scheduler.py:225-394 on the device: prefill, batched block denoising,
     merge/sync, periodic refresh, early EOS return, final selection.
 
-    ``forward_hook(kind)`` is replayed once per charged NFE in charge order
-    from the device trace.  ``forward_observer`` needs host copies of every
-    branch's KV before/after each step (the reference's replay harness) and is
-    not supported on the device path."""
-    if forward_observer is not None:
-        raise NotImplementedError("forward_observer needs host KV snapshots; not supported on the device path")
+    ``forward_hook(kind)`` fires once per charged NFE, as the forward is
+    charged (the host waits for each iteration's status); an exception from
+    the hook aborts the run like the reference's.  ``forward_observer(kind,
+    active, pre_rows, pre_caches, windows, outputs, post_caches)`` fires after
+    every batched block forward with host rows, device-backed ``KvCache``
+    snapshots before/after and the step's materialised ``DenoiseOutput``s
+    (scheduler.py:339-342) -- the replay harness of test_acceptance.py:183-204.
+    KV logging (``cfg.log_kv`` / ``cfg.log_consistency``) runs the step in
+    parts the same way."""
     cfg.validate()
-    if cfg.log_kv != "none" or cfg.log_consistency:
-        return _run_diagnostics(params, task, cfg, forward_hook)
-    return run_batch(params, [task], cfg, forward_hook=forward_hook, _single=_single)[0]
+    if forward_observer is not None or cfg.log_kv != "none" or cfg.log_consistency:
+        return _run_stepped(params, task, cfg, forward_hook, forward_observer, _hard_cap)
+    return run_batch(params, [task], cfg, forward_hook=forward_hook, _single=_single, _hard_cap=_hard_cap)[0]
 
 
-def _replay_hook(res, forward_hook):
-    for ev in res.trace:
-        if ev.kind == "init":
-            forward_hook("init")
-        elif ev.kind == "block_forward":
-            forward_hook("block")
-        elif ev.kind == "refresh":
-            forward_hook("refresh")
+def _hook_deltas(forward_hook, prev, ctrl_row):
+    """Fire forward_hook for each NFE charged since ``prev`` (init, block, refresh order)."""
+    now = [int(ctrl_row[_lib.C_NFE0]), int(ctrl_row[_lib.C_NFE1]), int(ctrl_row[_lib.C_NFE2])]
+    for i, kind in enumerate(("init", "block", "refresh")):
+        for _ in range(now[i] - prev[i]):
+            forward_hook(kind)
+    prev[:] = now
 
 
-def _run_diagnostics(params: ModelParams, task: Task, cfg: SchedulerConfig, forward_hook=None):
-    """run_blockbatch with the KV-space logging of scheduler.py:268-281,
-    288-294, 332-347 and 376-390: per block_forward / refresh event the
+def _run_stepped(params: ModelParams, task: Task, cfg: SchedulerConfig, forward_hook=None, forward_observer=None,
+                 hard_cap: int = 0):
+    """run_blockbatch with the step in parts (bb_prefill_part /
+    bb_block_step_part) so host callbacks see the state between the forward
+    and the commit/merge/sync that follows it: the forward observer
+    (scheduler.py:326-342) and the KV-space logging of scheduler.py:268-281,
+    288-294, 332-347 and 376-390 -- per block_forward / refresh event the
     ``kv_delta`` norm of each touched branch's cache change (log_kv), its
     vectorized cache ("full"), and ``E_before`` / ``E_after`` =
     ||kv_vectorize(cache) - kv_vectorize(full_forward(row).cache)|| around the
     forward (log_consistency); the init event carries each branch's cache norm.
-    The device runs the step in parts (bb_prefill_part / bb_block_step_part);
-    caches are gathered on the device (bb_kv_gather), fresh forwards run into
+    Caches are gathered on the device (bb_kv_gather), fresh forwards run into
     reserved scratch pages without changing the session (bb_fresh_kv), norms
     are fp64 device reductions (bb_sqdiff_norm).  Decisions, tokens, NFE and
     the rest of the trace are those of the plain run."""
     import torch
+    from .model import KvCache
     P = _check_call(params, cfg, [task], diagnostics=True)
-    s = Session(params, cfg, P, 1, trace=True, diagnostics=True)
+    diag = cfg.log_kv != "none" or cfg.log_consistency
+    s = Session(params, cfg, P, 1, trace=True, diagnostics=diag, logits=forward_observer is not None,
+                hard_cap=hard_cap)
     s.set_inputs(task.prompt[None], task.target[None])
     B = len(cfg.block_sizes)
     n = s.kv_numel()
-    snap = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(B)]
-    cur = torch.empty(n, dtype=torch.float32, device="cuda")
-    fresh = torch.empty(n, dtype=torch.float32, device="cuda")
+    d = params.dims
+    kv_shape = (d.layers, s.Lseq, d.n_kv_heads * d.hd)
+    snap = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(B)] if diag else []
+    cur = torch.empty(n, dtype=torch.float32, device="cuda") if diag else None
+    fresh = torch.empty(n, dtype=torch.float32, device="cuda") if cfg.log_consistency else None
     norms, full = cfg.log_kv != "none", cfg.log_kv == "full"
+    charged = [0, 0, 0]
+
+    def hooks():
+        if forward_hook is not None:
+            _hook_deltas(forward_hook, charged, s.ctrl_now()[0])
 
     def consistency(ks):
         out = {}
@@ -209,11 +238,11 @@ def _run_diagnostics(params: ModelParams, task: Task, cfg: SchedulerConfig, forw
     def after(ks, e_before):
         extra = {}
         if norms:
-            d = {}
+            dl = {}
             for k in ks:
                 s.kv_gather(0, k, cur)
-                d[k] = s.sqdiff_norm(cur, snap[k])
-            extra["kv_delta"] = d
+                dl[k] = s.sqdiff_norm(cur, snap[k])
+            extra["kv_delta"] = dl
         if full:
             kv = {}
             for k in ks:
@@ -231,6 +260,7 @@ def _run_diagnostics(params: ModelParams, task: Task, cfg: SchedulerConfig, forw
 
     # prefill: the init event's kv_delta is each branch's cache norm (delta from empty)
     s.prefill_part(0)
+    hooks()
     init_extra = {}
     if norms:
         init_extra["kv_delta"] = {}
@@ -256,57 +286,81 @@ def _run_diagnostics(params: ModelParams, task: Task, cfg: SchedulerConfig, forw
         s.block_step_part(0)
         c = s.ctrl_now()[0]
         active = mask_list(int(c[_lib.C_ACTIVE_MASK])) if c[_lib.C_STATUS] == 0 else []
-        eb = before(active) if active else None
+        eb = before(active) if (active and diag) else None
+        if active and forward_observer is not None:
+            toks = s.v_tokens[0].cpu().numpy()
+            brs = s.v_branch[0].cpu().numpy()
+            pre_rows = [SequenceRow(toks[k].astype(np.int64), P) for k in active]
+            pre_caches = [KvCache(vec=s.kv_vec(0, k), shape=kv_shape, valid=np.ones(s.Lseq, dtype=bool))
+                          for k in active]
+            from .model import BlockWindow
+            windows = [BlockWindow(int(brs[k, 0]), int(brs[k, 1])) for k in active]
         s.block_step_part(1)
-        if active:
+        hooks()
+        if active and forward_observer is not None:
+            outputs = s.head_outputs(active)
+            post = [KvCache(vec=s.kv_vec(0, k), shape=kv_shape, valid=np.ones(s.Lseq, dtype=bool)) for k in active]
+            forward_observer("block", list(active), pre_rows, pre_caches, windows, outputs, post)
+        if active and diag:
             block_extras.append(after(active, eb))
         s.block_step_part(2)
         if it % cfg.refresh_interval == 0:
             c = s.ctrl_now()[0]
             todo = mask_list(int(c[_lib.C_REFRESH_MASK])) if (c[_lib.C_STATUS] == 0 and c[_lib.C_REFRESH_DUE]) else []
-            eb = before(todo) if todo else None
+            eb = before(todo) if (todo and diag) else None
             s.refresh()
-            if todo:
+            hooks()
+            if todo and diag:
                 refresh_extras.append(after(todo, eb))
     s.stream.synchronize()
     res = s.results([task], params.vocab)[0]
-    bi = ri = 0
-    for ev in res.trace:
-        if ev.kind == "init":
-            ev.extra.update(init_extra)
-        elif ev.kind == "block_forward":
-            ev.extra.update(block_extras[bi])
-            bi += 1
-        elif ev.kind == "refresh":
-            ev.extra.update(refresh_extras[ri])
-            ri += 1
-    if bi != len(block_extras) or ri != len(refresh_extras):
-        raise ContractError("diagnostics out of step with the device trace")
-    if forward_hook is not None:
-        _replay_hook(res, forward_hook)
+    if diag:
+        bi = ri = 0
+        for ev in res.trace:
+            if ev.kind == "init":
+                ev.extra.update(init_extra)
+            elif ev.kind == "block_forward":
+                ev.extra.update(block_extras[bi])
+                bi += 1
+            elif ev.kind == "refresh":
+                ev.extra.update(refresh_extras[ri])
+                ri += 1
+        if bi != len(block_extras) or ri != len(refresh_extras):
+            raise ContractError("diagnostics out of step with the device trace")
     return res
 
 
 def run_batch(params: ModelParams, tasks: list, cfg: SchedulerConfig, forward_hook=None, trace: bool = True,
-              use_graph: bool = True, _single: bool = False) -> list:
+              use_graph: bool = True, _single: bool = False, _hard_cap: int = 0) -> list:
     """Many independent requests (same P, G) in one device session: every
     iteration runs one forward over all live requests' branch windows;
-    NFE, trace and termination stay per request."""
+    NFE, trace and termination stay per request.  With ``forward_hook`` the
+    host waits for each iteration (graph replay, then a status read) and fires
+    the hook for every NFE charged, request by request."""
     P = _check_call(params, cfg, tasks)
-    s = get_session(params, cfg, P, len(tasks), trace=trace or forward_hook is not None)
+    if _hard_cap:
+        s = Session(params, cfg, P, len(tasks), trace=trace or forward_hook is not None, hard_cap=_hard_cap)
+    else:
+        s = get_session(params, cfg, P, len(tasks), trace=trace or forward_hook is not None)
     s.set_inputs(np.stack([t.prompt for t in tasks]), np.stack([t.target for t in tasks]))
-    s.launch(use_graph=use_graph)
-    res = s.results(tasks, params.vocab, single=_single)
-    if forward_hook is not None:
-        for r in res:
-            for ev in r.trace:
-                if ev.kind == "init":
-                    forward_hook("init")
-                elif ev.kind == "block_forward":
-                    forward_hook("block")
-                elif ev.kind == "refresh":
-                    forward_hook("refresh")
-    return res
+    if forward_hook is None:
+        s.launch(use_graph=use_graph)
+    else:
+        charged = [[0, 0, 0] for _ in tasks]
+
+        def fire():
+            c = s.ctrl_now()
+            for r in range(len(tasks)):
+                _hook_deltas(forward_hook, charged[r], c[r])
+            return c
+        s.prefill()
+        c = fire()
+        it = 0
+        while it < s.max_iterations() and (c[:, _lib.C_STATUS] == 0).any():
+            it += 1
+            s.iteration(with_refresh=it % cfg.refresh_interval == 0, use_graph=use_graph)
+            c = fire()
+    return s.results(tasks, params.vocab, single=_single)
 
 
 # -------------------------------------------------------------- merge/sync seam

@@ -3,7 +3,7 @@
 Run in the build container (needs /root/reference; it does not travel to the
 GPU box — the fixtures it writes do):
 
-    python tests/golden/make_golden.py [--vanilla-only]   (vanilla + diag fixtures only)
+    python tests/golden/make_golden.py [--vanilla-only | --runaway-only]
 
 Outputs (all under tests/golden/):
   runs_ref.json     full-run results (tokens, NFE, winner, complete trace) of
@@ -22,6 +22,9 @@ Outputs (all under tests/golden/):
   kernels.json      reference confidence_transition / merge_sync outputs on
                     the fuzzed inputs of fuzz.py (inputs rebuilt from seeds).
   forward_c1.npz    reference full_forward / block_forward numerics (C1, seed 0).
+  runs_runaway.json reference run_blockbatch with the hard cap lowered to 16
+                    forwards (HARD_CAP_FACTOR = 0): forward_hook calls up to
+                    the RunawayError (scheduler.py:310, 324-325).
 """
 
 from __future__ import annotations
@@ -315,8 +318,38 @@ def gen_forward_c1():
     return res
 
 
+# ---- hard cap (scheduler.py:310, 324-325) and forward_hook order ------------
+
+def gen_runaway_runs():
+    """Reference runs with HARD_CAP_FACTOR = 0 (cap = 16 forwards): the
+    forward_hook calls up to the RunawayError, or the full list if the run
+    finishes under the cap."""
+    params, vocab = ref_params({})
+    cfg = bbs.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=128)
+    saved = bbs.HARD_CAP_FACTOR
+    runs = []
+    try:
+        bbs.HARD_CAP_FACTOR = 0
+        for s in range(6):
+            task = bbm.make_task(s, 16, 128, vocab)
+            calls = []
+            try:
+                r = bbs.run_blockbatch(params, task, cfg, forward_hook=calls.append)
+                runs.append({"seed": s, "raised": False, "calls": calls, "nfe": list(r.nfe.snapshot())})
+            except bbs.RunawayError:
+                runs.append({"seed": s, "raised": True, "calls": calls})
+    finally:
+        bbs.HARD_CAP_FACTOR = saved
+    return {"hard_cap": 16, "prompt_len": 16, "gen_len": 128, "block_sizes": [8, 16, 32], "runs": runs}
+
+
 def main():
     t0 = time.time()
+    with open(os.path.join(HERE, "runs_runaway.json"), "w") as fh:
+        json.dump(gen_runaway_runs(), fh, separators=(",", ":"))
+    if "--runaway-only" in sys.argv:
+        print(f"done in {time.time() - t0:.1f}s")
+        return
     with open(os.path.join(HERE, "runs_vanilla.json"), "w") as fh:
         json.dump(gen_vanilla_runs(), fh, separators=(",", ":"))
     with open(os.path.join(HERE, "runs_diag.json"), "w") as fh:

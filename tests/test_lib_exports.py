@@ -50,5 +50,5 @@ def test_sm100a_tensor_core_code_present():
 
 def test_model_desc_layout_matches_header():
     assert ctypes.sizeof(_lib.ModelDesc) == 18 * 4
-    assert ctypes.sizeof(_lib.SessionDesc) == (2 + 8 + 2 + 3 + 3 + 6) * 4
+    assert ctypes.sizeof(_lib.SessionDesc) == (2 + 8 + 2 + 3 + 3 + 9) * 4
     assert ctypes.sizeof(_lib.Weights) == 11 * 8
