@@ -110,7 +110,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- model / workload
-def make_model(cfgd):
+def make_model(cfgd, dtype="bf16"):
     import paper_2605_29233_b200 as bb
     if cfgd["shape"] == "llada":
         vocab, dims = bb.Vocab(size=bb.LLADA_8B_VOCAB), bb.LLADA_8B
@@ -122,7 +122,7 @@ def make_model(cfgd):
     if dims.max_len < needed:
         import dataclasses
         dims = dataclasses.replace(dims, max_len=needed)
-    params = bb.build_model(0, vocab, dims, head_scale=cfgd["head_scale"], gamma=cfgd["gamma"], dtype="bf16")
+    params = bb.build_model(0, vocab, dims, head_scale=cfgd["head_scale"], gamma=cfgd["gamma"], dtype=dtype)
     cfg = bb.SchedulerConfig(block_sizes=cfgd["bs"], gen_len=cfgd["G"], refresh_interval=cfgd["R"])
     return bb, params, cfg
 
@@ -171,13 +171,72 @@ def nfe_weighted_roofline(params, cfgd, rows_block, nfe_split, hbm_gbs, tflops, 
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
-def cpu_baseline(cfgd, nfe_split, tokens_per_req, budget_s=30.0):
-    """Time the oracle (NumPy fp32, all host threads) on a bounded sample of the
-    workload: 1 and 2 transformer layers of the real width + the LM head, for a
-    full forward (L rows: prefill/refresh) and one block step (every branch's
-    window), then extrapolate to the model depth and the GPU run's NFE split."""
+def nfe_split_for(config):
+    """The committed per-request NFE split + tokens/request (profiles/nfe_split.json)."""
+    d = json.load(open(os.path.join(HERE, "profiles", "nfe_split.json")))[config]
+    return tuple(d["nfe_split"]), float(d["tokens_per_request"]), d["source"]
+
+
+class CpuSampler:
+    """The oracle (oracle/bb_oracle.py, NumPy fp32, all host threads) on the
+    bench workload at FULL depth and width.  Weights of two distinct layers
+    are generated (counter hash, as on the device) and the model's layers
+    cycle through them: a forward's cost does not depend on the values, and
+    every layer still streams its ~0.9 GB of fp32 weights from DRAM (far
+    larger than any host cache).  One sample = one full forward of the shared
+    row (L rows: prefill / refresh) + one block step (every branch's window
+    against the prefill cache); a request = the committed NFE split of those
+    (a refresh is one full forward per non-done branch, as in
+    scheduler.py:379-383)."""
+
+    def __init__(self, cfgd, config):
+        from oracle import bb_oracle as O
+        import paper_2605_29233_b200.model as M
+        self.O, self.cfgd = O, cfgd
+        self.split, self.tok, self.src = nfe_split_for(config)
+        dims = M.LLADA_8B if cfgd["shape"] == "llada" else M.DREAM_7B
+        V = M.LLADA_8B_VOCAB if cfgd["shape"] == "llada" else M.DREAM_7B_VOCAB
+        self.P, self.G = cfgd["P"], cfgd["G"]
+        L = self.P + self.G
+        mk = dict(kind="llada", vocab_size=V, d_model=dims.d_model, n_heads=dims.n_heads,
+                  n_kv_heads=dims.n_kv_heads, head_dim=dims.hd, d_ff=dims.d_ff, max_len=L,
+                  rope_theta=dims.rope_theta, norm_eps=dims.norm_eps, qkv_bias=dims.qkv_bias,
+                  head_scale=cfgd["head_scale"], gamma=cfgd["gamma"])
+        t = time.perf_counter()
+        W2 = O.hash_weights(O.OArch(layers=2, **mk), 0)
+        per_layer = ("wqkv", "wo", "wg", "wu", "wd", "ln1", "ln2", "bqkv")
+        self.W = {k: ([v[l % 2] for l in range(dims.layers)] if k in per_layer else v) for k, v in W2.items()}
+        self.t_gen = time.perf_counter() - t
+        self.arch = O.OArch(layers=dims.layers, **mk)
+        task = O.make_task(0, self.P, self.G, V)
+        self.target = task.target
+        self.row = np.full(L, V + 1, dtype=np.int64)
+        self.row[:self.P] = task.prompt
+        self.layers = dims.layers
+
+    def sample(self):
+        O, P, L = self.O, self.P, self.P + self.G
+        t = time.perf_counter()
+        _, cache = O.full_forward(self.arch, self.W, self.row, P, self.target, cdtype=np.float32)
+        t_full = time.perf_counter() - t
+        t = time.perf_counter()
+        for b in self.cfgd["bs"]:
+            O.block_forward(self.arch, self.W, self.row, P, cache, P, min(P + b, L), self.target, cdtype=np.float32)
+        t_block = time.perf_counter() - t
+        n0, n1, n2 = self.split
+        t_req = n0 * t_full + n1 * t_block + n2 * len(self.cfgd["bs"]) * t_full
+        return self.tok / t_req, t_full, t_block
+
+    def describe(self, t_full, t_block, n):
+        return (f"oracle NumPy fp32 at full depth ({self.layers} layers) and width, {n} sample(s): "
+                f"full forward L={self.P + self.G} {t_full:.2f}s, block step over all {len(self.cfgd['bs'])} "
+                f"branch windows {t_block:.2f}s (medians); request = committed NFE split "
+                f"{tuple(round(x, 2) for x in self.split)} x those, {self.tok:.0f} tokens/request "
+                f"({self.src}); weights generated in {self.t_gen:.1f}s, not timed")
+
+
+def cpu_baseline(cfgd, config, samples=1):
     from oracle import bb_oracle as O
-    import paper_2605_29233_b200 as bb
     if cfgd["shape"] == "ref":
         arch = O.ref_arch(vocab_size=4096, layers=4, d_model=256, max_len=192, head_scale=2.0)
         W = O.philox_ref_weights(arch, 0)
@@ -188,53 +247,12 @@ def cpu_baseline(cfgd, nfe_split, tokens_per_req, budget_s=30.0):
         dt = time.perf_counter() - t0
         return {"value": r.tokens_decoded / dt, "unit": "decoded tokens/s", "cores": os.cpu_count(),
                 "kind": "port", "sample": f"one full run_blockbatch (seed 0) through the oracle, {dt:.1f}s"}
-    dims = bb.LLADA_8B if cfgd["shape"] == "llada" else bb.DREAM_7B
-    V = bb.LLADA_8B_VOCAB if cfgd["shape"] == "llada" else bb.DREAM_7B_VOCAB
-    P, G = cfgd["P"], cfgd["G"]
-    L = P + G
-
-    def arch_n(n):
-        return O.OArch(kind="llada", vocab_size=V, layers=n, d_model=dims.d_model, n_heads=dims.n_heads,
-                       n_kv_heads=dims.n_kv_heads, head_dim=dims.hd, d_ff=dims.d_ff, max_len=L,
-                       rope_theta=dims.rope_theta, norm_eps=dims.norm_eps, qkv_bias=dims.qkv_bias,
-                       head_scale=cfgd["head_scale"], gamma=cfgd["gamma"])
-    t_gen = time.perf_counter()
-    W2 = O.hash_weights(arch_n(2), 0)
-    W1 = {k: (v[:1] if k in ("wqkv", "wo", "wg", "wu", "wd", "ln1", "ln2", "bqkv") else v) for k, v in W2.items()}
-    t_gen = time.perf_counter() - t_gen
-    task = O.make_task(0, P, G, V)
-    row = np.full(L, V + 1, dtype=np.int64)
-    row[:P] = task.prompt
-
-    def timed_full(arch, W):
-        t = time.perf_counter()
-        o, c = O.full_forward(arch, W, row, P, task.target, cdtype=np.float32)
-        return time.perf_counter() - t, c
-
-    def timed_block(arch, W, cache):
-        t = time.perf_counter()
-        for b in cfgd["bs"]:
-            O.block_forward(arch, W, row, P, cache, P, min(P + b, L), task.target, cdtype=np.float32)
-        return time.perf_counter() - t
-    tf1, c1 = timed_full(arch_n(1), W1)
-    tb1 = timed_block(arch_n(1), W1, c1)
-    tf2, c2 = timed_full(arch_n(2), W2)
-    tb2 = timed_block(arch_n(2), W2, c2)
-    lay_f, lay_b = max(tf2 - tf1, 1e-6), max(tb2 - tb1, 1e-6)
-    head_f, head_b = max(tf1 - lay_f, 0.0), max(tb1 - lay_b, 0.0)
-    t_full = dims.layers * lay_f + head_f
-    t_block = dims.layers * lay_b + head_b
-    n_init, n_block, n_refresh = nfe_split
-    nb = len(cfgd["bs"])
-    t_req = n_init * t_full + n_block * t_block + n_refresh * nb * t_full
-    return {"value": tokens_per_req / t_req, "unit": "decoded tokens/s", "cores": os.cpu_count(),
-            "kind": "port",
-            "sample": (f"oracle NumPy fp32 forwards of 1 and 2 layers (+LM head) at full width: full forward "
-                       f"L={L} {tf1:.2f}s/{tf2:.2f}s, block step over all {nb} branch windows "
-                       f"{tb1:.2f}s/{tb2:.2f}s; extrapolated to {dims.layers} layers -> {t_full:.1f}s per full "
-                       f"forward, {t_block:.1f}s per block step; x GPU-run NFE split "
-                       f"{tuple(round(x, 1) for x in nfe_split)} and {tokens_per_req:.0f} tokens/request "
-                       f"(weights generated in {t_gen:.1f}s, not timed)")}
+    cs = CpuSampler(cfgd, config)
+    res = [cs.sample() for _ in range(samples)]
+    v = statistics.median(r[0] for r in res)
+    return {"value": v, "unit": "decoded tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": cs.describe(statistics.median(r[1] for r in res), statistics.median(r[2] for r in res),
+                                  samples)}
 
 
 # ---------------------------------------------------------------- main
@@ -246,6 +264,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "bf16x2"],
+                    help="bf16: bf16 activations / KV; bf16x2: bf16 weights with hi+lo bf16 activations / KV")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -256,13 +276,20 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        # reference arm: the oracle port of the reference's CPU path on the host cores
-        nfe_split, tok = (1.0, 60.0, 1.0), 256.0
-        est = os.path.join(HERE, "profiles", "nfe_split_c2.json")
-        if os.path.exists(est):
-            d = json.load(open(est))
-            nfe_split, tok = tuple(d["nfe_split"]), d["tokens_per_request"]
-        cb = cpu_baseline(cfgd, nfe_split, tok)
+        # reference arm: the oracle port of the reference's CPU path on the host
+        # cores, full depth; W untimed samples, then K timed samples (median)
+        if cfgd["shape"] == "ref":
+            cb = cpu_baseline(cfgd, args.config)
+        else:
+            cs = CpuSampler(cfgd, args.config)
+            for _ in range(args.warmup):
+                cs.sample()
+            res = [cs.sample() for _ in range(args.steps)]
+            vals = [r[0] for r in res]
+            cb = {"value": statistics.median(vals), "unit": "decoded tokens/s", "cores": os.cpu_count(),
+                  "kind": "port", "samples": [round(x, 4) for x in vals],
+                  "sample": cs.describe(statistics.median(r[1] for r in res), statistics.median(r[2] for r in res),
+                                        len(res))}
         line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": cb["unit"],
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -279,13 +306,13 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    bb, params, cfg = make_model(cfgd)
+    bb, params, cfg = make_model(cfgd, args.precision)
     from paper_2605_29233_b200.scheduler import get_session
     P, G = cfgd["P"], cfgd["G"]
     vocab = params.vocab
     s = get_session(params, cfg, P, 1, trace=False)
     K, Wm = args.steps, max(args.warmup, 1)
-    from paper_2605_29233_b200 import dp
+    from paper_2605_29233_b200 import dp, _lib
     # prompts: global request g -> seed 1000 + g, sharded round-robin over ranks
     mine = dp.shard(K * world, rank, world)
     tasks = ([bb.make_task(900000 + rank * 1000 + i, P, G, vocab) for i in range(Wm)]
@@ -358,21 +385,26 @@ def main():
 
     # ---- e2e through the public API (host buffers) ----
     e2e_tasks = tasks[Wm:Wm + K]  # same prompts as the device-resident run
-    h2d0, d2h0 = s.h2d_bytes, s.d2h_bytes
-    torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
+    # the public call exactly as a user makes it: run_blockbatch with its default
+    # trace on (the event records come back to the host every request)
+    from paper_2605_29233_b200.scheduler import get_session as _gs
+    s_e2e = _gs(params, cfg, P, 1, trace=True)
+    bb.run_blockbatch(params, tasks[0], cfg)  # untimed: builds the traced session's graphs
+    h2d0, d2h0 = s_e2e.h2d_bytes, s_e2e.d2h_bytes
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s.stream)
+    e0.record(s_e2e.stream)
     e2e_tok = 0
     for t in e2e_tasks:
-        r = bb.run_batch(params, [t], cfg, trace=False)[0]
+        r = bb.run_blockbatch(params, t, cfg)
         e2e_tok += r.tokens_decoded
-    e1.record(s.stream)
+    e1.record(s_e2e.stream)
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)
-    h2d = (s.h2d_bytes - h2d0) / K
-    d2h = (s.d2h_bytes - d2h0) / K
+    h2d = (s_e2e.h2d_bytes - h2d0) / K
+    d2h = (s_e2e.d2h_bytes - d2h0) / K
     e2e_local = torch.tensor([float(e2e_tok), e2e_ms], dtype=torch.float64, device="cuda")
     if dist is not None:
         alle = [torch.zeros_like(e2e_local) for _ in range(world)]
@@ -400,18 +432,22 @@ def main():
     rows = sum(cfgd["bs"])
     kinds = {0: (d.qkv_out, d.d_model), 1: (d.d_model, d.n_heads * d.hd), 2: (2 * d.d_ff, d.d_model),
              3: (d.d_model, d.d_ff)}
-    tot_bytes, tot_ns, launches = 0.0, 0.0, 0
+    tot_bytes, tot_ns, tot_ns_w, launches = 0.0, 0.0, 0.0, 0
     per_kind = {}
     for k, (n_out, kk) in kinds.items():
-        n_l, ns = gst[k][4], gst[k][3]
+        n_l, ns, ns_w = gst[k][4], gst[k][3], gst[k][2]
         if n_l == 0:
             continue
         byts = 2.0 * (n_out * kk + rows * kk + rows * n_out)  # weights + bf16 activations in/out
         tot_bytes += byts * n_l
         tot_ns += ns
+        tot_ns_w += ns_w
         launches += n_l
-        per_kind[["qkv", "o", "gate_up", "down"][k]] = {"avg_us": ns / n_l / 1e3,
-                                                         "GBps": byts * n_l / ns}
+        per_kind[["qkv", "o", "gate_up", "down"][k]] = {"avg_us": ns / n_l / 1e3, "GBps": byts * n_l / ns,
+                                                         "avg_us_after_wait": ns_w / n_l / 1e3}
+    # duration convention: min over CTAs of kernel ENTRY -> max over CTAs of exit,
+    # so the weight tiles prefetched before the PDL dependency wait are inside
+    # the window (and so is any overlap with the predecessor's tail)
     achieved = tot_bytes / tot_ns if tot_ns else 0.0   # bytes/ns == GB/s
     head_l, head_ns = gst[4][4], gst[4][3]
     nfe_mean = nfe.mean(axis=0)
@@ -421,6 +457,9 @@ def main():
             "traffic": None, "peak_source": peak_src,
             "kernel": "k_gemm_tc<64> tcgen05 weight-streaming GEMM (block-step QKV/O/gate-up/down)",
             "launches_timed": launches, "per_kind": per_kind,
+            "duration_convention": "kernel entry (before the pre-wait weight TMA) to last CTA exit, "
+                                   "min/max over CTAs, every launch in the timed region",
+            "frac_from_dependency_wait": (tot_bytes / tot_ns_w / hbm) if tot_ns_w else None,
             "head_gemm_GBps": (2.0 * params.vocab.n_out * d.d_model * head_l / head_ns) if head_ns else None,
             "step": {"bytes": step_b, "flops": step_f, "t_roof_ms": step_b / (hbm * 1e6),
                      "ms_per_nfe": ms_per_nfe, "frac": (step_b / (hbm * 1e6)) / ms_per_nfe},
@@ -434,12 +473,10 @@ def main():
             roof["traffic_source"] = tj.get("source")
         except Exception:
             pass
-    with open(os.path.join(HERE, "profiles", "nfe_split_c2.json") if args.config == "c2" else os.devnull, "w") as fh:
-        json.dump({"nfe_split": nfe_mean.tolist(), "tokens_per_request": float(tokens.mean())}, fh)
     cb = None
     if not args.no_cpu_baseline:
         try:
-            cb = cpu_baseline(cfgd, tuple(nfe_mean.tolist()), float(tokens.mean()))
+            cb = cpu_baseline(cfgd, args.config)
         except Exception as exc:  # never let the reported baseline sink the bench line
             cb = {"value": None, "unit": metric, "cores": os.cpu_count(), "kind": "port",
                   "sample": f"failed: {exc!r}"}
@@ -447,7 +484,7 @@ def main():
     line = {
         "metric": metric, "value": value, "unit": "decoded tokens/s", "n_gpus": world, "steps": K,
         "warmup": Wm, "ms_per_step": t_max_ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, make_task prompts)",
+        "vs_baseline": None, "dtype": args.precision, "data": "synthetic (random-init weights, make_task prompts)",
         "config": {"workload": cfgd["workload"], "branches": list(cfgd["bs"]), "prompt_len": P, "gen_len": G,
                    "refresh_interval": cfgd["R"], "head_scale": cfgd["head_scale"], "gamma": cfgd["gamma"],
                    "requests_per_gpu_per_step": 1, "parallelism": f"request-parallel dp{world}",
@@ -455,6 +492,9 @@ def main():
         "nfe_per_request": float(all_res[:, L:L + 3].sum(axis=1).mean()), "nfe_split": nfe_mean.tolist(),
         "requests": int(len(all_res)),
         "tokens_per_request": float(tokens.mean()), "ms_per_nfe": ms_per_nfe,
+        "dynamics_per_request": {k: float(ctrl[:, 0, w].mean()) for k, w in (
+            ("merges", _lib.C_MERGES), ("syncs", _lib.C_SYNCS), ("commits", _lib.C_COMMITS),
+            ("refreshes", _lib.C_REFRESHES), ("cow_pages", _lib.C_COW_PAGES))},
         "e2e": {"value": e2e_value, "unit": "decoded tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "roofline": roof, "cpu_baseline": cb, "clocks": clk.summary(), "gpu_launches": int(counters),

@@ -36,6 +36,9 @@ extern "C" {
 #define BB_ARCH_LLADA 1  /* LLaDA-8B / Dream-7B shape: RMSNorm, RoPE, MHA/GQA, SwiGLU, final norm */
 #define BB_DTYPE_F32 0   /* fp32 verification mode (SIMT kernels)            */
 #define BB_DTYPE_BF16 1  /* bf16 weights/activations/KV, fp32 accumulate (tcgen05) */
+#define BB_DTYPE_BF16X2 2 /* bf16 weights; every activation, q/K/V and head input stored as a
+                             bf16 hi + lo pair (x = hi + lo, ~2^-17 relative), both halves fed to the
+                             tcgen05 MMAs (parity-grade bf16: hd 128 only) */
 
 /* ModelParams (model.py:115-133) + ModelDims (model.py:66-70) + the LLaDA/Dream shape. */
 typedef struct {

@@ -16,6 +16,6 @@ from .model import (BlockWindow, DenoiseOutput, KvCache, ModelDims, ModelParams,
                     LLADA_8B, LLADA_8B_VOCAB, DREAM_7B, DREAM_7B_VOCAB)
 from .scheduler import (PackedQuery, SchedulerConfig, batched_block_forward, get_active_branches, init_full_forward,
                         merge_sync, pack_active_blocks, read_trace, run_blockbatch, run_batch, select_eos_winner,
-                        write_trace)
+                        write_trace, summary_row, write_summary, generated_tokens)
 
 __version__ = "0.1.0"

@@ -50,7 +50,7 @@ class SessionDesc(C.Structure):
 
 
 ARCH_REF, ARCH_LLADA = 0, 1
-DTYPE_F32, DTYPE_BF16 = 0, 1
+DTYPE_F32, DTYPE_BF16, DTYPE_BF16X2 = 0, 1, 2
 VIEW_TOKENS, VIEW_TARGET, VIEW_PROMPT, VIEW_CTRL, VIEW_BRANCH, VIEW_EVENTS = 0, 1, 2, 3, 4, 5
 VIEW_COVERED, VIEW_PM_M, VIEW_PM_S, VIEW_PAGES, VIEW_REFC = 6, 7, 8, 9, 10
 VIEW_HEAD_MASKED, VIEW_HEAD_M, VIEW_HEAD_S, VIEW_HEAD_ARG, VIEW_SLOT_POS, VIEW_SLOT_BR = 11, 12, 13, 14, 15, 16

@@ -58,9 +58,8 @@ struct Session {
   long long nodes_iter = 0, nodes_iter_ref = 0, nodes_prefill = 0, nodes_vanilla = 0;
   long long kernel_launches = 0, graph_launches = 0;
   unsigned long long* tstat = nullptr;  // [16][8] per-GEMM-kind live timing
-  unsigned long long* tsite = nullptr;  // [which 2][kind 5][layer] {min start, max end} (GEMM launch sites)
+  unsigned long long* tsite = nullptr;  // [which 2][kind 5][layer] {min entry, min wait return, max end} (GEMM launch sites)
   bool tsite_on = false;
-  int* tile_cnt = nullptr;              // fused-epilogue arrival counters (self-resetting)
   unsigned char* ns_tabs = nullptr;     // per-GEMM-shape stream-K piece counts
   size_t ns_used = 0, ns_cap = 0;
   struct NsShape {
@@ -68,9 +67,6 @@ struct Session {
     unsigned char* tab;
   };
   std::vector<NsShape> ns_shapes;
-  float* ss_blk = nullptr;              // [rows][d/128] residual sum-of-squares partials
-  float* ss_full = nullptr;
-  int ss_ld = 1;
   unsigned long long* klog = nullptr;  // BB_KLOG=1: kernel timeline (cudaMalloc'd)
   int* fresh_save = nullptr;           // [n_lp] page-table row saved by bb_fresh_kv
   double* sq_part = nullptr;           // [n_sms] bb_sqdiff_norm partial sums
@@ -115,10 +111,12 @@ static int validate_model(const bb_model_desc* m) {
   if (m->vocab_size < 2 || m->layers < 1 || m->d_model < 1 || m->max_len < 1) return BB_ERR_CONFIG;
   if (m->n_heads < 1 || m->n_kv_heads < 1 || m->n_heads % m->n_kv_heads) return BB_ERR_CONFIG;
   if (m->head_dim != 32 && m->head_dim != 64 && m->head_dim != 128 && m->head_dim != 256) return BB_ERR_CONFIG;
-  if (m->dtype != BB_DTYPE_F32 && m->dtype != BB_DTYPE_BF16) return BB_ERR_CONFIG;
+  if (m->dtype != BB_DTYPE_F32 && m->dtype != BB_DTYPE_BF16 && m->dtype != BB_DTYPE_BF16X2) return BB_ERR_CONFIG;
+  // split activations ride on the tcgen05 attention (head_dim 128) and the LLaDA-shape layers
+  if (m->dtype == BB_DTYPE_BF16X2 && (m->arch != BB_ARCH_LLADA || m->head_dim != 128)) return BB_ERR_CONFIG;
   if (m->arch != BB_ARCH_REF && m->arch != BB_ARCH_LLADA) return BB_ERR_CONFIG;
   if (m->arch == BB_ARCH_REF && (m->n_heads != 1 || m->head_dim != m->d_model || m->d_ff != 0)) return BB_ERR_CONFIG;
-  if (m->dtype == BB_DTYPE_BF16 && (m->d_model % 64 || (m->d_ff % 64) || (m->n_heads * m->head_dim) % 64))
+  if (m->dtype != BB_DTYPE_F32 && (m->d_model % 64 || (m->d_ff % 64) || (m->n_heads * m->head_dim) % 64))
     return BB_ERR_CONFIG;
   return BB_OK;
 }
@@ -138,7 +136,8 @@ static Dims make_dims(const bb_model_desc* m) {
   D.dff = m->d_ff;
   D.max_len = m->max_len;
   D.qkv_bias = m->qkv_bias;
-  D.dtype = m->dtype;
+  D.dtype = m->dtype == BB_DTYPE_BF16X2 ? BB_DTYPE_BF16 : m->dtype;  // storage type of weights / activations
+  D.split = m->dtype == BB_DTYPE_BF16X2;
   D.qkv_out = (m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
   D.attn_dim = m->n_heads * m->head_dim;
   D.kv_dim = m->n_kv_heads * m->head_dim;
@@ -180,6 +179,7 @@ static void plan(Session* s, char* base, bool dry) {
   st.covered = c.take<uint8_t>(R * B * L);
   view(BB_VIEW_COVERED, st.covered, R * B * L);
   st.pm_h = c.take<char>(R * B * L * D.d * e);
+  st.pm_h_lo = D.split ? c.take<char>(R * B * L * D.d * e) : nullptr;
   st.pm_m = c.take<float>(R * B * L);
   view(BB_VIEW_PM_M, st.pm_m, R * B * L * 4);
   st.pm_s = c.take<float>(R * B * L);
@@ -198,8 +198,10 @@ static void plan(Session* s, char* base, bool dry) {
   st.ptab = c.take<float>(R * B * L * B);
   st.ptab_ok = c.take<uint8_t>(R * B * L);
   const long long kv_el = (long long)D.layers * R * S.pool * D.nkv * S.ps * D.hd;
-  st.kv_k = c.take<char>(kv_el * e, 1024);
-  st.kv_v = c.take<char>(kv_el * e, 1024);
+  // split: each pool is followed by its lo pool (same layout, kv_lo elements on)
+  st.kv_lo = D.split ? kv_el : 0;
+  st.kv_k = c.take<char>(kv_el * e * (D.split ? 2 : 1), 1024);
+  st.kv_v = c.take<char>(kv_el * e * (D.split ? 2 : 1), 1024);
 
   auto pass = [&](Pass& P, int rows_alloc, int max_items, int item_rows, int full) {
     P.rows_alloc = rows_alloc;
@@ -220,6 +222,13 @@ static void plan(Session* s, char* base, bool dry) {
     P.q = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
     P.attn = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
     P.act = c.take<char>((long long)rows_alloc * (D.dff > 0 ? D.dff : 1) * e, 1024);
+    P.xn_lo = P.q_lo = P.attn_lo = P.act_lo = nullptr;
+    if (D.split) {
+      P.xn_lo = c.take<char>((long long)rows_alloc * D.d * e, 1024);
+      P.q_lo = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
+      P.attn_lo = c.take<char>((long long)rows_alloc * D.attn_dim * e, 1024);
+      P.act_lo = c.take<char>((long long)rows_alloc * (D.dff > 0 ? D.dff : 1) * e, 1024);
+    }
     P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
     P.row_rope = (!full && D.arch == BB_ARCH_LLADA) ? c.take<float>((long long)rows_alloc * D.hd) : nullptr;
     P.n_kz = full ? 1 : (item_rows + 63) / 64;
@@ -250,18 +259,14 @@ static void plan(Session* s, char* base, bool dry) {
   H.skip = c.take<int>(1);
   s->full_rows = c.take<int>(1);
   s->tstat = c.take<unsigned long long>(17 * 8);  // slot 16: GEMM phase marks (BB_GEMM_PH builds)
-  s->tsite = c.take<unsigned long long>((size_t)2 * 10 * D.layers);
+  s->tsite = c.take<unsigned long long>((size_t)3 * 10 * D.layers);
   s->tsite_on = live_stats();
   s->blk.atstat = s->tstat + 5 * 8;   // slots 5/6: block-pass attention (duration, start spread)
   s->full.atstat = s->tstat + 13 * 8; // slots 13/14: full-pass attention
-  s->tile_cnt = c.take<int>(8192);
   s->fresh_save = c.take<int>(S.n_lp);
   s->sq_part = c.take<double>(1024);
   s->ns_cap = 64 * 1024;
   s->ns_tabs = c.take<unsigned char>(s->ns_cap);
-  s->ss_ld = (D.d + 127) / 128;
-  s->ss_blk = c.take<float>((long long)s->blk.rows_alloc * s->ss_ld);
-  s->ss_full = c.take<float>((long long)s->full.rows_alloc * s->ss_ld);
   // GEMM partial planes: max over all stream-K GEMMs of (slots x rows x n_out)
   long long part = 1;
   if (D.dtype == BB_DTYPE_BF16) {
@@ -343,16 +348,20 @@ static int setup_gemms(Session* s) {
       const char* wgu = D.dff ? (const char*)W.wgu + (size_t)l * 2 * D.dff * D.d * e : nullptr;
       const char* wd = D.dff ? (const char*)W.wd + (size_t)l * D.d * D.dff * e : nullptr;
       if (D.dtype == BB_DTYPE_BF16) {
-        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
-        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
+        if (!tc_gemm_setup(lg.qkv, wqkv, D.qkv_out, D.d, P.xn, P.rows_alloc, G.BN, 0, s->n_sms, P.xn_lo))
+          return BB_ERR_CONFIG;
+        if (!tc_gemm_setup(lg.o, wo, D.d, D.attn_dim, P.attn, P.rows_alloc, G.BN, 0, s->n_sms, P.attn_lo))
+          return BB_ERR_CONFIG;
         if (D.dff) {
-          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
-          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, 0, s->n_sms)) return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.gu, wgu, 2 * D.dff, D.d, P.xn, P.rows_alloc, G.BN, 0, s->n_sms, P.xn_lo))
+            return BB_ERR_CONFIG;
+          if (!tc_gemm_setup(lg.dn, wd, D.d, D.dff, P.act, P.rows_alloc, G.BN, 0, s->n_sms, P.act_lo))
+            return BB_ERR_CONFIG;
         }
         TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
           GemmTcParams& p = all[g]->p;
-          p.tstat = s->tsite_on ? s->tsite + 2 * ((size_t)(which * 5 + g) * D.layers + l) : nullptr;
+          p.tstat = s->tsite_on ? s->tsite + 3 * ((size_t)(which * 5 + g) * D.layers + l) : nullptr;
           p.klog = s->D.klog;
           p.klog_cap = s->D.klog_cap;
           p.klog_id = 100 + which * 8 + g;
@@ -376,7 +385,8 @@ static int setup_gemms(Session* s) {
     }
   }
   if (D.dtype == BB_DTYPE_BF16) {
-    if (!tc_gemm_setup(s->head_tc, W.head, D.n_out, D.d, s->blk.xn, s->blk.rows_alloc, s->gb.BN, 1, s->n_sms))
+    if (!tc_gemm_setup(s->head_tc, W.head, D.n_out, D.d, s->blk.xn, s->blk.rows_alloc, s->gb.BN, 1, s->n_sms,
+                       s->blk.xn_lo))
       return BB_ERR_CONFIG;
     GemmTcParams& p = s->head_tc.p;
     p.head_part = s->H.hpart;
@@ -387,7 +397,7 @@ static int setup_gemms(Session* s) {
     p.spike_cut = D.spike_cut;
     p.spike_gain = D.spike_gain;
     p.skip = s->H.skip;
-    p.tstat = s->tsite_on ? s->tsite + 2 * ((size_t)4 * D.layers) : nullptr;
+    p.tstat = s->tsite_on ? s->tsite + 3 * ((size_t)4 * D.layers) : nullptr;
     p.klog = s->D.klog;
     p.klog_cap = s->D.klog_cap;
     p.klog_id = 104;
@@ -404,20 +414,24 @@ static PartRef pref_simt(const SimtGemm& g) {
 }
 
 // ------------------------------------------------------------------ forward pass
-// GEMM launch sites -> per-kind (sum of max end - min start, launches) in
-// tstat[kind] (block 0-3, full 8-11, head 4); sites reset for the next pass
+// GEMM launch sites -> per kind (block 0-3, full 8-11, head 4) in tstat[kind]:
+// [3] += max end - min kernel entry (the launch's whole duration, its pre-wait
+// weight prefetch included), [2] += max end - min dependency-wait return,
+// [4] += 1; sites reset for the next pass
 __global__ void k_tsite_fold(unsigned long long* site, int n_layers, unsigned long long* tstat) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 10 * n_layers) return;
-  unsigned long long* t = site + 2 * (size_t)i;
-  const unsigned long long t0 = t[0], t1 = t[1];
+  unsigned long long* t = site + 3 * (size_t)i;
+  const unsigned long long t0 = t[0], tw = t[1], t1 = t[2];
   if (t0 == ~0ull || t1 == 0ull) return;
   const int sk = i / n_layers, which = sk / 5, kind = sk % 5;
   unsigned long long* dst = tstat + 8 * (kind == 4 ? 4 : which * 8 + kind);
   atomicAdd(&dst[3], t1 > t0 ? t1 - t0 : 0ull);
+  atomicAdd(&dst[2], (tw != ~0ull && t1 > tw) ? t1 - tw : 0ull);
   atomicAdd(&dst[4], 1ull);
   t[0] = ~0ull;
-  t[1] = 0ull;
+  t[1] = ~0ull;
+  t[2] = 0ull;
 }
 
 static cudaError_t tsite_fold(Session* s, cudaStream_t st) {
@@ -706,14 +720,19 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.hard_cap = d->hard_cap > 0 ? d->hard_cap : 4 * S.G * S.B + 16;  // scheduler.py:310
   S.max_copies = S.B * (maxb / S.ps + 2);
   const int NR = S.NR;
-  s->gb.BN = NR <= 64 ? 64 : (NR <= 128 ? 128 : 256);
+  // rows per GEMM chunk (bf16x2: the MMA's N holds each row twice, hi and lo,
+  // so chunks carry at most 128 rows)
+  const bool split = s->D.split != 0;
+  s->gb.BN = NR <= 64 ? 64 : ((NR <= 128 || split) ? 128 : 256);
   // full pass (prefill / refresh): row chunks as wide as possible with little
   // padding (L = 320 -> 2 x 160, L = 192 -> 1 x 192, L = 3072 -> 12 x 256)
   {
-    const int cands[5] = {256, 192, 160, 128, 64};
+    const int cands_n[5] = {256, 192, 160, 128, 64}, cands_s[4] = {128, 96, 80, 64};
+    const int* cands = split ? cands_s : cands_n;
+    const int n_c = split ? 4 : 5;
     int best = 128;
     long long best_cost = -1;
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < n_c; ++i) {
       const int bn = cands[i];
       const long long chunks = (S.NF + bn - 1) / bn;
       const long long cost = chunks * bn + chunks * 32;  // padded rows + per-chunk weight re-read penalty
@@ -779,8 +798,8 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
     std::vector<unsigned long long> ts(17 * 8, 0ull);
     for (int k = 0; k < 16; ++k) ts[k * 8] = ~0ull;
     cudaMemcpy(s->tstat, ts.data(), ts.size() * 8, cudaMemcpyHostToDevice);
-    std::vector<unsigned long long> site((size_t)2 * 10 * s->D.layers, 0ull);
-    for (size_t i = 0; i < site.size(); i += 2) site[i] = ~0ull;
+    std::vector<unsigned long long> site((size_t)3 * 10 * s->D.layers, 0ull);
+    for (size_t i = 0; i < site.size(); i += 3) site[i] = site[i + 1] = ~0ull;
     cudaMemcpy(s->tsite, site.data(), site.size() * 8, cudaMemcpyHostToDevice);
   }
   if (cudaMallocHost(&s->host_ctrl, 4 * (size_t)s->S.R * C_WORDS * 4) != cudaSuccess) {
@@ -1053,7 +1072,8 @@ BB_API int bb_run_vanilla(void* sess, int max_iterations, int use_graph, void* s
   return BB_OK;
 }
 
-// live kernel timing: out[16][5] = (unused min, unused max, unused, sum ns, launches)
+// live kernel timing: out[16][5] = (unused min, unused max, GEMM sum ns from the dependency-wait
+// return, sum ns (GEMMs: from kernel entry), launches)
 // kinds 0-3: block-pass QKV, O, gate/up, down; 4: LM head; 8-11: full-pass QKV..down;
 // 5/13: block/full-pass tensor-core attention duration after its PDL wait,
 // 6/14: spread of that attention's CTA start times (cluster placement)

@@ -14,6 +14,8 @@
 #include <cooperative_groups.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "bb_common.cuh"
 #include "bb_launch.cuh"
 #include "bb_layers.cuh"
@@ -898,7 +900,12 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(
 constexpr int ATC_QR = 64, ATC_KC = 64, ATC_HD = 128;
 constexpr uint32_t ATC_SUB = 64 * 128;  // one [64 rows][64 bf16] SW128 sub-tile (bytes)
 
-template <int CS>
+// SPLIT (bf16x2 sessions): q, K and V are hi + lo bf16 pairs (lo planes
+// beside each); S = Qh.Kh + Qh.Kl + Ql.Kh and O += Ph.Vh + Pl.Vh + Ph.Vl
+// (the dropped lo x lo terms are ~2^-16 relative), the cluster merge
+// exchanges fp32 partials and the output is written as a hi + lo pair.
+// Shared memory doubles (176 KB: one CTA per SM).
+template <int CS, bool SPLIT>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     k_attn_tc(Dims D, Sess S, Pass P, DevState st, int layer, int rows_per_req) {
   klog_mark(D.klog, D.klog_cap, 24);
@@ -917,10 +924,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   constexpr int HD = ATC_HD, QR = ATC_QR, KC = ATC_KC;
   extern __shared__ __align__(1024) uint8_t smraw_tc[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw_tc) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                        // 2 sub-tiles (dims 0-63, 64-127)
-  uint8_t* sK = sQ + 2 * ATC_SUB;          // [2 buf][2 sub]
-  uint8_t* sV = sK + 4 * ATC_SUB;          // [2 buf][2 sub] (MN-major operand: row = key)
-  uint8_t* sPh = sV + 4 * ATC_SUB;         // [64 rows][64 keys] K-major
+  constexpr int NP = SPLIT ? 2 : 1;        // hi (+ lo) planes of q, K, V
+  uint8_t* sQ = sm;                        // [plane][2 sub-tiles (dims 0-63, 64-127)]
+  uint8_t* sK = sQ + NP * 2 * ATC_SUB;     // [plane][2 buf][2 sub]
+  uint8_t* sV = sK + NP * 4 * ATC_SUB;     // [plane][2 buf][2 sub] (MN-major operand: row = key)
+  uint8_t* sPh = sV + NP * 4 * ATC_SUB;    // [64 rows][64 keys] K-major
   uint8_t* sPl = sPh + ATC_SUB;
   __shared__ int sRow[QR], sBr[QR];
   __shared__ uint32_t sVis[2][32][2];  // [buf][branch][key word]: key visible to the branch
@@ -999,8 +1007,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     for (int i = threadIdx.x; i < QR * 16; i += blockDim.x) {
       const int rr = i >> 4, v = i & 15;
       const int slot = sRow[rr];
-      cp_async16(sQ + (v >> 3) * ATC_SUB + sw128_off(rr, v & 7),
-                 Qg + (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8, slot >= 0);
+      const long long qo = (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8;
+      cp_async16(sQ + (v >> 3) * ATC_SUB + sw128_off(rr, v & 7), Qg + qo, slot >= 0);
+      if (SPLIT)
+        cp_async16(sQ + 2 * ATC_SUB + (v >> 3) * ATC_SUB + sw128_off(rr, v & 7),
+                   reinterpret_cast<const bf*>(P.q_lo) + qo, slot >= 0);
     }
     cp_async_commit();
   }
@@ -1018,6 +1029,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
       const uint32_t so = (v >> 3) * ATC_SUB + sw128_off(j, v & 7);
       cp_async16(dK + so, Kg + (ok ? off : 0), ok);
       cp_async16(dV + so, Vg + (ok ? off : 0), ok);
+      if (SPLIT) {  // lo pools: kv_lo elements on; lo planes 4 sub-tiles on
+        cp_async16(dK + 4 * ATC_SUB + so, Kg + st.kv_lo + (ok ? off : 0), ok);
+        cp_async16(dV + 4 * ATC_SUB + so, Vg + st.kv_lo + (ok ? off : 0), ok);
+      }
     }
     cp_async_commit();
     // per-branch visibility bits of the chunk's keys (warp 0: keys 0-31, warp 1: 32-63)
@@ -1057,6 +1072,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
       for (int ks = 0; ks < HD / 16; ++ks) {
         const uint32_t sub = (ks >> 2) * ATC_SUB, ko = (ks & 3) * 32;
         tc_mma_bf16(tS, sdesc_sw128(q0 + sub + ko), sdesc_sw128(k0 + sub + ko), IDS, ks > 0 ? 1u : 0u);
+      }
+      if (SPLIT) {  // + Qh.Kl + Ql.Kh
+        const uint32_t ql = q0 + 2 * ATC_SUB, kl = k0 + 4 * ATC_SUB;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint32_t sub = (ks >> 2) * ATC_SUB, ko = (ks & 3) * 32;
+          tc_mma_bf16(tS, sdesc_sw128(q0 + sub + ko), sdesc_sw128(kl + sub + ko), IDS, 1u);
+          tc_mma_bf16(tS, sdesc_sw128(ql + sub + ko), sdesc_sw128(k0 + sub + ko), IDS, 1u);
+        }
       }
       tc_commit(&mbS);
     }
@@ -1108,7 +1132,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
         }
         const uint32_t off = sw128_off(rl, 4 * hh + c8);
         *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        if (ATT_TC_PLO) *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        if (ATT_TC_PLO || SPLIT) *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
       l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1128,15 +1152,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
       for (int kk = 0; kk < KC / 16; ++kk) {
         const uint64_t bd = sdesc_sw128_mn(v0 + kk * 2048, ATC_SUB, 1024);
         tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), bd, IDO, (ci > 0 || kk > 0) ? 1u : 0u);
-        if (ATT_TC_PLO) tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+        if (ATT_TC_PLO || SPLIT) tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+        if (SPLIT)  // + Ph.Vl
+          tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), sdesc_sw128_mn(v0 + 4 * ATC_SUB + kk * 2048, ATC_SUB, 1024), IDO,
+                      1u);
       }
       tc_commit(&mbP);
     }
   }
-  // partial state (m_ref, l, o / l) of my row half -> fp16 staging in the
-  // (now idle) K buffers: [QR][HD + 8] halves, (m, l) in the row padding
+  // partial state (m_ref, l, o / l) of my row half -> fp16 (SPLIT: fp32)
+  // staging in the (now idle) K buffers: [QR][HD + 8] elements, (m, l) in the
+  // row padding
   constexpr int OLD = HD + 8;
-  __half* sO = reinterpret_cast<__half*>(sK);
+  using ST = typename std::conditional<SPLIT, float, __half>::type;
+  ST* sO = reinterpret_cast<ST*>(sK);
   phase_mark(ph, 6, t0);
   if (n_chunks > 0) mbar_wait(&mbP, (n_chunks - 1) & 1);
   tc_fence_after();
@@ -1156,8 +1185,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
         for (int c = 0; c < 32; ++c) o[c] = 0.0f;
       }
 #pragma unroll
-      for (int c = 0; c < 32; c += 2)
-        *reinterpret_cast<__half2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+      for (int c = 0; c < 32; c += 2) {
+        if constexpr (SPLIT)
+          *reinterpret_cast<float2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = make_float2(o[c] * il, o[c + 1] * il);
+        else
+          *reinterpret_cast<__half2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+      }
     }
     if (hh == 0) *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, lsum);
   }
@@ -1175,14 +1208,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     float4 ov[CS];
 #pragma unroll
     for (int q = 0; q < CS; ++q) {
-      const __half* row = cluster.map_shared_rank(sO + lr * OLD, q);
+      const ST* row = cluster.map_shared_rank(sO + lr * OLD, q);
       const float2 ml = *reinterpret_cast<const float2*>(row + HD);
       mr[q] = ml.x;
       lv[q] = ml.y;
-      const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
-      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
-      ov[q] = make_float4(a.x, a.y, b.x, b.y);
+      if constexpr (SPLIT) {
+        ov[q] = *reinterpret_cast<const float4*>(row + c4);
+      } else {
+        const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+        ov[q] = make_float4(a.x, a.y, b.x, b.y);
+      }
     }
     if (slot < 0) continue;
     float M = -INFINITY;
@@ -1201,12 +1238,21 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
       acc.w += w * ov[q].w;
     }
     const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
-    bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4;
-    __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), p1 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    const long long oo = (long long)slot * D.attn_dim + h * HD + c4;
+    bf* out = reinterpret_cast<bf*>(P.attn) + oo;
+    const float4 y = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(y.x, y.y), p1 = __floats2bfloat162_rn(y.z, y.w);
     uint2 u;
     u.x = *reinterpret_cast<uint32_t*>(&p0);
     u.y = *reinterpret_cast<uint32_t*>(&p1);
     *reinterpret_cast<uint2*>(out) = u;
+    if (SPLIT) {  // lo = rn(y - hi)
+      const float2 f0 = __bfloat1622float2(p0), f1 = __bfloat1622float2(p1);
+      __nv_bfloat162 l0 = __floats2bfloat162_rn(y.x - f0.x, y.y - f0.y), l1 = __floats2bfloat162_rn(y.z - f1.x, y.w - f1.y);
+      u.x = *reinterpret_cast<uint32_t*>(&l0);
+      u.y = *reinterpret_cast<uint32_t*>(&l1);
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf*>(P.attn_lo) + oo) = u;
+    }
   }
   phase_mark(ph, 4, t0);  // (timeline) merged outputs stored
   cluster.sync();
@@ -1218,19 +1264,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   tstat_end(ats);
 }
 
-template <int CS>
+template <int CS, bool SPLIT>
 static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                   cudaStream_t s) {
   const int rows = P.full ? S.L : S.NRq;
-  const size_t smem = 1024 + (size_t)12 * ATC_SUB;  // keys stream through a static ring
+  // keys stream through a static ring: q 2, K 4, V 4 sub-tiles per plane + P hi/lo
+  const size_t smem = 1024 + (size_t)((SPLIT ? 2 : 1) * 10 + 2) * ATC_SUB;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_tc<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_attn_tc<CS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
   dim3 grid(S.R * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
-  launch_k(k_attn_tc<CS>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
+  launch_k(k_attn_tc<CS, SPLIT>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
   return cudaGetLastError();
 }
 
@@ -1246,7 +1293,7 @@ static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P, int tflags) {
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   const int rows = P.full ? S.L : S.NRq;
   const long long per = (long long)S.R * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
-  const long long wave = 2LL * S.n_sms;
+  const long long wave = (D.split ? 1LL : 2LL) * S.n_sms;  // CTAs per SM: 2 (99 KB), bf16x2 1 (177 KB)
   for (int cs = 8; cs > 1; cs >>= 1)
     if (per * cs <= wave) return cs;
   return 1;
@@ -1258,12 +1305,20 @@ template <int HD>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
                                int tflags, cudaStream_t s) {
   if constexpr (HD == 128) {
+    if (D.split) {  // bf16x2: the tcgen05 attention only
+      switch (att_cs_tc(D, S, P, tflags)) {
+        case 8: return attn_tc_launch<8, true>(D, S, P, st, layer, s);
+        case 4: return attn_tc_launch<4, true>(D, S, P, st, layer, s);
+        case 2: return attn_tc_launch<2, true>(D, S, P, st, layer, s);
+        default: return attn_tc_launch<1, true>(D, S, P, st, layer, s);
+      }
+    }
     if (!(tflags & 1)) {
       switch (att_cs_tc(D, S, P, tflags)) {
-        case 8: return attn_tc_launch<8>(D, S, P, st, layer, s);
-        case 4: return attn_tc_launch<4>(D, S, P, st, layer, s);
-        case 2: return attn_tc_launch<2>(D, S, P, st, layer, s);
-        default: return attn_tc_launch<1>(D, S, P, st, layer, s);
+        case 8: return attn_tc_launch<8, false>(D, S, P, st, layer, s);
+        case 4: return attn_tc_launch<4, false>(D, S, P, st, layer, s);
+        case 2: return attn_tc_launch<2, false>(D, S, P, st, layer, s);
+        default: return attn_tc_launch<1, false>(D, S, P, st, layer, s);
       }
     }
   }

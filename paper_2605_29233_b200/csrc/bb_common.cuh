@@ -205,11 +205,16 @@ __device__ __forceinline__ void tstat_end(unsigned long long* ts) {
 // Per-launch-site GEMM timing without a completion protocol: every CTA only
 // issues fire-and-forget reductions of its start / end into the site's
 // {min start, max end}; a fold kernel after each pass turns sites into sums.
-__device__ __forceinline__ void tsite_begin(unsigned long long* ts) {
+// GEMM launch sites: {min kernel entry, min dependency-wait return, max end}
+// over the launch's CTAs (fire-and-forget reductions; folded once per pass)
+__device__ __forceinline__ void tsite_entry(unsigned long long* ts) {
   if (ts != nullptr && threadIdx.x == 0) atomicMin(&ts[0], globaltimer_ns());
 }
+__device__ __forceinline__ void tsite_begin(unsigned long long* ts) {
+  if (ts != nullptr && threadIdx.x == 0) atomicMin(&ts[1], globaltimer_ns());
+}
 __device__ __forceinline__ void tsite_end(unsigned long long* ts) {
-  if (ts != nullptr && threadIdx.x == 0) atomicMax(&ts[1], globaltimer_ns());
+  if (ts != nullptr && threadIdx.x == 0) atomicMax(&ts[2], globaltimer_ns());
 }
 
 // Kernel timeline: CTA 0 stamps (id, %globaltimer) right after its PDL wait,
@@ -239,6 +244,13 @@ template <> struct Cvt<__nv_bfloat16> {
 };
 template <typename T> __device__ __forceinline__ float ldf(const T* p) { return Cvt<T>::to_f(*p); }
 template <typename T> __device__ __forceinline__ void stf(T* p, float v) { *p = Cvt<T>::from_f(v); }
+// bf16x2 storage: hi = rn(v), lo = rn(v - hi) into the lo plane `lo` (null:
+// plain storage).  hi + lo carries v to ~2^-17 relative.
+template <typename T> __device__ __forceinline__ void stf2(T* p, T* lo, float v) {
+  const T h = Cvt<T>::from_f(v);
+  *p = h;
+  if (lo != nullptr) *lo = Cvt<T>::from_f(v - Cvt<T>::to_f(h));
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

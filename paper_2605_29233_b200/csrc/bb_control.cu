@@ -831,6 +831,7 @@ __global__ void __launch_bounds__(256) k_merge_prep(Dims D, Sess S, DevState st,
     return;
   }
   const T* h = reinterpret_cast<const T*>(st.pm_h) + pmi * D.d;
+  const T* hl = st.pm_h_lo != nullptr ? reinterpret_cast<const T*>(st.pm_h_lo) + pmi * D.d : nullptr;
   const float m = st.pm_m[pmi], ssum = st.pm_s[pmi], boost = st.pm_boost[pmi];
   const int tg = st.target[(long long)r * S.G + (i - S.P)];
   for (int s = 0; s < S.B; ++s) {
@@ -845,6 +846,12 @@ __global__ void __launch_bounds__(256) k_merge_prep(Dims D, Sess S, DevState st,
       const T* wp = reinterpret_cast<const T*>(&wv);
 #pragma unroll
       for (int e = 0; e < VE; ++e) a = fmaf(ldf(hp + e), ldf(wp + e), a);
+      if (hl != nullptr) {  // bf16x2: the head input's lo plane (the head GEMM used h_hi + h_lo)
+        const uint4 lv = *reinterpret_cast<const uint4*>(hl + c);
+        const T* lp = reinterpret_cast<const T*>(&lv);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) a = fmaf(ldf(lp + e), ldf(wp + e), a);
+      }
     }
     a = warp_sum(a);
     float l = head_logit(a, D.head_scale, D.spike_cut, D.spike_gain);
@@ -1276,8 +1283,11 @@ __global__ void __launch_bounds__(256) k_kv_gather(Dims D, Sess S, DevState st, 
   for (int e = threadIdx.x; e < kv_dim; e += blockDim.x) {
     const int kvh = e / D.hd, i = e - kvh * D.hd;
     const long long src = lay + ((gpage * D.nkv + kvh) * S.ps + row) * D.hd + i;
-    o[e] = ldf(reinterpret_cast<const T*>(st.kv_k) + src);
-    o[kv_dim + e] = ldf(reinterpret_cast<const T*>(st.kv_v) + src);
+    const T* kp = reinterpret_cast<const T*>(st.kv_k) + src;
+    const T* vp = reinterpret_cast<const T*>(st.kv_v) + src;
+    // bf16x2: the cached value is hi + lo
+    o[e] = ldf(kp) + (st.kv_lo != 0 ? ldf(kp + st.kv_lo) : 0.0f);
+    o[kv_dim + e] = ldf(vp) + (st.kv_lo != 0 ? ldf(vp + st.kv_lo) : 0.0f);
   }
 }
 
@@ -1296,8 +1306,10 @@ __global__ void __launch_bounds__(256) k_kv_scatter(Dims D, Sess S, DevState st,
   for (int e = threadIdx.x; e < kv_dim; e += blockDim.x) {
     const int kvh = e / D.hd, i = e - kvh * D.hd;
     const long long dst = lay + ((gpage * D.nkv + kvh) * S.ps + row) * D.hd + i;
-    stf(reinterpret_cast<T*>(st.kv_k) + dst, o[e]);
-    stf(reinterpret_cast<T*>(st.kv_v) + dst, o[kv_dim + e]);
+    T* kp = reinterpret_cast<T*>(st.kv_k) + dst;
+    T* vp = reinterpret_cast<T*>(st.kv_v) + dst;
+    stf2(kp, st.kv_lo != 0 ? kp + st.kv_lo : nullptr, o[e]);
+    stf2(vp, st.kv_lo != 0 ? vp + st.kv_lo : nullptr, o[kv_dim + e]);
   }
 }
 
@@ -1406,6 +1418,14 @@ __global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st,
         K[dof + e] = a;
         V[dof + e] = b;
       }
+      if (st.kv_lo != 0) {  // bf16x2: the lo pools (kv_lo elements on)
+        const long long lo = st.kv_lo * (long long)sizeof(T) / 16;
+        for (long long e = threadIdx.x; e < vecs; e += blockDim.x) {
+          const uint4 a = K[lo + so + e], b = V[lo + so + e];
+          K[lo + dof + e] = a;
+          V[lo + dof + e] = b;
+        }
+      }
     }
   } else {
     const int vecs = (int)(D.d * sizeof(T) / 16);
@@ -1430,6 +1450,13 @@ __global__ void __launch_bounds__(512) k_copy_pages(Dims D, Sess S, DevState st,
                                                       (((long long)r * S.B + src) * S.L + pos) * D.d);
       uint4* b = reinterpret_cast<uint4*>(reinterpret_cast<T*>(st.pm_h) + (((long long)r * S.B + dst) * S.L + pos) * D.d);
       for (int e = threadIdx.x; e < vecs; e += blockDim.x) b[e] = a[e];
+      if (st.pm_h_lo != nullptr) {
+        const uint4* al = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(st.pm_h_lo) +
+                                                         (((long long)r * S.B + src) * S.L + pos) * D.d);
+        uint4* bl = reinterpret_cast<uint4*>(reinterpret_cast<T*>(st.pm_h_lo) +
+                                             (((long long)r * S.B + dst) * S.L + pos) * D.d);
+        for (int e = threadIdx.x; e < vecs; e += blockDim.x) bl[e] = al[e];
+      }
     }
   }
 }

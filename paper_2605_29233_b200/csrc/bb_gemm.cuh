@@ -55,49 +55,21 @@ __device__ __forceinline__ float part_sum(const float* __restrict__ part, long l
   return acc;
 }
 
-// Fused stream-K epilogue.  The CTA that completes a tile's last k-piece
-// (per-tile arrival counter) sums the pieces in slot order (deterministic)
-// and applies the consumer op in place of a separate post-GEMM kernel:
-//   kind 2  QKV: + bias, RoPE (pairs (i, i+hd/2) are tile-local for hd <= 128),
-//           q -> q buffer, k/v -> the row's branch KV page (the window splice)
-//   kind 3  gate/up: act = silu(gate) * up (gate/up rows interleaved per tile)
-//   kind 4  residual: x += out, per-(row, tile) sum of squares for RMSNorm
-// kind 0 keeps the raw partial planes (tests).
+// Epilogue of a whole-tile (mode 1) GEMM: kind 1 = LM head + confidence.
 struct EpiArgs {
   int kind;
-  int* tile_cnt;
-  const long long* slot_kvoff;  // per-row KV element offset within a layer (page, position)
-  long long kv_layer_elems;     // elements per layer of the KV pool
-  const int* slot_pos;
-  const int* slot_req;
-  const int* slot_br;
-  int nh, nkv, hd, rope;
-  const float* bias;
-  const float* rope_tab;
-  __nv_bfloat16* q;
-  int attn_dim;
-  __nv_bfloat16* kv_k;
-  __nv_bfloat16* kv_v;
-  long long kv_layer_off;
-  const int* pt;
-  int ps, P, n_pp, L, pool, B, n_lp;
-  __nv_bfloat16* act;
-  int dff;
-  float* x;
-  int d;
-  float* ss_part;
-  int ss_ld;
 };
 
 struct GemmTcParams {
   // mode 0: stream-K into fp32 partial planes (consumed by post kernels)
   // mode 1: whole tiles round-robin over a persistent grid, epilogue from TMEM
-  //         (epi.kind 1 = LM head, 2..4 fused consumer ops)
-  // mode 2: cluster split-K: `split` CTAs of a cluster each own 1/split of the
-  //         k-blocks of one tile; partial accumulators are reduced through
-  //         distributed shared memory in rank order, then the fused epilogue
+  //         (epi.kind 1 = LM head)
   int n_out, K, n_ntiles, n_chunks, KB, mode;
-  int split;
+  // bf16x2 activations: 0, or the real rows per chunk (= BN/2).  The B tile
+  // then stacks the chunk's hi rows [0, half) and lo rows [half, BN) (two TMA
+  // loads), the MMA runs N = BN, and the epilogue adds accumulator columns j
+  // and half + j: out = W.(x_hi + x_lo) with fp32 accumulation
+  int half;
   int rows_alloc;
   const int* rows_valid;  // device scalar or nullptr
   const int* skip;        // device scalar or nullptr: nonzero => no-op
@@ -123,7 +95,7 @@ struct GemmTcParams {
 };
 
 struct TcGemm {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmB2;  // tmB2: lo plane of the activations (bf16x2), else unused
   const void* W;
   GemmTcParams p;
   SplitK sk;
@@ -131,10 +103,10 @@ struct TcGemm {
   size_t smem;
 };
 
-// host API (bb_gemm.cu).  mode 0 = stream-K planes, 1 = LM head, 3 = fused
-// (picks tiles-only or cluster split-K from the tile count; epi set by caller)
+// host API (bb_gemm.cu).  mode 0 = stream-K planes, 1 = LM head
+// X_lo != nullptr: bf16x2 activations (BN real rows per chunk, MMA N = 2 BN)
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN,
-                   int mode, int max_grid);
+                   int mode, int max_grid, const void* X_lo = nullptr);
 cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s);
 
 struct SimtGemm {

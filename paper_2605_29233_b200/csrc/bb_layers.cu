@@ -36,6 +36,7 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 template <typename T> struct Vec4;
 template <> struct Vec4<float> {
   static __device__ __forceinline__ void st(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+  static __device__ __forceinline__ void st2(float* p, float*, float4 v) { *reinterpret_cast<float4*>(p) = v; }
   static __device__ __forceinline__ float4 ld(const float* p) { return *reinterpret_cast<const float4*>(p); }
 };
 template <> struct Vec4<__nv_bfloat16> {
@@ -45,6 +46,20 @@ template <> struct Vec4<__nv_bfloat16> {
     u.x = *reinterpret_cast<uint32_t*>(&a);
     u.y = *reinterpret_cast<uint32_t*>(&b);
     *reinterpret_cast<uint2*>(p) = u;
+  }
+  // bf16x2: hi plane at p, lo plane at lo (lo = rn(v - hi)); lo == nullptr: hi only
+  static __device__ __forceinline__ void st2(__nv_bfloat16* p, __nv_bfloat16* lo, float4 v) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+    if (lo == nullptr) return;
+    const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+    __nv_bfloat162 la = __floats2bfloat162_rn(v.x - fa.x, v.y - fa.y), lb = __floats2bfloat162_rn(v.z - fb.x, v.w - fb.y);
+    u.x = *reinterpret_cast<uint32_t*>(&la);
+    u.y = *reinterpret_cast<uint32_t*>(&lb);
+    *reinterpret_cast<uint2*>(lo) = u;
   }
   static __device__ __forceinline__ float4 ld(const __nv_bfloat16* p) {
     const uint2 u = *reinterpret_cast<const uint2*>(p);
@@ -70,6 +85,7 @@ __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restri
   }
   float* x = P.x + (long long)row * D.d;
   T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
+  T* xl = P.xn_lo != nullptr ? reinterpret_cast<T*>(P.xn_lo) + (long long)row * D.d : nullptr;
   if (P.row_rope != nullptr && rope != nullptr)  // per-row RoPE table for the layer-stream QKV finalize
     for (int i = threadIdx.x; i < (D.hd >> 1); i += blockDim.x)
       *reinterpret_cast<float2*>(P.row_rope + ((long long)row * (D.hd >> 1) + i) * 2) =
@@ -98,7 +114,7 @@ __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restri
       v.z *= inv * g.z;
       v.w *= inv * g.w;
     }
-    Vec4<T>::st(xn + c, v);
+    Vec4<T>::st2(xn + c, xl != nullptr ? xl + c : nullptr, v);
   }
 }
 
@@ -171,17 +187,20 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
     b = b2;
   }
   if (hh < D.nh) {
-    T* q = reinterpret_cast<T*>(P.q) + (long long)row * D.attn_dim + hh * D.hd;
-    stf(q + i, a);
-    stf(q + i + half, b);
+    const long long o = (long long)row * D.attn_dim + hh * D.hd;
+    T* q = reinterpret_cast<T*>(P.q) + o;
+    T* ql = P.q_lo != nullptr ? reinterpret_cast<T*>(P.q_lo) + o : nullptr;
+    stf2(q + i, ql != nullptr ? ql + i : nullptr, a);
+    stf2(q + i + half, ql != nullptr ? ql + i + half : nullptr, b);
     return;
   }
   const bool isk = hh < D.nh + D.nkv;
   const int kvh = isk ? hh - D.nh : hh - D.nh - D.nkv;
   const long long lay = (long long)layer * S.R * S.pool * D.nkv * S.ps * D.hd;
   T* dst = reinterpret_cast<T*>(isk ? st.kv_k : st.kv_v) + lay + kvo + (long long)kvh * S.ps * D.hd;
-  stf(dst + i, a);
-  stf(dst + i + half, b);
+  T* dl = st.kv_lo != 0 ? dst + st.kv_lo : nullptr;  // bf16x2: the lo pool
+  stf2(dst + i, dl != nullptr ? dl + i : nullptr, a);
+  stf2(dst + i + half, dl != nullptr ? dl + i + half : nullptr, b);
 }
 
 // ------------------------------------------------------------------ residual (+ norm)
@@ -193,6 +212,7 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
   const int row = blockIdx.x;
   float* x = P.x + (long long)row * D.d;
   T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
+  T* xl = P.xn_lo != nullptr ? reinterpret_cast<T*>(P.xn_lo) + (long long)row * D.d : nullptr;
   float ss = 0.0f;
 #if POST_RES_BATCH
   // d <= 4096: each thread owns <= 2 column groups.  Session constants (piece
@@ -265,7 +285,7 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
         v.z *= inv * g.z;
         v.w *= inv * g.w;
       }
-      Vec4<T>::st(xn + cc[u], v);
+      Vec4<T>::st2(xn + cc[u], xl != nullptr ? xl + cc[u] : nullptr, v);
     }
     return;
   }
@@ -304,41 +324,7 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
       v.z *= inv * g.z;
       v.w *= inv * g.w;
     }
-    Vec4<T>::st(xn + c, v);
-  }
-}
-
-// ------------------------------------------------------------------ RMSNorm (fused-epilogue path)
-// xn = x * rsqrt(mean(x^2) + eps) * g  with the row's sum of squares taken from
-// the per-(row, 128-column tile) partials the residual GEMM epilogue wrote
-// (summed in tile order: deterministic).  ln == nullptr -> xn = x.
-template <typename T>
-__global__ void __launch_bounds__(512) k_norm(Dims D, Pass P, const float* __restrict__ ss_part, int ss_ld,
-                                              const float* __restrict__ ln) {
-  pdl_enter();
-  klog_mark(D.klog, D.klog_cap, 6);
-  if (*P.skip) return;
-  const int row = blockIdx.x;
-  if (P.slot_pos[row] < 0) return;
-  float inv = 1.0f;
-  if (ln != nullptr) {
-    const float* sp = ss_part + (long long)row * ss_ld;
-    float ss = 0.0f;
-    for (int t = 0; t < ss_ld; ++t) ss += sp[t];
-    inv = 1.0f / sqrtf(ss / (float)D.d + D.eps);
-  }
-  const float* x = P.x + (long long)row * D.d;
-  T* xn = reinterpret_cast<T*>(P.xn) + (long long)row * D.d;
-  for (int c = threadIdx.x * 4; c < D.d; c += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4*>(x + c);
-    if (ln != nullptr) {
-      const float4 g = *reinterpret_cast<const float4*>(ln + c);
-      v.x *= inv * g.x;
-      v.y *= inv * g.y;
-      v.z *= inv * g.z;
-      v.w *= inv * g.w;
-    }
-    Vec4<T>::st(xn + c, v);
+    Vec4<T>::st2(xn + c, xl != nullptr ? xl + c : nullptr, v);
   }
 }
 
@@ -389,7 +375,8 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
   a.y = g.y / (1.0f + expf(-g.y)) * u.y;
   a.z = g.z / (1.0f + expf(-g.z)) * u.z;
   a.w = g.w / (1.0f + expf(-g.w)) * u.w;
-  Vec4<T>::st(reinterpret_cast<T*>(P.act) + (long long)row * D.dff + f, a);
+  const long long ao = (long long)row * D.dff + f;
+  Vec4<T>::st2(reinterpret_cast<T*>(P.act) + ao, P.act_lo != nullptr ? reinterpret_cast<T*>(P.act_lo) + ao : nullptr, a);
 }
 
 // ------------------------------------------------------------------ head side
@@ -405,6 +392,11 @@ __global__ void __launch_bounds__(256) k_gather_head(Dims D, Sess S, Pass full, 
   const T* a = reinterpret_cast<const T*>(full.xn) + src * D.d;
   T* o = reinterpret_cast<T*>(blk.xn) + (long long)slot * D.d;
   for (int c = threadIdx.x; c < D.d; c += blockDim.x) o[c] = a[c];
+  if (full.xn_lo != nullptr) {
+    const T* al = reinterpret_cast<const T*>(full.xn_lo) + src * D.d;
+    T* ol = reinterpret_cast<T*>(blk.xn_lo) + (long long)slot * D.d;
+    for (int c = threadIdx.x; c < D.d; c += blockDim.x) ol[c] = al[c];
+  }
 }
 
 __global__ void __launch_bounds__(128) k_head_tiles_f32(Dims D, Head H) {
@@ -506,6 +498,11 @@ __global__ void __launch_bounds__(256) k_head_reduce(Dims D, Sess S, Pass blk, H
   const T* src = reinterpret_cast<const T*>(blk.xn) + (long long)slot * D.d;
   T* dst = reinterpret_cast<T*>(st.pm_h) + pm * D.d;
   for (int c = threadIdx.x; c < D.d; c += blockDim.x) dst[c] = src[c];
+  if (st.pm_h_lo != nullptr) {
+    const T* sl = reinterpret_cast<const T*>(blk.xn_lo) + (long long)slot * D.d;
+    T* dl = reinterpret_cast<T*>(st.pm_h_lo) + pm * D.d;
+    for (int c = threadIdx.x; c < D.d; c += blockDim.x) dl[c] = sl[c];
+  }
 }
 
 // Materialised logits / probabilities of the last head pass (the seams'
@@ -558,12 +555,6 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
 
 cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s) {
   BB_DISPATCH(D, (launch_k(k_post_residual<T>, dim3(P.rows_alloc), dim3(512), (size_t)(0), s, D, P, pr, ln)));
-  return cudaGetLastError();
-}
-
-cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int ss_ld, const float* ln,
-                        cudaStream_t s) {
-  BB_DISPATCH(D, (launch_k(k_norm<T>, dim3(P.rows_alloc), dim3(512), (size_t)(0), s, D, P, ss_part, ss_ld, ln)));
   return cudaGetLastError();
 }
 

@@ -36,8 +36,6 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
                             int layer, const PartRef& pr, cudaStream_t s);
 cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s);
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s);
-cudaError_t launch_norm(const Dims& D, const Pass& P, const float* ss_part, int ss_ld, const float* ln,
-                        cudaStream_t s);
 // tflags: bb_session_desc.test_flags (tests only)
 cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, int tflags,
                         cudaStream_t s);

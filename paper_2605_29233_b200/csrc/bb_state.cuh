@@ -44,6 +44,7 @@ enum Br { B_START = 0, B_END, B_DONE, B_DEC, B_MERGED, B_SIZE, B_WORDS = 8 };
 struct Dims {
   int arch;  // 0 = reference synthetic denoiser, 1 = LLaDA/Dream shape
   int V, n_out, n_ext, layers, d, nh, nkv, hd, dff, max_len, qkv_bias, dtype;
+  int split;  // BB_DTYPE_BF16X2: dtype 1 storage with a bf16 lo plane beside every bf16 activation
   int qkv_out, attn_dim, kv_dim, n_vtiles;
   float eps, gamma, head_scale, spike_cut, spike_gain, attn_scale;
   int radius;
@@ -91,6 +92,8 @@ struct DevState {
   uint8_t* ptab_ok;   // [R][B][L]
   void* kv_k;         // [layers][R*pool][nkv][ps][hd] T
   void* kv_v;
+  long long kv_lo;    // split: element offset of the lo pool (kv_k + kv_lo, kv_v + kv_lo); 0 otherwise
+  void* pm_h_lo;      // split: lo plane of pm_h (else null)
 };
 
 struct Pass {
@@ -112,6 +115,11 @@ struct Pass {
   void* q;            // [rows_alloc][attn_dim] T
   void* attn;         // [rows_alloc][attn_dim] T
   void* act;          // [rows_alloc][dff] T
+  // split (bf16x2) sessions: the lo planes of xn / q / attn / act (same shapes), else null
+  void* xn_lo;
+  void* q_lo;
+  void* attn_lo;
+  void* act_lo;
   float* apart;       // [R][max_items][item_rows][nh][hd+2]
   float* row_rope;    // [rows_alloc][hd/2][2] RoPE (cos, sin) of each row's position (block pass, arch 1) or null
   // key lists of the tensor-core attention, built once per pass (the page

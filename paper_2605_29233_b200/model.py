@@ -362,7 +362,8 @@ class ModelParams:
             arch=_lib.ARCH_REF if d.arch == "ref" else _lib.ARCH_LLADA, vocab_size=self.vocab.size,
             layers=d.layers, d_model=d.d_model, n_heads=d.n_heads, n_kv_heads=d.n_kv_heads, head_dim=d.hd,
             d_ff=d.d_ff, max_len=d.max_len, qkv_bias=int(d.qkv_bias),
-            dtype=_lib.DTYPE_F32 if self.dtype == "f32" else _lib.DTYPE_BF16, rope_theta=d.rope_theta,
+            dtype={"f32": _lib.DTYPE_F32, "bf16": _lib.DTYPE_BF16, "bf16x2": _lib.DTYPE_BF16X2}[self.dtype],
+            rope_theta=d.rope_theta,
             norm_eps=d.norm_eps, gamma=self.gamma, radius=self.radius, head_scale=self.head_scale,
             spike_cut=self.spike_cut, spike_gain=self.spike_gain)
 
@@ -404,13 +405,20 @@ def _torch():
 def build_model(seed: int, vocab: Vocab, dims: ModelDims = ModelDims(), gamma: float = 8.0, radius: int = 4,
                 head_scale: float = 1.0, spike_cut: float = 0.72, spike_gain: float = 33.0,
                 dtype: str = "f32", init: str | None = None) -> ModelParams:
-    """model.py:210-241 on the device.  ``dtype`` "f32" (verification mode) or
-    "bf16"; ``init`` "philox" (reference draw, default for arch "ref") or
-    "hash" (device counter hash, default for arch "llada")."""
+    """model.py:210-241 on the device.  ``dtype``: "f32" (verification mode:
+    fp32 weights / activations / KV, SIMT kernels), "bf16" (bf16 weights,
+    activations and KV; tcgen05) or "bf16x2" (bf16 weights; every activation,
+    q/K/V and head input kept as a bf16 hi + lo pair that the tcgen05 MMAs
+    consume both halves of -- fp32-grade activations at bf16 weight traffic;
+    LLaDA/Dream shape with head_dim 128).  ``init`` "philox" (reference draw,
+    default for arch "ref") or "hash" (device counter hash, default for arch
+    "llada")."""
     if dims.layers < 1 or dims.d_model < 1 or dims.max_len < 1:
         raise ConfigError(f"non-positive model dimensions: {dims}")
-    if dtype not in ("f32", "bf16"):
+    if dtype not in ("f32", "bf16", "bf16x2"):
         raise ConfigError(f"unknown dtype {dtype!r}")
+    if dtype == "bf16x2" and (dims.arch != "llada" or dims.hd != 128):
+        raise ConfigError("bf16x2 needs the LLaDA/Dream architecture with head_dim 128")
     init = init or ("philox" if dims.arch == "ref" else "hash")
     if dims.arch == "ref" and (dims.n_heads != 1 or dims.hd != dims.d_model or dims.d_ff):
         raise ConfigError("the reference architecture is single-head, head_dim = d_model, no MLP")
@@ -450,7 +458,19 @@ def build_model(seed: int, vocab: Vocab, dims: ModelDims = ModelDims(), gamma: f
     return ModelParams(weights=weights, **kw)
 
 
+def verification_copy(params: ModelParams) -> ModelParams:
+    """The same model in fp32 verification mode: every weight upcast exactly
+    (a bf16 model's fp32 twin holds the identical bf16-rounded values), so a
+    bf16 run and its verification run differ only in arithmetic."""
+    if params.dtype == "f32":
+        return params
+    weights = {k: v.float() for k, v in params.weights.items()}
+    from dataclasses import replace
+    return replace(params, dtype="f32", weights=weights, _handle=[None], _sessions={})
+
+
 def _hash_weights(torch, vocab: Vocab, dims: ModelDims, seed: int, dtype: str) -> dict:
+    dtype = "bf16" if dtype == "bf16x2" else dtype  # bf16x2 keeps bf16 weights
     L = _lib.lib()
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
     cdt = _lib.DTYPE_F32 if dtype == "f32" else _lib.DTYPE_BF16

@@ -457,3 +457,42 @@ def read_trace(path) -> list[dict]:
         if header.get("schema") != TRACE_SCHEMA:
             raise ContractError(f"unknown trace schema: {header}")
         return [json.loads(line) for line in fh if line.strip()]
+
+
+# --------------------------------------------------------------------------
+# run summary CSV (the reference CLI's per-run table, cli.py:147-165)
+# --------------------------------------------------------------------------
+SUMMARY_FIELDS = ["task_seed", "mode", "block_size", "correct", "tokens_decoded", "eos_position", "nfe_init",
+                  "nfe_block", "nfe_refresh", "nfe_total", "tokens"]
+
+
+def generated_tokens(result, vocab) -> list[int]:
+    """analysis.py:160-171: generated tokens up to and including the first eos, masks excluded."""
+    out = []
+    for t in result.row.tokens[result.row.prompt_len:]:
+        t = int(t)
+        if t == vocab.mask_id:
+            break
+        out.append(t)
+        if t == vocab.eos_id:
+            break
+    return out
+
+
+def summary_row(seed: int, mode: str, result, vocab) -> dict:
+    """cli.py:157-165"""
+    return {"task_seed": seed, "mode": mode, "block_size": result.block_size, "correct": int(result.correct),
+            "tokens_decoded": result.tokens_decoded,
+            "eos_position": "" if result.eos_position is None else result.eos_position,
+            "nfe_init": result.nfe.nfe_init, "nfe_block": result.nfe.nfe_block,
+            "nfe_refresh": result.nfe.nfe_refresh, "nfe_total": result.nfe.total,
+            "tokens": " ".join(str(t) for t in generated_tokens(result, vocab))}
+
+
+def write_summary(path, rows: list[dict]) -> None:
+    """cli.py:147-154: the summary table as CSV (header + one row per run)."""
+    import csv
+    with open(path, "w", newline="") as fh:
+        w = csv.DictWriter(fh, fieldnames=SUMMARY_FIELDS)
+        w.writeheader()
+        w.writerows(rows)

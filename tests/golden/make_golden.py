@@ -22,6 +22,10 @@ Outputs (all under tests/golden/):
   kernels.json      reference confidence_transition / merge_sync outputs on
                     the fuzzed inputs of fuzz.py (inputs rebuilt from seeds).
   forward_c1.npz    reference full_forward / block_forward numerics (C1, seed 0).
+  summary_ref.csv   the reference CLI's run summary (cli.py:147-165,
+                    summary_row / write_summary) of every runs_ref.json run of
+                    the c1_hs2 and default_g4_eos configs (rebuilt as reference
+                    GenerationResults; --summary-only regenerates just this).
   runs_runaway.json reference run_blockbatch with the hard cap lowered to 16
                     forwards (HARD_CAP_FACTOR = 0): forward_hook calls up to
                     the RunawayError (scheduler.py:310, 324-325).
@@ -343,8 +347,33 @@ def gen_runaway_runs():
     return {"hard_cap": 16, "prompt_len": 16, "gen_len": 128, "block_sizes": [8, 16, 32], "runs": runs}
 
 
+SUMMARY_CONFIGS = ("c1_hs2", "default_g4_eos")
+
+
+def gen_summary_csv(path):
+    """The reference's own summary_row / write_summary over the golden runs."""
+    from blockbatch import cli as bbc
+    runs = json.load(open(os.path.join(HERE, "runs_ref.json")))
+    rows = []
+    for name in SUMMARY_CONFIGS:
+        g = runs[name]
+        vs = g["model"]["vocab_size"]
+        vocab = bbm.Vocab(size=vs, category_of={t: f"c{t % 4}" for t in range(vs)}) if vs != 32 else bbm.Vocab()
+        for seed, r in zip(g["seeds"], g["runs"]):
+            res = bbd.GenerationResult(row=bbm.SequenceRow(np.array(r["tokens"], dtype=np.int64), g["prompt_len"]),
+                                       branch_index=r["branch_index"], block_size=r["block_size"],
+                                       nfe=bbd.NfeCounter(*r["nfe"]), trace=[], correct=r["correct"],
+                                       tokens_decoded=r["tokens_decoded"], eos_position=r["eos_position"])
+            rows.append(bbc.summary_row(seed, f"blockbatch:{name}", res, vocab))
+    bbc.write_summary(path, rows)
+
+
 def main():
     t0 = time.time()
+    if "--summary-only" in sys.argv:
+        gen_summary_csv(os.path.join(HERE, "summary_ref.csv"))
+        print(f"done in {time.time() - t0:.1f}s")
+        return
     with open(os.path.join(HERE, "runs_runaway.json"), "w") as fh:
         json.dump(gen_runaway_runs(), fh, separators=(",", ":"))
     if "--runaway-only" in sys.argv:
@@ -364,6 +393,7 @@ def main():
     with open(os.path.join(HERE, "kernels.json"), "w") as fh:
         json.dump(gen_kernel_fixtures(), fh, separators=(",", ":"))
     np.savez_compressed(os.path.join(HERE, "forward_c1.npz"), **gen_forward_c1())
+    gen_summary_csv(os.path.join(HERE, "summary_ref.csv"))
     print(f"done in {time.time() - t0:.1f}s")
 
 

@@ -277,6 +277,17 @@ def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol):
                           f"hd128 tc={tc} cs={cs or 'auto'} kvh={kvh}", test_flags=flags)
 
 
+@pytest.mark.parametrize("kvh,gain,tol", [(2, 33.0, 2e-2), (1, 33.0, 2e-2), (2, 0.0, 2e-3)])
+def test_bf16x2_block_step_matches_exact_oracle(kvh, gain, tol):
+    """bf16x2 numerics (bf16 weights; hi + lo bf16 activations, q/K/V and head
+    input; both halves through the tcgen05 GEMMs and attention) vs the oracle
+    with NO activation rounding, at the north-star bar (max-abs <= 2e-2 on
+    normalised logits) WITH the spike epilogue (gain 33), MHA and GQA."""
+    g = LLADA["llada_tiny_bf16"]
+    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128), "bf16x2", gain, tol,
+                          f"bf16x2 hd128 kvh={kvh}")
+
+
 def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name, test_flags=0):
     from oracle import bb_oracle as O
     from paper_2605_29233_b200.engine import Session
@@ -285,7 +296,8 @@ def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name, test_f
     a, params = _llada_params(g, dtype, spike_gain)
     cfg = cfg_from(g["config"])
     arch = O.OArch(**a)
-    W = O.weights_as(O.hash_weights(arch, 0), dtype)
+    # bf16x2 is held to the oracle WITHOUT activation rounding (the model its bf16 weights define)
+    W = O.weights_as(O.hash_weights(arch, 0), "bf16" if dtype == "bf16x2" else dtype)
     rnd = O.bf16_round if dtype == "bf16" else None
     P, G = g["prompt_len"], g["gen_len"]
     worst_lp, worst_lse, agree, n = 0.0, 0.0, 0, 0
