@@ -51,6 +51,7 @@ struct Session {
   TcGemm head_tc;
   SimtGemm head_simt;
   float* part = nullptr;
+  AttnMaps am{};             // TMA views of the KV pools (bf16 hd-128 attention)
   int* full_rows = nullptr;  // device scalar: rows of the full pass
   char* ws = nullptr;
   size_t ws_bytes = 0;
@@ -232,7 +233,7 @@ static void plan(Session* s, char* base, bool dry) {
     P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
     P.row_rope = (!full && D.arch == BB_ARCH_LLADA) ? c.take<float>((long long)rows_alloc * D.hd) : nullptr;
     P.n_kz = full ? 1 : (item_rows + 63) / 64;
-    P.akey_cap = B * S.L;
+    P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries
     P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
     P.akey_n = c.take<int>((long long)R * P.n_kz * 2);
   };
@@ -384,6 +385,12 @@ static int setup_gemms(Session* s) {
       }
     }
   }
+  s->am.ok = false;
+  if (D.dtype == BB_DTYPE_BF16 && D.hd == 128 && s->S.ps == 16) {
+    const uint64_t rows = (uint64_t)D.layers * s->S.R * s->S.pool * D.nkv * s->S.ps;
+    s->am.ok = tma_map_bf16(&s->am.k, s->st.kv_k, (uint64_t)D.hd, rows, 16) &&
+               tma_map_bf16(&s->am.v, s->st.kv_v, (uint64_t)D.hd, rows, 16);
+  }
   if (D.dtype == BB_DTYPE_BF16) {
     if (!tc_gemm_setup(s->head_tc, W.head, D.n_out, D.d, s->blk.xn, s->blk.rows_alloc, s->gb.BN, 1, s->n_sms,
                        s->blk.xn_lo))
@@ -462,7 +469,7 @@ static cudaError_t forward(Session* s, Pass& P, PassGemms& G, cudaStream_t st) {
     PartRef pr;
     if ((e = run_gemm(s, lg.qkv, lg.sqkv, &pr, st)) != cudaSuccess) return e;
     if ((e = launch_post_qkv(D, s->S, P, s->st, W, l, pr, st)) != cudaSuccess) return e;
-    if ((e = launch_attn(D, s->S, P, s->st, l, s->tflags, st)) != cudaSuccess) return e;
+    if ((e = launch_attn(D, s->S, P, s->st, s->am, l, s->tflags, st)) != cudaSuccess) return e;
     if ((e = run_gemm(s, lg.o, lg.so, &pr, st)) != cudaSuccess) return e;
     if (D.dff) {
       if ((e = launch_post_residual(D, P, pr, W.ln2 + (size_t)l * D.d, st)) != cudaSuccess) return e;
@@ -727,9 +734,10 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   // full pass (prefill / refresh): row chunks as wide as possible with little
   // padding (L = 320 -> 2 x 160, L = 192 -> 1 x 192, L = 3072 -> 12 x 256)
   {
-    const int cands_n[5] = {256, 192, 160, 128, 64}, cands_s[4] = {128, 96, 80, 64};
+    // (the epilogue reads 32 accumulator columns at a time: rows per chunk % 32 == 0)
+    const int cands_n[5] = {256, 192, 160, 128, 64}, cands_s[3] = {128, 96, 64};
     const int* cands = split ? cands_s : cands_n;
-    const int n_c = split ? 4 : 5;
+    const int n_c = split ? 3 : 5;
     int best = 128;
     long long best_cost = -1;
     for (int i = 0; i < n_c; ++i) {

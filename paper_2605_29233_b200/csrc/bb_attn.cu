@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) k_attn_keys(Sess S, Pass P, DevState st, 
       sMsk[lp * S.B + n] = m;
       ++n;
     }
-    sCnt[lp] = n * (lp_end(S, lp) - lp_start(S, lp));
+    sCnt[lp] = n * S.ps;  // segments padded to ps entries (a 64-key chunk = whole pages)
   }
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan over lp, one warp, per-lane runs
@@ -272,9 +272,10 @@ __global__ void __launch_bounds__(256) k_attn_keys(Sess S, Pass P, DevState st, 
     const int base = sCnt[lp];
     const int nseg = (lp + 1 < S.n_lp ? sCnt[lp + 1] : s_tot) - base;
     for (int e = threadIdx.x & 31; e < nseg; e += 32) {
-      const int j = e / nk, row = e - j * nk;
+      const int j = e >> S.ps_shift, row = e & (S.ps - 1);
       const int pg = r * S.pool + sSeg[lp * S.B + j];
-      const int m = sMsk[lp * S.B + j], pos = s0 + row;
+      const int m = row < nk ? sMsk[lp * S.B + j] : 0;  // padding rows: visible to no branch
+      const int pos = s0 + row;
       bool win = false;
       for (int k = 0; k < S.B; ++k) win |= ((m >> k) & 1) && pos >= s_ws[k] && pos < s_we[k];
       out[2 * (base + e)] = pg * S.ps + row;
@@ -1281,6 +1282,382 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ warp-specialized tcgen05 attention
+// k_attn_fa: the k_attn_tc work split and math (M = 64 query rows, 64-key
+// chunks, S / O in TMEM, P as bf16 hi + lo, DSMEM cluster merge) with the
+// chunk pipeline taken apart into roles that run concurrently:
+//   warp 4 (producer): per chunk, the keys' branch-visibility words and the
+//     chunk's four 16-key KV pages -> an NS-deep shared-memory ring by TMA
+//     (128-byte-swizzled boxes of one page x 64 dims, complete_tx mbarrier);
+//     the key list pads every page segment to 16 entries (k_attn_keys), so a
+//     chunk is exactly four whole pages.
+//   warp 5 lane 0 (MMA issuer): S(ci) = Q.K(ci)^T into one of two TMEM S
+//     buffers as soon as the chunk landed and that buffer was read, THEN
+//     O += P(ci-1).V(ci-1) -- the score MMA of the next chunk overlaps the
+//     softmax of the current one; the P.V commit frees the ring slot.
+//   warps 0-3 (softmax): row max / lazy O rescale / P = 2^(s - m) as bf16
+//     hi + lo, exactly as k_attn_tc.
+// No __syncthreads in the chunk loop; every hand-off is an mbarrier.
+constexpr int AFA_THREADS = 192;
+
+template <int CS, int NS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
+    k_attn_fa(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Dims D, Sess S,
+              Pass P, DevState st, int layer, int rows_per_req) {
+  klog_mark(D.klog, D.klog_cap, 24);
+  if (P.pf_base != nullptr && threadIdx.x == 0) {
+    // this CTA's slice of the O projection's weights -> L2 (HBM is not saturated by the attention)
+    const long long n_cta = (long long)gridDim.x * gridDim.y * gridDim.z;
+    const long long cta = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+    const long long per = ((P.pf_layer_bytes + n_cta - 1) / n_cta + 127) & ~127LL;
+    const char* base = P.pf_base + (long long)layer * P.pf_layer_bytes;
+    for (long long o = cta * per; o < min((cta + 1) * per, P.pf_layer_bytes); o += 65536) {
+      const long long n = min(65536LL, min((cta + 1) * per, P.pf_layer_bytes) - o);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"((uint32_t)n) : "memory");
+    }
+  }
+  using bf = __nv_bfloat16;
+  constexpr int HD = ATC_HD, QR = ATC_QR, KC = ATC_KC;
+  constexpr uint32_t STAGE = 4 * ATC_SUB;  // K (2 sub-tiles) + V (2 sub-tiles)
+  extern __shared__ __align__(1024) uint8_t smraw_fa[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw_fa) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                  // 2 sub-tiles (dims 0-63, 64-127)
+  uint8_t* sKV = sQ + 2 * ATC_SUB;   // [NS][K sub 0, K sub 1, V sub 0, V sub 1]
+  uint8_t* sPh = sKV + NS * STAGE;   // [64 rows][64 keys] K-major
+  uint8_t* sPl = sPh + ATC_SUB;
+  __shared__ int sRow[QR], sBr[QR];
+  __shared__ uint32_t sVis[NS][32][2];  // [slot][branch][key word]
+  __shared__ int s_nk;
+  __shared__ __align__(8) uint64_t kfull[NS], kempty[NS], sfull[2], sfree[2], pfull, pvdone, qready;
+  __shared__ uint32_t s_tmem;
+
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int r = blockIdx.x / CS, h = blockIdx.y;
+  const int row0 = blockIdx.z * QR;
+  const int kvh = h / (D.nh / D.nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : blockIdx.z);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kfull[i], 1);
+      mbar_init(&kempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sfree[i], 4);
+    }
+    mbar_init(&pfull, 4);
+    mbar_init(&pvdone, 1);
+    mbar_init(&qready, 128);
+    fence_mbar_init();
+  }
+  if (warp == 4 && lane == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  if (warp == 5) tmem_alloc(&s_tmem, 256);  // S0, S1: 64 columns each; O: 128 columns
+  pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 3);
+  unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;
+  tstat_begin(ats);
+  if (threadIdx.x < QR) {
+    const int lr = row0 + threadIdx.x;
+    int slot = -1, br = 0;
+    if (lr < rows_per_req) {
+      const int sl = slot_base + lr;
+      br = P.slot_br[sl];
+      if (P.slot_pos[sl] >= 0 && !*P.skip) slot = sl;
+    }
+    sRow[threadIdx.x] = slot;
+    sBr[threadIdx.x] = br;
+  } else if (threadIdx.x == QR) {
+    s_nk = P.akey_n[2 * kb];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tS0 = s_tmem, tO = s_tmem + 128;
+  // keys split over the cluster in whole chunks (a chunk = four whole pages)
+  const int n_keys = s_nk;
+  const int nc_all = (n_keys + KC - 1) / KC;
+  const int c_begin = (int)((long long)nc_all * crank / CS);
+  const int n_chunks = (int)((long long)nc_all * (crank + 1) / CS) - c_begin;
+  const int k_begin = c_begin * KC;
+  const int2* ksrc = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + k_begin;
+  const int nk_cta = min(n_keys - k_begin, n_chunks * KC);
+
+  if (warp == 4) {
+    // ---------------- producer: visibility words + TMA page loads
+    const uint64_t pol = policy_evict_first();
+    const int lay_rows = layer * S.R * S.pool;  // (layer, page) -> row of the [rows][hd] KV view
+    for (int ci = 0; ci < n_chunks; ++ci) {
+      const int slot = ci % NS;
+      if (ci >= NS) mbar_wait(&kempty[slot], ((ci / NS) - 1) & 1);
+      const int i0 = ci * KC + lane, i1 = i0 + 32;
+      const int2 e0 = i0 < nk_cta ? ksrc[i0] : make_int2(0, 0);
+      const int2 e1 = i1 < nk_cta ? ksrc[i1] : make_int2(0, 0);
+      for (int b = 0; b < S.B; ++b) {
+        const uint32_t w0 = __ballot_sync(0xffffffffu, (e0.y >> b) & 1);
+        const uint32_t w1 = __ballot_sync(0xffffffffu, (e1.y >> b) & 1);
+        if (lane == 0) {
+          sVis[slot][b][0] = w0;
+          sVis[slot][b][1] = w1;
+        }
+      }
+      // global page of each 16-key group (entries 0, 16, 32, 48 of the chunk)
+      const int pg0 = __shfl_sync(0xffffffffu, e0.x, 0) >> 4, pg1 = __shfl_sync(0xffffffffu, e0.x, 16) >> 4;
+      const int pg2 = __shfl_sync(0xffffffffu, e1.x, 0) >> 4, pg3 = __shfl_sync(0xffffffffu, e1.x, 16) >> 4;
+      if (lane == 0) {
+        sVis[slot][31][0] = 0u;  // rows without a slot
+        sVis[slot][31][1] = 0u;
+        const int nk = min(KC, nk_cta - ci * KC);
+        // groups past the chunk's keys re-load group 0's page (finite data, masked out)
+        const int pgs[4] = {pg0, nk > 16 ? pg1 : pg0, nk > 32 ? pg2 : pg0, nk > 48 ? pg3 : pg0};
+        uint8_t* dst = sKV + slot * STAGE;
+        mbar_expect_tx(&kfull[slot], STAGE);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int row = ((lay_rows + pgs[g]) * D.nkv + kvh) * 16;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            tma_load_2d(dst + sub * ATC_SUB + g * 2048, &tmK, &kfull[slot], sub * 64, row, pol);
+            tma_load_2d(dst + (2 + sub) * ATC_SUB + g * 2048, &tmV, &kfull[slot], sub * 64, row, pol);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 5) {
+    // ---------------- MMA issuer
+    if (lane == 0 && n_chunks > 0) {
+      constexpr uint32_t IDS = idesc_bf16_f32(64, 64);
+      constexpr uint32_t IDO = idesc_bf16_f32(64, 128) | (1u << 16);  // B (V) MN-major
+      mbar_wait(&qready, 0);
+      tc_fence_after();
+      const uint32_t q0 = smem_u32(sQ), pa = smem_u32(sPh), pl = smem_u32(sPl);
+      for (int ci = 0; ci <= n_chunks; ++ci) {
+        if (ci < n_chunks) {
+          const int slot = ci % NS, sb = ci & 1;
+          mbar_wait(&kfull[slot], (ci / NS) & 1);
+          if (ci >= 2) mbar_wait(&sfree[sb], ((ci >> 1) - 1) & 1);
+          tc_fence_after();
+          const uint32_t k0 = smem_u32(sKV + slot * STAGE);
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const uint32_t sub = (ks >> 2) * ATC_SUB, ko = (ks & 3) * 32;
+            tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(q0 + sub + ko), sdesc_sw128(k0 + sub + ko), IDS,
+                        ks > 0 ? 1u : 0u);
+          }
+          tc_commit(&sfull[sb]);
+        }
+        if (ci >= 1) {
+          const int pc = ci - 1, pslot = pc % NS;
+          mbar_wait(&pfull, pc & 1);
+          tc_fence_after();
+          const uint32_t v0 = smem_u32(sKV + pslot * STAGE + 2 * ATC_SUB);
+#pragma unroll
+          for (int kk = 0; kk < KC / 16; ++kk) {
+            const uint64_t bd = sdesc_sw128_mn(v0 + kk * 2048, ATC_SUB, 1024);
+            tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), bd, IDO, (pc > 0 || kk > 0) ? 1u : 0u);
+            tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+          }
+          tc_commit(&kempty[pslot]);
+          tc_commit(&pvdone);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax warps 0-3
+    const int rl = 16 * warp + (lane & 15), hh = lane >> 4;  // my row, my key half (S) / dim half (O)
+    {
+      const bf* Qg = reinterpret_cast<const bf*>(P.q);
+      for (int i = threadIdx.x; i < QR * 16; i += 128) {
+        const int rr = i >> 4, v = i & 15;
+        const int slot = sRow[rr];
+        const long long qo = (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8;
+        cp_async16(sQ + (v >> 3) * ATC_SUB + sw128_off(rr, v & 7), Qg + qo, slot >= 0);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&qready);
+    }
+    const int br_row = sRow[rl] >= 0 ? sBr[rl] : 31;  // bit 31 is never set: no visible key
+    const float sl2 = D.attn_scale * 1.4426950408889634f;
+    float m_ref = -INFINITY, l_part = 0.0f;
+    const uint32_t tl = (uint32_t)(32 * warp) << 16;  // my TMEM lane quadrant
+    for (int ci = 0; ci < n_chunks; ++ci) {
+      const int slot = ci % NS, sb = ci & 1;
+      mbar_wait(&sfull[sb], (ci >> 1) & 1);
+      mbar_wait(&kfull[slot], (ci / NS) & 1);  // acquire the producer's visibility words
+      tc_fence_after();
+      float s[32];
+      tmem_ld16x2<32>(tS0 + 64 * sb + tl, s);  // row rl, keys 32*hh + [0, 32)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfree[sb]);
+      const uint32_t vw = sVis[slot][br_row][hh];
+      float mx4[4] = {m_ref, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        s[c] = ((vw >> c) & 1u) ? s[c] * sl2 : -INFINITY;
+        mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+      }
+      float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      m_new = fmaxf(m_new, __shfl_xor_sync(0xffffffffu, m_new, 16));
+      const bool grow = m_new > m_ref + 8.0f;  // (also the first visible key: m_ref = -inf)
+      const float f = !grow ? 1.0f : (m_ref == -INFINITY ? 0.0f : ex2_ftz(m_ref - m_new));
+      // P(ci-1).V done: the P tile is free and O is stable
+      if (ci > 0) {
+        mbar_wait(&pvdone, (ci - 1) & 1);
+        tc_fence_after();
+      }
+      if (ci > 0 && __any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+        float o[32];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          tmem_ld16x2<64>(tO + tl + 32 * q, o);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] *= f;
+          tmem_st16x2<64>(tO + tl + 32 * q, o);
+        }
+      }
+      if (grow) {
+        l_part *= f;
+        m_ref = m_new;
+      }
+      const float mb = m_ref == -INFINITY ? 0.0f : m_ref;
+      {
+        float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int c8 = 0; c8 < 4; ++c8) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float p0 = ex2_ftz(s[8 * c8 + 2 * e] - mb), p1 = ex2_ftz(s[8 * c8 + 2 * e + 1] - mb);
+            ls[e] += p0 + p1;
+            split_bf2(p0, p1, hi[e], lo[e]);
+          }
+          const uint32_t off = sw128_off(rl, 4 * hh + c8);
+          *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull);
+    }
+    if (n_chunks > 0) {
+      mbar_wait(&pvdone, (n_chunks - 1) & 1);
+      tc_fence_after();
+    }
+    // partial state (m_ref, l, o / l) of my row half -> fp16 staging in the
+    // (now idle) KV ring: [QR][HD + 8] halves, (m, l) in the row padding
+    constexpr int OLD = HD + 8;
+    __half* sO = reinterpret_cast<__half*>(sKV);
+    const float lsum = l_part + __shfl_xor_sync(0xffffffffu, l_part, 16);
+    const float il = lsum > 0.0f ? 1.0f / lsum : 0.0f;
+    float o[32];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (n_chunks > 0) {
+        tmem_ld16x2<64>(tO + tl + 32 * q, o);  // dims 64*hh + 32*q + [0, 32)
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] = 0.0f;
+      }
+#pragma unroll
+      for (int c = 0; c < 32; c += 2)
+        *reinterpret_cast<__half2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+    }
+    if (hh == 0) *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, lsum);
+  }
+  tc_fence_before();
+  cluster.sync();
+  if (threadIdx.x < 128) {
+    // merge rows [crank*RPC, (crank+1)*RPC) over the cluster (pull; fixed rank order)
+    constexpr int OLD = HD + 8;
+    const __half* sO = reinterpret_cast<const __half*>(sKV);
+    constexpr int RPC = QR / CS, V4 = HD / 4, NMI = (RPC * V4 + 127) / 128;
+#pragma unroll
+    for (int k = 0; k < NMI; ++k) {
+      const int i = threadIdx.x + k * 128;
+      if (i >= RPC * V4) continue;
+      const int lr = crank * RPC + i / V4, c4 = (i % V4) * 4;
+      const int slot = sRow[lr];
+      float mr[CS], lv[CS];
+      float4 ov[CS];
+#pragma unroll
+      for (int q = 0; q < CS; ++q) {
+        const __half* row = cluster.map_shared_rank(sO + lr * OLD, q);
+        const float2 ml = *reinterpret_cast<const float2*>(row + HD);
+        mr[q] = ml.x;
+        lv[q] = ml.y;
+        const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+        ov[q] = make_float4(a.x, a.y, b.x, b.y);
+      }
+      if (slot < 0) continue;
+      float M = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) M = fmaxf(M, mr[q]);
+      float Lsum = 0.0f;
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < CS; ++q) {
+        if (mr[q] == -INFINITY || lv[q] <= 0.0f) continue;
+        const float w = ex2_ftz(mr[q] - M) * lv[q];
+        Lsum += w;
+        acc.x += w * ov[q].x;
+        acc.y += w * ov[q].y;
+        acc.z += w * ov[q].z;
+        acc.w += w * ov[q].w;
+      }
+      const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
+      bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4;
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), p1 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&p0);
+      u.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(out) = u;
+    }
+  }
+  cluster.sync();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(s_tmem, 256);
+  }
+  tstat_end(ats);
+}
+
+template <int NS>
+constexpr size_t attn_fa_smem() {
+  return 1024 + (size_t)(2 + 4 * NS + 2) * ATC_SUB;
+}
+
+template <int CS, int NS>
+static cudaError_t attn_fa_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st,
+                                  const AttnMaps& am, int layer, cudaStream_t s) {
+  const int rows = P.full ? S.L : S.NRq;
+  constexpr size_t smem = attn_fa_smem<NS>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_fa<CS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(S.R * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
+  launch_k(k_attn_fa<CS, NS>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, D, S, P, st, layer, rows);
+  return cudaGetLastError();
+}
+
 // tcgen05 attention for hd = 128 in every pass (block, prefill, refresh).
 // Measured (C5 block attention 222 vs 262 us per launch for the mma.sync
 // kernel, C5 16.7 vs 17.9 ms/NFE; C2 attention slot 16.8 vs 19.4 us).
@@ -1288,12 +1665,12 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
 // grid fits one wave, else 1 (splitting keys over a cluster only pays while
 // the (request, head, row tile) units alone cannot fill the GPU).  C5 full
 // passes (1536 units): CS 8 / 4 / 2 = 1020 / 829 / 731 us per launch.
-static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P, int tflags) {
+static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P, int tflags, int per_sm) {
   const int forced = (tflags >> 4) & 15;
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   const int rows = P.full ? S.L : S.NRq;
   const long long per = (long long)S.R * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
-  const long long wave = (D.split ? 1LL : 2LL) * S.n_sms;  // CTAs per SM: 2 (99 KB), bf16x2 1 (177 KB)
+  const long long wave = (long long)per_sm * S.n_sms;  // resident CTAs per SM x SMs
   for (int cs = 8; cs > 1; cs >>= 1)
     if (per * cs <= wave) return cs;
   return 1;
@@ -1301,12 +1678,25 @@ static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P, int tflags) {
 
 // test flag bit 0 (BB_TF_ATTN_MMA_SYNC): the mma.sync kernel at hd 128 (tests
 // compare the two tensor-core attentions; never set on the product path)
+#ifndef ATT_FA_NS
+#define ATT_FA_NS 2  // KV ring stages of k_attn_fa (2: 99 KB, two CTAs per SM)
+#endif
 template <int HD>
-static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer,
-                               int tflags, cudaStream_t s) {
+static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const AttnMaps& am,
+                               int layer, int tflags, cudaStream_t s) {
   if constexpr (HD == 128) {
+    // product path: the warp-specialized TMA-fed kernel (test flag bit 1 = k_attn_tc)
+    if (!D.split && am.ok && !(tflags & 3)) {
+      constexpr int per_sm = attn_fa_smem<ATT_FA_NS>() <= 112 * 1024 ? 2 : 1;
+      switch (att_cs_tc(D, S, P, tflags, per_sm)) {
+        case 8: return attn_fa_launch<8, ATT_FA_NS>(D, S, P, st, am, layer, s);
+        case 4: return attn_fa_launch<4, ATT_FA_NS>(D, S, P, st, am, layer, s);
+        case 2: return attn_fa_launch<2, ATT_FA_NS>(D, S, P, st, am, layer, s);
+        default: return attn_fa_launch<1, ATT_FA_NS>(D, S, P, st, am, layer, s);
+      }
+    }
     if (D.split) {  // bf16x2: the tcgen05 attention only
-      switch (att_cs_tc(D, S, P, tflags)) {
+      switch (att_cs_tc(D, S, P, tflags, 1)) {
         case 8: return attn_tc_launch<8, true>(D, S, P, st, layer, s);
         case 4: return attn_tc_launch<4, true>(D, S, P, st, layer, s);
         case 2: return attn_tc_launch<2, true>(D, S, P, st, layer, s);
@@ -1314,7 +1704,7 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
       }
     }
     if (!(tflags & 1)) {
-      switch (att_cs_tc(D, S, P, tflags)) {
+      switch (att_cs_tc(D, S, P, tflags, 2)) {
         case 8: return attn_tc_launch<8, false>(D, S, P, st, layer, s);
         case 4: return attn_tc_launch<4, false>(D, S, P, st, layer, s);
         case 2: return attn_tc_launch<2, false>(D, S, P, st, layer, s);
@@ -1415,14 +1805,15 @@ static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const De
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, int tflags,
-                        cudaStream_t s) {
+cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const AttnMaps& am, int layer,
+                        int tflags, cudaStream_t s) {
   const int max_items = P.full ? 1 : S.max_items;
   cudaError_t e = cudaErrorInvalidValue;
   dim3 cgrid(P.rows_alloc, D.nh);
   const int cthreads = D.hd < 256 ? D.hd : 256;
   if (D.dtype == 1 && (D.hd == 64 || D.hd == 128))
-    return D.hd == 64 ? attn_seg_hd<64>(D, S, P, st, layer, tflags, s) : attn_seg_hd<128>(D, S, P, st, layer, tflags, s);
+    return D.hd == 64 ? attn_seg_hd<64>(D, S, P, st, am, layer, tflags, s)
+                      : attn_seg_hd<128>(D, S, P, st, am, layer, tflags, s);
   if (D.dtype == 1) {
     using T = __nv_bfloat16;
     if (D.hd == 256) e = attn_hd<T, 256>(D, S, P, st, layer, max_items, s);

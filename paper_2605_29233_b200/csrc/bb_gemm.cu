@@ -456,10 +456,15 @@ static bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t
   return r == CUDA_SUCCESS;
 }
 
+bool tma_map_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+  return make_tmap(m, base, inner, outer, box_outer);
+}
+
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN, int mode,
                    int max_grid, const void* X_lo) {
   const int mma_n = X_lo != nullptr ? 2 * BN : BN;  // bf16x2: hi + lo rows of a chunk in one MMA
   if (mma_n != 64 && mma_n != 128 && mma_n != 160 && mma_n != 192 && mma_n != 256) return false;
+  if (BN % 32 != 0) return false;  // the epilogue reads 32 accumulator columns (rows) at a time
   if (K % 8 != 0) return false;  // 16-byte row stride for TMA
   memset(&g, 0, sizeof(g));
   g.BN = mma_n;

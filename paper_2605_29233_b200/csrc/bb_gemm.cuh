@@ -108,6 +108,8 @@ struct TcGemm {
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN,
                    int mode, int max_grid, const void* X_lo = nullptr);
 cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s);
+// 2-D bf16 tensor map [outer][inner], boxes of box_outer rows x 64 elements, 128-byte swizzle
+bool tma_map_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer);
 
 struct SimtGemm {
   const float* W;

@@ -36,9 +36,15 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
                             int layer, const PartRef& pr, cudaStream_t s);
 cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr, const float* ln, cudaStream_t s);
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s);
+// TMA views of the K / V page pools for the warp-specialized attention:
+// [layers * R * pool * nkv * ps rows][hd] bf16, boxes of one 16-row page x 64 dims, 128-byte swizzle
+struct AttnMaps {
+  CUtensorMap k, v;
+  bool ok;
+};
 // tflags: bb_session_desc.test_flags (tests only)
-cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, int layer, int tflags,
-                        cudaStream_t s);
+cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const AttnMaps& am, int layer,
+                        int tflags, cudaStream_t s);
 cudaError_t launch_attn_keys(const Dims& D, const Sess& S, const Pass& P, const DevState& st, cudaStream_t s);
 cudaError_t launch_gather_head(const Dims& D, const Sess& S, const Pass& full, const Pass& blk, const Head& H,
                                int branch_filter, cudaStream_t s);

@@ -62,33 +62,62 @@ def first_divergence(ta, tb):
     return None
 
 
+def compare(seeds, prod, ref):
+    rows, n_nfe, n_tok, n_trace = [], 0, 0, 0
+    for seed, a, b in zip(seeds, prod, ref):
+        ta, tb = [rec(e) for e in a.trace], [rec(e) for e in b.trace]
+        div = first_divergence(ta, tb)
+        same_nfe = a.nfe.snapshot() == b.nfe.snapshot()
+        same_tok = bool(np.array_equal(a.row.tokens, b.row.tokens)) and a.branch_index == b.branch_index
+        n_nfe += same_nfe
+        n_tok += same_tok
+        n_trace += div is None
+        p = {"seed": seed, "nfe_prod": list(a.nfe.snapshot()), "nfe_f32": list(b.nfe.snapshot()),
+             "same_nfe": same_nfe, "same_tokens": same_tok, "same_trace": div is None,
+             "tokens_decoded": [a.tokens_decoded, b.tokens_decoded],
+             "token_diffs": int((a.row.tokens != b.row.tokens).sum()),
+             "stats_prod": a.stats, "stats_f32": b.stats}
+        if div is not None:
+            i, ea, eb = div
+            p["first_divergence"] = {"index": i, "of": [len(ta), len(tb)], "prod": ea, "f32": eb}
+        rows.append(p)
+    n = len(seeds)
+    summary = {"prompts": n, "same_nfe": n_nfe, "same_tokens": n_tok, "same_trace": n_trace,
+               "frac_same_nfe": n_nfe / n, "frac_same_tokens": n_tok / n, "frac_same_trace": n_trace / n,
+               "mean_nfe_prod": float(np.mean([r.nfe.total for r in prod])),
+               "mean_nfe_f32": float(np.mean([r.nfe.total for r in ref])),
+               "per_request_prod": {k: float(np.mean([r.stats[k] for r in prod]))
+                                    for k in ("merges", "syncs", "commits", "refreshes")}}
+    return rows, summary
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
     ap.add_argument("--n", type=int, default=64)
     ap.add_argument("--seed0", type=int, default=0)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--test-flags", type=int, default=0, help="session test flags of the bf16 run (A/B only)")
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "bf16x2"], help="the product run's numerics")
+    ap.add_argument("--dtype", default="bf16x2", help="comma list of product numerics (bf16, bf16x2)")
     args = ap.parse_args()
     import torch
     from paper_2605_29233_b200.model import verification_copy
     cfgd = bench.CONFIGS[args.config]
-    bb, p16, cfg = bench.make_model(cfgd, args.dtype)
-    p32 = verification_copy(p16)
+    dtypes = args.dtype.split(",")
+    bb, p0, cfg = bench.make_model(cfgd, dtypes[0])
+    p32 = verification_copy(p0)
+    models = {dtypes[0]: p0}
+    for dt in dtypes[1:]:  # same bf16 weights, other activation numerics
+        from dataclasses import replace
+        models[dt] = replace(p0, dtype=dt, _handle=[None], _sessions={})
     torch.cuda.synchronize()
     seeds = list(range(args.seed0, args.seed0 + args.n))
-    tasks = [bb.make_task(s, cfgd["P"], cfgd["G"], p16.vocab) for s in seeds]
-    out = {"config": args.config, "dtype": args.dtype, "workload": cfgd["workload"], "head_scale": cfgd["head_scale"],
-           "gamma": cfgd["gamma"], "seeds": [seeds[0], seeds[-1]], "prompts": []}
-    t_run = {"bf16": 0.0, "f32": 0.0}
+    tasks = [bb.make_task(s, cfgd["P"], cfgd["G"], p0.vocab) for s in seeds]
+    out = {"config": args.config, "workload": cfgd["workload"], "head_scale": cfgd["head_scale"],
+           "gamma": cfgd["gamma"], "seeds": [seeds[0], seeds[-1]], "reference": "device fp32 verification path, same weights",
+           "products": {}}
+    t_run = {}
     res = {}
-    for name, params in (("bf16", p16), ("f32", p32)):
-        if name == "bf16" and args.test_flags:  # pre-seat the session run_blockbatch will use
-            from paper_2605_29233_b200.engine import Session
-            from paper_2605_29233_b200.scheduler import _cfg_key
-            params._sessions[_cfg_key(cfg, cfgd["P"], 1, True)] = Session(params, cfg, cfgd["P"], 1,
-                                                                         test_flags=args.test_flags)
+    for name, params in list(models.items()) + [("f32", p32)]:
         rr = []
         t0 = time.time()
         for t in tasks:
@@ -97,39 +126,16 @@ def main():
         t_run[name] = time.time() - t0
         res[name] = rr
         print(f"[parity] {name}: {len(rr)} prompts in {t_run[name]:.1f}s", file=sys.stderr, flush=True)
-    n_nfe = n_tok = n_trace = 0
-    for seed, a, b in zip(seeds, res["bf16"], res["f32"]):
-        ta, tb = [rec(e) for e in a.trace], [rec(e) for e in b.trace]
-        div = first_divergence(ta, tb)
-        same_nfe = a.nfe.snapshot() == b.nfe.snapshot()
-        same_tok = bool(np.array_equal(a.row.tokens, b.row.tokens)) and a.branch_index == b.branch_index
-        n_nfe += same_nfe
-        n_tok += same_tok
-        n_trace += div is None
-        p = {"seed": seed, "nfe_bf16": list(a.nfe.snapshot()), "nfe_f32": list(b.nfe.snapshot()),
-             "same_nfe": same_nfe, "same_tokens": same_tok, "same_trace": div is None,
-             "tokens_decoded": [a.tokens_decoded, b.tokens_decoded],
-             "token_diffs": int((a.row.tokens != b.row.tokens).sum()),
-             "stats_bf16": a.stats, "stats_f32": b.stats}
-        if div is not None:
-            i, ea, eb = div
-            p["first_divergence"] = {"index": i, "of": [len(ta), len(tb)], "bf16": ea, "f32": eb}
-        out["prompts"].append(p)
-    n = len(seeds)
-    st16 = [r.stats for r in res["bf16"]]
-    out["summary"] = {
-        "prompts": n, "same_nfe": n_nfe, "same_tokens": n_tok, "same_trace": n_trace,
-        "frac_same_nfe": n_nfe / n, "frac_same_tokens": n_tok / n, "frac_same_trace": n_trace / n,
-        "mean_nfe_bf16": float(np.mean([r.nfe.total for r in res["bf16"]])),
-        "mean_nfe_f32": float(np.mean([r.nfe.total for r in res["f32"]])),
-        "per_request_bf16": {k: float(np.mean([s[k] for s in st16])) for k in ("merges", "syncs", "commits", "refreshes")},
-        "wall_s": t_run}
-    js = json.dumps(out)
+    for dt in dtypes:
+        rows, summary = compare(seeds, res[dt], res["f32"])
+        summary["wall_s"] = t_run[dt]
+        out["products"][dt] = {"summary": summary, "prompts": rows}
+        print(json.dumps({"dtype": dt, **summary}))
+    out["wall_s_f32"] = t_run["f32"]
     if args.out:
         os.makedirs(os.path.dirname(args.out), exist_ok=True)
         with open(args.out, "w") as f:
-            f.write(js + "\n")
-    print(json.dumps(out["summary"]))
+            f.write(json.dumps(out) + "\n")
 
 
 if __name__ == "__main__":

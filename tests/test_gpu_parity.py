@@ -260,32 +260,55 @@ def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol):
     _block_step_vs_oracle(LLADA[name], None, dtype, spike_gain, tol, name)
 
 
-@pytest.mark.parametrize("tc,cs,kvh,gain,tol", [("0", "", 2, 0.0, 2e-2), ("1", "", 2, 0.0, 2e-2), ("1", "1", 2, 0.0, 2e-2),
-                                                ("0", "1", 2, 0.0, 2e-2), ("1", "", 1, 0.0, 2e-2),
-                                                ("1", "", 2, 33.0, 1e-1), ("0", "", 2, 33.0, 1e-1)])
+@pytest.mark.parametrize("tc,cs,kvh,gain,tol", [("mma", "", 2, 0.0, 2e-2), ("fa", "", 2, 0.0, 2e-2), ("fa", "1", 2, 0.0, 2e-2),
+                                                ("mma", "1", 2, 0.0, 2e-2), ("fa", "", 1, 0.0, 2e-2),
+                                                ("fa", "", 2, 33.0, 1e-1), ("mma", "", 2, 33.0, 1e-1),
+                                                ("tc", "", 2, 0.0, 2e-2), ("tc", "1", 1, 0.0, 2e-2),
+                                                ("fa", "2", 1, 0.0, 2e-2), ("fa", "4", 2, 0.0, 2e-2)])
 def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol):
     """The block step at head_dim 128 (the LLaDA-8B head size; the tiny
-    fixtures use 64), with the tcgen05 attention (the default, S and O in
-    TMEM) and with the mma.sync attention (test flag 1), against the oracle at the bf16
-    tolerance of the block-step test.  cs=1: one CTA per (head, row tile)
-    takes every key (several chunks: the online-softmax rescale path).
-    kvh=1: grouped-query attention (2 query heads share one KV head).  gain 33:
-    the spike epilogue (x34 on raw-logit error) at the prefill test's tolerance."""
-    flags = (0 if tc == "1" else 1) | ((int(cs) if cs else 0) << 4)
+    fixtures use 64) with each tensor-core attention: the warp-specialized
+    TMA-fed tcgen05 kernel (fa, the product path), the single-role tcgen05
+    kernel (tc, test flag 2) and the mma.sync kernel (mma, test flag 1),
+    against the oracle at the bf16 tolerance of the block-step test.  cs=1:
+    one CTA per (head, row tile) takes every key (several chunks: the
+    online-softmax rescale path and the KV ring wrap).  kvh=1: grouped-query
+    attention (2 query heads share one KV head).  gain 33: the spike epilogue
+    (x34 on raw-logit error) at the prefill test's tolerance."""
+    flags = {"fa": 0, "mma": 1, "tc": 2}[tc] | ((int(cs) if cs else 0) << 4)
     g = LLADA["llada_tiny_bf16"]
     _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128), "bf16", gain, tol,
                           f"hd128 tc={tc} cs={cs or 'auto'} kvh={kvh}", test_flags=flags)
 
 
-@pytest.mark.parametrize("kvh,gain,tol", [(2, 33.0, 2e-2), (1, 33.0, 2e-2), (2, 0.0, 2e-3)])
-def test_bf16x2_block_step_matches_exact_oracle(kvh, gain, tol):
+@pytest.mark.parametrize("tc,cs,P,G", [("fa", "", 600, 200), ("fa", "1", 600, 200), ("tc", "1", 600, 200),
+                                       ("fa", "2", 1000, 120)])
+def test_block_step_long_context_attention_matches_oracle(tc, cs, P, G):
+    """Long rows through the hd-128 tensor-core attentions: a 600-token
+    prompt (its last page is partly filled: padded key-list segment) and
+    ~800 keys per row, i.e. a dozen 64-key chunks per CTA (the KV ring wraps
+    several times; lazy O rescale across chunks), vs the oracle."""
+    flags = {"fa": 0, "tc": 2}[tc] | ((int(cs) if cs else 0) << 4)
+    g = LLADA["llada_tiny_bf16"]
+    g = dict(g, prompt_len=P, gen_len=G, config=dict(g["config"], gen_len=G), seeds=g["seeds"][:2])
+    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=1, head_dim=128, max_len=P + G), "bf16", 0.0, 2e-2,
+                          f"long hd128 {tc} cs={cs or 'auto'} L={P + G}", test_flags=flags)
+
+
+@pytest.mark.parametrize("kvh,gain,tol,P,G", [(2, 33.0, 2e-2, 32, 64), (1, 33.0, 2e-2, 32, 64),
+                                              (2, 0.0, 2e-3, 32, 64), (2, 33.0, 2e-2, 64, 256),
+                                              (2, 33.0, 2e-2, 48, 80)])
+def test_bf16x2_block_step_matches_exact_oracle(kvh, gain, tol, P, G):
     """bf16x2 numerics (bf16 weights; hi + lo bf16 activations, q/K/V and head
     input; both halves through the tcgen05 GEMMs and attention) vs the oracle
     with NO activation rounding, at the north-star bar (max-abs <= 2e-2 on
-    normalised logits) WITH the spike epilogue (gain 33), MHA and GQA."""
+    normalised logits) WITH the spike epilogue (gain 33), MHA and GQA.  The
+    (P, G) cases give full-pass row chunks of 96 (L=96), 64 x 5 / 128 (L=320)
+    and a ragged last chunk (L=128: one chunk of 128)."""
     g = LLADA["llada_tiny_bf16"]
-    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128), "bf16x2", gain, tol,
-                          f"bf16x2 hd128 kvh={kvh}")
+    g = dict(g, prompt_len=P, gen_len=G, config=dict(g["config"], gen_len=G))
+    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128, max_len=max(192, P + G)), "bf16x2",
+                          gain, tol, f"bf16x2 hd128 kvh={kvh} L={P + G}")
 
 
 def _block_step_vs_oracle(g, arch_override, dtype, spike_gain, tol, name, test_flags=0):
