@@ -50,6 +50,9 @@ CONFIGS = {
                shape="dream", P=64, G=512, bs=(4, 16, 32), R=2, head_scale=0.4, gamma=8.0),
     "c5": dict(workload="LLaDA-8B-shape long context: 2048-token prompt, branches {8,16,32,64}, gen 1024",
                shape="llada", P=2048, G=1024, bs=(8, 16, 32, 64), R=32, head_scale=0.4, gamma=8.0),
+    "c4": dict(workload="LLaDA-8B-shape random-init, 256 synthetic prompts sharded request-parallel over the GPUs, "
+                        "32 requests batched per device step, branches {8,16,32}, gen 256",
+               shape="llada", P=64, G=256, bs=(8, 16, 32), R=32, head_scale=0.4, gamma=8.0, n_prompts=256, batch=32),
     "c1": dict(workload="reference synthetic model 4L d256 V4096, P64, branches {8,16,32}, gen 128 (bf16)",
                shape="ref", P=64, G=128, bs=(8, 16, 32), R=32, head_scale=2.0, gamma=8.0),
 }
@@ -255,6 +258,114 @@ def cpu_baseline(cfgd, config, samples=1):
                                   samples)}
 
 
+# ---------------------------------------------------------------- C4: request-parallel, batched
+def bench_c4(args, cfgd, bb, params, cfg, rank, world, dist, local):
+    """BASELINE config C4: n_prompts prompts sharded round-robin over the ranks
+    (dp.shard; no per-step collective), each rank running its share in device
+    sessions of `batch` requests (every live request's branch windows stacked
+    into one forward per iteration, scheduler.run_batch).  A step = one batch;
+    all of a rank's batches are timed.  value = decoded tokens of all ranks /
+    max-rank time; one all-gather of the results at the end."""
+    import torch
+    from paper_2605_29233_b200 import dp, _lib
+    from paper_2605_29233_b200.scheduler import get_session
+    P, G, Rb = cfgd["P"], cfgd["G"], cfgd["batch"]
+    mine = dp.shard(cfgd["n_prompts"], rank, world)
+    nbat = (len(mine) + Rb - 1) // Rb
+    Wm = max(args.warmup, 1)
+    s = get_session(params, cfg, P, Rb, trace=False)
+    warm = [bb.make_task(900000 + rank * 1000 + i, P, G, params.vocab) for i in range(Rb)]
+    batches = [[bb.make_task(1000 + g, P, G, params.vocab) for g in mine[b * Rb:(b + 1) * Rb]] for b in range(nbat)]
+    while batches and len(batches[-1]) < Rb:  # pad the last batch with repeats (counted once)
+        batches[-1].append(batches[-1][-1])
+    n_real = [min(Rb, len(mine) - b * Rb) for b in range(nbat)]
+
+    def dev(ts):
+        return (torch.tensor(np.stack([t.prompt for t in ts]).astype(np.int32), device="cuda"),
+                torch.tensor(np.stack([t.target for t in ts]).astype(np.int32), device="cuda"))
+    wp, wt = dev(warm)
+    inputs = [dev(b) for b in batches]
+    for _ in range(Wm):
+        s.set_inputs(wp, wt)
+        s.launch()
+    s.stream.synchronize()
+    launches0 = s.counters()["kernel_launches"]
+    snaps = [(torch.zeros(Rb, 32, dtype=torch.int32, device="cuda"),
+              torch.zeros(Rb, len(cfgd["bs"]), 8, dtype=torch.int32, device="cuda")) for _ in range(nbat)]
+    its = []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(s.stream)
+        for b in range(nbat):
+            s.set_inputs(*inputs[b])
+            its.append(s.launch())
+            s.snapshot(*snaps[b])
+        ev1.record(s.stream)
+        ev1.synchronize()
+    t_ms = ev0.elapsed_time(ev1)
+    launches = s.counters()["kernel_launches"] - launches0
+    tok = 0.0
+    nfe = []
+    dyn = {"merges": 0.0, "syncs": 0.0, "commits": 0.0}
+    for b in range(nbat):
+        c, br = snaps[b][0].cpu().numpy(), snaps[b][1].cpu().numpy()
+        if not (c[:n_real[b], _lib.C_STATUS] == 1).all():
+            raise RuntimeError("requests did not finish")
+        for r in range(n_real[b]):
+            tok += float(br[r, c[r, _lib.C_WINNER], _lib.B_DEC])
+            nfe.append(c[r, _lib.C_NFE0:_lib.C_NFE2 + 1].astype(np.int64))
+            for k, w in (("merges", _lib.C_MERGES), ("syncs", _lib.C_SYNCS), ("commits", _lib.C_COMMITS)):
+                dyn[k] += float(c[r, w])
+    # e2e: the same prompts through run_batch with host inputs (pinned H2D, D2H of the results)
+    h2d0, d2h0 = s.h2d_bytes, s.d2h_bytes
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s.stream)
+    e2e_tok = 0.0
+    for b in range(nbat):
+        rs = bb.run_batch(params, batches[b], cfg, trace=False)
+        e2e_tok += sum(r.tokens_decoded for r in rs[:n_real[b]])
+    e1.record(s.stream)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    loc = torch.tensor([tok, t_ms, e2e_tok, e2e_ms, float(len(nfe)), float(sum(x.sum() for x in nfe))],
+                       dtype=torch.float64, device="cuda")
+    if dist is not None:
+        allv = [torch.zeros_like(loc) for _ in range(world)]
+        dist.all_gather(allv, loc)
+        allv = torch.stack(allv).cpu().numpy()
+    else:
+        allv = loc.cpu().numpy()[None]
+    if rank == 0:
+        t_max = allv[:, 1].max()
+        n_req = allv[:, 4].sum()
+        line = {"metric": "decoded tokens/s", "value": allv[:, 0].sum() / (t_max / 1e3), "unit": "decoded tokens/s",
+                "n_gpus": world, "steps": nbat, "warmup": Wm, "ms_per_step": t_max / max(nbat, 1),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
+                "data": "synthetic (random-init weights, make_task prompts)",
+                "config": {"workload": cfgd["workload"], "branches": list(cfgd["bs"]), "prompt_len": P, "gen_len": G,
+                           "prompts": cfgd["n_prompts"], "requests_per_session": Rb,
+                           "parallelism": f"request-parallel dp{world}",
+                           "l2": "inputs larger than L2 (16 GB of weights streamed per batched step)"},
+                "requests": int(n_req), "nfe_per_request": allv[:, 5].sum() / max(n_req, 1),
+                "ms_per_batched_iteration": float(t_ms / max(sum(its), 1)),
+                "dynamics_per_request": {k: v / max(len(nfe), 1) for k, v in dyn.items()},
+                "e2e": {"value": allv[:, 2].sum() / (allv[:, 3].max() / 1e3), "unit": "decoded tokens/s",
+                        "h2d_bytes_per_step": (s.h2d_bytes - h2d0) / max(nbat, 1),
+                        "d2h_bytes_per_step": (s.d2h_bytes - d2h0) / max(nbat, 1)},
+                "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
+                "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -307,6 +418,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     bb, params, cfg = make_model(cfgd, args.precision)
+    if args.config == "c4":
+        return bench_c4(args, cfgd, bb, params, cfg, rank, world, dist, local)
     from paper_2605_29233_b200.scheduler import get_session
     P, G = cfgd["P"], cfgd["G"]
     vocab = params.vocab

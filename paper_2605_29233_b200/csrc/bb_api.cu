@@ -390,6 +390,11 @@ static int setup_gemms(Session* s) {
     const uint64_t rows = (uint64_t)D.layers * s->S.R * s->S.pool * D.nkv * s->S.ps;
     s->am.ok = tma_map_bf16(&s->am.k, s->st.kv_k, (uint64_t)D.hd, rows, 16) &&
                tma_map_bf16(&s->am.v, s->st.kv_v, (uint64_t)D.hd, rows, 16);
+    s->am.kl = s->am.k;
+    s->am.vl = s->am.v;
+    if (s->am.ok && D.split)
+      s->am.ok = tma_map_bf16(&s->am.kl, (const __nv_bfloat16*)s->st.kv_k + s->st.kv_lo, (uint64_t)D.hd, rows, 16) &&
+                 tma_map_bf16(&s->am.vl, (const __nv_bfloat16*)s->st.kv_v + s->st.kv_lo, (uint64_t)D.hd, rows, 16);
   }
   if (D.dtype == BB_DTYPE_BF16) {
     if (!tc_gemm_setup(s->head_tc, W.head, D.n_out, D.d, s->blk.xn, s->blk.rows_alloc, s->gb.BN, 1, s->n_sms,

@@ -1298,11 +1298,15 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
 //   warps 0-3 (softmax): row max / lazy O rescale / P = 2^(s - m) as bf16
 //     hi + lo, exactly as k_attn_tc.
 // No __syncthreads in the chunk loop; every hand-off is an mbarrier.
+// SPLIT (bf16x2 sessions): q / K / V hi + lo planes (the lo pools through
+// their own TMA views), S = Qh.Kh + Qh.Kl + Ql.Kh, O += Ph.Vh + Pl.Vh + Ph.Vl,
+// fp32 cluster merge, hi + lo output (see k_attn_tc).
 constexpr int AFA_THREADS = 192;
 
-template <int CS, int NS>
+template <int CS, int NS, bool SPLIT>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
-    k_attn_fa(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Dims D, Sess S,
+    k_attn_fa(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+              const __grid_constant__ CUtensorMap tmKl, const __grid_constant__ CUtensorMap tmVl, Dims D, Sess S,
               Pass P, DevState st, int layer, int rows_per_req) {
   klog_mark(D.klog, D.klog_cap, 24);
   if (P.pf_base != nullptr && threadIdx.x == 0) {
@@ -1318,11 +1322,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   }
   using bf = __nv_bfloat16;
   constexpr int HD = ATC_HD, QR = ATC_QR, KC = ATC_KC;
-  constexpr uint32_t STAGE = 4 * ATC_SUB;  // K (2 sub-tiles) + V (2 sub-tiles)
+  constexpr int NP = SPLIT ? 2 : 1;             // hi (+ lo) planes
+  constexpr uint32_t STAGE = NP * 4 * ATC_SUB;  // [K hi 2 sub, V hi 2 sub (, K lo 2, V lo 2)]
   extern __shared__ __align__(1024) uint8_t smraw_fa[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw_fa) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                  // 2 sub-tiles (dims 0-63, 64-127)
-  uint8_t* sKV = sQ + 2 * ATC_SUB;   // [NS][K sub 0, K sub 1, V sub 0, V sub 1]
+  uint8_t* sQ = sm;                       // [plane][2 sub-tiles (dims 0-63, 64-127)]
+  uint8_t* sKV = sQ + NP * 2 * ATC_SUB;   // [NS] stages
   uint8_t* sPh = sKV + NS * STAGE;   // [64 rows][64 keys] K-major
   uint8_t* sPl = sPh + ATC_SUB;
   __shared__ int sRow[QR], sBr[QR];
@@ -1358,6 +1363,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   if (warp == 4 && lane == 0) {
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
+    if (SPLIT) {
+      tma_prefetch_desc(&tmKl);
+      tma_prefetch_desc(&tmVl);
+    }
   }
   if (warp == 5) tmem_alloc(&s_tmem, 256);  // S0, S1: 64 columns each; O: 128 columns
   pdl_enter();
@@ -1391,27 +1400,37 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   const int nk_cta = min(n_keys - k_begin, n_chunks * KC);
 
   if (warp == 4) {
-    // ---------------- producer: visibility words + TMA page loads
-    const uint64_t pol = policy_evict_first();
-    const int lay_rows = layer * S.R * S.pool;  // (layer, page) -> row of the [rows][hd] KV view
+    // ---------------- producer: visibility words + TMA page loads.  The key
+    // entries of chunk ci+1 are read (global) while chunk ci waits for its
+    // ring slot, so the key-list latency stays off the load chain.
+    const uint64_t pol = policy_evict_normal();  // the prompt's pages are re-read by other row tiles
+    const int lay_rows = layer * S.R * S.pool;   // (layer, page) -> row of the [rows][hd] KV view
+    auto entries = [&](int ci, int2& e0, int2& e1) {
+      const int i0 = ci * KC + lane, i1 = i0 + 32;
+      e0 = (ci < n_chunks && i0 < nk_cta) ? ksrc[i0] : make_int2(0, 0);
+      e1 = (ci < n_chunks && i1 < nk_cta) ? ksrc[i1] : make_int2(0, 0);
+    };
+    int2 e0, e1, n0, n1;
+    entries(0, e0, e1);
     for (int ci = 0; ci < n_chunks; ++ci) {
       const int slot = ci % NS;
-      if (ci >= NS) mbar_wait(&kempty[slot], ((ci / NS) - 1) & 1);
-      const int i0 = ci * KC + lane, i1 = i0 + 32;
-      const int2 e0 = i0 < nk_cta ? ksrc[i0] : make_int2(0, 0);
-      const int2 e1 = i1 < nk_cta ? ksrc[i1] : make_int2(0, 0);
-      for (int b = 0; b < S.B; ++b) {
-        const uint32_t w0 = __ballot_sync(0xffffffffu, (e0.y >> b) & 1);
-        const uint32_t w1 = __ballot_sync(0xffffffffu, (e1.y >> b) & 1);
-        if (lane == 0) {
-          sVis[slot][b][0] = w0;
-          sVis[slot][b][1] = w1;
-        }
+      uint32_t vis[2 * MAXB];
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        vis[2 * b] = __ballot_sync(0xffffffffu, b < S.B && ((e0.y >> b) & 1));
+        vis[2 * b + 1] = __ballot_sync(0xffffffffu, b < S.B && ((e1.y >> b) & 1));
       }
       // global page of each 16-key group (entries 0, 16, 32, 48 of the chunk)
       const int pg0 = __shfl_sync(0xffffffffu, e0.x, 0) >> 4, pg1 = __shfl_sync(0xffffffffu, e0.x, 16) >> 4;
       const int pg2 = __shfl_sync(0xffffffffu, e1.x, 0) >> 4, pg3 = __shfl_sync(0xffffffffu, e1.x, 16) >> 4;
+      entries(ci + 1, n0, n1);
+      if (ci >= NS) mbar_wait(&kempty[slot], ((ci / NS) - 1) & 1);
       if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) {
+          sVis[slot][b][0] = vis[2 * b];
+          sVis[slot][b][1] = vis[2 * b + 1];
+        }
         sVis[slot][31][0] = 0u;  // rows without a slot
         sVis[slot][31][1] = 0u;
         const int nk = min(KC, nk_cta - ci * KC);
@@ -1426,9 +1445,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
           for (int sub = 0; sub < 2; ++sub) {
             tma_load_2d(dst + sub * ATC_SUB + g * 2048, &tmK, &kfull[slot], sub * 64, row, pol);
             tma_load_2d(dst + (2 + sub) * ATC_SUB + g * 2048, &tmV, &kfull[slot], sub * 64, row, pol);
+            if (SPLIT) {
+              tma_load_2d(dst + (4 + sub) * ATC_SUB + g * 2048, &tmKl, &kfull[slot], sub * 64, row, pol);
+              tma_load_2d(dst + (6 + sub) * ATC_SUB + g * 2048, &tmVl, &kfull[slot], sub * 64, row, pol);
+            }
           }
         }
       }
+      e0 = n0;
+      e1 = n1;
       __syncwarp();
     }
   } else if (warp == 5) {
@@ -1452,6 +1477,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
             tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(q0 + sub + ko), sdesc_sw128(k0 + sub + ko), IDS,
                         ks > 0 ? 1u : 0u);
           }
+          if (SPLIT) {  // + Qh.Kl + Ql.Kh
+            const uint32_t ql = q0 + 2 * ATC_SUB, kl = k0 + 4 * ATC_SUB;
+#pragma unroll
+            for (int ks = 0; ks < HD / 16; ++ks) {
+              const uint32_t sub = (ks >> 2) * ATC_SUB, ko = (ks & 3) * 32;
+              tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(q0 + sub + ko), sdesc_sw128(kl + sub + ko), IDS, 1u);
+              tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(ql + sub + ko), sdesc_sw128(k0 + sub + ko), IDS, 1u);
+            }
+          }
           tc_commit(&sfull[sb]);
         }
         if (ci >= 1) {
@@ -1464,6 +1498,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
             const uint64_t bd = sdesc_sw128_mn(v0 + kk * 2048, ATC_SUB, 1024);
             tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), bd, IDO, (pc > 0 || kk > 0) ? 1u : 0u);
             tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+            if (SPLIT)  // + Ph.Vl
+              tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), sdesc_sw128_mn(v0 + 4 * ATC_SUB + kk * 2048, ATC_SUB, 1024),
+                          IDO, 1u);
           }
           tc_commit(&kempty[pslot]);
           tc_commit(&pvdone);
@@ -1481,6 +1518,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
         const int slot = sRow[rr];
         const long long qo = (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8;
         cp_async16(sQ + (v >> 3) * ATC_SUB + sw128_off(rr, v & 7), Qg + qo, slot >= 0);
+        if (SPLIT)
+          cp_async16(sQ + 2 * ATC_SUB + (v >> 3) * ATC_SUB + sw128_off(rr, v & 7),
+                     reinterpret_cast<const bf*>(P.q_lo) + qo, slot >= 0);
       }
       cp_async_commit();
       cp_async_wait<0>();
@@ -1512,12 +1552,30 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
       m_new = fmaxf(m_new, __shfl_xor_sync(0xffffffffu, m_new, 16));
       const bool grow = m_new > m_ref + 8.0f;  // (also the first visible key: m_ref = -inf)
       const float f = !grow ? 1.0f : (m_ref == -INFINITY ? 0.0f : ex2_ftz(m_ref - m_new));
+      const float m_old = m_ref;
+      if (grow) {
+        l_part *= f;
+        m_ref = m_new;
+      }
+      const float mb = m_ref == -INFINITY ? 0.0f : m_ref;
+      // P = 2^(s - m) as bf16 hi + lo in registers first: only the stores wait for P(ci-1).V
+      uint32_t phi[16], plo[16];
+      {
+        float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float p0 = ex2_ftz(s[2 * e] - mb), p1 = ex2_ftz(s[2 * e + 1] - mb);
+          ls[e & 3] += p0 + p1;
+          split_bf2(p0, p1, phi[e], plo[e]);
+        }
+        l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      }
       // P(ci-1).V done: the P tile is free and O is stable
       if (ci > 0) {
         mbar_wait(&pvdone, (ci - 1) & 1);
         tc_fence_after();
       }
-      if (ci > 0 && __any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+      if (ci > 0 && __any_sync(0xffffffffu, grow && m_old != -INFINITY)) {
         float o[32];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -1527,27 +1585,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
           tmem_st16x2<64>(tO + tl + 32 * q, o);
         }
       }
-      if (grow) {
-        l_part *= f;
-        m_ref = m_new;
-      }
-      const float mb = m_ref == -INFINITY ? 0.0f : m_ref;
-      {
-        float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
-          uint32_t hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float p0 = ex2_ftz(s[8 * c8 + 2 * e] - mb), p1 = ex2_ftz(s[8 * c8 + 2 * e + 1] - mb);
-            ls[e] += p0 + p1;
-            split_bf2(p0, p1, hi[e], lo[e]);
-          }
-          const uint32_t off = sw128_off(rl, 4 * hh + c8);
-          *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      for (int c8 = 0; c8 < 4; ++c8) {
+        const uint32_t off = sw128_off(rl, 4 * hh + c8);
+        *reinterpret_cast<uint4*>(sPh + off) = make_uint4(phi[4 * c8], phi[4 * c8 + 1], phi[4 * c8 + 2], phi[4 * c8 + 3]);
+        *reinterpret_cast<uint4*>(sPl + off) = make_uint4(plo[4 * c8], plo[4 * c8 + 1], plo[4 * c8 + 2], plo[4 * c8 + 3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
@@ -1558,10 +1600,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
       mbar_wait(&pvdone, (n_chunks - 1) & 1);
       tc_fence_after();
     }
-    // partial state (m_ref, l, o / l) of my row half -> fp16 staging in the
-    // (now idle) KV ring: [QR][HD + 8] halves, (m, l) in the row padding
+    // partial state (m_ref, l, o / l) of my row half -> fp16 (SPLIT: fp32)
+    // staging in the (now idle) KV ring: [QR][HD + 8], (m, l) in the row padding
     constexpr int OLD = HD + 8;
-    __half* sO = reinterpret_cast<__half*>(sKV);
+    using ST = typename std::conditional<SPLIT, float, __half>::type;
+    ST* sO = reinterpret_cast<ST*>(sKV);
     const float lsum = l_part + __shfl_xor_sync(0xffffffffu, l_part, 16);
     const float il = lsum > 0.0f ? 1.0f / lsum : 0.0f;
     float o[32];
@@ -1574,8 +1617,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
         for (int c = 0; c < 32; ++c) o[c] = 0.0f;
       }
 #pragma unroll
-      for (int c = 0; c < 32; c += 2)
-        *reinterpret_cast<__half2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+      for (int c = 0; c < 32; c += 2) {
+        if constexpr (SPLIT)
+          *reinterpret_cast<float2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = make_float2(o[c] * il, o[c + 1] * il);
+        else
+          *reinterpret_cast<__half2*>(sO + rl * OLD + 64 * hh + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+      }
     }
     if (hh == 0) *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, lsum);
   }
@@ -1584,7 +1631,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   if (threadIdx.x < 128) {
     // merge rows [crank*RPC, (crank+1)*RPC) over the cluster (pull; fixed rank order)
     constexpr int OLD = HD + 8;
-    const __half* sO = reinterpret_cast<const __half*>(sKV);
+    using ST = typename std::conditional<SPLIT, float, __half>::type;
+    const ST* sO = reinterpret_cast<const ST*>(sKV);
     constexpr int RPC = QR / CS, V4 = HD / 4, NMI = (RPC * V4 + 127) / 128;
 #pragma unroll
     for (int k = 0; k < NMI; ++k) {
@@ -1596,14 +1644,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
       float4 ov[CS];
 #pragma unroll
       for (int q = 0; q < CS; ++q) {
-        const __half* row = cluster.map_shared_rank(sO + lr * OLD, q);
+        const ST* row = cluster.map_shared_rank(sO + lr * OLD, q);
         const float2 ml = *reinterpret_cast<const float2*>(row + HD);
         mr[q] = ml.x;
         lv[q] = ml.y;
-        const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
-        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
-        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
-        ov[q] = make_float4(a.x, a.y, b.x, b.y);
+        if constexpr (SPLIT) {
+          ov[q] = *reinterpret_cast<const float4*>(row + c4);
+        } else {
+          const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+          ov[q] = make_float4(a.x, a.y, b.x, b.y);
+        }
       }
       if (slot < 0) continue;
       float M = -INFINITY;
@@ -1622,12 +1674,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
         acc.w += w * ov[q].w;
       }
       const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
-      bf* out = reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4;
-      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), p1 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+      const long long oo = (long long)slot * D.attn_dim + h * HD + c4;
+      const float4 y = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(y.x, y.y), p1 = __floats2bfloat162_rn(y.z, y.w);
       uint2 u;
       u.x = *reinterpret_cast<uint32_t*>(&p0);
       u.y = *reinterpret_cast<uint32_t*>(&p1);
-      *reinterpret_cast<uint2*>(out) = u;
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf*>(P.attn) + oo) = u;
+      if (SPLIT) {  // lo = rn(y - hi)
+        const float2 f0 = __bfloat1622float2(p0), f1 = __bfloat1622float2(p1);
+        __nv_bfloat162 l0 = __floats2bfloat162_rn(y.x - f0.x, y.y - f0.y), l1 = __floats2bfloat162_rn(y.z - f1.x, y.w - f1.y);
+        u.x = *reinterpret_cast<uint32_t*>(&l0);
+        u.y = *reinterpret_cast<uint32_t*>(&l1);
+        *reinterpret_cast<uint2*>(reinterpret_cast<bf*>(P.attn_lo) + oo) = u;
+      }
     }
   }
   cluster.sync();
@@ -1638,23 +1698,25 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   tstat_end(ats);
 }
 
-template <int NS>
+template <int NS, bool SPLIT>
 constexpr size_t attn_fa_smem() {
-  return 1024 + (size_t)(2 + 4 * NS + 2) * ATC_SUB;
+  return 1024 + (size_t)((SPLIT ? 2 : 1) * (2 + 4 * NS) + 2) * ATC_SUB;  // q, KV ring, P hi + lo
 }
 
-template <int CS, int NS>
+template <int CS, int NS, bool SPLIT>
 static cudaError_t attn_fa_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st,
                                   const AttnMaps& am, int layer, cudaStream_t s) {
   const int rows = P.full ? S.L : S.NRq;
-  constexpr size_t smem = attn_fa_smem<NS>();
+  constexpr size_t smem = attn_fa_smem<NS, SPLIT>();
+  static_assert(smem <= 227 * 1024, "k_attn_fa shared memory");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_fa<CS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_attn_fa<CS, NS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   dim3 grid(S.R * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
-  launch_k(k_attn_fa<CS, NS>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, D, S, P, st, layer, rows);
+  launch_k(k_attn_fa<CS, NS, SPLIT>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, am.kl, am.vl, D, S, P, st,
+           layer, rows);
   return cudaGetLastError();
 }
 
@@ -1681,18 +1743,62 @@ static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P, int tflags, in
 #ifndef ATT_FA_NS
 #define ATT_FA_NS 2  // KV ring stages of k_attn_fa (2: 99 KB, two CTAs per SM)
 #endif
+// Resident CTAs of k_attn_fa<CS> in clusters (occupancy API, cached): the
+// cluster placement, not smem alone, bounds how many fit at once.
+template <int CS, int NS, bool SPLIT>
+static long long fa_slots() {
+  static long long v = -1;
+  if (v < 0) {
+    constexpr size_t smem = attn_fa_smem<NS, SPLIT>();
+    cudaFuncSetAttribute(k_attn_fa<CS, NS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS * 64);
+    cfg.blockDim = dim3(AFA_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)k_attn_fa<CS, NS, SPLIT>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148 / CS;
+    }
+    v = (long long)n * CS;
+  }
+  return v;
+}
+// Cluster size of k_attn_fa: the largest CS whose grid runs in at most two
+// waves.  The chunk loop runs at a per-SM rate, so splitting a (request,
+// head, row tile)'s keys finer mainly evens out the SMs' loads (row tiles
+// see different key counts); measured C5 block pass CS 1/2/4/8 = 321 / 173
+// / 91 / 76 us, C5 full pass 651 / 641 / 715 / 886 us (1536 units).
+template <int NS, bool SPLIT>
+static int att_cs_fa(const Dims& D, const Sess& S, const Pass& P, int tflags) {
+  const int forced = (tflags >> 4) & 15;
+  if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
+  const int rows = P.full ? S.L : S.NRq;
+  const long long per = (long long)S.R * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
+  if (per * 8 <= 2 * fa_slots<8, NS, SPLIT>()) return 8;
+  if (per * 4 <= 2 * fa_slots<4, NS, SPLIT>()) return 4;
+  if (per * 2 <= 2 * fa_slots<2, NS, SPLIT>()) return 2;
+  return 1;
+}
 template <int HD>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const AttnMaps& am,
                                int layer, int tflags, cudaStream_t s) {
   if constexpr (HD == 128) {
     // product path: the warp-specialized TMA-fed kernel (test flag bit 1 = k_attn_tc)
-    if (!D.split && am.ok && !(tflags & 3)) {
-      constexpr int per_sm = attn_fa_smem<ATT_FA_NS>() <= 112 * 1024 ? 2 : 1;
-      switch (att_cs_tc(D, S, P, tflags, per_sm)) {
-        case 8: return attn_fa_launch<8, ATT_FA_NS>(D, S, P, st, am, layer, s);
-        case 4: return attn_fa_launch<4, ATT_FA_NS>(D, S, P, st, am, layer, s);
-        case 2: return attn_fa_launch<2, ATT_FA_NS>(D, S, P, st, am, layer, s);
-        default: return attn_fa_launch<1, ATT_FA_NS>(D, S, P, st, am, layer, s);
+    if (am.ok && !(tflags & 3)) {
+      if (D.split) {
+        switch (att_cs_fa<2, true>(D, S, P, tflags)) {
+          case 8: return attn_fa_launch<8, 2, true>(D, S, P, st, am, layer, s);
+          case 4: return attn_fa_launch<4, 2, true>(D, S, P, st, am, layer, s);
+          case 2: return attn_fa_launch<2, 2, true>(D, S, P, st, am, layer, s);
+          default: return attn_fa_launch<1, 2, true>(D, S, P, st, am, layer, s);
+        }
+      }
+      switch (att_cs_fa<ATT_FA_NS, false>(D, S, P, tflags)) {
+        case 8: return attn_fa_launch<8, ATT_FA_NS, false>(D, S, P, st, am, layer, s);
+        case 4: return attn_fa_launch<4, ATT_FA_NS, false>(D, S, P, st, am, layer, s);
+        case 2: return attn_fa_launch<2, ATT_FA_NS, false>(D, S, P, st, am, layer, s);
+        default: return attn_fa_launch<1, ATT_FA_NS, false>(D, S, P, st, am, layer, s);
       }
     }
     if (D.split) {  // bf16x2: the tcgen05 attention only

@@ -63,18 +63,23 @@ struct UnitIter {
   }
 };
 
-// One CTA per SM with a deep TMA pipeline (8 x 24 KB stages at BN=64): a
+// One CTA per SM with a deep TMA pipeline (9 x 24 KB stages at BN=64): a
 // streaming CTA needs ~100+ KB in flight to pull its share of HBM bandwidth.
-template <int BN>
+// HEAD: the LM-head epilogue's reduction scratch takes a stage's worth of
+// shared memory; the stream-K GEMMs use it for one more stage.
+template <int BN, bool HEAD>
 struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGES = BN >= 192 ? 4 : (BN >= 160 ? 5 : (BN >= 128 ? 6 : 8));
-  static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   // LM-head epilogue: per-warp (max, argmax, sum) rows + a 32x33 transpose tile per warp
-  static constexpr size_t RED = ((size_t)3 * 4 * BN + 4 * 32 * 33) * 4;
+  static constexpr size_t RED = HEAD ? ((size_t)3 * 4 * BN + 4 * 32 * 33) * 4 : 0;
+  static constexpr size_t BUDGET = 227 * 1024 - 1024 - 256 - RED;  // dynamic smem for the stages
+  static constexpr int STAGES_FIT = (int)(BUDGET / (A_BYTES + B_BYTES));
+  static constexpr int STAGES = STAGES_FIT > 10 ? 10 : STAGES_FIT;
+  static constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16 +
                                  RED;
+  static_assert(SMEM <= 227 * 1024, "GEMM shared memory");
 };
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -160,11 +165,11 @@ __device__ __forceinline__ void head_rows_t(const GemmTcParams& p, const float (
 #ifndef BB_GEMM_PH
 #define BB_GEMM_PH 0  // 1: timeline-session phase marks (GemmTcParams::ph); costs ~1% when built in
 #endif
-template <int BN>
+template <int BN, bool HEAD>
 __global__ void __launch_bounds__(192)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmB2, const GemmTcParams p) {
-  using C = TcCfg<BN>;
+  using C = TcCfg<BN, HEAD>;
   namespace cg = cooperative_groups;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(192)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* red = reinterpret_cast<float*>(tslot + 4);  // LM-head reduction / fused-epilogue staging
+  float* red = reinterpret_cast<float*>(tslot + 4);  // LM-head reduction scratch (HEAD instances)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = p.n_ntiles * p.n_chunks;
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(192)
             }
           }
         }
-      } else if (p.epi.kind == 1) {
+      } else if (HEAD) {
 #pragma unroll 1
         for (int j0 = 0; j0 < rows_c; j0 += 32) {
           float v[32];
@@ -509,36 +514,36 @@ bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, in
       const int ns = sk_owner(t * p.KB + p.KB - 1, T, g.grid) - sk_owner(t * p.KB, T, g.grid) + 1;
       if (ns > g.max_slots) g.max_slots = ns;
     }
-  g.smem = mma_n == 64 ? TcCfg<64>::SMEM
-           : mma_n == 128 ? TcCfg<128>::SMEM
-           : mma_n == 160 ? TcCfg<160>::SMEM
-           : mma_n == 192 ? TcCfg<192>::SMEM
-                          : TcCfg<256>::SMEM;
   return true;
 }
 
-template <int BN>
+template <int BN, bool HEAD>
 static cudaError_t launch_bn(const TcGemm& g, cudaStream_t s) {
+  using C = TcCfg<BN, HEAD>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)TcCfg<BN>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, HEAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  launch_k(k_gemm_tc<BN>, dim3(g.grid), dim3(192), (size_t)(TcCfg<BN>::SMEM), s, g.tmA, g.tmB, g.tmB2, g.p);
+  launch_k(k_gemm_tc<BN, HEAD>, dim3(g.grid), dim3(192), (size_t)C::SMEM, s, g.tmA, g.tmB, g.tmB2, g.p);
   return cudaGetLastError();
 }
 
-cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s) {
+template <bool HEAD>
+static cudaError_t launch_mode(const TcGemm& g, cudaStream_t s) {
   switch (g.BN) {
-    case 64: return launch_bn<64>(g, s);
-    case 128: return launch_bn<128>(g, s);
-    case 160: return launch_bn<160>(g, s);
-    case 192: return launch_bn<192>(g, s);
-    case 256: return launch_bn<256>(g, s);
+    case 64: return launch_bn<64, HEAD>(g, s);
+    case 128: return launch_bn<128, HEAD>(g, s);
+    case 160: return launch_bn<160, HEAD>(g, s);
+    case 192: return launch_bn<192, HEAD>(g, s);
+    case 256: return launch_bn<256, HEAD>(g, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s) {
+  return g.p.mode == 1 ? launch_mode<true>(g, s) : launch_mode<false>(g, s);
 }
 
 // ------------------------------------------------------------------ SIMT fp32

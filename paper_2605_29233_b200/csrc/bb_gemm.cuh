@@ -100,7 +100,6 @@ struct TcGemm {
   GemmTcParams p;
   SplitK sk;
   int BN, grid, max_slots;
-  size_t smem;
 };
 
 // host API (bb_gemm.cu).  mode 0 = stream-K planes, 1 = LM head

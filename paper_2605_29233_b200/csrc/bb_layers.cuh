@@ -39,7 +39,7 @@ cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cuda
 // TMA views of the K / V page pools for the warp-specialized attention:
 // [layers * R * pool * nkv * ps rows][hd] bf16, boxes of one 16-row page x 64 dims, 128-byte swizzle
 struct AttnMaps {
-  CUtensorMap k, v;
+  CUtensorMap k, v, kl, vl;  // kl / vl: the lo pools (bf16x2), else copies of k / v
   bool ok;
 };
 // tflags: bb_session_desc.test_flags (tests only)

@@ -15,7 +15,11 @@ vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
 cfg = bb.SchedulerConfig(block_sizes=_CFG[2], gen_len=G)
 params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=0.4, gamma=8.0, dtype="bf16")
 R = int(os.environ.get("BB_TL_R", "1"))  # requests per session (multi-request batching)
-s = get_session(params, cfg, P, R, trace=False)
+if os.environ.get("BB_TL_TFLAGS"):  # session test flags (A/B: attention kernel / cluster size)
+    from paper_2605_29233_b200.engine import Session
+    s = Session(params, cfg, P, R, trace=False, test_flags=int(os.environ["BB_TL_TFLAGS"]))
+else:
+    s = get_session(params, cfg, P, R, trace=False)
 
 
 def inputs(seed0):
