@@ -232,7 +232,9 @@ static void plan(Session* s, char* base, bool dry) {
     }
     P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
     P.row_rope = (!full && D.arch == BB_ARCH_LLADA) ? c.take<float>((long long)rows_alloc * D.hd) : nullptr;
-    P.n_kz = full ? 1 : (item_rows + 63) / 64;
+    // the M = 128 tcgen05 attention (bf16, hd 128, 16-row pages) reads 128-row key tiles
+    P.kz_shift = (D.dtype == BB_DTYPE_BF16 && !D.split && D.hd == 128 && S.ps == 16 && !(s->tflags & 7)) ? 7 : 6;
+    P.n_kz = full ? 1 : (item_rows + (1 << P.kz_shift) - 1) >> P.kz_shift;
     P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries
     P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
     P.akey_n = c.take<int>((long long)R * P.n_kz * 2);
@@ -387,6 +389,7 @@ static int setup_gemms(Session* s) {
   }
   s->am.ok = false;
   if (D.dtype == BB_DTYPE_BF16 && D.hd == 128 && s->S.ps == 16) {
+    attn_prepare();
     const uint64_t rows = (uint64_t)D.layers * s->S.R * s->S.pool * D.nkv * s->S.ps;
     s->am.ok = tma_map_bf16(&s->am.k, s->st.kv_k, (uint64_t)D.hd, rows, 16) &&
                tma_map_bf16(&s->am.v, s->st.kv_v, (uint64_t)D.hd, rows, 16);

@@ -12,6 +12,7 @@
 // unnormalised (o, m, l) partial; k_attn_combine merges the partials of the
 // items covering each row (flash-decoding style LSE merge, fixed order).
 #include <cooperative_groups.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <type_traits>
@@ -206,7 +207,8 @@ __global__ void __launch_bounds__(256) k_attn_keys(Sess S, Pass P, DevState st, 
   if (threadIdx.x == 0) s_bmask = 0;
   __syncthreads();
   const bool skip = *P.skip != 0;
-  for (int lr = kz * 64 + (int)threadIdx.x; lr < min(rows_per_req, kz * 64 + 64) && !skip; lr += blockDim.x) {
+  const int kr0 = kz << P.kz_shift, kr1 = min(rows_per_req, kr0 + (1 << P.kz_shift));
+  for (int lr = kr0 + (int)threadIdx.x; lr < kr1 && !skip; lr += blockDim.x) {
     const int sl = slot_base + lr;
     if (P.slot_pos[sl] >= 0) atomicOr(&s_bmask, 1 << P.slot_br[sl]);
   }
@@ -393,7 +395,7 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int slot_base = P.full ? r * S.L : r * S.NRq;
-  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : blockIdx.z);
+  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * 64) >> P.kz_shift));
   if (threadIdx.x < QR) {
     const int lr = row0 + threadIdx.x;
     int slot = -1, br = 0, pos = -1;
@@ -947,7 +949,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rl = 16 * warp + (lane & 15), hh = lane >> 4;  // my row, my key half (S) / dim half (O)
   const int slot_base = P.full ? r * S.L : r * S.NRq;
-  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : blockIdx.z);
+  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * 64) >> P.kz_shift));
 
   if (threadIdx.x == 0) {
     mbar_init(&mbS, 1);
@@ -1344,7 +1346,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot_base = P.full ? r * S.L : r * S.NRq;
-  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : blockIdx.z);
+  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * 64) >> P.kz_shift));
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -1720,6 +1722,427 @@ static cudaError_t attn_fa_launch(const Dims& D, const Sess& S, const Pass& P, c
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ M = 128 warp-specialized attention
+// k_attn_fa128: k_attn_fa's roles and pipeline on 128-row query tiles (one
+// tcgen05 M=128 accumulator: TMEM lane = query row, so each softmax thread
+// owns one whole row -- no lane pairs, no shuffles), half the MMA
+// instructions per row of the M=64 kernel, and a key tile's K/V pages read
+// once for up to 128 rows (every branch window of a C2 / C5 block pass).
+//   smem: q 32 KB | NS x (K 16 KB + V 16 KB) | P hi 16 KB + lo 16 KB
+//   TMEM: S0, S1 (64 columns each), O (128 columns)
+constexpr int AF8_QR = 128;
+constexpr uint32_t AF8_SUB = 128 * 128;  // one [128 rows][64 bf16] SW128 sub-tile (bytes)
+
+template <int CS, int NS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
+    k_attn_fa128(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Dims D, Sess S,
+                 Pass P, DevState st, int layer, int rows_per_req) {
+  klog_mark(D.klog, D.klog_cap, 24);
+  if (P.pf_base != nullptr && threadIdx.x == 0) {
+    // this CTA's slice of the O projection's weights -> L2 (HBM is not saturated by the attention)
+    const long long n_cta = (long long)gridDim.x * gridDim.y * gridDim.z;
+    const long long cta = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+    const long long per = ((P.pf_layer_bytes + n_cta - 1) / n_cta + 127) & ~127LL;
+    const char* base = P.pf_base + (long long)layer * P.pf_layer_bytes;
+    for (long long o = cta * per; o < min((cta + 1) * per, P.pf_layer_bytes); o += 65536) {
+      const long long n = min(65536LL, min((cta + 1) * per, P.pf_layer_bytes) - o);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"((uint32_t)n) : "memory");
+    }
+  }
+  using bf = __nv_bfloat16;
+  constexpr int HD = ATC_HD, QR = AF8_QR, KC = ATC_KC;
+  constexpr uint32_t STAGE = 4 * ATC_SUB;  // K (2 x [64 keys][64 dims]) + V (2 x [64 keys][64 dims])
+  extern __shared__ __align__(1024) uint8_t smraw_f8[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw_f8) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                 // 2 sub-tiles [128 rows][64 dims]
+  uint8_t* sKV = sQ + 2 * AF8_SUB;  // [NS] stages
+  uint8_t* sPh = sKV + NS * STAGE;  // [128 rows][64 keys] K-major
+  uint8_t* sPl = sPh + AF8_SUB;
+  __shared__ int sRow[QR], sBr[QR];
+  __shared__ uint32_t sVis[NS][32][2];  // [slot][branch][key word]
+  __shared__ int s_nk;
+  __shared__ __align__(8) uint64_t kfull[NS], kempty[NS], sfull[2], sfree[2], pfull, pvdone, qready;
+  __shared__ uint32_t s_tmem;
+
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int r = blockIdx.x / CS, h = blockIdx.y;
+  const int row0 = blockIdx.z * QR;
+  const int kvh = h / (D.nh / D.nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * QR) >> P.kz_shift));
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kfull[i], 1);
+      mbar_init(&kempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sfree[i], 4);
+    }
+    mbar_init(&pfull, 4);
+    mbar_init(&pvdone, 1);
+    mbar_init(&qready, 128);
+    fence_mbar_init();
+  }
+  if (warp == 4 && lane == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  if (warp == 5) tmem_alloc(&s_tmem, 256);  // S0, S1: 64 columns each; O: 128 columns
+  pdl_enter();
+  klog_mark(D.klog, D.klog_cap, 3);
+  unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;
+  tstat_begin(ats);
+  if (threadIdx.x < QR) {
+    const int lr = row0 + threadIdx.x;
+    int slot = -1, br = 0;
+    if (lr < rows_per_req) {
+      const int sl = slot_base + lr;
+      br = P.slot_br[sl];
+      if (P.slot_pos[sl] >= 0 && !*P.skip) slot = sl;
+    }
+    sRow[threadIdx.x] = slot;
+    sBr[threadIdx.x] = br;
+  } else if (threadIdx.x == QR) {
+    s_nk = P.akey_n[2 * kb];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tS0 = s_tmem, tO = s_tmem + 128;
+  const int n_keys = s_nk;
+  const int nc_all = (n_keys + KC - 1) / KC;
+  const int c_begin = (int)((long long)nc_all * crank / CS);
+  const int n_chunks = (int)((long long)nc_all * (crank + 1) / CS) - c_begin;
+  const int k_begin = c_begin * KC;
+  const int2* ksrc = reinterpret_cast<const int2*>(P.akeys) + kb * P.akey_cap + k_begin;
+  const int nk_cta = min(n_keys - k_begin, n_chunks * KC);
+
+  if (warp == 4) {
+    // ---------------- producer (as k_attn_fa)
+    const uint64_t pol = policy_evict_normal();
+    const int lay_rows = layer * S.R * S.pool;
+    auto entries = [&](int ci, int2& e0, int2& e1) {
+      const int i0 = ci * KC + lane, i1 = i0 + 32;
+      e0 = (ci < n_chunks && i0 < nk_cta) ? ksrc[i0] : make_int2(0, 0);
+      e1 = (ci < n_chunks && i1 < nk_cta) ? ksrc[i1] : make_int2(0, 0);
+    };
+    int2 e0, e1, n0, n1;
+    entries(0, e0, e1);
+    for (int ci = 0; ci < n_chunks; ++ci) {
+      const int slot = ci % NS;
+      uint32_t vis[2 * MAXB];
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        vis[2 * b] = __ballot_sync(0xffffffffu, b < S.B && ((e0.y >> b) & 1));
+        vis[2 * b + 1] = __ballot_sync(0xffffffffu, b < S.B && ((e1.y >> b) & 1));
+      }
+      const int pg0 = __shfl_sync(0xffffffffu, e0.x, 0) >> 4, pg1 = __shfl_sync(0xffffffffu, e0.x, 16) >> 4;
+      const int pg2 = __shfl_sync(0xffffffffu, e1.x, 0) >> 4, pg3 = __shfl_sync(0xffffffffu, e1.x, 16) >> 4;
+      entries(ci + 1, n0, n1);
+      if (ci >= NS) mbar_wait(&kempty[slot], ((ci / NS) - 1) & 1);
+      if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) {
+          sVis[slot][b][0] = vis[2 * b];
+          sVis[slot][b][1] = vis[2 * b + 1];
+        }
+        sVis[slot][31][0] = 0u;
+        sVis[slot][31][1] = 0u;
+        const int nk = min(KC, nk_cta - ci * KC);
+        const int pgs[4] = {pg0, nk > 16 ? pg1 : pg0, nk > 32 ? pg2 : pg0, nk > 48 ? pg3 : pg0};
+        uint8_t* dst = sKV + slot * STAGE;
+        mbar_expect_tx(&kfull[slot], STAGE);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int row = ((lay_rows + pgs[g]) * D.nkv + kvh) * 16;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            tma_load_2d(dst + sub * ATC_SUB + g * 2048, &tmK, &kfull[slot], sub * 64, row, pol);
+            tma_load_2d(dst + (2 + sub) * ATC_SUB + g * 2048, &tmV, &kfull[slot], sub * 64, row, pol);
+          }
+        }
+      }
+      e0 = n0;
+      e1 = n1;
+      __syncwarp();
+    }
+  } else if (warp == 5) {
+    // ---------------- MMA issuer: S(ci) before P(ci-1).V
+    if (lane == 0 && n_chunks > 0) {
+      constexpr uint32_t IDS = idesc_bf16_f32(128, 64);
+      constexpr uint32_t IDO = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
+      mbar_wait(&qready, 0);
+      tc_fence_after();
+      const uint32_t q0 = smem_u32(sQ), pa = smem_u32(sPh), pl = smem_u32(sPl);
+      for (int ci = 0; ci <= n_chunks; ++ci) {
+        if (ci < n_chunks) {
+          const int slot = ci % NS, sb = ci & 1;
+          mbar_wait(&kfull[slot], (ci / NS) & 1);
+          if (ci >= 2) mbar_wait(&sfree[sb], ((ci >> 1) - 1) & 1);
+          tc_fence_after();
+          const uint32_t k0 = smem_u32(sKV + slot * STAGE);
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const uint32_t ko = (ks & 3) * 32;
+            tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(q0 + (ks >> 2) * AF8_SUB + ko),
+                        sdesc_sw128(k0 + (ks >> 2) * ATC_SUB + ko), IDS, ks > 0 ? 1u : 0u);
+          }
+          tc_commit(&sfull[sb]);
+        }
+        if (ci >= 1) {
+          const int pc = ci - 1, pslot = pc % NS;
+          mbar_wait(&pfull, pc & 1);
+          tc_fence_after();
+          const uint32_t v0 = smem_u32(sKV + pslot * STAGE + 2 * ATC_SUB);
+#pragma unroll
+          for (int kk = 0; kk < KC / 16; ++kk) {
+            const uint64_t bd = sdesc_sw128_mn(v0 + kk * 2048, ATC_SUB, 1024);
+            tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), bd, IDO, (pc > 0 || kk > 0) ? 1u : 0u);
+            tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+          }
+          tc_commit(&kempty[pslot]);
+          tc_commit(&pvdone);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax warps 0-3: thread t owns query row t (TMEM lane t)
+    const int rl = threadIdx.x;
+    {
+      const bf* Qg = reinterpret_cast<const bf*>(P.q);
+      for (int i = threadIdx.x; i < QR * 16; i += 128) {
+        const int rr = i >> 4, v = i & 15;
+        const int slot = sRow[rr];
+        const long long qo = (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8;
+        cp_async16(sQ + (v >> 3) * AF8_SUB + sw128_off(rr, v & 7), Qg + qo, slot >= 0);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&qready);
+    }
+    const int br_row = sRow[rl] >= 0 ? sBr[rl] : 31;  // bit 31 is never set: no visible key
+    const float sl2 = D.attn_scale * 1.4426950408889634f;
+    float m_ref = -INFINITY, l_part = 0.0f;
+    const uint32_t tl = (uint32_t)(32 * warp) << 16;  // my TMEM lane quadrant
+    for (int ci = 0; ci < n_chunks; ++ci) {
+      const int slot = ci % NS, sb = ci & 1;
+      mbar_wait(&sfull[sb], (ci >> 1) & 1);
+      mbar_wait(&kfull[slot], (ci / NS) & 1);  // acquire the producer's visibility words
+      tc_fence_after();
+      float s[64];
+      {
+        float a[32], b[32];
+        tmem_ld32(tS0 + 64 * sb + tl, a);
+        tmem_ld32(tS0 + 64 * sb + tl + 32, b);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          s[c] = a[c];
+          s[32 + c] = b[c];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfree[sb]);
+      const uint32_t v0 = sVis[slot][br_row][0], v1 = sVis[slot][br_row][1];
+      float mx4[4] = {m_ref, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const uint32_t vw = c < 32 ? v0 : v1;
+        s[c] = ((vw >> (c & 31)) & 1u) ? s[c] * sl2 : -INFINITY;
+        mx4[c & 3] = fmaxf(mx4[c & 3], s[c]);
+      }
+      const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      const bool grow = m_new > m_ref + 8.0f;  // (also the first visible key: m_ref = -inf)
+      const float f = !grow ? 1.0f : (m_ref == -INFINITY ? 0.0f : ex2_ftz(m_ref - m_new));
+      const float m_old = m_ref;
+      if (grow) {
+        l_part *= f;
+        m_ref = m_new;
+      }
+      const float mb = m_ref == -INFINITY ? 0.0f : m_ref;
+      {
+        float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          s[c] = ex2_ftz(s[c] - mb);
+          ls[c & 3] += s[c];
+        }
+        l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      }
+      // P(ci-1).V done: the P tile is free and O is stable
+      if (ci > 0) {
+        mbar_wait(&pvdone, (ci - 1) & 1);
+        tc_fence_after();
+      }
+      if (ci > 0 && __any_sync(0xffffffffu, grow && m_old != -INFINITY)) {
+        float o[32];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          tmem_ld32(tO + tl + 32 * q, o);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] *= f;
+          tmem_st32(tO + tl + 32 * q, o);
+        }
+      }
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_bf2(s[8 * c8 + 2 * e], s[8 * c8 + 2 * e + 1], hi[e], lo[e]);
+        const uint32_t off = sw128_off(rl, c8);
+        *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull);
+    }
+    if (n_chunks > 0) {
+      mbar_wait(&pvdone, (n_chunks - 1) & 1);
+      tc_fence_after();
+    }
+    // partial state (m_ref, l, o / l) of my row -> fp16 staging in the idle KV ring
+    constexpr int OLD = HD + 8;
+    __half* sO = reinterpret_cast<__half*>(sKV);
+    const float il = l_part > 0.0f ? 1.0f / l_part : 0.0f;
+    float o[32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (n_chunks > 0) {
+        tmem_ld32(tO + tl + 32 * q, o);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] = 0.0f;
+      }
+#pragma unroll
+      for (int c = 0; c < 32; c += 2)
+        *reinterpret_cast<__half2*>(sO + rl * OLD + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+    }
+    *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, l_part);
+  }
+  tc_fence_before();
+  cluster.sync();
+  if (threadIdx.x < 128) {
+    // merge rows [crank*RPC, (crank+1)*RPC) over the cluster (pull; fixed rank order)
+    constexpr int OLD = HD + 8;
+    const __half* sO = reinterpret_cast<const __half*>(sKV);
+    constexpr int RPC = QR / CS, V4 = HD / 4, NMI = (RPC * V4 + 127) / 128;
+#pragma unroll
+    for (int k = 0; k < NMI; ++k) {
+      const int i = threadIdx.x + k * 128;
+      if (i >= RPC * V4) continue;
+      const int lr = crank * RPC + i / V4, c4 = (i % V4) * 4;
+      const int slot = sRow[lr];
+      if (slot < 0) continue;
+      float mr[CS], lv[CS];
+      float4 ov[CS];
+#pragma unroll
+      for (int q = 0; q < CS; ++q) {
+        const __half* row = cluster.map_shared_rank(sO + lr * OLD, q);
+        const float2 ml = *reinterpret_cast<const float2*>(row + HD);
+        mr[q] = ml.x;
+        lv[q] = ml.y;
+        const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+        ov[q] = make_float4(a.x, a.y, b.x, b.y);
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) M = fmaxf(M, mr[q]);
+      float Lsum = 0.0f;
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < CS; ++q) {
+        if (mr[q] == -INFINITY || lv[q] <= 0.0f) continue;
+        const float w = ex2_ftz(mr[q] - M) * lv[q];
+        Lsum += w;
+        acc.x += w * ov[q].x;
+        acc.y += w * ov[q].y;
+        acc.z += w * ov[q].z;
+        acc.w += w * ov[q].w;
+      }
+      const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), p1 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&p0);
+      u.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4) = u;
+    }
+  }
+  cluster.sync();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(s_tmem, 256);
+  }
+  tstat_end(ats);
+}
+
+template <int NS>
+constexpr size_t attn_f8_smem() {
+  return 1024 + (size_t)4 * AF8_SUB + (size_t)NS * 4 * ATC_SUB;  // q 32 KB + P 32 KB + KV ring
+}
+
+template <int CS, int NS>
+static long long f8_slots() {
+  static long long v = -1;
+  if (v < 0) {
+    constexpr size_t smem = attn_f8_smem<NS>();
+    cudaFuncSetAttribute(k_attn_fa128<CS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS * 64);
+    cfg.blockDim = dim3(AFA_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)k_attn_fa128<CS, NS>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148 / CS;
+    }
+    v = (long long)n * CS;
+    if (getenv("BB_DEBUG")) fprintf(stderr, "[bb200] k_attn_fa128<%d,%d>: %d resident clusters\n", CS, NS, n);
+  }
+  return v;
+}
+
+template <int CS, int NS>
+static cudaError_t attn_f8_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st,
+                                  const AttnMaps& am, int layer, cudaStream_t s) {
+  const int rows = P.full ? S.L : S.NRq;
+  constexpr size_t smem = attn_f8_smem<NS>();
+  static_assert(smem <= 227 * 1024, "k_attn_fa128 shared memory");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_fa128<CS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(S.R * CS, D.nh, (rows + AF8_QR - 1) / AF8_QR);
+  launch_k(k_attn_fa128<CS, NS>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, D, S, P, st, layer, rows);
+  return cudaGetLastError();
+}
+
+#ifndef ATT_F8_NS
+#define ATT_F8_NS 3  // KV ring stages of k_attn_fa128 (one CTA per SM)
+#endif
+template <int NS>
+static int att_cs_f8(const Dims& D, const Sess& S, const Pass& P, int tflags) {
+  const int forced = (tflags >> 4) & 15;
+  if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
+  const int rows = P.full ? S.L : S.NRq;
+  const long long per = (long long)S.R * D.nh * ((rows + AF8_QR - 1) / AF8_QR);
+  if (per * 8 <= 2 * f8_slots<8, NS>()) return 8;
+  if (per * 4 <= 2 * f8_slots<4, NS>()) return 4;
+  if (per * 2 <= 2 * f8_slots<2, NS>()) return 2;
+  return 1;
+}
+
 // tcgen05 attention for hd = 128 in every pass (block, prefill, refresh).
 // Measured (C5 block attention 222 vs 262 us per launch for the mma.sync
 // kernel, C5 16.7 vs 17.9 ms/NFE; C2 attention slot 16.8 vs 19.4 us).
@@ -1761,6 +2184,7 @@ static long long fa_slots() {
       n = 148 / CS;
     }
     v = (long long)n * CS;
+    if (getenv("BB_DEBUG")) fprintf(stderr, "[bb200] k_attn_fa<%d,%d,%d>: %d resident clusters\n", CS, NS, (int)SPLIT, n);
   }
   return v;
 }
@@ -1784,7 +2208,17 @@ template <int HD>
 static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const AttnMaps& am,
                                int layer, int tflags, cudaStream_t s) {
   if constexpr (HD == 128) {
-    // product path: the warp-specialized TMA-fed kernel (test flag bit 1 = k_attn_tc)
+    // product path: the warp-specialized TMA-fed kernels -- M = 128 row tiles
+    // (bf16), M = 64 (bf16x2, whose q / KV planes double the shared memory);
+    // test flag bit 1 = k_attn_tc, bit 2 = the M = 64 kernel for bf16
+    if (am.ok && !(tflags & 3) && P.kz_shift == 7) {
+      switch (att_cs_f8<ATT_F8_NS>(D, S, P, tflags)) {
+        case 8: return attn_f8_launch<8, ATT_F8_NS>(D, S, P, st, am, layer, s);
+        case 4: return attn_f8_launch<4, ATT_F8_NS>(D, S, P, st, am, layer, s);
+        case 2: return attn_f8_launch<2, ATT_F8_NS>(D, S, P, st, am, layer, s);
+        default: return attn_f8_launch<1, ATT_F8_NS>(D, S, P, st, am, layer, s);
+      }
+    }
     if (am.ok && !(tflags & 3)) {
       if (D.split) {
         switch (att_cs_fa<2, true>(D, S, P, tflags)) {
@@ -1909,6 +2343,21 @@ static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const De
   dim3 grid(S.R * max_items, D.nh, (max_rows + QT - 1) / QT);
   launch_k(k_attn<T, HD>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, max_items);
   return cudaGetLastError();
+}
+
+
+// Occupancy queries of the k_attn_fa instances (cluster residency), run at
+// session creation: they are not allowed inside a stream capture.
+void attn_prepare() {
+  f8_slots<8, ATT_F8_NS>();
+  f8_slots<4, ATT_F8_NS>();
+  f8_slots<2, ATT_F8_NS>();
+  fa_slots<8, ATT_FA_NS, false>();
+  fa_slots<4, ATT_FA_NS, false>();
+  fa_slots<2, ATT_FA_NS, false>();
+  fa_slots<8, 2, true>();
+  fa_slots<4, 2, true>();
+  fa_slots<2, 2, true>();
 }
 
 cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const AttnMaps& am, int layer,

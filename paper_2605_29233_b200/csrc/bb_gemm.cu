@@ -82,6 +82,18 @@ struct TcCfg {
   static_assert(SMEM <= 227 * 1024, "GEMM shared memory");
 };
 
+// Tile order.  Stream-K (mode 0): chunk-outer (tile = chunk * n_ntiles +
+// ntile; the piece-count tables and consumers assume it).  Whole tiles
+// (mode 1, LM head): ntile-outer, so the row chunks of one weight tile run on
+// neighbouring CTAs at the same time and the weight tile is read from HBM
+// once (chunk-outer would re-stream the 1 GB head once per chunk).
+__device__ __forceinline__ int tile_ntile(const GemmTcParams& p, int t) {
+  return p.mode == 1 ? t / p.n_chunks : t % p.n_ntiles;
+}
+__device__ __forceinline__ int tile_chunk(const GemmTcParams& p, int t) {
+  return p.mode == 1 ? t % p.n_chunks : t / p.n_ntiles;
+}
+
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ SplitK sk_of(const GemmTcParams& p, int G) {
@@ -220,7 +232,7 @@ __global__ void __launch_bounds__(192)
     UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
     Unit u;
     while (pre < C::STAGES && it.next(u)) {
-      const int ntile = u.tile % p.n_ntiles;
+      const int ntile = tile_ntile(p, u.tile);
       for (int kb = u.kb0; kb < u.kb1 && pre < C::STAGES; ++kb, ++pre) {
         mbar_expect_tx_only(&full[pre], C::A_BYTES);
         tma_load_2d(sA + pre * C::A_BYTES, &tmA, &full[pre], kb * 64, ntile * 128, pol_w);
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(192)
       UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
       Unit u;
       while (it.next(u)) {
-        const int ntile = u.tile % p.n_ntiles, chunk = u.tile / p.n_ntiles;
+        const int ntile = tile_ntile(p, u.tile), chunk = tile_chunk(p, u.tile);
         // (row chunks are never fully padding: rows_alloc = round_up(rows, BN))
         for (int kb = u.kb0; kb < u.kb1; ++kb, ++issued) {
           if (issued < pre) {
@@ -343,7 +355,7 @@ __global__ void __launch_bounds__(192)
     UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
     Unit u;
     while (it.next(u)) {
-      const int ntile = u.tile % p.n_ntiles, chunk = u.tile / p.n_ntiles;
+      const int ntile = tile_ntile(p, u.tile), chunk = tile_chunk(p, u.tile);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int n = ntile * 128 + q * 32 + lane;

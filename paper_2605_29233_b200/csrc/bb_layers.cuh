@@ -42,6 +42,7 @@ struct AttnMaps {
   CUtensorMap k, v, kl, vl;  // kl / vl: the lo pools (bf16x2), else copies of k / v
   bool ok;
 };
+void attn_prepare();  // host-side occupancy queries (call outside stream capture)
 // tflags: bb_session_desc.test_flags (tests only)
 cudaError_t launch_attn(const Dims& D, const Sess& S, const Pass& P, const DevState& st, const AttnMaps& am, int layer,
                         int tflags, cudaStream_t s);

@@ -128,7 +128,9 @@ struct Pass {
   int* akeys;         // [R][n_kz][akey_cap][2]
   int* akey_n;        // [R][n_kz][2] (n_keys, first key of the generation pages)
   int akey_cap;
-  int n_kz;           // key tiles per request (block pass: 64-row tiles; full pass: 1)
+  int n_kz;           // key tiles per request (block pass: (1 << kz_shift)-row tiles; full pass: 1)
+  int kz_shift;       // log2 rows per key tile: 7 for the M = 128 attention, else 6 (a key list of a
+                      // 128-row tile serves its 64-row halves too: a superset of their keys)
   unsigned long long* atstat;  // live attention timing: [0..7] duration, [8..15] CTA start spread
   // L2 prefetch of the next GEMM's weights issued by the attention CTAs (HBM is
   // idle during the attention): layer l's bytes at pf_base + l * pf_layer_bytes

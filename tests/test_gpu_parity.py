@@ -264,31 +264,35 @@ def test_block_step_head_numerics_match_oracle(name, dtype, spike_gain, tol):
                                                 ("mma", "1", 2, 0.0, 2e-2), ("fa", "", 1, 0.0, 2e-2),
                                                 ("fa", "", 2, 33.0, 1e-1), ("mma", "", 2, 33.0, 1e-1),
                                                 ("tc", "", 2, 0.0, 2e-2), ("tc", "1", 1, 0.0, 2e-2),
-                                                ("fa", "2", 1, 0.0, 2e-2), ("fa", "4", 2, 0.0, 2e-2)])
+                                                ("fa", "2", 1, 0.0, 2e-2), ("fa", "4", 2, 0.0, 2e-2),
+                                                ("fa64", "", 2, 0.0, 2e-2), ("fa64", "1", 1, 0.0, 2e-2),
+                                                ("fa64", "", 2, 33.0, 1e-1)])
 def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol):
     """The block step at head_dim 128 (the LLaDA-8B head size; the tiny
     fixtures use 64) with each tensor-core attention: the warp-specialized
-    TMA-fed tcgen05 kernel (fa, the product path), the single-role tcgen05
-    kernel (tc, test flag 2) and the mma.sync kernel (mma, test flag 1),
+    TMA-fed tcgen05 kernels on 128-row tiles (fa, the product path) and on
+    64-row tiles (fa64, test flag 4; the bf16x2 path's layout), the
+    single-role tcgen05 kernel (tc, test flag 2) and the mma.sync kernel
+    (mma, test flag 1),
     against the oracle at the bf16 tolerance of the block-step test.  cs=1:
     one CTA per (head, row tile) takes every key (several chunks: the
     online-softmax rescale path and the KV ring wrap).  kvh=1: grouped-query
     attention (2 query heads share one KV head).  gain 33: the spike epilogue
     (x34 on raw-logit error) at the prefill test's tolerance."""
-    flags = {"fa": 0, "mma": 1, "tc": 2}[tc] | ((int(cs) if cs else 0) << 4)
+    flags = {"fa": 0, "mma": 1, "tc": 2, "fa64": 4}[tc] | ((int(cs) if cs else 0) << 4)
     g = LLADA["llada_tiny_bf16"]
     _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=kvh, head_dim=128), "bf16", gain, tol,
                           f"hd128 tc={tc} cs={cs or 'auto'} kvh={kvh}", test_flags=flags)
 
 
 @pytest.mark.parametrize("tc,cs,P,G", [("fa", "", 600, 200), ("fa", "1", 600, 200), ("tc", "1", 600, 200),
-                                       ("fa", "2", 1000, 120)])
+                                       ("fa", "2", 1000, 120), ("fa64", "", 600, 200), ("fa64", "1", 1000, 120)])
 def test_block_step_long_context_attention_matches_oracle(tc, cs, P, G):
     """Long rows through the hd-128 tensor-core attentions: a 600-token
     prompt (its last page is partly filled: padded key-list segment) and
     ~800 keys per row, i.e. a dozen 64-key chunks per CTA (the KV ring wraps
     several times; lazy O rescale across chunks), vs the oracle."""
-    flags = {"fa": 0, "tc": 2}[tc] | ((int(cs) if cs else 0) << 4)
+    flags = {"fa": 0, "tc": 2, "fa64": 4}[tc] | ((int(cs) if cs else 0) << 4)
     g = LLADA["llada_tiny_bf16"]
     g = dict(g, prompt_len=P, gen_len=G, config=dict(g["config"], gen_len=G), seeds=g["seeds"][:2])
     _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=1, head_dim=128, max_len=P + G), "bf16", 0.0, 2e-2,
