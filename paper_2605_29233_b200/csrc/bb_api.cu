@@ -232,8 +232,11 @@ static void plan(Session* s, char* base, bool dry) {
     }
     P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
     P.row_rope = (!full && D.arch == BB_ARCH_LLADA) ? c.take<float>((long long)rows_alloc * D.hd) : nullptr;
-    // the M = 128 tcgen05 attention (bf16, hd 128, 16-row pages) reads 128-row key tiles
-    P.kz_shift = (D.dtype == BB_DTYPE_BF16 && !D.split && D.hd == 128 && S.ps == 16 && !(s->tflags & 7)) ? 7 : 6;
+    // the M = 128 tcgen05 attention (bf16, hd 128, 16-row pages; passes whose rows per request
+    // exceed one 64-row tile: full passes, C5-size windows) reads 128-row key tiles; block passes
+    // of <= 64 rows per request keep the 64-row kernel (two CTAs per SM, no half-empty tiles)
+    P.kz_shift = (D.dtype == BB_DTYPE_BF16 && !D.split && D.hd == 128 && S.ps == 16 && !(s->tflags & 7) &&
+                  (full || item_rows > 64)) ? 7 : 6;
     P.n_kz = full ? 1 : (item_rows + (1 << P.kz_shift) - 1) >> P.kz_shift;
     P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries
     P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);

@@ -285,18 +285,23 @@ def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol):
                           f"hd128 tc={tc} cs={cs or 'auto'} kvh={kvh}", test_flags=flags)
 
 
-@pytest.mark.parametrize("tc,cs,P,G", [("fa", "", 600, 200), ("fa", "1", 600, 200), ("tc", "1", 600, 200),
-                                       ("fa", "2", 1000, 120), ("fa64", "", 600, 200), ("fa64", "1", 1000, 120)])
-def test_block_step_long_context_attention_matches_oracle(tc, cs, P, G):
+@pytest.mark.parametrize("tc,cs,P,G,bs", [("fa", "", 600, 200, 3), ("fa", "1", 600, 200, 3), ("tc", "1", 600, 200, 3),
+                                          ("fa", "2", 1000, 120, 3), ("fa64", "", 600, 200, 3),
+                                          ("fa64", "1", 1000, 120, 3), ("fa", "", 600, 200, 4), ("fa", "1", 600, 200, 4),
+                                          ("fa", "8", 1000, 120, 4), ("fa64", "", 600, 200, 4)])
+def test_block_step_long_context_attention_matches_oracle(tc, cs, P, G, bs):
     """Long rows through the hd-128 tensor-core attentions: a 600-token
     prompt (its last page is partly filled: padded key-list segment) and
     ~800 keys per row, i.e. a dozen 64-key chunks per CTA (the KV ring wraps
-    several times; lazy O rescale across chunks), vs the oracle."""
+    several times; lazy O rescale across chunks), vs the oracle.  bs=4:
+    branches {8,16,32,64} (120 window rows, the C5 layout: the block pass
+    runs the 128-row-tile kernel, one key tile for all four branches)."""
     flags = {"fa": 0, "tc": 2, "fa64": 4}[tc] | ((int(cs) if cs else 0) << 4)
     g = LLADA["llada_tiny_bf16"]
-    g = dict(g, prompt_len=P, gen_len=G, config=dict(g["config"], gen_len=G), seeds=g["seeds"][:2])
+    bsz = [8, 16, 32] if bs == 3 else [8, 16, 32, 64]
+    g = dict(g, prompt_len=P, gen_len=G, config=dict(g["config"], gen_len=G, block_sizes=bsz), seeds=g["seeds"][:2])
     _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=1, head_dim=128, max_len=P + G), "bf16", 0.0, 2e-2,
-                          f"long hd128 {tc} cs={cs or 'auto'} L={P + G}", test_flags=flags)
+                          f"long hd128 {tc} cs={cs or 'auto'} L={P + G} B={len(bsz)}", test_flags=flags)
 
 
 @pytest.mark.parametrize("kvh,gain,tol,P,G", [(2, 33.0, 2e-2, 32, 64), (1, 33.0, 2e-2, 32, 64),
