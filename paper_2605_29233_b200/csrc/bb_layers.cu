@@ -119,14 +119,14 @@ __global__ void __launch_bounds__(512) k_embed(Dims D, Pass P, const T* __restri
 }
 
 // ------------------------------------------------------------------ post QKV
-// CTA = (row, group of heads of the fused q|k|v output); one thread per
-// (i, i+hd/2) pair of one head.
+// CTA = (rows blockIdx.x + k * gridDim.x, group of heads of the fused q|k|v
+// output); one thread per (i, i+hd/2) pair of one head.  (Batched sessions
+// have thousands of rows: the grid is capped and CTAs loop over rows.)
 template <typename T>
-__global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
-                                                  const float* __restrict__ rope, int layer, PartRef pr) {
-  pdl_launch();  // the successor launches now; our own loads follow
+__device__ __forceinline__ void post_qkv_row(const Dims& D, const Sess& S, const Pass& P, const DevState& st,
+                                             const float* __restrict__ bias, const float* __restrict__ rope, int layer,
+                                             const PartRef& pr, int row) {
   const int half = D.hd >> 1;
-  const int row = blockIdx.x;
   const int hh = blockIdx.y * (blockDim.x / half) + threadIdx.x / half, i = threadIdx.x % half;
   const bool live_hh = hh < D.nh + 2 * D.nkv;
   const int c0 = hh * D.hd + i, c1 = c0 + half;
@@ -201,6 +201,15 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
   T* dl = st.kv_lo != 0 ? dst + st.kv_lo : nullptr;  // bf16x2: the lo pool
   stf2(dst + i, dl != nullptr ? dl + i : nullptr, a);
   stf2(dst + i + half, dl != nullptr ? dl + i + half : nullptr, b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
+                                                  const float* __restrict__ rope, int layer, PartRef pr) {
+  pdl_launch();  // the successor launches now; our own loads follow (the first row's
+                 // session constants before the dependency wait, inside post_qkv_row)
+  for (int row = blockIdx.x; row < P.rows_alloc; row += gridDim.x)
+    post_qkv_row<T>(D, S, P, st, bias, rope, layer, pr, row);
 }
 
 // ------------------------------------------------------------------ residual (+ norm)
@@ -330,9 +339,7 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
 
 // ------------------------------------------------------------------ SwiGLU
 template <typename T>
-__global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
-  pdl_launch();  // the successor launches now; our own loads follow
-  const int row = blockIdx.y;
+__device__ __forceinline__ void post_gu_row(const Dims& D, const Pass& P, const PartRef& pr, int row) {
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int cg = ((f >> 6) << 7) + (f & 63);  // 4 gate features in one 64-block; up at +64
   // piece count: a session constant, read before the dependency wait
@@ -377,6 +384,13 @@ __global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
   a.w = g.w / (1.0f + expf(-g.w)) * u.w;
   const long long ao = (long long)row * D.dff + f;
   Vec4<T>::st2(reinterpret_cast<T*>(P.act) + ao, P.act_lo != nullptr ? reinterpret_cast<T*>(P.act_lo) + ao : nullptr, a);
+}
+
+// CTA = (1024 features, rows blockIdx.y + k * gridDim.y)
+template <typename T>
+__global__ void __launch_bounds__(256) k_post_gu(Dims D, Pass P, PartRef pr) {
+  pdl_launch();  // the successor launches now; our own loads follow
+  for (int row = blockIdx.y; row < P.rows_alloc; row += gridDim.y) post_gu_row<T>(D, P, pr, row);
 }
 
 // ------------------------------------------------------------------ head side
@@ -548,7 +562,7 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
   (void)smem;
   const int heads = D.nh + 2 * D.nkv, half = D.hd / 2;
   const int hpb = half >= 512 ? 1 : 512 / half;  // heads per CTA
-  dim3 grid(P.rows_alloc, (heads + hpb - 1) / hpb);
+  dim3 grid(P.rows_alloc < 2 * S.n_sms ? P.rows_alloc : 2 * S.n_sms, (heads + hpb - 1) / hpb);
   BB_DISPATCH(D, (launch_k(k_post_qkv<T>, dim3(grid), dim3(hpb * half), (size_t)(0), s, D, S, P, st, bias, W.rope, layer, pr)));
   return cudaGetLastError();
 }
@@ -559,7 +573,7 @@ cudaError_t launch_post_residual(const Dims& D, const Pass& P, const PartRef& pr
 }
 
 cudaError_t launch_post_gu(const Dims& D, const Pass& P, const PartRef& pr, cudaStream_t s) {
-  dim3 grid((D.dff / 4 + 255) / 256, P.rows_alloc);
+  dim3 grid((D.dff / 4 + 255) / 256, P.rows_alloc < 296 ? P.rows_alloc : 296);
   BB_DISPATCH(D, (launch_k(k_post_gu<T>, dim3(grid), dim3(256), (size_t)(0), s, D, P, pr)));
   return cudaGetLastError();
 }
