@@ -1170,6 +1170,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   using ST = typename std::conditional<SPLIT, float, __half>::type;
   ST* sO = reinterpret_cast<ST*>(sK);
   phase_mark(ph, 6, t0);
+  // every P.V phase is observed (the loop waits phases 0 .. n-3 before reusing a buffer)
+  if (n_chunks > 1) mbar_wait(&mbP, (n_chunks - 2) & 1);
   if (n_chunks > 0) mbar_wait(&mbP, (n_chunks - 1) & 1);
   tc_fence_after();
   __syncthreads();

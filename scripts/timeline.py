@@ -13,7 +13,7 @@ _CFG = {"c2": (64, 256, (8, 16, 32)), "c5": (2048, 1024, (8, 16, 32, 64))}[os.en
 P, G = _CFG[0], _CFG[1]
 vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
 cfg = bb.SchedulerConfig(block_sizes=_CFG[2], gen_len=G)
-params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=0.4, gamma=8.0, dtype="bf16")
+params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=0.4, gamma=8.0, dtype=os.environ.get("BB_TL_DTYPE", "bf16"))
 R = int(os.environ.get("BB_TL_R", "1"))  # requests per session (multi-request batching)
 if os.environ.get("BB_TL_TFLAGS"):  # session test flags (A/B: attention kernel / cluster size)
     from paper_2605_29233_b200.engine import Session
