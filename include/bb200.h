@@ -85,8 +85,8 @@ typedef struct {
   int test_flags;      /* tests only (0 on the product path): bit 0 = mma.sync attention at
                           head_dim 128; bit 1 = the single-role tcgen05 attention (k_attn_tc)
                           instead of the warp-specialized one; bit 2 = the warp-specialized
-                          attention on 64-row instead of 128-row tiles; bits 4-7 = forced
-                          cluster size */
+                          attention on 64-row instead of 128-row tiles; bit 3 = no block-pass
+                          compaction in batched sessions; bits 4-7 = forced cluster size */
   int logits;          /* 1: the LM head also keeps raw logits (bb_head_logits; forward observers) */
   int seam;            /* 1: step-operator seam session (bb_seam_*): private pages per branch */
   int hard_cap;        /* > 0: override the forward cap 4*G*B+16 (scheduler.py:310; tests) */

@@ -241,6 +241,8 @@ static void plan(Session* s, char* base, bool dry) {
     P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries
     P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
     P.akey_n = c.take<int>((long long)R * P.n_kz * 2);
+    P.req_base = c.take<int>(R);
+    P.rows_live = c.take<int>(1);
   };
   pass(s->blk, round_up(S.NR, s->gb.BN), S.max_items, S.NRq, 0);
   pass(s->full, round_up(S.NF, s->gf.BN), 1, S.L, 1);
@@ -375,6 +377,10 @@ static int setup_gemms(Session* s) {
           p.part = s->part;
           p.skip = P.skip;
           p.rows_valid = which == 1 ? s->full_rows : nullptr;
+          if (which == 0 && s->S.compact) {  // batched: only the live requests' rows
+            p.rows_valid = p.rows_dyn = s->blk.rows_live;
+            all[g]->sk.rows_dyn = s->blk.rows_live;
+          }
         }
       } else {
         lg.sqkv = SimtGemm{(const float*)wqkv, (const float*)P.xn, D.qkv_out, D.d, P.rows_alloc,
@@ -415,6 +421,7 @@ static int setup_gemms(Session* s) {
     p.spike_cut = D.spike_cut;
     p.spike_gain = D.spike_gain;
     p.skip = s->H.skip;
+    if (s->S.compact) p.rows_valid = p.rows_dyn = s->blk.rows_live;
     p.tstat = s->tsite_on ? s->tsite + 3 * ((size_t)4 * D.layers) : nullptr;
     p.klog = s->D.klog;
     p.klog_cap = s->D.klog_cap;
@@ -541,6 +548,7 @@ static int enqueue_block_step_part(Session* s, int part, cudaStream_t st) {
   if (part == 0) {
     CK(cudaMemsetAsync(s->blk.skip, 1, sizeof(int), st));
     CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
+    if (S.compact) CK(launch_block_bases(D, S, s->st, s->blk, s->H, st));
     CK(launch_block_pack(D, S, s->st, s->blk, s->H, st));
     CK(launch_copy_pages(D, S, s->st, 0, st));
   } else if (part == 1) {
@@ -737,6 +745,8 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   S.trace = d->trace;
   S.hard_cap = d->hard_cap > 0 ? d->hard_cap : 4 * S.G * S.B + 16;  // scheduler.py:310
   S.max_copies = S.B * (maxb / S.ps + 2);
+  // test flag bit 3: keep the static block-pass layout in a batched session (A/B)
+  S.compact = (S.R > 1 && s->D.dtype == BB_DTYPE_BF16 && !d->seam && !d->diagnostics && !(d->test_flags & 8)) ? 1 : 0;
   const int NR = S.NR;
   // rows per GEMM chunk (bf16x2: the MMA's N holds each row twice, hi and lo,
   // so chunks carry at most 128 rows)
@@ -813,6 +823,12 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   cudaMemcpy(s->full.slot_pos, neg.data(), s->full.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->H.masked, zero.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->full_rows, &s->S.NF, sizeof(int), cudaMemcpyHostToDevice);
+  {
+    std::vector<int> base(s->S.R);
+    for (int r = 0; r < s->S.R; ++r) base[r] = r * s->S.NRq;
+    cudaMemcpy(s->blk.req_base, base.data(), base.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(s->blk.rows_live, &s->S.NR, sizeof(int), cudaMemcpyHostToDevice);
+  }
   {
     std::vector<unsigned long long> ts(17 * 8, 0ull);
     for (int k = 0; k < 16; ++k) ts[k * 8] = ~0ull;

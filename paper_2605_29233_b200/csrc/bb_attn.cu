@@ -203,12 +203,12 @@ __global__ void __launch_bounds__(256) k_attn_keys(Sess S, Pass P, DevState st, 
   int* sMsk = sSeg + S.n_lp * S.B;        // [n_lp][B] branch mask of segment
   __shared__ int s_bmask, s_tot, s_gen0;
   const int r = blockIdx.x, kz = blockIdx.y;
-  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  const int slot_base = P.full ? r * S.L : blk_base(S, P, r);  // -1: finished request (compacting session)
   if (threadIdx.x == 0) s_bmask = 0;
   __syncthreads();
   const bool skip = *P.skip != 0;
   const int kr0 = kz << P.kz_shift, kr1 = min(rows_per_req, kr0 + (1 << P.kz_shift));
-  for (int lr = kr0 + (int)threadIdx.x; lr < kr1 && !skip; lr += blockDim.x) {
+  for (int lr = kr0 + (int)threadIdx.x; lr < kr1 && !skip && slot_base >= 0; lr += blockDim.x) {
     const int sl = slot_base + lr;
     if (P.slot_pos[sl] >= 0) atomicOr(&s_bmask, 1 << P.slot_br[sl]);
   }
@@ -394,12 +394,12 @@ __global__ void __cluster_dims__(ATT_CS, 1, 1) __launch_bounds__(128)
   const int row0 = blockIdx.z * QR;
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  const int slot_base = P.full ? r * S.L : blk_base(S, P, r);  // (after pdl_enter) -1: finished request
   const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * 64) >> P.kz_shift));
   if (threadIdx.x < QR) {
     const int lr = row0 + threadIdx.x;
     int slot = -1, br = 0, pos = -1;
-    if (lr < rows_per_req) {
+    if (lr < rows_per_req && slot_base >= 0) {
       const int sl = slot_base + lr;
       pos = P.slot_pos[sl];
       br = P.slot_br[sl];
@@ -948,7 +948,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rl = 16 * warp + (lane & 15), hh = lane >> 4;  // my row, my key half (S) / dim half (O)
-  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  int slot_base = -1;  // block pass: read after the dependency wait (compacting sessions rewrite it)
   const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * 64) >> P.kz_shift));
 
   if (threadIdx.x == 0) {
@@ -958,6 +958,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   }
   if (warp == 0) tmem_alloc(&s_tmem, 256);  // S: 64 columns, O: 128 columns
   pdl_enter();
+  slot_base = P.full ? r * S.L : blk_base(S, P, r);  // -1: finished request (compacting session)
   klog_mark(D.klog, D.klog_cap, 3);
   unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;
   tstat_begin(ats);
@@ -967,7 +968,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   if (threadIdx.x < QR) {
     const int lr = row0 + threadIdx.x;
     int slot = -1, br = 0;
-    if (lr < rows_per_req) {
+    if (lr < rows_per_req && slot_base >= 0) {
       const int sl = slot_base + lr;
       br = P.slot_br[sl];
       if (P.slot_pos[sl] >= 0 && !*P.skip) slot = sl;
@@ -1063,10 +1064,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
     // the next chunk's gather (its buffer was last read by S and P.V of ci-1)
     cp_async_wait<0>();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (ci + 1 < n_chunks) {
-      if (ci > 0) mbar_wait(&mbP, (ci - 1) & 1);
-      load_chunk(ci + 1, buf ^ 1);
-    }
+    // P.V of chunk ci-1 done (every phase is observed in order: parity waits
+    // must never fall two phases behind): its K/V buffer is free
+    if (ci > 0) mbar_wait(&mbP, (ci - 1) & 1);
+    if (ci + 1 < n_chunks) load_chunk(ci + 1, buf ^ 1);
     __syncthreads();
     if (threadIdx.x == 0) {
       tc_fence_after();
@@ -1170,8 +1171,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(128)
   using ST = typename std::conditional<SPLIT, float, __half>::type;
   ST* sO = reinterpret_cast<ST*>(sK);
   phase_mark(ph, 6, t0);
-  // every P.V phase is observed (the loop waits phases 0 .. n-3 before reusing a buffer)
-  if (n_chunks > 1) mbar_wait(&mbP, (n_chunks - 2) & 1);
   if (n_chunks > 0) mbar_wait(&mbP, (n_chunks - 1) & 1);
   tc_fence_after();
   __syncthreads();
@@ -1347,7 +1346,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   const int row0 = blockIdx.z * QR;
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  int slot_base = -1;  // block pass: read after the dependency wait (compacting sessions rewrite it)
   const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * 64) >> P.kz_shift));
 
   if (threadIdx.x == 0) {
@@ -1374,13 +1373,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   }
   if (warp == 5) tmem_alloc(&s_tmem, 256);  // S0, S1: 64 columns each; O: 128 columns
   pdl_enter();
+  slot_base = P.full ? r * S.L : blk_base(S, P, r);  // -1: finished request (compacting session)
   klog_mark(D.klog, D.klog_cap, 3);
   unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;
   tstat_begin(ats);
   if (threadIdx.x < QR) {
     const int lr = row0 + threadIdx.x;
     int slot = -1, br = 0;
-    if (lr < rows_per_req) {
+    if (lr < rows_per_req && slot_base >= 0) {
       const int sl = slot_base + lr;
       br = P.slot_br[sl];
       if (P.slot_pos[sl] >= 0 && !*P.skip) slot = sl;
@@ -1773,7 +1773,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   const int row0 = blockIdx.z * QR;
   const int kvh = h / (D.nh / D.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot_base = P.full ? r * S.L : r * S.NRq;
+  int slot_base = -1;  // block pass: read after the dependency wait (compacting sessions rewrite it)
   const long long kb = (long long)r * P.n_kz + (P.full ? 0 : ((blockIdx.z * QR) >> P.kz_shift));
 
   if (threadIdx.x == 0) {
@@ -1796,13 +1796,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   }
   if (warp == 5) tmem_alloc(&s_tmem, 256);  // S0, S1: 64 columns each; O: 128 columns
   pdl_enter();
+  slot_base = P.full ? r * S.L : blk_base(S, P, r);  // -1: finished request (compacting session)
   klog_mark(D.klog, D.klog_cap, 3);
   unsigned long long* const ats = D.klog != nullptr ? P.atstat : nullptr;
   tstat_begin(ats);
   if (threadIdx.x < QR) {
     const int lr = row0 + threadIdx.x;
     int slot = -1, br = 0;
-    if (lr < rows_per_req) {
+    if (lr < rows_per_req && slot_base >= 0) {
       const int sl = slot_base + lr;
       br = P.slot_br[sl];
       if (P.slot_pos[sl] >= 0 && !*P.skip) slot = sl;

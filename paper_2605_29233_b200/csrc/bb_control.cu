@@ -395,7 +395,12 @@ __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk,
     full.slot_tok[row] = c.rows[p];
     full.slot_kvoff[row] = kv_row_off(D, S, st, r, 0, p);
   }
-  // head slots: each branch's initial window over the base row
+  // head slots: each branch's initial window over the base row (every request
+  // is live at prefill: the static slot layout, also restored for compaction)
+  if (threadIdx.x == 0) {
+    blk.req_base[r] = r * S.NRq;
+    if (r == 0) *blk.rows_live = S.NR;
+  }
   const int* target = st.target + (long long)r * S.G;
   for (int i = threadIdx.x; i < S.NRq; i += blockDim.x) {
     const int slot = r * S.NRq + i;
@@ -457,7 +462,7 @@ __device__ int eq1_commit(const float* conf, const int* arg, const int* pos, con
 __device__ int apply_commits(RC& c, const Pass& blk, const Head& H, int k, float tau) {
   __shared__ float redf[32];
   __shared__ int redi[32];
-  const int slot0 = c.r * c.S->NRq + c.S->off[k];
+  const int slot0 = blk_base(*c.S, blk, c.r) + c.S->off[k];
   const int n = c.S->bs[k];
   int star = 0x7fffffff;
   for (int base = 0; base < n; base += blockDim.x) {
@@ -529,6 +534,7 @@ __device__ void pack_block_pass(RC& c, int active, const Pass& blk, const Head& 
   const Dims& D = *c.D;
   const Sess& S = *c.S;
   const int r = c.r;
+  const int base = blk_base(S, blk, r);  // -1: a finished request of a compacting session (no slots)
   if (threadIdx.x == 0) {
     c.ctrl[C_NCOPY] = 0;
     if (active) {
@@ -581,15 +587,15 @@ __device__ void pack_block_pass(RC& c, int active, const Pass& blk, const Head& 
     int rows = 0;
     for (int k = 0; k < MAXB; ++k) {
       const bool a = k < S.B && ((active >> k) & 1);
-      blk.rng_off[r * MAXB + k] = r * S.NRq + (k < S.B ? S.off[k] : 0);
+      blk.rng_off[r * MAXB + k] = base + (k < S.B ? S.off[k] : 0);
       blk.rng_cnt[r * MAXB + k] = a ? c.B_(k, B_END) - c.B_(k, B_START) : 0;
       rows += blk.rng_cnt[r * MAXB + k];
     }
     c.ctrl[C_BLOCK_ROWS] = rows;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < S.NRq; i += blockDim.x) {
-    const int slot = r * S.NRq + i;
+  for (int i = threadIdx.x; i < S.NRq && base >= 0; i += blockDim.x) {
+    const int slot = base + i;
     int k = -1;
     for (int kk = 0; kk < S.B; ++kk)
       if (i >= S.off[kk] && i < S.off[kk] + S.bs[kk]) k = kk;
@@ -611,6 +617,30 @@ __device__ void pack_block_pass(RC& c, int active, const Pass& blk, const Head& 
       H.boost[slot] = 0.0f;
       H.tgt[slot] = -1;
     }
+  }
+}
+
+// Compacting sessions: the block pass's slots go to the live requests only,
+// in request order (request r's NRq slots start at rank(r) * NRq), and the
+// GEMMs / head size their work by rows_live -- finished requests of a batch
+// cost no rows.  Slots past rows_live are cleared (padding).  One CTA.
+__global__ void k_block_bases(Dims D, Sess S, DevState st, Pass blk, Head H) {
+  pdl_enter();
+  __shared__ int s_live;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int r = 0; r < S.R; ++r) {
+      const bool live = st.ctrl[(long long)r * C_WORDS + C_STATUS] == 0;
+      blk.req_base[r] = live ? n * S.NRq : -1;
+      n += live ? 1 : 0;
+    }
+    s_live = n * S.NRq;
+    *blk.rows_live = s_live;
+  }
+  __syncthreads();
+  for (int slot = s_live + (int)threadIdx.x; slot < S.NR; slot += blockDim.x) {
+    blk.slot_pos[slot] = -1;
+    H.masked[slot] = 0;
   }
 }
 
@@ -1123,8 +1153,9 @@ __global__ void k_refresh_pack(Dims D, Sess S, DevState st, Pass full, Pass blk,
     full.slot_kvoff[row] = live ? kv_row_off(D, S, st, r, k, p) : 0;
   }
   const int* target = st.target + (long long)r * S.G;
-  for (int j = threadIdx.x; j < S.bs[k]; j += blockDim.x) {
-    const int slot = r * S.NRq + S.off[k] + j;
+  const int rbase = blk_base(S, blk, r);
+  for (int j = threadIdx.x; j < S.bs[k] && rbase >= 0; j += blockDim.x) {
+    const int slot = rbase + S.off[k] + j;
     const int pos = c.B_(k, B_START) + j;
     const bool in = live && pos < c.B_(k, B_END) && c.rows[k * S.L + pos] == c.mask_id;
     blk.slot_req[slot] = r;
@@ -1226,8 +1257,9 @@ __global__ void k_vanilla_pack(Dims D, Sess S, DevState st, Pass full, Pass blk,
     full.slot_kvoff[row] = live ? kv_row_off(D, S, st, r, 0, p) : 0;
   }
   const int* target = st.target + (long long)r * S.G;
-  for (int j = threadIdx.x; j < S.NRq; j += blockDim.x) {
-    const int slot = r * S.NRq + j;
+  const int vbase = blk_base(S, blk, r);
+  for (int j = threadIdx.x; j < S.NRq && vbase >= 0; j += blockDim.x) {
+    const int slot = vbase + j;
     const int pos = S.P + j;
     const bool in = live && pos < end && c.rows[pos] == c.mask_id;
     blk.slot_req[slot] = r;
@@ -1254,7 +1286,8 @@ __global__ void k_vanilla_commit(Dims D, Sess S, DevState st, Pass blk, Head H) 
   if (!s_live) return;
   // only this request's slots are masked when its round is live
   bool any = false;
-  for (int j = threadIdx.x; j < S.NRq; j += blockDim.x) any |= H.masked[c.r * S.NRq + j] != 0;
+  const int vbase = blk_base(S, blk, c.r);
+  for (int j = threadIdx.x; j < S.NRq && vbase >= 0; j += blockDim.x) any |= H.masked[vbase + j] != 0;
   if (!__syncthreads_or(any)) return;
   const int n = apply_commits(c, blk, H, 0, 1.0f);  // tau 1.0: the most confident position (decoding.py:311)
   const int dec = c.count_decoded(0);
@@ -1561,6 +1594,11 @@ cudaError_t launch_prefill_post(const Dims& D, const Sess& S, const DevState& st
     a = true;
   }
   launch_k(k_prefill_post, dim3(S.R), dim3(256), (size_t)(rc_smem(S)), s, D, S, st, blk, H);
+  return cudaGetLastError();
+}
+cudaError_t launch_block_bases(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                               cudaStream_t s) {
+  launch_k(k_block_bases, dim3(1), dim3(256), (size_t)0, s, D, S, st, blk, H);
   return cudaGetLastError();
 }
 cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,

@@ -87,11 +87,11 @@ struct TcCfg {
 // (mode 1, LM head): ntile-outer, so the row chunks of one weight tile run on
 // neighbouring CTAs at the same time and the weight tile is read from HBM
 // once (chunk-outer would re-stream the 1 GB head once per chunk).
-__device__ __forceinline__ int tile_ntile(const GemmTcParams& p, int t) {
-  return p.mode == 1 ? t / p.n_chunks : t % p.n_ntiles;
+__device__ __forceinline__ int tile_ntile(const GemmTcParams& p, int t, int nch) {
+  return p.mode == 1 ? t / nch : t % p.n_ntiles;
 }
-__device__ __forceinline__ int tile_chunk(const GemmTcParams& p, int t) {
-  return p.mode == 1 ? t % p.n_chunks : t / p.n_ntiles;
+__device__ __forceinline__ int tile_chunk(const GemmTcParams& p, int t, int nch) {
+  return p.mode == 1 ? t % nch : t / p.n_ntiles;
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(192)
     int pre = 0;
     UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
     Unit u;
-    while (pre < C::STAGES && it.next(u)) {
-      const int ntile = tile_ntile(p, u.tile);
+    // (a compacting session's row count is only known after the dependency wait: no prefetch)
+    while (p.rows_dyn == nullptr && pre < C::STAGES && it.next(u)) {
+      const int ntile = tile_ntile(p, u.tile, p.n_chunks);
       for (int kb = u.kb0; kb < u.kb1 && pre < C::STAGES; ++kb, ++pre) {
         mbar_expect_tx_only(&full[pre], C::A_BYTES);
         tma_load_2d(sA + pre * C::A_BYTES, &tmA, &full[pre], kb * 64, ntile * 128, pol_w);
@@ -253,6 +254,10 @@ __global__ void __launch_bounds__(192)
   if (threadIdx.x == 0) gph(7);   // producer (issued the weight prefetch first)
   const bool skipped = p.skip != nullptr && *p.skip != 0;
   const int rows_valid = skipped ? 0 : (p.rows_valid != nullptr ? *p.rows_valid : p.rows_alloc);
+  // row chunks this launch computes (compacting sessions: the live rows only)
+  const int rows_c0 = p.half ? p.half : BN;
+  const int nch = p.rows_dyn != nullptr ? min(p.n_chunks, (*p.rows_dyn + rows_c0 - 1) / rows_c0) : p.n_chunks;
+  const int n_tiles_eff = p.n_ntiles * nch;
   if (skipped) {
     // drain the prefetched weight tiles before exiting (async copies into our smem)
     __syncthreads();
@@ -284,10 +289,10 @@ __global__ void __launch_bounds__(192)
         tma_load_2d(sB + st * C::B_BYTES, &tmB, &full[st], kb * 64, chunk * rows_c, pol_x);
         if (p.half) tma_load_2d(sB + st * C::B_BYTES + p.half * 128, &tmB2, &full[st], kb * 64, chunk * rows_c, pol_x);
       };
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode);
       Unit u;
       while (it.next(u)) {
-        const int ntile = tile_ntile(p, u.tile), chunk = tile_chunk(p, u.tile);
+        const int ntile = tile_ntile(p, u.tile, nch), chunk = tile_chunk(p, u.tile, nch);
         // (row chunks are never fully padding: rows_alloc = round_up(rows, BN))
         for (int kb = u.kb0; kb < u.kb1; ++kb, ++issued) {
           if (issued < pre) {
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(192)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode);
       Unit u;
       bool first = true;
       while (it.next(u)) {
@@ -352,10 +357,10 @@ __global__ void __launch_bounds__(192)
     const int et = threadIdx.x - 64;
     int acc = 0;
     uint32_t aphase = 0;
-    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode);
     Unit u;
     while (it.next(u)) {
-      const int ntile = tile_ntile(p, u.tile), chunk = tile_chunk(p, u.tile);
+      const int ntile = tile_ntile(p, u.tile, nch), chunk = tile_chunk(p, u.tile, nch);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int n = ntile * 128 + q * 32 + lane;

@@ -130,7 +130,12 @@ __device__ __forceinline__ void post_qkv_row(const Dims& D, const Sess& S, const
   const int hh = blockIdx.y * (blockDim.x / half) + threadIdx.x / half, i = threadIdx.x % half;
   const bool live_hh = hh < D.nh + 2 * D.nkv;
   const int c0 = hh * D.hd + i, c1 = c0 + half;
-  // session constants (piece count, bias) before the dependency wait
+  // session constants (piece count, bias) before the dependency wait -- except
+  // in compacting sessions, whose piece counts follow this step's live rows
+  if (pr.sk.rows_dyn != nullptr) {
+    pdl_wait();
+    if (row >= *pr.sk.rows_dyn) return;  // past the live requests' rows
+  }
   const int ns = live_hh ? sk_nslots(pr.sk, row, c0) : 0;
   float ba = 0.0f, bb = 0.0f;
   if (bias != nullptr && live_hh) {
@@ -232,6 +237,10 @@ __global__ void __launch_bounds__(512) k_post_residual(Dims D, Pass P, PartRef p
   if (D.d <= NG * 4 * (int)blockDim.x) {
     float4 xv[NG], w[NG][NSU], gv[NG];
     int ns[NG], cc[NG];
+    if (pr.sk.rows_dyn != nullptr) {  // compacting session: piece counts follow the live rows
+      pdl_wait();
+      if (row >= *pr.sk.rows_dyn) return;
+    }
 #pragma unroll
     for (int u = 0; u < NG; ++u) {
       cc[u] = (threadIdx.x + u * blockDim.x) * 4;
@@ -342,7 +351,12 @@ template <typename T>
 __device__ __forceinline__ void post_gu_row(const Dims& D, const Pass& P, const PartRef& pr, int row) {
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int cg = ((f >> 6) << 7) + (f & 63);  // 4 gate features in one 64-block; up at +64
-  // piece count: a session constant, read before the dependency wait
+  // piece count: a session constant, read before the dependency wait (compacting
+  // sessions: it follows this step's live rows)
+  if (pr.sk.rows_dyn != nullptr) {
+    pdl_wait();
+    if (row >= *pr.sk.rows_dyn) return;
+  }
   const int ns = f < D.dff ? sk_nslots(pr.sk, row, cg) : 0;
   pdl_wait();
   klog_mark(D.klog, D.klog_cap, 5);

@@ -60,6 +60,8 @@ cudaError_t launch_prefill_init(const Dims& D, const Sess& S, const DevState& st
                                 const Head& H, cudaStream_t s);
 cudaError_t launch_prefill_post(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
                                 cudaStream_t s);
+cudaError_t launch_block_bases(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
+                               cudaStream_t s);
 cudaError_t launch_block_pack(const Dims& D, const Sess& S, const DevState& st, const Pass& blk, const Head& H,
                               cudaStream_t s);
 cudaError_t launch_copy_pages(const Dims& D, const Sess& S, const DevState& st, int with_pm, cudaStream_t s);

@@ -68,6 +68,8 @@ struct Sess {
   int ev_cap, trace, hard_cap, max_copies;
   int diag;           // diagnostics session: the last n_lp pages of each request's pool are scratch
   int n_sms;          // SMs of the device (grid sizing)
+  int compact;        // batched tcgen05 sessions: block-pass rows of the live requests only
+                      // (Pass::req_base / rows_live), so finished requests cost no GEMM rows
 };
 
 struct DevState {
@@ -132,6 +134,11 @@ struct Pass {
   int kz_shift;       // log2 rows per key tile: 7 for the M = 128 attention, else 6 (a key list of a
                       // 128-row tile serves its 64-row halves too: a superset of their keys)
   unsigned long long* atstat;  // live attention timing: [0..7] duration, [8..15] CTA start spread
+  // block pass of a compacting session: per request the first slot of its NRq
+  // slots this iteration (-1: finished), and the slots in use (a device
+  // scalar the GEMMs size their work by); static r * NRq otherwise
+  int* req_base;      // [R]
+  int* rows_live;
   // L2 prefetch of the next GEMM's weights issued by the attention CTAs (HBM is
   // idle during the attention): layer l's bytes at pf_base + l * pf_layer_bytes
   const char* pf_base;
@@ -157,6 +164,14 @@ struct Head {
 // tables; only the SIMT (fp32 / head_dim 32,256) path needs planned items
 __host__ __device__ inline bool uses_items(const Dims& D) {
   return !(D.dtype == 1 && (D.hd == 64 || D.hd == 128));
+}
+
+// first block-pass slot of request r (-1: finished, compacting sessions only)
+__host__ __device__ inline int blk_base(const Sess& S, const Pass& blk, int r) {
+#ifdef __CUDA_ARCH__
+  if (S.compact) return blk.req_base[r];
+#endif
+  return r * S.NRq;
 }
 
 __host__ __device__ inline int lp_start(const Sess& s, int lp) {

@@ -300,3 +300,38 @@ def test_model_memory_is_released():
     gc.collect()
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated() <= before
+
+
+def test_batched_compaction_matches_static_layout():
+    """Batched bf16x2 sessions compact the block pass to the live requests
+    (finished requests cost no GEMM rows): the decisions equal those of the
+    same batch with the static per-request layout (test flag 8) and of the
+    requests run alone, on a 4-request batch whose requests finish at
+    different iterations."""
+    from paper_2605_29233_b200.engine import Session
+    from paper_2605_29233_b200.scheduler import _cfg_key
+    dims = bb.ModelDims(layers=2, d_model=256, max_len=192, arch="llada", n_heads=2, n_kv_heads=2, head_dim=128,
+                        d_ff=512, rope_theta=500000.0)
+    vocab = bb.Vocab(size=1000)
+    cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=64)
+    tasks = [bb.make_task(s, 32, 64, vocab) for s in range(4)]
+
+    def run(flags):
+        p = bb.build_model(0, vocab, dims, head_scale=0.25, dtype="bf16x2")
+        if flags:
+            p._sessions[_cfg_key(cfg, 32, len(tasks), True)] = Session(p, cfg, 32, len(tasks), test_flags=flags)
+        return [(r.nfe.snapshot(), r.row.tokens.tolist()) for r in bb.run_batch(p, tasks, cfg)]
+    compact, static = run(0), run(8)
+    single = []
+    p1 = bb.build_model(0, vocab, dims, head_scale=0.25, dtype="bf16x2")
+    for t in tasks:
+        r = bb.run_blockbatch(p1, t, cfg)
+        single.append((r.nfe.snapshot(), r.row.tokens.tolist()))
+    nfes = [c[0] for c in compact]
+    assert len(set(n[1] for n in nfes)) > 1, "requests should finish at different iterations"
+    same_static = sum(a == b for a, b in zip(compact, static))
+    same_single = sum(a == b for a, b in zip(compact, single))
+    print(f"compacted vs static: {same_static}/4, vs single requests: {same_single}/4, static vs single "
+          f"{sum(a == b for a, b in zip(static, single))}/4; nfe {nfes} / {[x[0] for x in static]} / "
+          f"{[x[0] for x in single]}")
+    assert same_static >= 3 and same_single >= 3
