@@ -155,6 +155,14 @@ static Dims make_dims(const bb_model_desc* m) {
 
 static size_t esz(const Dims& D) { return D.dtype == BB_DTYPE_BF16 ? 2 : 4; }
 
+// Fixed k-pieces per weight tile for a compacting session's block-pass GEMMs:
+// enough pieces that one row chunk alone still feeds ~2 units per CTA.
+static int fixed_np(int ntiles, int G, int KB) {
+  int np = (2 * G + ntiles - 1) / ntiles;
+  np = np < 1 ? 1 : (np > 8 ? 8 : np);
+  return np > KB ? KB : np;
+}
+
 // Workspace plan.  dry = size query.
 static void plan(Session* s, char* base, bool dry) {
   const Dims& D = s->D;
@@ -285,13 +293,17 @@ static void plan(Session* s, char* base, bool dry) {
       const int BN = which == 0 ? s->gb.BN : s->gf.BN;
       for (int g = 0; g < 4; ++g) {
         if (outs[g] == 0) continue;
-        const int ntiles = (outs[g] + 127) / 128, nch = rows / BN, KB = (ks[g] + 63) / 64;
-        const long long T = (long long)ntiles * nch * KB;
-        const int G = (int)(T < s->n_sms ? T : s->n_sms);
+        const int ntiles = (outs[g] + 127) / 128, nch_all = rows / BN, KB = (ks[g] + 63) / 64;
+        const long long T_all = (long long)ntiles * nch_all * KB;
+        const int G = (int)(T_all < s->n_sms ? T_all : s->n_sms);
         int ms = 1;
-        for (long long t = 0; t < (long long)ntiles * nch; ++t) {
-          const int ns = sk_owner(t * KB + KB - 1, T, G) - sk_owner(t * KB, T, G) + 1;
-          ms = ns > ms ? ns : ms;
+        if (which == 0 && S.compact) {
+          ms = fixed_np(ntiles, G, KB);  // fixed pieces per tile
+        } else {
+          for (long long t = 0; t < (long long)ntiles * nch_all; ++t) {
+            const int ns = sk_owner(t * KB + KB - 1, T_all, G) - sk_owner(t * KB, T_all, G) + 1;
+            ms = ns > ms ? ns : ms;
+          }
         }
         const long long need = (long long)ms * rows * outs[g];
         part = need > part ? need : part;
@@ -377,9 +389,11 @@ static int setup_gemms(Session* s) {
           p.part = s->part;
           p.skip = P.skip;
           p.rows_valid = which == 1 ? s->full_rows : nullptr;
-          if (which == 0 && s->S.compact) {  // batched: only the live requests' rows
-            p.rows_valid = p.rows_dyn = s->blk.rows_live;
-            all[g]->sk.rows_dyn = s->blk.rows_live;
+          if (which == 0 && s->S.compact) {
+            // batched: fixed k-pieces per tile (sums independent of how many requests are
+            // live) and only the live requests' row chunks (test flag 256: all chunks)
+            p.np = all[g]->sk.np = fixed_np(p.n_ntiles, all[g]->grid, p.KB);
+            if (!(s->tflags & 256)) p.rows_valid = p.rows_dyn = s->blk.rows_live;
           }
         }
       } else {
@@ -421,7 +435,7 @@ static int setup_gemms(Session* s) {
     p.spike_cut = D.spike_cut;
     p.spike_gain = D.spike_gain;
     p.skip = s->H.skip;
-    if (s->S.compact) p.rows_valid = p.rows_dyn = s->blk.rows_live;
+    if (s->S.compact && !(s->tflags & (256 | 512))) p.rows_valid = p.rows_dyn = s->blk.rows_live;
     p.tstat = s->tsite_on ? s->tsite + 3 * ((size_t)4 * D.layers) : nullptr;
     p.klog = s->D.klog;
     p.klog_cap = s->D.klog_cap;

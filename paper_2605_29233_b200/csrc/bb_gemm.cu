@@ -26,13 +26,22 @@ struct Unit {
   int tile, kb0, kb1, slot;
 };
 
+// Work units of a CTA.  mode 0: stream-K over the flattened (tile, k-block)
+// space; mode 0 with np > 0 (compacting sessions): every tile is cut into np
+// fixed k-pieces (piece q = plane q) and the pieces are dealt out in
+// contiguous runs -- a tile's sums then do not depend on how many row chunks
+// the launch computes; mode 1: whole tiles round-robin.
 struct UnitIter {
   long long x, end, T;
-  int KB, G, c, mode, n_tiles;
-  __device__ UnitIter(int c_, int G_, int KB_, int n_tiles_, int mode_)
-      : c(c_), G(G_), KB(KB_), n_tiles(n_tiles_), mode(mode_) {
+  int KB, G, c, mode, n_tiles, np;
+  __device__ UnitIter(int c_, int G_, int KB_, int n_tiles_, int mode_, int np_ = 0)
+      : c(c_), G(G_), KB(KB_), n_tiles(n_tiles_), mode(mode_), np(np_) {
     T = (long long)n_tiles * KB;
-    if (mode == 0) {
+    if (mode == 0 && np > 0) {
+      const long long TP = (long long)n_tiles * np;
+      x = (long long)c * TP / G;
+      end = (long long)(c + 1) * TP / G;
+    } else if (mode == 0) {
       x = (long long)c * T / G;
       end = (long long)(c + 1) * T / G;
     } else {
@@ -48,6 +57,15 @@ struct UnitIter {
       u.kb1 = KB;
       u.slot = 0;
       x += G;
+      return true;
+    }
+    if (np > 0) {
+      const int q = (int)(x % np);
+      u.tile = (int)(x / np);
+      u.kb0 = q * KB / np;
+      u.kb1 = (q + 1) * KB / np;
+      u.slot = q;
+      x += 1;
       return true;
     }
     const int tile = (int)(x / KB);
@@ -289,7 +307,7 @@ __global__ void __launch_bounds__(192)
         tma_load_2d(sB + st * C::B_BYTES, &tmB, &full[st], kb * 64, chunk * rows_c, pol_x);
         if (p.half) tma_load_2d(sB + st * C::B_BYTES + p.half * 128, &tmB2, &full[st], kb * 64, chunk * rows_c, pol_x);
       };
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode, p.np);
       Unit u;
       while (it.next(u)) {
         const int ntile = tile_ntile(p, u.tile, nch), chunk = tile_chunk(p, u.tile, nch);
@@ -320,7 +338,7 @@ __global__ void __launch_bounds__(192)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode);
+      UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode, p.np);
       Unit u;
       bool first = true;
       while (it.next(u)) {
@@ -357,7 +375,7 @@ __global__ void __launch_bounds__(192)
     const int et = threadIdx.x - 64;
     int acc = 0;
     uint32_t aphase = 0;
-    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode);
+    UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles_eff, p.mode, p.np);
     Unit u;
     while (it.next(u)) {
       const int ntile = tile_ntile(p, u.tile, nch), chunk = tile_chunk(p, u.tile, nch);

@@ -30,7 +30,8 @@ struct SplitK {
   int BN;        // rows per chunk
   const unsigned char* ns_tab;  // optional [n_tiles] precomputed piece counts
   const int* rows_dyn;          // compacting sessions: device scalar of rows in use; the GEMM
-                                // splits only ceil(rows/BN) chunks (T follows; ns_tab unused)
+                                // computes only ceil(rows/BN) chunks
+  int np;                       // > 0: fixed pieces per tile (compacting sessions; ns = np)
 };
 
 // owner CTA of flattened k-block y (largest c with floor(c*T/G) <= y)
@@ -39,18 +40,13 @@ __host__ __device__ inline int sk_owner(long long y, long long T, int G) {
 }
 __host__ __device__ inline int sk_nslots(const SplitK& s, int row, int n) {
   if (s.T == 0) return 1;
+  if (s.np > 0) return s.np;
   const long long tile = (long long)(row / s.BN) * s.n_ntiles + (n >> 7);
-  long long T = s.T;
 #ifdef __CUDA_ARCH__
-  if (s.rows_dyn != nullptr) {
-    const int nch = min(s.n_chunks, (*s.rows_dyn + s.BN - 1) / s.BN);
-    T = (long long)s.n_ntiles * nch * s.KB;
-  } else if (s.ns_tab != nullptr) {
-    return s.ns_tab[tile];
-  }
+  if (s.ns_tab != nullptr) return s.ns_tab[tile];
 #endif
   const long long first = tile * s.KB, last = first + s.KB - 1;
-  return sk_owner(last, T, s.G) - sk_owner(first, T, s.G) + 1;
+  return sk_owner(last, s.T, s.G) - sk_owner(first, s.T, s.G) + 1;
 }
 
 // Sum of the partial planes for output element (row, n).
@@ -80,7 +76,8 @@ struct GemmTcParams {
   int half;
   int rows_alloc;
   const int* rows_valid;  // device scalar or nullptr
-  const int* rows_dyn;    // compacting sessions: rows in use (device scalar); only those chunks are split
+  const int* rows_dyn;    // compacting sessions: rows in use (device scalar); only those chunks are computed
+  int np;                 // mode 0: > 0 = fixed pieces per tile (see UnitIter)
   const int* skip;        // device scalar or nullptr: nonzero => no-op
   // mode 0
   float* part;
