@@ -156,10 +156,12 @@ static Dims make_dims(const bb_model_desc* m) {
 static size_t esz(const Dims& D) { return D.dtype == BB_DTYPE_BF16 ? 2 : 4; }
 
 // Fixed k-pieces per weight tile for a compacting session's block-pass GEMMs:
-// enough pieces that one row chunk alone still feeds ~2 units per CTA.
-static int fixed_np(int ntiles, int G, int KB) {
-  int np = (2 * G + ntiles - 1) / ntiles;
-  np = np < 1 ? 1 : (np > 8 ? 8 : np);
+// ~2 units per CTA when every row chunk is live (tiles = weight tiles x
+// chunks), at least 2 so a batch's tail (one live chunk) still spreads, at
+// most 8 (the consumers sum that many planes per element).
+static int fixed_np(int tiles, int G, int KB) {
+  int np = (2 * G + tiles - 1) / tiles;
+  np = np < 2 ? 2 : (np > 8 ? 8 : np);
   return np > KB ? KB : np;
 }
 
@@ -240,11 +242,12 @@ static void plan(Session* s, char* base, bool dry) {
     }
     P.apart = c.take<float>(R * max_items * (long long)item_rows * D.nh * (D.hd + 2));
     P.row_rope = (!full && D.arch == BB_ARCH_LLADA) ? c.take<float>((long long)rows_alloc * D.hd) : nullptr;
-    // the M = 128 tcgen05 attention (bf16, hd 128, 16-row pages; passes whose rows per request
-    // exceed one 64-row tile: full passes, C5-size windows) reads 128-row key tiles; block passes
-    // of <= 64 rows per request keep the 64-row kernel (two CTAs per SM, no half-empty tiles)
+    // the M = 128 tcgen05 attention (bf16, hd 128, 16-row pages) reads 128-row key tiles: block
+    // passes with > 64 rows per request (C5 windows: 120) and long full passes (L >= 1024; C5
+    // 484 vs 633 us per launch); short full passes and <= 64-row windows keep the 64-row kernel
+    // (two CTAs per SM, no half-empty tiles; C2 full pass 14.9 vs 26.3 us)
     P.kz_shift = (D.dtype == BB_DTYPE_BF16 && !D.split && D.hd == 128 && S.ps == 16 && !(s->tflags & 7) &&
-                  (full || item_rows > 64)) ? 7 : 6;
+                  (full ? S.L >= 1024 : item_rows > 64)) ? 7 : 6;
     P.n_kz = full ? 1 : (item_rows + (1 << P.kz_shift) - 1) >> P.kz_shift;
     P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries
     P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
@@ -298,7 +301,7 @@ static void plan(Session* s, char* base, bool dry) {
         const int G = (int)(T_all < s->n_sms ? T_all : s->n_sms);
         int ms = 1;
         if (which == 0 && S.compact) {
-          ms = fixed_np(ntiles, G, KB);  // fixed pieces per tile
+          ms = fixed_np(ntiles * nch_all, G, KB);  // fixed pieces per tile
         } else {
           for (long long t = 0; t < (long long)ntiles * nch_all; ++t) {
             const int ns = sk_owner(t * KB + KB - 1, T_all, G) - sk_owner(t * KB, T_all, G) + 1;
@@ -392,7 +395,7 @@ static int setup_gemms(Session* s) {
           if (which == 0 && s->S.compact) {
             // batched: fixed k-pieces per tile (sums independent of how many requests are
             // live) and only the live requests' row chunks (test flag 256: all chunks)
-            p.np = all[g]->sk.np = fixed_np(p.n_ntiles, all[g]->grid, p.KB);
+            p.np = all[g]->sk.np = fixed_np(p.n_ntiles * p.n_chunks, all[g]->grid, p.KB);
             if (!(s->tflags & 256)) p.rows_valid = p.rows_dyn = s->blk.rows_live;
           }
         }
