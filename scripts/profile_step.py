@@ -13,7 +13,8 @@ _CFG = {"c2": (64, 256, (8, 16, 32)), "c5": (2048, 1024, (8, 16, 32, 64))}[os.en
 P, G = _CFG[0], _CFG[1]
 vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
 cfg = bb.SchedulerConfig(block_sizes=_CFG[2], gen_len=G)
-params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=HS, gamma=GAMMA, dtype="bf16", init="hash")
+params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=HS, gamma=GAMMA, dtype=os.environ.get("BB_DTYPE", "bf16x2"),
+                         init="hash")
 task = bb.make_task(2, P, G, vocab)
 s = get_session(params, cfg, P, 1)
 s.set_inputs(task.prompt[None], task.target[None])
