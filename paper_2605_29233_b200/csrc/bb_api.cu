@@ -246,7 +246,7 @@ static void plan(Session* s, char* base, bool dry) {
     // passes with > 64 rows per request (C5 windows: 120) and long full passes (L >= 1024; C5
     // 484 vs 633 us per launch); short full passes and <= 64-row windows keep the 64-row kernel
     // (two CTAs per SM, no half-empty tiles; C2 full pass 14.9 vs 26.3 us)
-    P.kz_shift = (D.dtype == BB_DTYPE_BF16 && !D.split && D.hd == 128 && S.ps == 16 && !(s->tflags & 7) &&
+    P.kz_shift = (D.dtype == BB_DTYPE_BF16 && D.hd == 128 && S.ps == 16 && !(s->tflags & 7) &&
                   (full ? S.L >= 1024 : item_rows > 64)) ? 7 : 6;
     P.n_kz = full ? 1 : (item_rows + (1 << P.kz_shift) - 1) >> P.kz_shift;
     P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries

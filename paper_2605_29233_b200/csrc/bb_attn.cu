@@ -1730,14 +1730,18 @@ static cudaError_t attn_fa_launch(const Dims& D, const Sess& S, const Pass& P, c
 // owns one whole row -- no lane pairs, no shuffles), half the MMA
 // instructions per row of the M=64 kernel, and a key tile's K/V pages read
 // once for up to 128 rows (every branch window of a C2 / C5 block pass).
-//   smem: q 32 KB | NS x (K 16 KB + V 16 KB) | P hi 16 KB + lo 16 KB
+//   smem: q 32 KB | NS x (K 16 KB + V 16 KB) | NPB x P (hi 16 KB + lo 16 KB)
 //   TMEM: S0, S1 (64 columns each), O (128 columns)
+// SPLIT (bf16x2): q / K / V hi + lo planes (the products of k_attn_fa's SPLIT
+// instance), fp32 cluster merge, hi + lo output; q 64 KB + 2 x 64 KB stages +
+// one P buffer = the whole opt-in shared memory.
 constexpr int AF8_QR = 128;
 constexpr uint32_t AF8_SUB = 128 * 128;  // one [128 rows][64 bf16] SW128 sub-tile (bytes)
 
-template <int CS, int NS>
+template <int CS, int NS, bool SPLIT>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
-    k_attn_fa128(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Dims D, Sess S,
+    k_attn_fa128(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                 const __grid_constant__ CUtensorMap tmKl, const __grid_constant__ CUtensorMap tmVl, Dims D, Sess S,
                  Pass P, DevState st, int layer, int rows_per_req) {
   klog_mark(D.klog, D.klog_cap, 24);
   if (P.pf_base != nullptr && threadIdx.x == 0) {
@@ -1753,17 +1757,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   }
   using bf = __nv_bfloat16;
   constexpr int HD = ATC_HD, QR = AF8_QR, KC = ATC_KC;
-  constexpr uint32_t STAGE = 4 * ATC_SUB;  // K (2 x [64 keys][64 dims]) + V (2 x [64 keys][64 dims])
+  constexpr int NP = SPLIT ? 2 : 1;              // hi (+ lo) planes
+  constexpr int NPB = SPLIT ? 1 : 2;             // P buffers
+  constexpr uint32_t STAGE = NP * 4 * ATC_SUB;   // [K hi 2 sub, V hi 2 sub (, K lo 2, V lo 2)], sub = [64 keys][64 dims]
   extern __shared__ __align__(1024) uint8_t smraw_f8[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw_f8) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                 // 2 sub-tiles [128 rows][64 dims]
-  uint8_t* sKV = sQ + 2 * AF8_SUB;  // [NS] stages
-  uint8_t* sPh = sKV + NS * STAGE;  // [128 rows][64 keys] K-major
-  uint8_t* sPl = sPh + AF8_SUB;
+  uint8_t* sQ = sm;                      // [plane][2 sub-tiles [128 rows][64 dims]]
+  uint8_t* sKV = sQ + NP * 2 * AF8_SUB;  // [NS] stages
+  uint8_t* sP = sKV + NS * STAGE;   // [2 buffers][hi, lo][128 rows][64 keys] K-major
   __shared__ int sRow[QR], sBr[QR];
   __shared__ uint32_t sVis[NS][32][2];  // [slot][branch][key word]
   __shared__ int s_nk;
-  __shared__ __align__(8) uint64_t kfull[NS], kempty[NS], sfull[2], sfree[2], pfull, pvdone, qready;
+  // P is double-buffered (chunk c in buffer c & 1, hand-offs on pfull / pvdone[c & 1]): the
+  // softmax of chunk ci waits only for P(ci-2).V (long done) -- or P(ci-1).V when O must be rescaled
+  __shared__ __align__(8) uint64_t kfull[NS], kempty[NS], sfull[2], sfree[2], pfull[2], pvdone[2], qready;
   __shared__ uint32_t s_tmem;
 
   namespace cg = cooperative_groups;
@@ -1785,14 +1792,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
       mbar_init(&sfull[i], 1);
       mbar_init(&sfree[i], 4);
     }
-    mbar_init(&pfull, 4);
-    mbar_init(&pvdone, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&pfull[i], 4);
+      mbar_init(&pvdone[i], 1);
+    }
     mbar_init(&qready, 128);
     fence_mbar_init();
   }
   if (warp == 4 && lane == 0) {
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
+    if (SPLIT) {
+      tma_prefetch_desc(&tmKl);
+      tma_prefetch_desc(&tmVl);
+    }
   }
   if (warp == 5) tmem_alloc(&s_tmem, 256);  // S0, S1: 64 columns each; O: 128 columns
   pdl_enter();
@@ -1867,6 +1880,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
           for (int sub = 0; sub < 2; ++sub) {
             tma_load_2d(dst + sub * ATC_SUB + g * 2048, &tmK, &kfull[slot], sub * 64, row, pol);
             tma_load_2d(dst + (2 + sub) * ATC_SUB + g * 2048, &tmV, &kfull[slot], sub * 64, row, pol);
+            if (SPLIT) {
+              tma_load_2d(dst + (4 + sub) * ATC_SUB + g * 2048, &tmKl, &kfull[slot], sub * 64, row, pol);
+              tma_load_2d(dst + (6 + sub) * ATC_SUB + g * 2048, &tmVl, &kfull[slot], sub * 64, row, pol);
+            }
           }
         }
       }
@@ -1881,7 +1898,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
       constexpr uint32_t IDO = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
       mbar_wait(&qready, 0);
       tc_fence_after();
-      const uint32_t q0 = smem_u32(sQ), pa = smem_u32(sPh), pl = smem_u32(sPl);
+      const uint32_t q0 = smem_u32(sQ);
       for (int ci = 0; ci <= n_chunks; ++ci) {
         if (ci < n_chunks) {
           const int slot = ci % NS, sb = ci & 1;
@@ -1895,21 +1912,36 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
             tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(q0 + (ks >> 2) * AF8_SUB + ko),
                         sdesc_sw128(k0 + (ks >> 2) * ATC_SUB + ko), IDS, ks > 0 ? 1u : 0u);
           }
+          if (SPLIT) {  // + Qh.Kl + Ql.Kh
+            const uint32_t ql = q0 + 2 * AF8_SUB, kl = k0 + 4 * ATC_SUB;
+#pragma unroll
+            for (int ks = 0; ks < HD / 16; ++ks) {
+              const uint32_t ko = (ks & 3) * 32;
+              tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(q0 + (ks >> 2) * AF8_SUB + ko),
+                          sdesc_sw128(kl + (ks >> 2) * ATC_SUB + ko), IDS, 1u);
+              tc_mma_bf16(tS0 + 64 * sb, sdesc_sw128(ql + (ks >> 2) * AF8_SUB + ko),
+                          sdesc_sw128(k0 + (ks >> 2) * ATC_SUB + ko), IDS, 1u);
+            }
+          }
           tc_commit(&sfull[sb]);
         }
         if (ci >= 1) {
-          const int pc = ci - 1, pslot = pc % NS;
-          mbar_wait(&pfull, pc & 1);
+          const int pc = ci - 1, pslot = pc % NS, pb = pc % NPB;
+          mbar_wait(&pfull[pb], (pc / NPB) & 1);
           tc_fence_after();
           const uint32_t v0 = smem_u32(sKV + pslot * STAGE + 2 * ATC_SUB);
+          const uint32_t pa = smem_u32(sP + pb * 2 * AF8_SUB), pl = pa + AF8_SUB;
 #pragma unroll
           for (int kk = 0; kk < KC / 16; ++kk) {
             const uint64_t bd = sdesc_sw128_mn(v0 + kk * 2048, ATC_SUB, 1024);
             tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), bd, IDO, (pc > 0 || kk > 0) ? 1u : 0u);
             tc_mma_bf16(tO, sdesc_sw128(pl + kk * 32), bd, IDO, 1u);
+            if (SPLIT)  // + Ph.Vl
+              tc_mma_bf16(tO, sdesc_sw128(pa + kk * 32), sdesc_sw128_mn(v0 + 4 * ATC_SUB + kk * 2048, ATC_SUB, 1024),
+                          IDO, 1u);
           }
           tc_commit(&kempty[pslot]);
-          tc_commit(&pvdone);
+          tc_commit(&pvdone[pb]);
         }
       }
     }
@@ -1924,6 +1956,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
         const int slot = sRow[rr];
         const long long qo = (long long)(slot >= 0 ? slot : 0) * D.attn_dim + h * HD + v * 8;
         cp_async16(sQ + (v >> 3) * AF8_SUB + sw128_off(rr, v & 7), Qg + qo, slot >= 0);
+        if (SPLIT)
+          cp_async16(sQ + 2 * AF8_SUB + (v >> 3) * AF8_SUB + sw128_off(rr, v & 7),
+                     reinterpret_cast<const bf*>(P.q_lo) + qo, slot >= 0);
       }
       cp_async_commit();
       cp_async_wait<0>();
@@ -1979,12 +2014,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
         }
         l_part += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       }
-      // P(ci-1).V done: the P tile is free and O is stable
-      if (ci > 0) {
-        mbar_wait(&pvdone, (ci - 1) & 1);
-        tc_fence_after();
+      // P buffer free (two buffers: P(ci-2).V done; one: P(ci-1).V done); a rescale also
+      // needs O stable: P(ci-1).V done
+      const int pb = ci % NPB;
+      const bool rescale = ci > 0 && __any_sync(0xffffffffu, grow && m_old != -INFINITY);
+      if (NPB == 2) {
+        if (ci >= 2) mbar_wait(&pvdone[pb], ((ci - 2) >> 1) & 1);
+        if (rescale) mbar_wait(&pvdone[pb ^ 1], ((ci - 1) >> 1) & 1);
+      } else if (ci >= 1) {
+        mbar_wait(&pvdone[0], (ci - 1) & 1);
       }
-      if (ci > 0 && __any_sync(0xffffffffu, grow && m_old != -INFINITY)) {
+      if (ci >= 1) tc_fence_after();
+      if (rescale) {
         float o[32];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -2000,21 +2041,22 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
 #pragma unroll
         for (int e = 0; e < 4; ++e) split_bf2(s[8 * c8 + 2 * e], s[8 * c8 + 2 * e + 1], hi[e], lo[e]);
         const uint32_t off = sw128_off(rl, c8);
-        *reinterpret_cast<uint4*>(sPh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(sPl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        *reinterpret_cast<uint4*>(sP + pb * 2 * AF8_SUB + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(sP + (pb * 2 + 1) * AF8_SUB + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull);
+      if (lane == 0) mbar_arrive(&pfull[pb]);
     }
-    if (n_chunks > 0) {
-      mbar_wait(&pvdone, (n_chunks - 1) & 1);
+    if (n_chunks > 0) {  // the last P.V (its commit also covers every earlier one)
+      mbar_wait(&pvdone[(n_chunks - 1) % NPB], ((n_chunks - 1) / NPB) & 1);
       tc_fence_after();
     }
-    // partial state (m_ref, l, o / l) of my row -> fp16 staging in the idle KV ring
+    // partial state (m_ref, l, o / l) of my row -> fp16 (SPLIT: fp32) staging in the idle KV ring
     constexpr int OLD = HD + 8;
-    __half* sO = reinterpret_cast<__half*>(sKV);
+    using ST = typename std::conditional<SPLIT, float, __half>::type;
+    ST* sO = reinterpret_cast<ST*>(sKV);
     const float il = l_part > 0.0f ? 1.0f / l_part : 0.0f;
     float o[32];
 #pragma unroll
@@ -2026,8 +2068,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
         for (int c = 0; c < 32; ++c) o[c] = 0.0f;
       }
 #pragma unroll
-      for (int c = 0; c < 32; c += 2)
-        *reinterpret_cast<__half2*>(sO + rl * OLD + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+      for (int c = 0; c < 32; c += 2) {
+        if constexpr (SPLIT)
+          *reinterpret_cast<float2*>(sO + rl * OLD + 32 * q + c) = make_float2(o[c] * il, o[c + 1] * il);
+        else
+          *reinterpret_cast<__half2*>(sO + rl * OLD + 32 * q + c) = __floats2half2_rn(o[c] * il, o[c + 1] * il);
+      }
     }
     *reinterpret_cast<float2*>(sO + rl * OLD + HD) = make_float2(m_ref, l_part);
   }
@@ -2036,7 +2082,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   if (threadIdx.x < 128) {
     // merge rows [crank*RPC, (crank+1)*RPC) over the cluster (pull; fixed rank order)
     constexpr int OLD = HD + 8;
-    const __half* sO = reinterpret_cast<const __half*>(sKV);
+    using ST = typename std::conditional<SPLIT, float, __half>::type;
+    const ST* sO = reinterpret_cast<const ST*>(sKV);
     constexpr int RPC = QR / CS, V4 = HD / 4, NMI = (RPC * V4 + 127) / 128;
 #pragma unroll
     for (int k = 0; k < NMI; ++k) {
@@ -2049,14 +2096,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
       float4 ov[CS];
 #pragma unroll
       for (int q = 0; q < CS; ++q) {
-        const __half* row = cluster.map_shared_rank(sO + lr * OLD, q);
+        const ST* row = cluster.map_shared_rank(sO + lr * OLD, q);
         const float2 ml = *reinterpret_cast<const float2*>(row + HD);
         mr[q] = ml.x;
         lv[q] = ml.y;
-        const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
-        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
-        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
-        ov[q] = make_float4(a.x, a.y, b.x, b.y);
+        if constexpr (SPLIT) {
+          ov[q] = *reinterpret_cast<const float4*>(row + c4);
+        } else {
+          const uint2 u = *reinterpret_cast<const uint2*>(row + c4);
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+          ov[q] = make_float4(a.x, a.y, b.x, b.y);
+        }
       }
       float M = -INFINITY;
 #pragma unroll
@@ -2074,11 +2125,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
         acc.w += w * ov[q].w;
       }
       const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
-      __nv_bfloat162 p0 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), p1 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+      const long long oo = (long long)slot * D.attn_dim + h * HD + c4;
+      const float4 y = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(y.x, y.y), p1 = __floats2bfloat162_rn(y.z, y.w);
       uint2 u;
       u.x = *reinterpret_cast<uint32_t*>(&p0);
       u.y = *reinterpret_cast<uint32_t*>(&p1);
-      *reinterpret_cast<uint2*>(reinterpret_cast<bf*>(P.attn) + (long long)slot * D.attn_dim + h * HD + c4) = u;
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf*>(P.attn) + oo) = u;
+      if (SPLIT) {  // lo = rn(y - hi)
+        const float2 f0 = __bfloat1622float2(p0), f1 = __bfloat1622float2(p1);
+        __nv_bfloat162 l0 = __floats2bfloat162_rn(y.x - f0.x, y.y - f0.y), l1 = __floats2bfloat162_rn(y.z - f1.x, y.w - f1.y);
+        u.x = *reinterpret_cast<uint32_t*>(&l0);
+        u.y = *reinterpret_cast<uint32_t*>(&l1);
+        *reinterpret_cast<uint2*>(reinterpret_cast<bf*>(P.attn_lo) + oo) = u;
+      }
     }
   }
   cluster.sync();
@@ -2089,60 +2149,63 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(AFA_THREADS)
   tstat_end(ats);
 }
 
-template <int NS>
+template <int NS, bool SPLIT>
 constexpr size_t attn_f8_smem() {
-  return 1024 + (size_t)4 * AF8_SUB + (size_t)NS * 4 * ATC_SUB;  // q 32 KB + P 32 KB + KV ring
+  // q (hi (+ lo)) + P buffers (2 plain, 1 SPLIT; hi + lo each) + the KV ring
+  return 1024 + (size_t)(SPLIT ? 4 + 2 : 2 + 4) * AF8_SUB + (size_t)NS * (SPLIT ? 8 : 4) * ATC_SUB;
 }
 
-template <int CS, int NS>
+template <int CS, int NS, bool SPLIT>
 static long long f8_slots() {
   static long long v = -1;
   if (v < 0) {
-    constexpr size_t smem = attn_f8_smem<NS>();
-    cudaFuncSetAttribute(k_attn_fa128<CS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    constexpr size_t smem = attn_f8_smem<NS, SPLIT>();
+    cudaFuncSetAttribute(k_attn_fa128<CS, NS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CS * 64);
     cfg.blockDim = dim3(AFA_THREADS);
     cfg.dynamicSmemBytes = smem;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void*)k_attn_fa128<CS, NS>, &cfg) != cudaSuccess || n <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)k_attn_fa128<CS, NS, SPLIT>, &cfg) != cudaSuccess || n <= 0) {
       cudaGetLastError();
       n = 148 / CS;
     }
     v = (long long)n * CS;
-    if (getenv("BB_DEBUG")) fprintf(stderr, "[bb200] k_attn_fa128<%d,%d>: %d resident clusters\n", CS, NS, n);
+    if (getenv("BB_DEBUG"))
+      fprintf(stderr, "[bb200] k_attn_fa128<%d,%d,%d>: %d resident clusters\n", CS, NS, (int)SPLIT, n);
   }
   return v;
 }
 
-template <int CS, int NS>
+template <int CS, int NS, bool SPLIT>
 static cudaError_t attn_f8_launch(const Dims& D, const Sess& S, const Pass& P, const DevState& st,
                                   const AttnMaps& am, int layer, cudaStream_t s) {
   const int rows = P.full ? S.L : S.NRq;
-  constexpr size_t smem = attn_f8_smem<NS>();
-  static_assert(smem <= 227 * 1024, "k_attn_fa128 shared memory");
+  constexpr size_t smem = attn_f8_smem<NS, SPLIT>();
+  static_assert(smem + 2048 <= 232448, "k_attn_fa128 shared memory (dynamic + static)");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_fa128<CS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_attn_fa128<CS, NS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   dim3 grid(S.R * CS, D.nh, (rows + AF8_QR - 1) / AF8_QR);
-  launch_k(k_attn_fa128<CS, NS>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, D, S, P, st, layer, rows);
+  launch_k(k_attn_fa128<CS, NS, SPLIT>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, am.kl, am.vl, D, S, P, st,
+           layer, rows);
   return cudaGetLastError();
 }
 
 #ifndef ATT_F8_NS
-#define ATT_F8_NS 3  // KV ring stages of k_attn_fa128 (one CTA per SM)
+#define ATT_F8_NS 3  // KV ring stages of k_attn_fa128 (one CTA per SM); the SPLIT instance has 2
 #endif
-template <int NS>
+template <int NS, bool SPLIT>
 static int att_cs_f8(const Dims& D, const Sess& S, const Pass& P, int tflags) {
   const int forced = (tflags >> 4) & 15;
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   const int rows = P.full ? S.L : S.NRq;
   const long long per = (long long)S.R * D.nh * ((rows + AF8_QR - 1) / AF8_QR);
-  if (per * 8 <= 2 * f8_slots<8, NS>()) return 8;
-  if (per * 4 <= 2 * f8_slots<4, NS>()) return 4;
-  if (per * 2 <= 2 * f8_slots<2, NS>()) return 2;
+  if (per * 8 <= 2 * f8_slots<8, NS, SPLIT>()) return 8;
+  if (per * 4 <= 2 * f8_slots<4, NS, SPLIT>()) return 4;
+  if (per * 2 <= 2 * f8_slots<2, NS, SPLIT>()) return 2;
   return 1;
 }
 
@@ -2215,11 +2278,19 @@ static cudaError_t attn_seg_hd(const Dims& D, const Sess& S, const Pass& P, cons
     // (bf16), M = 64 (bf16x2, whose q / KV planes double the shared memory);
     // test flag bit 1 = k_attn_tc, bit 2 = the M = 64 kernel for bf16
     if (am.ok && !(tflags & 3) && P.kz_shift == 7) {
-      switch (att_cs_f8<ATT_F8_NS>(D, S, P, tflags)) {
-        case 8: return attn_f8_launch<8, ATT_F8_NS>(D, S, P, st, am, layer, s);
-        case 4: return attn_f8_launch<4, ATT_F8_NS>(D, S, P, st, am, layer, s);
-        case 2: return attn_f8_launch<2, ATT_F8_NS>(D, S, P, st, am, layer, s);
-        default: return attn_f8_launch<1, ATT_F8_NS>(D, S, P, st, am, layer, s);
+      if (D.split) {
+        switch (att_cs_f8<2, true>(D, S, P, tflags)) {
+          case 8: return attn_f8_launch<8, 2, true>(D, S, P, st, am, layer, s);
+          case 4: return attn_f8_launch<4, 2, true>(D, S, P, st, am, layer, s);
+          case 2: return attn_f8_launch<2, 2, true>(D, S, P, st, am, layer, s);
+          default: return attn_f8_launch<1, 2, true>(D, S, P, st, am, layer, s);
+        }
+      }
+      switch (att_cs_f8<ATT_F8_NS, false>(D, S, P, tflags)) {
+        case 8: return attn_f8_launch<8, ATT_F8_NS, false>(D, S, P, st, am, layer, s);
+        case 4: return attn_f8_launch<4, ATT_F8_NS, false>(D, S, P, st, am, layer, s);
+        case 2: return attn_f8_launch<2, ATT_F8_NS, false>(D, S, P, st, am, layer, s);
+        default: return attn_f8_launch<1, ATT_F8_NS, false>(D, S, P, st, am, layer, s);
       }
     }
     if (am.ok && !(tflags & 3)) {
@@ -2352,9 +2423,12 @@ static cudaError_t attn_hd(const Dims& D, const Sess& S, const Pass& P, const De
 // Occupancy queries of the k_attn_fa instances (cluster residency), run at
 // session creation: they are not allowed inside a stream capture.
 void attn_prepare() {
-  f8_slots<8, ATT_F8_NS>();
-  f8_slots<4, ATT_F8_NS>();
-  f8_slots<2, ATT_F8_NS>();
+  f8_slots<8, ATT_F8_NS, false>();
+  f8_slots<4, ATT_F8_NS, false>();
+  f8_slots<2, ATT_F8_NS, false>();
+  f8_slots<8, 2, true>();
+  f8_slots<4, 2, true>();
+  f8_slots<2, 2, true>();
   fa_slots<8, ATT_FA_NS, false>();
   fa_slots<4, ATT_FA_NS, false>();
   fa_slots<2, ATT_FA_NS, false>();

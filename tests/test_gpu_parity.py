@@ -312,19 +312,23 @@ def test_block_step_hd128_attention_matches_oracle(tc, cs, kvh, gain, tol):
 @pytest.mark.parametrize("tc,cs,P,G,bs", [("fa", "", 600, 200, 3), ("fa", "1", 600, 200, 3), ("tc", "1", 600, 200, 3),
                                           ("fa", "2", 1000, 120, 3), ("fa64", "", 600, 200, 3),
                                           ("fa64", "1", 1000, 120, 3), ("fa", "", 600, 200, 4), ("fa", "1", 600, 200, 4),
-                                          ("fa", "8", 1000, 120, 4), ("fa64", "", 600, 200, 4)])
+                                          ("fa", "8", 1000, 120, 4), ("fa64", "", 600, 200, 4),
+                                          ("x2", "", 1000, 120, 4), ("x2", "1", 600, 200, 4), ("x2", "", 600, 200, 3)])
 def test_block_step_long_context_attention_matches_oracle(tc, cs, P, G, bs):
     """Long rows through the hd-128 tensor-core attentions: a 600-token
     prompt (its last page is partly filled: padded key-list segment) and
     ~800 keys per row, i.e. a dozen 64-key chunks per CTA (the KV ring wraps
     several times; lazy O rescale across chunks), vs the oracle.  bs=4:
     branches {8,16,32,64} (120 window rows, the C5 layout: the block pass
-    runs the 128-row-tile kernel, one key tile for all four branches)."""
-    flags = {"fa": 0, "tc": 2, "fa64": 4}[tc] | ((int(cs) if cs else 0) << 4)
+    runs the 128-row-tile kernel, one key tile for all four branches).  x2:
+    the bf16x2 numerics (SPLIT attention instances; spike gain 33) held to the
+    north-star bar against the oracle without activation rounding."""
+    flags = {"fa": 0, "tc": 2, "fa64": 4, "x2": 0}[tc] | ((int(cs) if cs else 0) << 4)
     g = LLADA["llada_tiny_bf16"]
     bsz = [8, 16, 32] if bs == 3 else [8, 16, 32, 64]
     g = dict(g, prompt_len=P, gen_len=G, config=dict(g["config"], gen_len=G, block_sizes=bsz), seeds=g["seeds"][:2])
-    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=1, head_dim=128, max_len=P + G), "bf16", 0.0, 2e-2,
+    dtype, gain = ("bf16x2", 33.0) if tc == "x2" else ("bf16", 0.0)
+    _block_step_vs_oracle(g, dict(n_heads=2, n_kv_heads=1, head_dim=128, max_len=P + G), dtype, gain, 2e-2,
                           f"long hd128 {tc} cs={cs or 'auto'} L={P + G} B={len(bsz)}", test_flags=flags)
 
 
