@@ -109,7 +109,9 @@ typedef struct {
 #define BB_VIEW_HEAD_ARG 14 /* int32 [NR]          argmax (lowest id)        */
 #define BB_VIEW_SLOT_POS 15 /* int32 [NR]          position of the slot      */
 #define BB_VIEW_SLOT_BR 16 /* int32 [NR]           branch of the slot        */
-#define BB_VIEW_COUNT 17
+#define BB_VIEW_INIT_GEN 17 /* int32 [R][G]        initial generation row (input): token or -1 =
+                               mask (single_branch_decode preset, decoding.py:194-212) */
+#define BB_VIEW_COUNT 18
 
 BB_API int bb_session_workspace_bytes(const void* model, const bb_session_desc* d, size_t* bytes);
 BB_API int bb_session_create(void* model, const bb_session_desc* d, void* workspace, size_t bytes, void** sess);

@@ -54,6 +54,7 @@ DTYPE_F32, DTYPE_BF16, DTYPE_BF16X2 = 0, 1, 2
 VIEW_TOKENS, VIEW_TARGET, VIEW_PROMPT, VIEW_CTRL, VIEW_BRANCH, VIEW_EVENTS = 0, 1, 2, 3, 4, 5
 VIEW_COVERED, VIEW_PM_M, VIEW_PM_S, VIEW_PAGES, VIEW_REFC = 6, 7, 8, 9, 10
 VIEW_HEAD_MASKED, VIEW_HEAD_M, VIEW_HEAD_S, VIEW_HEAD_ARG, VIEW_SLOT_POS, VIEW_SLOT_BR = 11, 12, 13, 14, 15, 16
+VIEW_INIT_GEN = 17
 # per-request control words (csrc/bb_state.cuh: enum Ctrl)
 (C_STATUS, C_WINNER, C_EOS, C_ITER, C_SINCE_REFRESH, C_NFE0, C_NFE1, C_NFE2, C_NEV, C_REFRESH_DUE,
  C_EV_OVERFLOW, C_ACTIVE_MASK, C_REFRESH_MASK, C_NCOPY, C_NPMCOPY, C_MERGES, C_SYNCS, C_COMMITS,

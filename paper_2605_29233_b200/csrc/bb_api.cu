@@ -183,6 +183,8 @@ static void plan(Session* s, char* base, bool dry) {
   view(BB_VIEW_TARGET, st.target, R * S.G * 4);
   st.prompt = c.take<int>(R * S.P);
   view(BB_VIEW_PROMPT, st.prompt, R * S.P * 4);
+  st.init_gen = c.take<int>(R * S.G);
+  view(BB_VIEW_INIT_GEN, st.init_gen, R * S.G * 4);
   st.ctrl = c.take<int>(R * C_WORDS);
   view(BB_VIEW_CTRL, st.ctrl, R * C_WORDS * 4);
   st.br = c.take<int>(R * B * B_WORDS);
@@ -246,8 +248,11 @@ static void plan(Session* s, char* base, bool dry) {
     // passes with > 64 rows per request (C5 windows: 120) and long full passes (L >= 1024; C5
     // 484 vs 633 us per launch); short full passes and <= 64-row windows keep the 64-row kernel
     // (two CTAs per SM, no half-empty tiles; C2 full pass 14.9 vs 26.3 us)
+#ifndef ATT_F8_MIN_ROWS
+#define ATT_F8_MIN_ROWS 64  // block passes with more rows per request use the 128-row attention
+#endif
     P.kz_shift = (D.dtype == BB_DTYPE_BF16 && D.hd == 128 && S.ps == 16 && !(s->tflags & 7) &&
-                  (full ? S.L >= 1024 : item_rows > 64)) ? 7 : 6;
+                  (full ? S.L >= 1024 : item_rows > ATT_F8_MIN_ROWS)) ? 7 : 6;
     P.n_kz = full ? 1 : (item_rows + (1 << P.kz_shift) - 1) >> P.kz_shift;
     P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries
     P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
@@ -840,6 +845,7 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   cudaMemcpy(s->full.slot_pos, neg.data(), s->full.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->H.masked, zero.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->full_rows, &s->S.NF, sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemset(s->st.init_gen, 0xFF, (size_t)s->S.R * s->S.G * 4);  // no presets: every position masked
   {
     std::vector<int> base(s->S.R);
     for (int r = 0; r < s->S.R; ++r) base[r] = r * s->S.NRq;

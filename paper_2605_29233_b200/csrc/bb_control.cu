@@ -336,8 +336,10 @@ __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk,
   RC_SETUP();
   const int r = c.r;
   const int* prompt = st.prompt + (long long)r * S.P;
+  const int* init_gen = st.init_gen + (long long)r * S.G;  // presets (decoding.py:194-200), -1 = mask
   for (int k = 0; k < S.B; ++k)
-    for (int i = threadIdx.x; i < S.L; i += blockDim.x) c.rows[k * S.L + i] = i < S.P ? prompt[i] : c.mask_id;
+    for (int i = threadIdx.x; i < S.L; i += blockDim.x)
+      c.rows[k * S.L + i] = i < S.P ? prompt[i] : (init_gen[i - S.P] >= 0 ? init_gen[i - S.P] : c.mask_id);
   if (threadIdx.x < C_WORDS) c.ctrl[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int k = 0; k < S.B; ++k) {
@@ -415,7 +417,7 @@ __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk,
     blk.slot_req[slot] = r;
     blk.slot_br[slot] = k < 0 ? 0 : k;
     blk.slot_pos[slot] = pos;
-    H.masked[slot] = pos >= 0 ? 1 : 0;
+    H.masked[slot] = (pos >= 0 && c.rows[pos] == c.mask_id) ? 1 : 0;  // preset positions are not queried
     if (pos >= 0) slot_boost(D, S, c.rows, target, pos, &H.boost[slot], &H.tgt[slot]);
     else {
       H.boost[slot] = 0.0f;

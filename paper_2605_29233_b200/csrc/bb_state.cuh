@@ -76,6 +76,7 @@ struct DevState {
   int* tokens;
   int* target;  // [R][G]
   int* prompt;  // [R][P]
+  int* init_gen;  // [R][G] initial generation row: token, or -1 = mask (presets)
   int* ctrl;
   int* br;
   uint8_t* covered;   // [R][B][L]

@@ -204,14 +204,23 @@ def single_branch_decode(params, task, cfg: DecodeConfig, preset=None):
     Runs on the device as a singleton BlockBatch session: with one branch,
     merge and sync disabled, the loops are identical (criterion 04,
     test_acceptance.py:164-180)."""
-    from .scheduler import SchedulerConfig, run_blockbatch
+    from .scheduler import SchedulerConfig, run_batch, run_blockbatch
     cfg.validate()
-    if preset:
-        raise ConfigError("preset commits are not supported on the device path")
-    return run_blockbatch(params, task, SchedulerConfig(block_sizes=(cfg.block_size,), tau_conf=cfg.tau_conf,
-                                                        refresh_interval=cfg.refresh_interval,
-                                                        gen_len=cfg.gen_len, merge_enabled=False,
-                                                        sync_enabled=False), _single=True)
+    scfg = SchedulerConfig(block_sizes=(cfg.block_size,), tau_conf=cfg.tau_conf,
+                           refresh_interval=cfg.refresh_interval, gen_len=cfg.gen_len, merge_enabled=False,
+                           sync_enabled=False)
+    if not preset:
+        return run_blockbatch(params, task, scfg, _single=True)
+    # apply_preset (decoding.py:194-200): committed tokens placed before the prefill
+    if cfg.gen_len != task.gen_len:
+        raise ConfigError("cfg.gen_len does not match the task")
+    P = task.prompt_len
+    init_gen = np.full((1, task.gen_len), -1, dtype=np.int64)
+    for pos, tok in preset:
+        if pos < P or pos >= P + task.gen_len:
+            raise ContractError(f"preset position {pos} outside the generation region")
+        init_gen[0, pos - P] = tok
+    return run_batch(params, [task], scfg, _single=True, _init_gen=init_gen)[0]
 
 
 def vanilla_decode(params, task, cfg: DecodeConfig):

@@ -68,6 +68,8 @@ class Session:
         self.v_tokens = self._view(_lib.VIEW_TOKENS, torch.int32, (self.R, self.B, self.Lseq))
         self.v_target = self._view(_lib.VIEW_TARGET, torch.int32, (self.R, self.G))
         self.v_prompt = self._view(_lib.VIEW_PROMPT, torch.int32, (self.R, self.P))
+        self.v_init_gen = self._view(_lib.VIEW_INIT_GEN, torch.int32, (self.R, self.G))
+        self._preset_dirty = False
         self.v_ctrl = self._view(_lib.VIEW_CTRL, torch.int32, (self.R, _lib.C_WORDS))
         self.v_branch = self._view(_lib.VIEW_BRANCH, torch.int32, (self.R, self.B, _lib.B_WORDS))
         self.v_events = self._view(_lib.VIEW_EVENTS, torch.int32, (self.R, self.ev_cap, _lib.EVW))
@@ -94,12 +96,21 @@ class Session:
             pass
 
     # ---------------------------------------------------------------- inputs
-    def set_inputs(self, prompts, targets):
+    def set_inputs(self, prompts, targets, init_gen=None):
         """prompts [R, P], targets [R, G]: host arrays (copied H2D on the session
-        stream) or CUDA tensors (copied D2D after the producing stream's work)."""
+        stream) or CUDA tensors (copied D2D after the producing stream's work).
+        init_gen [R, G] (optional): the initial generation row, token or -1 =
+        mask (single_branch_decode presets)."""
         torch = _torch()
         self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
+            if init_gen is not None or self._preset_dirty:
+                g = np.full((self.R, self.G), -1, dtype=np.int32) if init_gen is None else \
+                    np.ascontiguousarray(np.asarray(init_gen), dtype=np.int32)
+                t = torch.from_numpy(g).pin_memory()
+                self.v_init_gen.copy_(t, non_blocking=True)
+                self.h2d_bytes += t.numel() * 4
+                self._preset_dirty = init_gen is not None
             for dst, src in ((self.v_prompt, prompts), (self.v_target, targets)):
                 if isinstance(src, torch.Tensor) and src.is_cuda:
                     t = src if src.dtype == torch.int32 else src.to(torch.int32)

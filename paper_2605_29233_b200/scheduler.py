@@ -331,7 +331,7 @@ def _run_stepped(params: ModelParams, task: Task, cfg: SchedulerConfig, forward_
 
 
 def run_batch(params: ModelParams, tasks: list, cfg: SchedulerConfig, forward_hook=None, trace: bool = True,
-              use_graph: bool = True, _single: bool = False, _hard_cap: int = 0) -> list:
+              use_graph: bool = True, _single: bool = False, _hard_cap: int = 0, _init_gen=None) -> list:
     """Many independent requests (same P, G) in one device session: every
     iteration runs one forward over all live requests' branch windows;
     NFE, trace and termination stay per request.  With ``forward_hook`` the
@@ -342,7 +342,7 @@ def run_batch(params: ModelParams, tasks: list, cfg: SchedulerConfig, forward_ho
         s = Session(params, cfg, P, len(tasks), trace=trace or forward_hook is not None, hard_cap=_hard_cap)
     else:
         s = get_session(params, cfg, P, len(tasks), trace=trace or forward_hook is not None)
-    s.set_inputs(np.stack([t.prompt for t in tasks]), np.stack([t.target for t in tasks]))
+    s.set_inputs(np.stack([t.prompt for t in tasks]), np.stack([t.target for t in tasks]), init_gen=_init_gen)
     if forward_hook is None:
         s.launch(use_graph=use_graph)
     else:

@@ -26,6 +26,9 @@ Outputs (all under tests/golden/):
                     summary_row / write_summary) of every runs_ref.json run of
                     the c1_hs2 and default_g4_eos configs (rebuilt as reference
                     GenerationResults; --summary-only regenerates just this).
+  runs_preset.json  the reference's single_branch_decode with preset commits
+                    (decoding.py:194-212): target tokens, a wrong token and an
+                    eos placed before the prefill (--preset-only regenerates it).
   runs_runaway.json reference run_blockbatch with the hard cap lowered to 16
                     forwards (HARD_CAP_FACTOR = 0): forward_hook calls up to
                     the RunawayError (scheduler.py:310, 324-325).
@@ -347,6 +350,26 @@ def gen_runaway_runs():
     return {"hard_cap": 16, "prompt_len": 16, "gen_len": 128, "block_sizes": [8, 16, 32], "runs": runs}
 
 
+def gen_preset_runs():
+    """single_branch_decode(preset=...) on the default model: per seed a preset
+    of two target tokens, one wrong token and (odd seeds) an eos."""
+    params, vocab = ref_params({})
+    P, G = 16, 64
+    runs = []
+    for s in range(4):
+        task = bbm.make_task(s, P, G, vocab)
+        preset = [(P + 1, int(task.target[1])), (P + 5, int(task.target[5])),
+                  (P + 9, int((task.target[9] + 1) % vocab.size))]
+        if s % 2:
+            preset.append((P + 40, vocab.eos_id))
+        for b in (4, 16):
+            r = bbd.single_branch_decode(params, task, bbd.DecodeConfig(block_size=b, gen_len=G), preset=preset)
+            rec = result_record(r)
+            rec.update(seed=s, block=b, preset=preset)
+            runs.append(rec)
+    return {"prompt_len": P, "gen_len": G, "runs": runs}
+
+
 SUMMARY_CONFIGS = ("c1_hs2", "default_g4_eos")
 
 
@@ -370,6 +393,11 @@ def gen_summary_csv(path):
 
 def main():
     t0 = time.time()
+    if "--preset-only" in sys.argv:
+        with open(os.path.join(HERE, "runs_preset.json"), "w") as fh:
+            json.dump(gen_preset_runs(), fh, separators=(",", ":"))
+        print(f"done in {time.time() - t0:.1f}s")
+        return
     if "--summary-only" in sys.argv:
         gen_summary_csv(os.path.join(HERE, "summary_ref.csv"))
         print(f"done in {time.time() - t0:.1f}s")
@@ -394,6 +422,8 @@ def main():
         json.dump(gen_kernel_fixtures(), fh, separators=(",", ":"))
     np.savez_compressed(os.path.join(HERE, "forward_c1.npz"), **gen_forward_c1())
     gen_summary_csv(os.path.join(HERE, "summary_ref.csv"))
+    with open(os.path.join(HERE, "runs_preset.json"), "w") as fh:
+        json.dump(gen_preset_runs(), fh, separators=(",", ":"))
     print(f"done in {time.time() - t0:.1f}s")
 
 

@@ -188,6 +188,27 @@ def test_merge_sync_kernel_bit_exact_on_reference_fixtures():
             assert [int(x) for x in b.prob_covered] == w["covered"]
 
 
+PRESET = goldens.load("runs_preset.json")
+
+
+def test_single_branch_decode_with_preset_matches_reference():
+    """single_branch_decode(preset=...) (decoding.py:194-212): preset tokens
+    (target, wrong, eos) placed in the row before the prefill; tokens, NFE
+    and every trace record bit-exact vs the reference's own runs (fp32)."""
+    params = ref_model(REF["default_b4_128_g64"]["model"])
+    for want in PRESET["runs"]:
+        task = bb.make_task(want["seed"], PRESET["prompt_len"], PRESET["gen_len"], params.vocab)
+        preset = [tuple(p) for p in want["preset"]]
+        r = bb.single_branch_decode(params, task, bb.DecodeConfig(block_size=want["block"], gen_len=64), preset=preset)
+        assert [int(t) for t in r.row.tokens] == want["tokens"], (want["seed"], want["block"])
+        assert list(r.nfe.snapshot()) == want["nfe"]
+        assert r.tokens_decoded == want["tokens_decoded"]
+        assert goldens.diff_trace([e.to_record() for e in r.trace], want["trace"]) is None
+    task = bb.make_task(0, PRESET["prompt_len"], PRESET["gen_len"], params.vocab)
+    with pytest.raises(bb.ContractError):  # decoding.py:198-199
+        bb.single_branch_decode(params, task, bb.DecodeConfig(block_size=4, gen_len=64), preset=[(3, 1)])
+
+
 def test_deterministic_reruns():
     g = REF["c1_hs2"]
     params = ref_model(g["model"])
