@@ -342,11 +342,13 @@ __global__ void k_prefill_init(Dims D, Sess S, DevState st, Pass full, Pass blk,
       c.rows[k * S.L + i] = i < S.P ? prompt[i] : (init_gen[i - S.P] >= 0 ? init_gen[i - S.P] : c.mask_id);
   if (threadIdx.x < C_WORDS) c.ctrl[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
+    int n_preset = 0;  // refresh_decoded counts them before the first forward (decoding.py:212-218)
+    for (int i = 0; i < S.G; ++i) n_preset += init_gen[i] >= 0;
     for (int k = 0; k < S.B; ++k) {
       c.B_(k, B_START) = S.P;
       c.B_(k, B_END) = min(S.P + S.bs[k], S.L);
       c.B_(k, B_DONE) = 0;
-      c.B_(k, B_DEC) = 0;
+      c.B_(k, B_DEC) = n_preset;
       c.B_(k, B_MERGED) = 0;
       c.B_(k, B_SIZE) = S.bs[k];
       c.B_(k, 6) = 0;

@@ -20,11 +20,12 @@ s = get_session(params, cfg, P, 1)
 s.set_inputs(task.prompt[None], task.target[None])
 s.prefill()
 use_graph = os.environ.get("BB_GRAPH", "0") == "1"
-for it in range(1, 6):
+N_SKIP = int(os.environ.get("BB_PROF_SKIP", 5))  # iterations run before the profiled window
+for it in range(1, N_SKIP + 1):
     s.iteration(it % cfg.refresh_interval == 0, use_graph)
 s.stream.synchronize()
 torch.cuda.profiler.start()
-for it in range(6, 6 + N_PROF):
+for it in range(N_SKIP + 1, N_SKIP + 1 + N_PROF):
     s.iteration(it % cfg.refresh_interval == 0, use_graph)
 s.stream.synchronize()
 torch.cuda.profiler.stop()
