@@ -86,7 +86,8 @@ typedef struct {
                           head_dim 128; bit 1 = the single-role tcgen05 attention (k_attn_tc)
                           instead of the warp-specialized one; bit 2 = the warp-specialized
                           attention on 64-row instead of 128-row tiles; bit 3 = no block-pass
-                          compaction in batched sessions; bits 4-7 = forced cluster size */
+                          compaction in batched sessions; bits 4-7 = forced cluster size;
+                          bit 10 = full-pass GEMMs always stream-K (no grouped whole tiles) */
   int logits;          /* 1: the LM head also keeps raw logits (bb_head_logits; forward observers) */
   int seam;            /* 1: step-operator seam session (bb_seam_*): private pages per branch */
   int hard_cap;        /* > 0: override the forward cap 4*G*B+16 (scheduler.py:310; tests) */

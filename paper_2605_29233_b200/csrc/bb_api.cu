@@ -334,6 +334,9 @@ static PartRef pref_tc(const TcGemm& g, const float* part) {
 
 // per-tile stream-K piece counts (avoids 64-bit divisions in consumers);
 // one table per distinct GEMM shape (all layers share them)
+#ifndef GEMM_RR_ROUNDS
+#define GEMM_RR_ROUNDS 12  // full-pass GEMMs with at least this many rounds of whole tiles run mode 2
+#endif
 static int attach_ns_table(Session* s, TcGemm& g) {
   const long long tiles = (long long)g.p.n_ntiles * g.p.n_chunks;
   for (auto& e : s->ns_shapes)
@@ -393,7 +396,12 @@ static int setup_gemms(Session* s) {
           p.klog = s->D.klog;
           p.klog_cap = s->D.klog_cap;
           p.klog_id = 100 + which * 8 + g;
-          if (attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
+          if (which == 1 && !(s->tflags & 1024)) {
+            // large full passes: whole tiles in L2-friendly groups (test flag 1024: stream-K)
+            const int kin = g == 1 ? D.attn_dim : (g == 3 ? D.dff : D.d);
+            tc_gemm_round_robin(*all[g], GEMM_RR_ROUNDS, kin * 2 * (P.xn_lo != nullptr ? 2 : 1));
+          }
+          if (p.mode == 0 && attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
           p.part = s->part;
           p.skip = P.skip;
           p.rows_valid = which == 1 ? s->full_rows : nullptr;

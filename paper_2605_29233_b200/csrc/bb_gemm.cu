@@ -44,14 +44,14 @@ struct UnitIter {
     } else if (mode == 0) {
       x = (long long)c * T / G;
       end = (long long)(c + 1) * T / G;
-    } else {
+    } else {  // modes 1, 2: whole tiles round-robin
       x = c;
       end = n_tiles;
     }
   }
   __device__ bool next(Unit& u) {
     if (x >= end) return false;
-    if (mode == 1) {
+    if (mode != 0) {
       u.tile = (int)x;
       u.kb0 = 0;
       u.kb1 = KB;
@@ -105,10 +105,21 @@ struct TcCfg {
 // (mode 1, LM head): ntile-outer, so the row chunks of one weight tile run on
 // neighbouring CTAs at the same time and the weight tile is read from HBM
 // once (chunk-outer would re-stream the 1 GB head once per chunk).
+// Mode 2: groups of gc row chunks; inside a group the gc chunks of one weight
+// tile are consecutive (ntile-major).  (Walking the fixed pieces of compacting
+// sessions ntile-outer the same way measured 1% slower: chunk-outer kept.)
 __device__ __forceinline__ int tile_ntile(const GemmTcParams& p, int t, int nch) {
+  if (p.mode == 2) {
+    const int span = p.n_ntiles * p.gc, g = t / span, gcs = min(p.gc, nch - g * p.gc);
+    return (t - g * span) / gcs;
+  }
   return p.mode == 1 ? t / nch : t % p.n_ntiles;
 }
 __device__ __forceinline__ int tile_chunk(const GemmTcParams& p, int t, int nch) {
+  if (p.mode == 2) {
+    const int span = p.n_ntiles * p.gc, g = t / span, gcs = min(p.gc, nch - g * p.gc);
+    return g * p.gc + (t - g * span) % gcs;
+  }
   return p.mode == 1 ? t % nch : t / p.n_ntiles;
 }
 
@@ -245,7 +256,9 @@ __global__ void __launch_bounds__(192)
   // B tiles) are only touched after the dependency wait.
   pdl_launch();
   if (warp == 0 && lane == 0) {
-    const uint64_t pol_w = policy_evict_first();
+    // streamed weights are read once (evict first); mode 2 re-reads each weight tile
+    // for the gc chunks of its group
+    const uint64_t pol_w = p.mode == 2 ? policy_evict_normal() : policy_evict_first();
     int pre = 0;
     UnitIter it(blockIdx.x, gridDim.x, p.KB, n_tiles, p.mode);
     Unit u;
@@ -295,7 +308,7 @@ __global__ void __launch_bounds__(192)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_w = p.mode == 2 ? policy_evict_normal() : policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       int stage_i = 0;
       uint32_t phase = 0;
@@ -395,8 +408,8 @@ __global__ void __launch_bounds__(192)
           for (int j = 0; j < 32; ++j) v[j] += w[j];
         }
       };
-      if (p.mode == 0) {
-        // stream-K: raw fp32 partial planes for the post-GEMM kernels
+      if (p.mode != 1) {
+        // stream-K (mode 2: plane 0): raw fp32 partial planes for the post-GEMM kernels
         float* dst = p.part + (long long)u.slot * p.plane + n;
 #pragma unroll 1
         for (int j0 = 0; j0 < rows_c; j0 += 32) {
@@ -575,6 +588,18 @@ static cudaError_t launch_mode(const TcGemm& g, cudaStream_t s) {
     case 256: return launch_bn<256, HEAD>(g, s);
   }
   return cudaErrorInvalidValue;
+}
+
+void tc_gemm_round_robin(TcGemm& g, int min_rounds, int act_row_bytes) {
+  GemmTcParams& p = g.p;
+  if (p.mode != 0 || (long long)p.n_ntiles * p.n_chunks < (long long)min_rounds * g.grid) return;
+  p.mode = 2;
+  // a group's activations (gc chunks x rows x K, both planes) ~ 32 MB of L2
+  const long long chunk_bytes = (long long)(p.half ? p.half : g.BN) * act_row_bytes;
+  long long gc = (32ll << 20) / (chunk_bytes > 0 ? chunk_bytes : 1);
+  p.gc = (int)(gc < 4 ? 4 : (gc > 16 ? 16 : gc));
+  g.sk.np = 1;  // one piece per tile: the consumers read plane 0 only
+  g.max_slots = 1;
 }
 
 cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s) {

@@ -68,7 +68,12 @@ struct GemmTcParams {
   // mode 0: stream-K into fp32 partial planes (consumed by post kernels)
   // mode 1: whole tiles round-robin over a persistent grid, epilogue from TMEM
   //         (epi.kind 1 = LM head)
-  int n_out, K, n_ntiles, n_chunks, KB, mode;
+  // mode 2: whole tiles round-robin into partial plane 0 (one piece per tile), tiles in
+  //         groups of gc row chunks, weight-tile-major inside a group: a round's tiles
+  //         share a few weight tiles and the group's activations stay in L2 (large
+  //         full passes, where stream-K's spread-out ranges re-streamed every weight
+  //         tile from HBM once per row chunk)
+  int n_out, K, n_ntiles, n_chunks, KB, mode, gc;
   // bf16x2 activations: 0, or the real rows per chunk (= BN/2).  The B tile
   // then stacks the chunk's hi rows [0, half) and lo rows [half, BN) (two TMA
   // loads), the MMA runs N = BN, and the epilogue adds accumulator columns j
@@ -113,6 +118,9 @@ struct TcGemm {
 bool tc_gemm_setup(TcGemm& g, const void* W, int n_out, int K, const void* X, int rows_alloc, int BN,
                    int mode, int max_grid, const void* X_lo = nullptr);
 cudaError_t tc_gemm_launch(const TcGemm& g, cudaStream_t s);
+// mode 0 -> mode 2 when the tiles fill at least `min_rounds` rounds of the grid
+// (full passes; never for compacting sessions, whose consumers read np planes)
+void tc_gemm_round_robin(TcGemm& g, int min_rounds, int act_row_bytes);
 // 2-D bf16 tensor map [outer][inner], boxes of box_outer rows x 64 elements, 128-byte swizzle
 bool tma_map_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer);
 
