@@ -13,6 +13,15 @@
 #include "bb_launch.cuh"
 #include "bb_layers.cuh"
 
+#ifndef POST_QKV_VEC
+#define POST_QKV_VEC 1  // bf16 sessions: 4 dims per thread in k_post_qkv4
+#endif
+#ifndef POST_QKV_MINB
+#define POST_QKV_MINB 2
+#endif
+#ifndef POST_QKV_NSU
+#define POST_QKV_NSU 2
+#endif
 #ifndef POST_RES_BATCH
 #define POST_RES_BATCH 1  // residual: all plane loads of a thread issued before use
 #endif
@@ -208,6 +217,94 @@ __device__ __forceinline__ void post_qkv_row(const Dims& D, const Sess& S, const
   stf2(dst + i + half, dl != nullptr ? dl + i + half : nullptr, b);
 }
 
+__device__ __forceinline__ void rope_rot(float& a, float& b, float c, float s) {
+  const float a2 = a * c - b * s, b2 = b * c + a * s;
+  a = a2;
+  b = b2;
+}
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
+// post_qkv_row with 4 dims (and their 4 RoPE partners) per thread: float4 plane
+// loads and 8-byte bf16 stores, so a thread keeps 4x the bytes in flight (large
+// full passes are bound by the loads in flight).  Per element the same operations
+// in the same order as post_qkv_row.
+template <typename T>
+__device__ __forceinline__ void post_qkv_row4(const Dims& D, const Sess& S, const Pass& P, const DevState& st,
+                                              const float* __restrict__ bias, const float* __restrict__ rope, int layer,
+                                              const PartRef& pr, int row) {
+  const int half = D.hd >> 1, tph = half >> 2;  // threads per head
+  const int hh = blockIdx.y * (blockDim.x / tph) + threadIdx.x / tph, i = (threadIdx.x % tph) * 4;
+  const bool live_hh = hh < D.nh + 2 * D.nkv;
+  const int c0 = hh * D.hd + i, c1 = c0 + half;
+  if (pr.sk.rows_dyn != nullptr) {
+    pdl_wait();
+    if (row >= *pr.sk.rows_dyn) return;
+  }
+  const int ns = live_hh ? sk_nslots(pr.sk, row, c0) : 0;
+  float4 ba = make_float4(0.0f, 0.0f, 0.0f, 0.0f), bb = ba;
+  if (bias != nullptr && live_hh) {
+    ba = ld4(bias + c0);
+    bb = ld4(bias + c1);
+  }
+  pdl_wait();
+  klog_mark(D.klog, D.klog_cap, 2);
+  const int skip = *P.skip, pos = P.slot_pos[row];
+  const long long kvo = hh >= D.nh && live_hh ? P.slot_kvoff[row] : 0;
+  constexpr int NSU = POST_QKV_NSU;  // planes loaded up front
+  const float* pa = pr.part + (long long)row * pr.ldp + c0;
+  float4 wa[NSU], wb[NSU];
+#pragma unroll
+  for (int k = 0; k < NSU; ++k)
+    if (k < ns) {
+      wa[k] = ld4(pa + (long long)k * pr.plane);
+      wb[k] = ld4(pa + (long long)k * pr.plane + half);
+    }
+  if (skip || pos < 0 || !live_hh) return;
+  float4 a = wa[0], b = wb[0];
+#pragma unroll
+  for (int k = 1; k < NSU; ++k)
+    if (k < ns) {
+      add4(a, wa[k]);
+      add4(b, wb[k]);
+    }
+  for (int k = NSU; k < ns; ++k) {
+    add4(a, ld4(pa + (long long)k * pr.plane));
+    add4(b, ld4(pa + (long long)k * pr.plane + half));
+  }
+  if (bias != nullptr) {
+    add4(a, ba);
+    add4(b, bb);
+  }
+  if (D.arch == 1 && hh < D.nh + D.nkv) {
+    const float4 r01 = ld4(rope + ((long long)pos * half + i) * 2), r23 = ld4(rope + ((long long)pos * half + i + 2) * 2);
+    rope_rot(a.x, b.x, r01.x, r01.y);
+    rope_rot(a.y, b.y, r01.z, r01.w);
+    rope_rot(a.z, b.z, r23.x, r23.y);
+    rope_rot(a.w, b.w, r23.z, r23.w);
+  }
+  if (hh < D.nh) {
+    const long long o = (long long)row * D.attn_dim + hh * D.hd;
+    T* q = reinterpret_cast<T*>(P.q) + o;
+    T* ql = P.q_lo != nullptr ? reinterpret_cast<T*>(P.q_lo) + o : nullptr;
+    Vec4<T>::st2(q + i, ql != nullptr ? ql + i : nullptr, a);
+    Vec4<T>::st2(q + i + half, ql != nullptr ? ql + i + half : nullptr, b);
+    return;
+  }
+  const bool isk = hh < D.nh + D.nkv;
+  const int kvh = isk ? hh - D.nh : hh - D.nh - D.nkv;
+  const long long lay = (long long)layer * S.R * S.pool * D.nkv * S.ps * D.hd;
+  T* dst = reinterpret_cast<T*>(isk ? st.kv_k : st.kv_v) + lay + kvo + (long long)kvh * S.ps * D.hd;
+  T* dl = st.kv_lo != 0 ? dst + st.kv_lo : nullptr;  // bf16x2: the lo pool
+  Vec4<T>::st2(dst + i, dl != nullptr ? dl + i : nullptr, a);
+  Vec4<T>::st2(dst + i + half, dl != nullptr ? dl + i + half : nullptr, b);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
                                                   const float* __restrict__ rope, int layer, PartRef pr) {
@@ -215,6 +312,14 @@ __global__ void __launch_bounds__(512) k_post_qkv(Dims D, Sess S, Pass P, DevSta
                  // session constants before the dependency wait, inside post_qkv_row)
   for (int row = blockIdx.x; row < P.rows_alloc; row += gridDim.x)
     post_qkv_row<T>(D, S, P, st, bias, rope, layer, pr, row);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, POST_QKV_MINB) k_post_qkv4(Dims D, Sess S, Pass P, DevState st, const float* __restrict__ bias,
+                                                   const float* __restrict__ rope, int layer, PartRef pr) {
+  pdl_launch();
+  for (int row = blockIdx.x; row < P.rows_alloc; row += gridDim.x)
+    post_qkv_row4<T>(D, S, P, st, bias, rope, layer, pr, row);
 }
 
 // ------------------------------------------------------------------ residual (+ norm)
@@ -575,6 +680,14 @@ cudaError_t launch_post_qkv(const Dims& D, const Sess& S, const Pass& P, const D
   const size_t smem = (size_t)D.qkv_out * sizeof(float);
   (void)smem;
   const int heads = D.nh + 2 * D.nkv, half = D.hd / 2;
+  if (POST_QKV_VEC && D.dtype == 1 && half % 4 == 0 && half / 4 <= 512 && (512 % (half / 4)) == 0) {
+    const int hpb = 512 / (half / 4);  // heads per CTA, 4 dims per thread
+    const int gy = (heads + hpb - 1) / hpb;
+    dim3 grid(P.rows_alloc < 4 * S.n_sms ? P.rows_alloc : 4 * S.n_sms, gy);
+    launch_k(k_post_qkv4<__nv_bfloat16>, dim3(grid), dim3(hpb * (half / 4)), (size_t)0, s, D, S, P, st, bias, W.rope,
+             layer, pr);
+    return cudaGetLastError();
+  }
   const int hpb = half >= 512 ? 1 : 512 / half;  // heads per CTA
   dim3 grid(P.rows_alloc < 2 * S.n_sms ? P.rows_alloc : 2 * S.n_sms, (heads + hpb - 1) / hpb);
   BB_DISPATCH(D, (launch_k(k_post_qkv<T>, dim3(grid), dim3(hpb * half), (size_t)(0), s, D, S, P, st, bias, W.rope, layer, pr)));
