@@ -259,6 +259,18 @@ def cpu_baseline(cfgd, config, samples=1):
 
 
 # ---------------------------------------------------------------- C4: request-parallel, batched
+def _session(params, cfg, P, R, args):
+    """The device session of the timed runs; --test-flags (A/B measurements
+    only, e.g. 2048 = per-branch refresh passes) builds it with those flags."""
+    from paper_2605_29233_b200.scheduler import get_session, _cfg_key
+    if args.test_flags:
+        from paper_2605_29233_b200.engine import Session
+        s = Session(params, cfg, P, R, trace=False, test_flags=args.test_flags)
+        params._sessions[_cfg_key(cfg, P, R, False)] = s
+        return s
+    return get_session(params, cfg, P, R, trace=False)
+
+
 def bench_c4(args, cfgd, bb, params, cfg, rank, world, dist, local):
     """BASELINE config C4: n_prompts prompts sharded round-robin over the ranks
     (dp.shard; no per-step collective), each rank running its share in device
@@ -273,7 +285,7 @@ def bench_c4(args, cfgd, bb, params, cfg, rank, world, dist, local):
     mine = dp.shard(cfgd["n_prompts"], rank, world)
     nbat = (len(mine) + Rb - 1) // Rb
     Wm = max(args.warmup, 1)
-    s = get_session(params, cfg, P, Rb, trace=False)
+    s = _session(params, cfg, P, Rb, args)
     warm = [bb.make_task(900000 + rank * 1000 + i, P, G, params.vocab) for i in range(Rb)]
     batches = [[bb.make_task(1000 + g, P, G, params.vocab) for g in mine[b * Rb:(b + 1) * Rb]] for b in range(nbat)]
     while batches and len(batches[-1]) < Rb:  # pad the last batch with repeats (counted once)
@@ -378,10 +390,21 @@ def main():
     ap.add_argument("--precision", default="bf16x2", choices=["bf16", "bf16x2"],
                     help="bf16x2 (default, the numerics that meet the north-star logit tolerance): bf16 weights "
                          "with hi+lo bf16 activations / KV; bf16: bf16 activations / KV")
+    ap.add_argument("--batch", type=int, default=None, help="c4: requests per device session (default 32)")
+    ap.add_argument("--prompts", type=int, default=None, help="c4: total prompts (default 256)")
+    ap.add_argument("--test-flags", type=int, default=0,
+                    help="A/B only: session test flags of the timed runs (bb_session_desc.test_flags)")
     ap.add_argument("--no-variant", action="store_true",
                     help="skip the same-run device measurement of the other numerics mode")
     args = ap.parse_args()
-    cfgd = CONFIGS[args.config]
+    cfgd = dict(CONFIGS[args.config])
+    if args.config == "c4":
+        if args.batch:
+            cfgd["batch"] = args.batch
+        if args.prompts:
+            cfgd["n_prompts"] = args.prompts
+        cfgd["workload"] = (f"LLaDA-8B-shape random-init, {cfgd['n_prompts']} synthetic prompts sharded request-parallel "
+                            f"over the GPUs, {cfgd['batch']} requests batched per device step, branches {{8,16,32}}, gen 256")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -426,7 +449,7 @@ def main():
     from paper_2605_29233_b200.scheduler import get_session
     P, G = cfgd["P"], cfgd["G"]
     vocab = params.vocab
-    s = get_session(params, cfg, P, 1, trace=False)
+    s = _session(params, cfg, P, 1, args)
     K, Wm = args.steps, max(args.warmup, 1)
     from paper_2605_29233_b200 import dp, _lib
     # prompts: global request g -> seed 1000 + g, sharded round-robin over ranks

@@ -87,7 +87,8 @@ typedef struct {
                           instead of the warp-specialized one; bit 2 = the warp-specialized
                           attention on 64-row instead of 128-row tiles; bit 3 = no block-pass
                           compaction in batched sessions; bits 4-7 = forced cluster size;
-                          bit 10 = full-pass GEMMs always stream-K (no grouped whole tiles) */
+                          bit 10 = full-pass GEMMs always stream-K (no grouped whole tiles);
+                          bit 11 = refresh as one full pass per branch (no stacked pass) */
   int logits;          /* 1: the LM head also keeps raw logits (bb_head_logits; forward observers) */
   int seam;            /* 1: step-operator seam session (bb_seam_*): private pages per branch */
   int hard_cap;        /* > 0: override the forward cap 4*G*B+16 (scheduler.py:310; tests) */

@@ -46,13 +46,16 @@ struct Session {
   Sess S;
   DevState st;
   Pass blk, full;
+  Pass fullr;                // stacked refresh: the full pass's buffers, B sequences per request
+  bool stack_refresh = false;
   Head H;
-  PassGemms gb, gf;
+  PassGemms gb, gf, gr;
   TcGemm head_tc;
   SimtGemm head_simt;
   float* part = nullptr;
   AttnMaps am{};             // TMA views of the KV pools (bf16 hd-128 attention)
   int* full_rows = nullptr;  // device scalar: rows of the full pass
+  int* fullr_rows = nullptr; // device scalar: rows of the stacked refresh pass
   char* ws = nullptr;
   size_t ws_bytes = 0;
   cudaGraphExec_t g_iter = nullptr, g_iter_ref = nullptr, g_prefill = nullptr, g_vanilla = nullptr;
@@ -216,7 +219,7 @@ static void plan(Session* s, char* base, bool dry) {
   st.kv_k = c.take<char>(kv_el * e * (D.split ? 2 : 1), 1024);
   st.kv_v = c.take<char>(kv_el * e * (D.split ? 2 : 1), 1024);
 
-  auto pass = [&](Pass& P, int rows_alloc, int max_items, int item_rows, int full) {
+  auto pass = [&](Pass& P, int rows_alloc, int max_items, int item_rows, int full, int groups) {
     P.rows_alloc = rows_alloc;
     P.full = full;
     P.item_rows = item_rows;
@@ -255,13 +258,22 @@ static void plan(Session* s, char* base, bool dry) {
                   (full ? S.L >= 1024 : item_rows > ATT_F8_MIN_ROWS)) ? 7 : 6;
     P.n_kz = full ? 1 : (item_rows + (1 << P.kz_shift) - 1) >> P.kz_shift;
     P.akey_cap = B * S.n_lp * S.ps;  // every page segment padded to ps entries
-    P.akeys = c.take<int>((long long)R * P.n_kz * P.akey_cap * 2);
-    P.akey_n = c.take<int>((long long)R * P.n_kz * 2);
+    P.akeys = c.take<int>((long long)groups * P.n_kz * P.akey_cap * 2);
+    P.akey_n = c.take<int>((long long)groups * P.n_kz * 2);
     P.req_base = c.take<int>(R);
     P.rows_live = c.take<int>(1);
   };
-  pass(s->blk, round_up(S.NR, s->gb.BN), S.max_items, S.NRq, 0);
-  pass(s->full, round_up(S.NF, s->gf.BN), 1, S.L, 1);
+  pass(s->blk, round_up(S.NR, s->gb.BN), S.max_items, S.NRq, 0, S.R);
+  {
+    // the stacked refresh pass shares the full pass's buffers (sized for the larger)
+    const int rows_f = round_up(S.NF, s->gf.BN);
+    const int rows_r = s->stack_refresh ? round_up(S.NF * S.B, s->gr.BN) : 0;
+    pass(s->full, rows_f > rows_r ? rows_f : rows_r, 1, S.L, 1, s->stack_refresh ? S.R * S.B : S.R);
+    s->full.rows_alloc = rows_f;
+    s->fullr = s->full;
+    s->fullr.rows_alloc = rows_r;
+    s->fullr.nseq = S.B;
+  }
   Head& H = s->H;
   const int rb = s->blk.rows_alloc;
   H.masked = c.take<int>(rb);
@@ -282,11 +294,13 @@ static void plan(Session* s, char* base, bool dry) {
   view(BB_VIEW_SLOT_BR, s->blk.slot_br, (size_t)rb * 4);
   H.skip = c.take<int>(1);
   s->full_rows = c.take<int>(1);
+  s->fullr_rows = c.take<int>(1);
   s->tstat = c.take<unsigned long long>(17 * 8);  // slot 16: GEMM phase marks (BB_GEMM_PH builds)
   s->tsite = c.take<unsigned long long>((size_t)3 * 10 * D.layers);
   s->tsite_on = live_stats();
   s->blk.atstat = s->tstat + 5 * 8;   // slots 5/6: block-pass attention (duration, start spread)
   s->full.atstat = s->tstat + 13 * 8; // slots 13/14: full-pass attention
+  s->fullr.atstat = s->full.atstat;
   s->fresh_save = c.take<int>(S.n_lp);
   s->sq_part = c.take<double>(1024);
   s->ns_cap = 64 * 1024;
@@ -296,9 +310,9 @@ static void plan(Session* s, char* base, bool dry) {
   if (D.dtype == BB_DTYPE_BF16) {
     const int outs[4] = {D.qkv_out, D.d, 2 * D.dff, D.d};
     const int ks[4] = {D.d, D.attn_dim, D.d, D.dff};
-    for (int which = 0; which < 2; ++which) {
-      const int rows = which == 0 ? s->blk.rows_alloc : s->full.rows_alloc;
-      const int BN = which == 0 ? s->gb.BN : s->gf.BN;
+    for (int which = 0; which < (s->stack_refresh ? 3 : 2); ++which) {
+      const int rows = which == 0 ? s->blk.rows_alloc : (which == 1 ? s->full.rows_alloc : s->fullr.rows_alloc);
+      const int BN = which == 0 ? s->gb.BN : (which == 1 ? s->gf.BN : s->gr.BN);
       for (int g = 0; g < 4; ++g) {
         if (outs[g] == 0) continue;
         const int ntiles = (outs[g] + 127) / 128, nch_all = rows / BN, KB = (ks[g] + 63) / 64;
@@ -318,9 +332,13 @@ static void plan(Session* s, char* base, bool dry) {
       }
     }
   } else {
+    // SIMT GEMMs write every allocated row of their pass (block passes can
+    // have more rows than the full pass: a seam session's 192-row full pass
+    // vs its 256-row block pass)
     const int outs[4] = {D.qkv_out, D.d, 2 * D.dff, D.d};
+    const long long rows = std::max(s->blk.rows_alloc, s->full.rows_alloc);
     for (int g = 0; g < 4; ++g) {
-      const long long need = (long long)s->full.rows_alloc * outs[g];
+      const long long need = rows * outs[g];
       part = need > part ? need : part;
     }
   }
@@ -368,9 +386,11 @@ static int setup_gemms(Session* s) {
     s->blk.pf_base = (const char*)W.wo;
     s->blk.pf_layer_bytes = (long long)D.d * D.attn_dim * (long long)e;
   }
-  for (int which = 0; which < 2; ++which) {
-    Pass& P = which == 0 ? s->blk : s->full;
-    PassGemms& G = which == 0 ? s->gb : s->gf;
+  s->fullr.pf_base = nullptr;
+  for (int which = 0; which < (s->stack_refresh ? 3 : 2); ++which) {
+    Pass& P = which == 0 ? s->blk : (which == 1 ? s->full : s->fullr);
+    PassGemms& G = which == 0 ? s->gb : (which == 1 ? s->gf : s->gr);
+    int* rows_full = which == 2 ? s->fullr_rows : s->full_rows;
     G.layers.resize(D.layers);
     for (int l = 0; l < D.layers; ++l) {
       LayerGemms& lg = G.layers[l];
@@ -392,11 +412,12 @@ static int setup_gemms(Session* s) {
         TcGemm* all[4] = {&lg.qkv, &lg.o, &lg.gu, &lg.dn};
         for (int g = 0; g < (D.dff ? 4 : 2); ++g) {
           GemmTcParams& p = all[g]->p;
-          p.tstat = s->tsite_on ? s->tsite + 3 * ((size_t)(which * 5 + g) * D.layers + l) : nullptr;
+          const int wk = which > 1 ? 1 : which;  // the stacked refresh reports as a full pass
+          p.tstat = s->tsite_on ? s->tsite + 3 * ((size_t)(wk * 5 + g) * D.layers + l) : nullptr;
           p.klog = s->D.klog;
           p.klog_cap = s->D.klog_cap;
-          p.klog_id = 100 + which * 8 + g;
-          if (which == 1 && !(s->tflags & 1024)) {
+          p.klog_id = 100 + wk * 8 + g;
+          if (which >= 1 && !(s->tflags & 1024)) {
             // large full passes: whole tiles in L2-friendly groups (test flag 1024: stream-K)
             const int kin = g == 1 ? D.attn_dim : (g == 3 ? D.dff : D.d);
             tc_gemm_round_robin(*all[g], GEMM_RR_ROUNDS, kin * 2 * (P.xn_lo != nullptr ? 2 : 1));
@@ -404,7 +425,7 @@ static int setup_gemms(Session* s) {
           if (p.mode == 0 && attach_ns_table(s, *all[g]) != BB_OK) return BB_ERR_NOMEM;
           p.part = s->part;
           p.skip = P.skip;
-          p.rows_valid = which == 1 ? s->full_rows : nullptr;
+          p.rows_valid = which >= 1 ? rows_full : nullptr;
           if (which == 0 && s->S.compact) {
             // batched: fixed k-pieces per tile (sums independent of how many requests are
             // live) and only the live requests' row chunks (test flag 256: all chunks)
@@ -414,14 +435,14 @@ static int setup_gemms(Session* s) {
         }
       } else {
         lg.sqkv = SimtGemm{(const float*)wqkv, (const float*)P.xn, D.qkv_out, D.d, P.rows_alloc,
-                           which == 1 ? s->full_rows : nullptr, P.skip, s->part, D.qkv_out};
+                           which >= 1 ? rows_full : nullptr, P.skip, s->part, D.qkv_out};
         lg.so = SimtGemm{(const float*)wo, (const float*)P.attn, D.d, D.attn_dim, P.rows_alloc,
-                         which == 1 ? s->full_rows : nullptr, P.skip, s->part, D.d};
+                         which >= 1 ? rows_full : nullptr, P.skip, s->part, D.d};
         if (D.dff) {
           lg.sgu = SimtGemm{(const float*)wgu, (const float*)P.xn, 2 * D.dff, D.d, P.rows_alloc,
-                            which == 1 ? s->full_rows : nullptr, P.skip, s->part, 2 * D.dff};
+                            which >= 1 ? rows_full : nullptr, P.skip, s->part, 2 * D.dff};
           lg.sdn = SimtGemm{(const float*)wd, (const float*)P.act, D.d, D.dff, P.rows_alloc,
-                            which == 1 ? s->full_rows : nullptr, P.skip, s->part, D.d};
+                            which >= 1 ? rows_full : nullptr, P.skip, s->part, D.d};
         }
       }
     }
@@ -606,6 +627,18 @@ static int enqueue_refresh(Session* s, cudaStream_t st) {
   const Dims& D = s->D;
   const Sess& S = s->S;
   CK(cudaMemsetAsync(s->H.skip, 1, sizeof(int), st));
+  if (s->stack_refresh) {
+    // every refreshing branch in one B x L pass: the weights stream once per
+    // refresh instead of once per branch (refresh loop, scheduler.py:379-383)
+    CK(cudaMemsetAsync(s->fullr.skip, 1, sizeof(int), st));
+    CK(launch_refresh_pack(D, S, s->st, s->fullr, s->blk, s->H, -1, st));
+    CK(launch_attn_keys(D, S, s->fullr, s->st, st));
+    CK(forward(s, s->fullr, s->gr, st));
+    CK(launch_gather_head(D, S, s->fullr, s->blk, s->H, -1, st));
+    CK(head(s, st));
+    CK(launch_refresh_end(D, S, s->st, st));
+    return BB_OK;
+  }
   for (int k = 0; k < S.B; ++k) {
     CK(cudaMemsetAsync(s->full.skip, 1, sizeof(int), st));
     CK(launch_refresh_pack(D, S, s->st, s->full, s->blk, s->H, k, st));
@@ -784,7 +817,7 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
   s->gb.BN = NR <= 64 ? 64 : ((NR <= 128 || split) ? 128 : 256);
   // full pass (prefill / refresh): row chunks as wide as possible with little
   // padding (L = 320 -> 2 x 160, L = 192 -> 1 x 192, L = 3072 -> 12 x 256)
-  {
+  auto full_bn = [&](long long rows) {
     // (the epilogue reads 32 accumulator columns at a time: rows per chunk % 32 == 0)
     const int cands_n[5] = {256, 192, 160, 128, 64}, cands_s[3] = {128, 96, 64};
     const int* cands = split ? cands_s : cands_n;
@@ -793,15 +826,21 @@ static int make_session(Model* M, const bb_session_desc* d, Session* s) {
     long long best_cost = -1;
     for (int i = 0; i < n_c; ++i) {
       const int bn = cands[i];
-      const long long chunks = (S.NF + bn - 1) / bn;
+      const long long chunks = (rows + bn - 1) / bn;
       const long long cost = chunks * bn + chunks * 32;  // padded rows + per-chunk weight re-read penalty
       if (best_cost < 0 || cost < best_cost) {
         best_cost = cost;
         best = bn;
       }
     }
-    s->gf.BN = best;
-  }
+    return best;
+  };
+  s->gf.BN = full_bn(S.NF);
+  // refresh: every refreshing branch stacked into one B x L pass on the
+  // key-list attention paths (the per-branch SIMT items keep one pass per
+  // branch; test flag bit 11 forces that everywhere)
+  s->stack_refresh = s->D.dtype == BB_DTYPE_BF16 && !uses_items(s->D) && S.B > 1 && !(d->test_flags & 2048);
+  s->gr.BN = s->stack_refresh ? full_bn((long long)S.NF * S.B) : s->gf.BN;
   return BB_OK;
 }
 
@@ -850,9 +889,15 @@ BB_API int bb_session_create(void* model, const bb_session_desc* d, void* worksp
   std::vector<int> neg(std::max(s->blk.rows_alloc, s->full.rows_alloc), -1);
   std::vector<int> zero(neg.size(), 0);
   cudaMemcpy(s->blk.slot_pos, neg.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(s->full.slot_pos, neg.data(), s->full.rows_alloc * 4, cudaMemcpyHostToDevice);
+  const int full_buf_rows = std::max(s->full.rows_alloc, s->fullr.rows_alloc);
+  if ((int)neg.size() < full_buf_rows) neg.resize(full_buf_rows, -1);
+  cudaMemcpy(s->full.slot_pos, neg.data(), (size_t)full_buf_rows * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->H.masked, zero.data(), s->blk.rows_alloc * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(s->full_rows, &s->S.NF, sizeof(int), cudaMemcpyHostToDevice);
+  {
+    const int nr = s->S.NF * s->S.B;
+    cudaMemcpy(s->fullr_rows, &nr, sizeof(int), cudaMemcpyHostToDevice);
+  }
   cudaMemset(s->st.init_gen, 0xFF, (size_t)s->S.R * s->S.G * 4);  // no presets: every position masked
   {
     std::vector<int> base(s->S.R);

@@ -202,8 +202,10 @@ __global__ void __launch_bounds__(256) k_attn_keys(Sess S, Pass P, DevState st, 
   int* sSeg = sCnt + S.n_lp + 1;          // [n_lp][B] physical page of segment
   int* sMsk = sSeg + S.n_lp * S.B;        // [n_lp][B] branch mask of segment
   __shared__ int s_bmask, s_tot, s_gen0;
-  const int r = blockIdx.x, kz = blockIdx.y;
-  const int slot_base = P.full ? r * S.L : blk_base(S, P, r);  // -1: finished request (compacting session)
+  // full passes: row group g = (request r, sequence); the stacked refresh's
+  // sequence is branch g % nseq, whose rows alone set the branch mask below
+  const int g = blockIdx.x, r = P.full ? g / P.nseq : g, kz = blockIdx.y;
+  const int slot_base = P.full ? g * S.L : blk_base(S, P, r);  // -1: finished request (compacting session)
   if (threadIdx.x == 0) s_bmask = 0;
   __syncthreads();
   const bool skip = *P.skip != 0;
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(256) k_attn_keys(Sess S, Pass P, DevState st, 
     }
   }
   __syncthreads();
-  const long long kb = (long long)r * P.n_kz + kz;
+  const long long kb = (long long)g * P.n_kz + kz;
   int* out = P.akeys + kb * P.akey_cap * 2;
   // block pass: keys at a window position of one of their branches are
   // rewritten by this step's splice (KEY_WIN) -- the attention loads every
@@ -299,7 +301,7 @@ cudaError_t launch_attn_keys(const Dims& D, const Sess& S, const Pass& P, const 
     cudaFuncSetAttribute(k_attn_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  launch_k(k_attn_keys, dim3(S.R, P.n_kz), dim3(256), smem, s, S, P, st, rows);
+  launch_k(k_attn_keys, dim3(pass_groups(S, P), P.n_kz), dim3(256), smem, s, S, P, st, rows);
   return cudaGetLastError();
 }
 
@@ -804,7 +806,7 @@ static cudaError_t attn_seg_launch(const Dims& D, const Sess& S, const Pass& P, 
     attr = true;
   }
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-  dim3 grid(S.R * CS, D.nh, (rows + 63) / 64);
+  dim3 grid(pass_groups(S, P) * CS, D.nh, (rows + 63) / 64);
   launch_k(k_attn_seg<HD, CS>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
   return cudaGetLastError();
 }
@@ -819,7 +821,7 @@ static int att_cs(const Dims& D, const Sess& S, const Pass& P, int tflags) {
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   if (P.full) return 8;  // full passes: 1-CTA clusters measured 1.3% slower per C2 request
   const int rows = S.NRq;
-  const long long per = (long long)S.R * D.nh * ((rows + 63) / 64);
+  const long long per = (long long)pass_groups(S, P) * D.nh * ((rows + 63) / 64);
   const long long wave = 2LL * S.n_sms;
   if (per * 8 <= wave) return 8;
   if (per * 4 <= wave) return 4;
@@ -1280,7 +1282,7 @@ static cudaError_t attn_tc_launch(const Dims& D, const Sess& S, const Pass& P, c
     attr = true;
   }
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-  dim3 grid(S.R * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
+  dim3 grid(pass_groups(S, P) * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
   launch_k(k_attn_tc<CS, SPLIT>, dim3(grid), dim3(128), (size_t)(smem), s, D, S, P, st, layer, rows);
   return cudaGetLastError();
 }
@@ -1720,7 +1722,7 @@ static cudaError_t attn_fa_launch(const Dims& D, const Sess& S, const Pass& P, c
     cudaFuncSetAttribute(k_attn_fa<CS, NS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dim3 grid(S.R * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
+  dim3 grid(pass_groups(S, P) * CS, D.nh, (rows + ATC_QR - 1) / ATC_QR);
   launch_k(k_attn_fa<CS, NS, SPLIT>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, am.kl, am.vl, D, S, P, st,
            layer, rows);
   return cudaGetLastError();
@@ -2205,7 +2207,7 @@ static cudaError_t attn_f8_launch(const Dims& D, const Sess& S, const Pass& P, c
     cudaFuncSetAttribute(k_attn_fa128<CS, NS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dim3 grid(S.R * CS, D.nh, (rows + AF8_QR - 1) / AF8_QR);
+  dim3 grid(pass_groups(S, P) * CS, D.nh, (rows + AF8_QR - 1) / AF8_QR);
   launch_k(k_attn_fa128<CS, NS, SPLIT>, dim3(grid), dim3(AFA_THREADS), smem, s, am.k, am.v, am.kl, am.vl, D, S, P, st,
            layer, rows);
   return cudaGetLastError();
@@ -2219,7 +2221,7 @@ static int att_cs_f8(const Dims& D, const Sess& S, const Pass& P, int tflags) {
   const int forced = (tflags >> 4) & 15;
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   const int rows = P.full ? S.L : S.NRq;
-  const long long per = (long long)S.R * D.nh * ((rows + AF8_QR - 1) / AF8_QR);
+  const long long per = (long long)pass_groups(S, P) * D.nh * ((rows + AF8_QR - 1) / AF8_QR);
   if (per * 8 <= 2 * f8_slots<8, NS, SPLIT>()) return 8;
   if (per * 4 <= 2 * f8_slots<4, NS, SPLIT>()) return 4;
   if (per * 2 <= 2 * f8_slots<2, NS, SPLIT>()) return 2;
@@ -2237,7 +2239,7 @@ static int att_cs_tc(const Dims& D, const Sess& S, const Pass& P, int tflags, in
   const int forced = (tflags >> 4) & 15;
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   const int rows = P.full ? S.L : S.NRq;
-  const long long per = (long long)S.R * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
+  const long long per = (long long)pass_groups(S, P) * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
   const long long wave = (long long)per_sm * S.n_sms;  // resident CTAs per SM x SMs
   for (int cs = 8; cs > 1; cs >>= 1)
     if (per * cs <= wave) return cs;
@@ -2281,7 +2283,7 @@ static int att_cs_fa(const Dims& D, const Sess& S, const Pass& P, int tflags) {
   const int forced = (tflags >> 4) & 15;
   if (forced == 8 || forced == 4 || forced == 2 || forced == 1) return forced;
   const int rows = P.full ? S.L : S.NRq;
-  const long long per = (long long)S.R * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
+  const long long per = (long long)pass_groups(S, P) * D.nh * ((rows + ATC_QR - 1) / ATC_QR);
   if (per * 8 <= 2 * fa_slots<8, NS, SPLIT>()) return 8;
   if (per * 4 <= 2 * fa_slots<4, NS, SPLIT>()) return 4;
   if (per * 2 <= 2 * fa_slots<2, NS, SPLIT>()) return 2;

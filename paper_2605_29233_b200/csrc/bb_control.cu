@@ -1123,53 +1123,73 @@ __global__ void k_merge_sync(Dims D, Sess S, DevState st, int after_prefill) {
 }
 
 // ------------------------------------------------------------------ refresh
+// k >= 0: branch k's full pass (rows r * L + p); k = -1: every refreshing
+// branch stacked into one pass (full.nseq = B; branch kk at rows
+// (r * B + kk) * L + p, its own key list).  The page allocations run in the
+// same branch order either way, so both give the same page tables.
 __global__ void k_refresh_pack(Dims D, Sess S, DevState st, Pass full, Pass blk, Head H, int k) {
   pdl_enter();
   klog_mark(D.klog, D.klog_cap, 16);
   RC_SETUP();
   const int r = c.r;
   load_request(c);
-  const bool live = c.ctrl[C_STATUS] == 0 && c.ctrl[C_REFRESH_DUE] && ((c.ctrl[C_REFRESH_MASK] >> k) & 1);
+  const bool due = c.ctrl[C_STATUS] == 0 && c.ctrl[C_REFRESH_DUE];
+  const int rmask = c.ctrl[C_REFRESH_MASK];
+  const int k0 = k < 0 ? 0 : k, k1 = k < 0 ? S.B : k + 1;
+  auto live_of = [&](int kk) { return due && ((rmask >> kk) & 1) && kk >= k0 && kk < k1; };
+  auto group_of = [&](int kk) { return r * full.nseq + (k < 0 ? kk : 0); };
   if (threadIdx.x == 0) {
+    int nl = 0;
     for (int kk = 0; kk < MAXB; ++kk) {
-      full.rng_off[r * MAXB + kk] = r * S.L;
-      full.rng_cnt[r * MAXB + kk] = (live && kk == k) ? S.L : 0;
+      const bool lv = kk < S.B && live_of(kk);
+      full.rng_off[r * MAXB + kk] = (kk < S.B ? group_of(kk) : r * full.nseq) * S.L;
+      full.rng_cnt[r * MAXB + kk] = lv ? S.L : 0;
+      nl += lv ? 1 : 0;
     }
-    full.n_items[r] = live ? 1 : 0;
-    if (live) {
+    // planned attention items (SIMT path): one per-branch pass only
+    full.n_items[r] = (k >= 0 && nl) ? 1 : 0;
+    if (k >= 0 && nl) {
       int* it = full.items + (long long)r * ITW;
       it[0] = 1 << k;
       it[1] = 0;
       it[2] = S.n_lp;
       it[3] = k;
-      for (int lp = 0; lp < S.n_lp; ++lp) c.write_intent(k, lp, false);  // fully rewritten
+    }
+    for (int kk = k0; kk < k1; ++kk)
+      if (live_of(kk))
+        for (int lp = 0; lp < S.n_lp; ++lp) c.write_intent(kk, lp, false);  // fully rewritten
+    if (nl) {
       *full.skip = 0;
       *H.skip = 0;
     }
   }
   __syncthreads();
-  for (int p = threadIdx.x; p < S.L; p += blockDim.x) {
-    const int row = r * S.L + p;
-    full.slot_pos[row] = live ? p : -1;
-    full.slot_req[row] = r;
-    full.slot_br[row] = k;
-    full.slot_tok[row] = c.rows[k * S.L + p];
-    full.slot_kvoff[row] = live ? kv_row_off(D, S, st, r, k, p) : 0;
-  }
-  const int* target = st.target + (long long)r * S.G;
-  const int rbase = blk_base(S, blk, r);
-  for (int j = threadIdx.x; j < S.bs[k] && rbase >= 0; j += blockDim.x) {
-    const int slot = rbase + S.off[k] + j;
-    const int pos = c.B_(k, B_START) + j;
-    const bool in = live && pos < c.B_(k, B_END) && c.rows[k * S.L + pos] == c.mask_id;
-    blk.slot_req[slot] = r;
-    blk.slot_br[slot] = k;
-    blk.slot_pos[slot] = in ? pos : -1;
-    H.masked[slot] = in ? 1 : 0;
-    if (in) slot_boost(D, S, c.rows + k * S.L, target, pos, &H.boost[slot], &H.tgt[slot]);
-    else {
-      H.boost[slot] = 0.0f;
-      H.tgt[slot] = -1;
+  for (int kk = k0; kk < k1; ++kk) {
+    const bool live = live_of(kk);
+    const int g = group_of(kk);
+    for (int p = threadIdx.x; p < S.L; p += blockDim.x) {
+      const int row = g * S.L + p;
+      full.slot_pos[row] = live ? p : -1;
+      full.slot_req[row] = r;
+      full.slot_br[row] = kk;
+      full.slot_tok[row] = c.rows[kk * S.L + p];
+      full.slot_kvoff[row] = live ? kv_row_off(D, S, st, r, kk, p) : 0;
+    }
+    const int* target = st.target + (long long)r * S.G;
+    const int rbase = blk_base(S, blk, r);
+    for (int j = threadIdx.x; j < S.bs[kk] && rbase >= 0; j += blockDim.x) {
+      const int slot = rbase + S.off[kk] + j;
+      const int pos = c.B_(kk, B_START) + j;
+      const bool in = live && pos < c.B_(kk, B_END) && c.rows[kk * S.L + pos] == c.mask_id;
+      blk.slot_req[slot] = r;
+      blk.slot_br[slot] = kk;
+      blk.slot_pos[slot] = in ? pos : -1;
+      H.masked[slot] = in ? 1 : 0;
+      if (in) slot_boost(D, S, c.rows + kk * S.L, target, pos, &H.boost[slot], &H.tgt[slot]);
+      else {
+        H.boost[slot] = 0.0f;
+        H.tgt[slot] = -1;
+      }
     }
   }
 }

@@ -521,7 +521,9 @@ __global__ void __launch_bounds__(256) k_gather_head(Dims D, Sess S, Pass full, 
   const int slot = blockIdx.x;
   if (!H.masked[slot]) return;
   if (filter >= 0 && blk.slot_br[slot] != filter) return;
-  const long long src = (long long)blk.slot_req[slot] * S.L + blk.slot_pos[slot];
+  // the full-pass row of (request, position): sequence = branch in the stacked refresh
+  const int seq = full.nseq > 1 ? blk.slot_br[slot] : 0;
+  const long long src = ((long long)blk.slot_req[slot] * full.nseq + seq) * S.L + blk.slot_pos[slot];
   const T* a = reinterpret_cast<const T*>(full.xn) + src * D.d;
   T* o = reinterpret_cast<T*>(blk.xn) + (long long)slot * D.d;
   for (int c = threadIdx.x; c < D.d; c += blockDim.x) o[c] = a[c];

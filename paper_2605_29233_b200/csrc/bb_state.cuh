@@ -102,6 +102,9 @@ struct DevState {
 struct Pass {
   int rows_alloc;
   int full;           // 1 = full forward (prefill/refresh), 0 = block step
+  int nseq = 1;       // full pass: sequences per request, L rows each -- 1 (prefill, per-branch
+                      // passes), or B for the stacked refresh (request r, branch k at rows
+                      // (r * B + k) * L); the attention's row groups are (request, sequence)
   int* slot_pos;      // [rows_alloc] (-1 = padding)
   int* slot_req;
   int* slot_br;
@@ -166,6 +169,9 @@ struct Head {
 __host__ __device__ inline bool uses_items(const Dims& D) {
   return !(D.dtype == 1 && (D.hd == 64 || D.hd == 128));
 }
+
+// row groups of a pass: one per request (block pass) or per (request, sequence) (full pass)
+__host__ __device__ inline int pass_groups(const Sess& S, const Pass& P) { return P.full ? S.R * P.nseq : S.R; }
 
 // first block-pass slot of request r (-1: finished, compacting sessions only)
 __host__ __device__ inline int blk_base(const Sess& S, const Pass& blk, int r) {

@@ -335,3 +335,71 @@ def test_batched_compaction_matches_static_layout():
           f"{sum(a == b for a, b in zip(static, single))}/4; nfe {nfes} / {[x[0] for x in static]} / "
           f"{[x[0] for x in single]}")
     assert same_static >= 3 and same_single >= 3
+
+
+def _refresh_model(dtype):
+    dims = bb.ModelDims(layers=2, d_model=256, max_len=192, arch="llada", n_heads=2, n_kv_heads=2, head_dim=128,
+                        d_ff=512, rope_theta=500000.0)
+    return bb.build_model(0, bb.Vocab(size=1000), dims, head_scale=0.25, dtype=dtype)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "bf16x2"])
+def test_stacked_refresh_kv_matches_per_branch_passes(dtype):
+    """The stacked refresh (every refreshing branch in one B x L full pass,
+    own key list per (request, branch)) writes the same caches as one full
+    pass per branch (test flag 2048; the reference's loop, scheduler.py:379-383):
+    after prefill + one block step + refresh, every branch's kv_vectorize of
+    both requests of a 2-request session agrees (the GEMM row chunking differs,
+    so within bf16 rounding, not bitwise), and the page tables are identical."""
+    import torch
+    from paper_2605_29233_b200.engine import Session
+    p = _refresh_model(dtype)
+    vocab = p.vocab
+    cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=64, refresh_interval=1)
+    tasks = [bb.make_task(s, 32, 64, vocab) for s in (3, 4)]
+    prompts = np.stack([t.prompt for t in tasks])
+    targets = np.stack([t.target for t in tasks])
+    out = {}
+    for flags in (0, 2048):
+        s = Session(p, cfg, 32, 2, test_flags=flags)
+        s.set_inputs(prompts, targets)
+        s.prefill()
+        s.iteration(True, use_graph=False)
+        ctrl = s.ctrl_now()
+        assert (ctrl[:, 18] == 1).all(), ctrl[:, 18]  # C_REFRESHES: one refresh charged per request
+        out[flags] = ([[s.kv_vec(r, k).cpu().numpy() for k in range(3)] for r in range(2)],
+                      s.v_pages.cpu().numpy().copy() if hasattr(s, "v_pages") else None, ctrl.copy())
+        del s
+        torch.cuda.synchronize()
+    (kv_a, pt_a, c_a), (kv_b, pt_b, c_b) = out[0], out[2048]
+    if pt_a is not None:
+        assert np.array_equal(pt_a, pt_b)
+    worst = 0.0
+    for r in range(2):
+        for k in range(3):
+            a, b = kv_a[r][k], kv_b[r][k]
+            assert np.isfinite(a).all()
+            worst = max(worst, float(np.abs(a - b).max() / (np.abs(b).max() + 1e-30)))
+    tol = 2e-2 if dtype == "bf16" else 1e-4
+    print(f"{dtype}: stacked vs per-branch refresh KV max rel diff {worst:.2e}")
+    assert worst <= tol
+
+
+def test_stacked_refresh_whole_runs_match_per_branch_passes():
+    """Whole bf16x2 runs with a refresh every 4 iterations: stacked refresh vs
+    one full pass per branch (test flag 2048) give the same NFE and tokens."""
+    from paper_2605_29233_b200.engine import Session
+    from paper_2605_29233_b200.scheduler import _cfg_key
+    cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=64, refresh_interval=4)
+    tasks = [bb.make_task(s, 32, 64, bb.Vocab(size=1000)) for s in range(6)]
+
+    def run(flags):
+        p = _refresh_model("bf16x2")
+        p._sessions[_cfg_key(cfg, 32, 1, True)] = Session(p, cfg, 32, 1, test_flags=flags)
+        res = [bb.run_blockbatch(p, t, cfg) for t in tasks]
+        return [(r.nfe.snapshot(), r.row.tokens.tolist()) for r in res]
+    a, b = run(0), run(2048)
+    assert all(x[0][2] > 0 for x in a), "every run should refresh"
+    same = sum(x == y for x, y in zip(a, b))
+    print(f"stacked vs per-branch refresh: {same}/6 identical runs; nfe {[x[0] for x in a]} / {[x[0] for x in b]}")
+    assert same >= 5
