@@ -51,8 +51,8 @@ CONFIGS = {
     "c5": dict(workload="LLaDA-8B-shape long context: 2048-token prompt, branches {8,16,32,64}, gen 1024",
                shape="llada", P=2048, G=1024, bs=(8, 16, 32, 64), R=32, head_scale=0.4, gamma=8.0),
     "c4": dict(workload="LLaDA-8B-shape random-init, 256 synthetic prompts sharded request-parallel over the GPUs, "
-                        "32 requests batched per device step, branches {8,16,32}, gen 256",
-               shape="llada", P=64, G=256, bs=(8, 16, 32), R=32, head_scale=0.4, gamma=8.0, n_prompts=256, batch=32),
+                        "8 requests batched per device step, branches {8,16,32}, gen 256",
+               shape="llada", P=64, G=256, bs=(8, 16, 32), R=32, head_scale=0.4, gamma=8.0, n_prompts=256, batch=8),
     "c1": dict(workload="reference synthetic model 4L d256 V4096, P64, branches {8,16,32}, gen 128 (bf16)",
                shape="ref", P=64, G=128, bs=(8, 16, 32), R=32, head_scale=2.0, gamma=8.0),
 }
@@ -390,7 +390,9 @@ def main():
     ap.add_argument("--precision", default="bf16x2", choices=["bf16", "bf16x2"],
                     help="bf16x2 (default, the numerics that meet the north-star logit tolerance): bf16 weights "
                          "with hi+lo bf16 activations / KV; bf16: bf16 activations / KV")
-    ap.add_argument("--batch", type=int, default=None, help="c4: requests per device session (default 32)")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="c4: requests per device session (default 8: the best of 1-32 measured, "
+                         "profiles/r02/c4_batch/)")
     ap.add_argument("--prompts", type=int, default=None, help="c4: total prompts (default 256)")
     ap.add_argument("--test-flags", type=int, default=0,
                     help="A/B only: session test flags of the timed runs (bb_session_desc.test_flags)")
