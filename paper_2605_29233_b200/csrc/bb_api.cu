@@ -8,6 +8,8 @@
 #include <cmath>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: host ranges for nsys / ncu --nvtx
+
 #include "bb200.h"
 #include "bb_common.cuh"
 #include "bb_gemm.cuh"
@@ -997,13 +999,23 @@ BB_API int bb_iteration(void* sess, int with_refresh, int use_graph, void* strea
 // session: prefill, then iterations until all requests finished (status 1) or
 // failed (< 0).  Refresh is enqueued after every refresh_interval-th iteration
 // (the device asserts that it matches its own counter).  Status words are
-// polled asynchronously two iterations behind, so the host never stalls the
-// GPU; the (at most two) extra iterations are device-side no-ops.
+// polled asynchronously one iteration behind, so the host never stalls the
+// GPU; the (at most one) extra iteration is a device-side no-op.
+namespace {
+struct NvtxRange {  // host-side range (enqueue + polling) of a bb_run phase
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out) {
   Session* s = (Session*)sess;
   if (!s) return BB_ERR_CONTRACT;
+  NvtxRange run_range("bb_run");
   cudaStream_t st = (cudaStream_t)stream;
   int rc = BB_OK;
+  {
+  NvtxRange prefill_range("bb_run:prefill");
   if (use_graph) {
     if (!s->g_prefill) {
       rc = capture(s, 2, st, &s->g_prefill, &s->nodes_prefill);
@@ -1016,13 +1028,17 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
     rc = enqueue_prefill(s, st);
     if (rc != BB_OK) return rc;
   }
+  }
   const int R = s->S.R;
   const size_t cb = (size_t)R * C_WORDS * 4;
   CK(cudaMemcpyAsync(s->host_ctrl, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(s->ev[0], st));
   int it = 0;
   bool finished = false;
-  const int lag = 2;
+  // status polled one iteration behind: while the host waits for iteration
+  // it - 1, iteration it is already queued, so the GPU never idles and at most
+  // one extra (no-op) iteration runs after the last request finished
+  const int lag = 1;
   int checked = -1;
   while (!finished && it < max_iterations) {
     // check the status copied `lag` iterations ago
@@ -1036,7 +1052,9 @@ BB_API int bb_run(void* sess, int max_iterations, int use_graph, void* stream, i
       if (finished) break;
     }
     ++it;
-    rc = bb_iteration(s, it % s->S.refresh_interval == 0, use_graph, st);
+    const bool with_refresh = it % s->S.refresh_interval == 0;
+    NvtxRange it_range(with_refresh ? "bb_run:iteration+refresh" : "bb_run:iteration");
+    rc = bb_iteration(s, with_refresh, use_graph, st);
     if (rc != BB_OK) return rc;
     CK(cudaMemcpyAsync(s->host_ctrl + (size_t)(it & 3) * R * C_WORDS, s->st.ctrl, cb, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(s->ev[it & 3], st));
@@ -1137,7 +1155,7 @@ BB_API int bb_sqdiff_norm(void* sess, const float* a, const float* b, long long 
 // vanilla_decode (decoding.py:279-321) for every request of a session with
 // one branch of block size gen_len: initial rows, then rounds (one full
 // forward each, captured once into a graph) until every request finished;
-// status polled two rounds behind like bb_run.
+// status polled one round behind like bb_run.
 BB_API int bb_run_vanilla(void* sess, int max_iterations, int use_graph, void* stream, int* iterations_out) {
   Session* s = (Session*)sess;
   if (!s) return BB_ERR_CONTRACT;
@@ -1151,7 +1169,7 @@ BB_API int bb_run_vanilla(void* sess, int max_iterations, int use_graph, void* s
   CK(cudaEventRecord(s->ev[0], st));
   int it = 0, checked = -1;
   bool finished = false;
-  const int lag = 2;
+  const int lag = 1;
   while (!finished && it < max_iterations) {
     const int chk = it - lag;
     if (chk >= 0 && chk > checked) {
