@@ -615,7 +615,7 @@ def main():
         except Exception:
             pass
     cb = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only (the other ranks would idle in a barrier)
         try:
             cb = cpu_baseline(cfgd, args.config)
         except Exception as exc:  # never let the reported baseline sink the bench line
