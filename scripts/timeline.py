@@ -1,6 +1,7 @@
-"""Real (graph + PDL) per-kernel timeline of one C2 request from the device
-kernel log (BB_KLOG=1): each kernel's slot = time from its predecessor's
-completion to its own completion (next kernel's stamp)."""
+"""Real (graph + PDL) per-kernel timeline of one request of a bench config
+(BB_TL_CFG = c2 | c3 | c5, BB_TL_DTYPE = bf16 | bf16x2) from the device kernel
+log (BB_KLOG=1): each kernel's slot = time from its predecessor's completion
+to its own completion (next kernel's stamp)."""
 import collections, json, os, sys
 os.environ["BB_KLOG"] = "1"
 sys.path.insert(0, '.')
@@ -9,11 +10,12 @@ import torch
 import paper_2605_29233_b200 as bb
 from paper_2605_29233_b200.scheduler import get_session
 
-_CFG = {"c2": (64, 256, (8, 16, 32)), "c5": (2048, 1024, (8, 16, 32, 64))}[os.environ.get("BB_TL_CFG", "c2")]
-P, G = _CFG[0], _CFG[1]
-vocab = bb.Vocab(size=bb.LLADA_8B_VOCAB)
-cfg = bb.SchedulerConfig(block_sizes=_CFG[2], gen_len=G)
-params = bb.build_model(0, vocab, bb.LLADA_8B, head_scale=0.4, gamma=8.0, dtype=os.environ.get("BB_TL_DTYPE", "bf16"))
+# the bench's workload table (c2 / c3 / c5): same shapes, scheduler config, head_scale
+import bench  # noqa: E402
+_cfgd = bench.CONFIGS[os.environ.get("BB_TL_CFG", "c2")]
+bb, params, cfg = bench.make_model(_cfgd, os.environ.get("BB_TL_DTYPE", "bf16"))
+P, G = _cfgd["P"], _cfgd["G"]
+vocab = params.vocab
 R = int(os.environ.get("BB_TL_R", "1"))  # requests per session (multi-request batching)
 if os.environ.get("BB_TL_TFLAGS"):  # session test flags (A/B: attention kernel / cluster size)
     from paper_2605_29233_b200.engine import Session
