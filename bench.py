@@ -596,7 +596,7 @@ def main():
     ms_per_nfe = t_ms / max(nfe.sum(), 1)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": None, "peak_source": peak_src,
-            "kernel": "k_gemm_tc<64> tcgen05 weight-streaming GEMM (block-step QKV/O/gate-up/down)",
+            "kernel": f"k_gemm_tc<{s.info[11]},0> tcgen05 weight-streaming GEMM (block-step QKV/O/gate-up/down)",
             "launches_timed": launches, "per_kind": per_kind,
             "duration_convention": "kernel entry (before the pre-wait weight TMA) to last CTA exit, "
                                    "min/max over CTAs, every launch in the timed region",

@@ -637,6 +637,10 @@ static int enqueue_refresh(Session* s, cudaStream_t st) {
     CK(launch_attn_keys(D, S, s->fullr, s->st, st));
     CK(forward(s, s->fullr, s->gr, st));
     CK(launch_gather_head(D, S, s->fullr, s->blk, s->H, -1, st));
+    // rows [R*L, R*B*L) are padding of the R*L-row passes (prefill, vanilla,
+    // fresh_kv): back to -1, or their post kernels would write the stale rows'
+    // K/V into the next request's pages
+    CK(cudaMemsetAsync(s->full.slot_pos + S.NF, 0xFF, (size_t)(s->fullr.rows_alloc - S.NF) * sizeof(int), st));
     CK(head(s, st));
     CK(launch_refresh_end(D, S, s->st, st));
     return BB_OK;

@@ -478,3 +478,27 @@ def test_live_gemm_stats_count_every_launch():
     assert gs[4][4] == 2 and gs[4][3] > 0  # LM head: prefill + block step
     gs = s.gemm_stats(reset=False)
     assert all(gs[k][4] == 0 for k in (0, 1, 2, 3, 4, 8, 9, 10, 11))
+
+
+# fp32 verification-path NFE triples of C2 seeds 36..45 (profiles/r02/parity/
+# parity_c2_bf16x2_final_seeds0-199.json); bf16x2 matches all ten
+C2_F32_NFE = {36: (1, 34, 1), 37: (1, 75, 2), 38: (1, 36, 1), 39: (1, 36, 1), 40: (1, 70, 2),
+              41: (1, 24, 0), 42: (1, 54, 1), 43: (1, 35, 1), 44: (1, 37, 1), 45: (1, 44, 1)}
+
+
+def test_c2_bf16x2_session_reuse_matches_fp32_decisions():
+    """Full-size C2 (LLaDA-8B shape, bf16x2) requests run back to back on one
+    session, each after the previous one's stacked refresh: the decisions equal
+    the fp32 verification path's on every prompt.  (Regression: the stacked
+    refresh once left live rows in the prefill pass's padding, whose K/V writes
+    raced with the next request's prompt rows -- seed 41 ran 7 block NFEs
+    instead of 24.)"""
+    import bench
+    _, params, cfg = bench.make_model(bench.CONFIGS["c2"], "bf16x2")
+    got = {}
+    for seed in sorted(C2_F32_NFE):
+        t = bb.make_task(seed, 64, 256, params.vocab)
+        got[seed] = bb.run_blockbatch(params, t, cfg).nfe.snapshot()
+    bad = {s: (got[s], C2_F32_NFE[s]) for s in got if got[s] != C2_F32_NFE[s]}
+    del params
+    assert not bad, bad

@@ -337,37 +337,42 @@ def test_batched_compaction_matches_static_layout():
     assert same_static >= 3 and same_single >= 3
 
 
-def _refresh_model(dtype):
-    dims = bb.ModelDims(layers=2, d_model=256, max_len=192, arch="llada", n_heads=2, n_kv_heads=2, head_dim=128,
+def _refresh_model(dtype, max_len=192):
+    dims = bb.ModelDims(layers=2, d_model=256, max_len=max_len, arch="llada", n_heads=2, n_kv_heads=2, head_dim=128,
                         d_ff=512, rope_theta=500000.0)
     return bb.build_model(0, bb.Vocab(size=1000), dims, head_scale=0.25, dtype=dtype)
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "bf16x2"])
-def test_stacked_refresh_kv_matches_per_branch_passes(dtype):
+@pytest.mark.parametrize("dtype,P,G,bsz", [("bf16", 32, 64, (8, 16, 32)), ("bf16x2", 32, 64, (8, 16, 32)),
+                                           ("bf16", 1024, 64, (8, 16, 32, 64)),
+                                           ("bf16x2", 1024, 64, (8, 16, 32, 64))])
+def test_stacked_refresh_kv_matches_per_branch_passes(dtype, P, G, bsz):
     """The stacked refresh (every refreshing branch in one B x L full pass,
     own key list per (request, branch)) writes the same caches as one full
     pass per branch (test flag 2048; the reference's loop, scheduler.py:379-383):
     after prefill + one block step + refresh, every branch's kv_vectorize of
     both requests of a 2-request session agrees (the GEMM row chunking differs,
-    so within bf16 rounding, not bitwise), and the page tables are identical."""
+    so within bf16 rounding, not bitwise), and the page tables are identical.
+    L = 1088 runs the full passes on the 128-row attention (C5's kernel) over
+    4 branches' row groups."""
     import torch
     from paper_2605_29233_b200.engine import Session
-    p = _refresh_model(dtype)
+    p = _refresh_model(dtype, max_len=max(192, P + G))
     vocab = p.vocab
-    cfg = bb.SchedulerConfig(block_sizes=(8, 16, 32), gen_len=64, refresh_interval=1)
-    tasks = [bb.make_task(s, 32, 64, vocab) for s in (3, 4)]
+    nb = len(bsz)
+    cfg = bb.SchedulerConfig(block_sizes=bsz, gen_len=G, refresh_interval=1)
+    tasks = [bb.make_task(s, P, G, vocab) for s in (3, 4)]
     prompts = np.stack([t.prompt for t in tasks])
     targets = np.stack([t.target for t in tasks])
     out = {}
     for flags in (0, 2048):
-        s = Session(p, cfg, 32, 2, test_flags=flags)
+        s = Session(p, cfg, P, 2, test_flags=flags)
         s.set_inputs(prompts, targets)
         s.prefill()
         s.iteration(True, use_graph=False)
         ctrl = s.ctrl_now()
         assert (ctrl[:, 18] == 1).all(), ctrl[:, 18]  # C_REFRESHES: one refresh charged per request
-        out[flags] = ([[s.kv_vec(r, k).cpu().numpy() for k in range(3)] for r in range(2)],
+        out[flags] = ([[s.kv_vec(r, k).cpu().numpy() for k in range(nb)] for r in range(2)],
                       s.v_pages.cpu().numpy().copy() if hasattr(s, "v_pages") else None, ctrl.copy())
         del s
         torch.cuda.synchronize()
@@ -376,12 +381,12 @@ def test_stacked_refresh_kv_matches_per_branch_passes(dtype):
         assert np.array_equal(pt_a, pt_b)
     worst = 0.0
     for r in range(2):
-        for k in range(3):
+        for k in range(nb):
             a, b = kv_a[r][k], kv_b[r][k]
             assert np.isfinite(a).all()
             worst = max(worst, float(np.abs(a - b).max() / (np.abs(b).max() + 1e-30)))
     tol = 2e-2 if dtype == "bf16" else 1e-4
-    print(f"{dtype}: stacked vs per-branch refresh KV max rel diff {worst:.2e}")
+    print(f"{dtype} L={P + G}: stacked vs per-branch refresh KV max rel diff {worst:.2e}")
     assert worst <= tol
 
 
