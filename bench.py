@@ -596,7 +596,9 @@ def main():
     ms_per_nfe = t_ms / max(nfe.sum(), 1)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": None, "peak_source": peak_src,
-            "kernel": f"k_gemm_tc<{s.info[11]},0> tcgen05 weight-streaming GEMM (block-step QKV/O/gate-up/down)",
+            # (bf16x2: the MMA's N holds every row twice, hi and lo -> the <2 * rows-per-chunk> instance)
+            "kernel": f"k_gemm_tc<{s.info[11] * (2 if args.precision == 'bf16x2' else 1)},0> tcgen05 "
+                      "weight-streaming GEMM (block-step QKV/O/gate-up/down)",
             "launches_timed": launches, "per_kind": per_kind,
             "duration_convention": "kernel entry (before the pre-wait weight TMA) to last CTA exit, "
                                    "min/max over CTAs, every launch in the timed region",
